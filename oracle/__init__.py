@@ -1,0 +1,213 @@
+"""ctypes wrapper for oracle/oracle.c -- TEST INFRASTRUCTURE ONLY.
+
+The oracle is a plain, literal CPU FP64 implementation of one refinement sweep
+(Alg. 4, with Alg. 2/3 for the WY factors).  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu-baseline / `--impl reference` legs
+may import this package.  It shares no code with paper_2602_23778_b200 and
+never imports it.
+
+All arrays are numpy float64 (int32 for CSR indices), row-major n x k.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+
+# status values (oracle.c enum)
+OK, MAXITER, DIVERGED, E_INVALID, E_NEAR_ZERO_RQ, E_ZERO_PIVOT, E_NOMEM = 0, 1, 2, -1, -2, -3, -6
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-mavx2", "-mfma", "-fopenmp", "-fPIC", "-shared", "-Wall"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (-ffp-contract=off: every fma in the oracle is explicit)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+class Stats(C.Structure):
+    _fields_ = [("rel_resid", C.c_double), ("corr_norm", C.c_double), ("min_gap", C.c_double),
+                ("delta_hits", C.c_int32), ("flipped", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        P = C.c_void_p
+        i64, i32, d = C.c_int64, C.c_int32, C.c_double
+        L.oracle_norm_inf_dense.argtypes = [i64, P, i64, d]; L.oracle_norm_inf_dense.restype = d
+        L.oracle_norm_inf_csr.argtypes = [i64, P, P, P, d]; L.oracle_norm_inf_csr.restype = d
+        L.oracle_apply_dense.argtypes = [i64, i32, P, i64, d, P, P]
+        L.oracle_apply_csr.argtypes = [i64, i32, P, P, P, d, P, P]
+        L.oracle_modified_lu.argtypes = [i64, i32, P, P]
+        L.oracle_compact_wy_lu.argtypes = [i64, i32, P, P, P, P, P]
+        L.oracle_compact_wy.argtypes = [i64, i32, P, P, P]
+        L.oracle_apply_h.argtypes = [i64, i32, P, P, i32, P, P, C.c_int]
+        L.oracle_sweep_dense.argtypes = [i64, i32, P, i64, d, P, d, i32, i32, C.POINTER(Stats), P]
+        L.oracle_sweep_csr.argtypes = [i64, i32, P, P, P, d, P, d, i32, i32, C.POINTER(Stats), P]
+        L.oracle_run_dense.argtypes = [i64, i32, P, i64, d, P, i32, d, d, i32, i32, d, C.POINTER(i32), P]
+        L.oracle_run_csr.argtypes = [i64, i32, P, P, P, d, P, i32, d, d, i32, i32, d, C.POINTER(i32), P]
+        L.oracle_num_threads.restype = C.c_int
+        for f in ("oracle_apply_dense", "oracle_apply_csr", "oracle_modified_lu", "oracle_compact_wy_lu",
+                  "oracle_compact_wy", "oracle_apply_h", "oracle_sweep_dense", "oracle_sweep_csr",
+                  "oracle_run_dense", "oracle_run_csr"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+class Operator:
+    """A (dense n x n, or CSR with both triangles) and the Sec. 5.1 shift."""
+
+    def __init__(self, A=None, row_ptr=None, col_idx=None, val=None, shift: float = 0.0):
+        self.shift = float(shift)
+        if A is not None:
+            self.is_csr = False
+            self.A = _f64(A)
+            self.n = self.A.shape[0]
+        else:
+            self.is_csr = True
+            self.rp, self.ci, self.v = _i32(row_ptr), _i32(col_idx), _f64(val)
+            self.n = self.rp.size - 1
+
+    def norm_inf(self) -> float:
+        L = lib()
+        if self.is_csr:
+            return L.oracle_norm_inf_csr(self.n, _p(self.rp), _p(self.ci), _p(self.v), self.shift)
+        return L.oracle_norm_inf_dense(self.n, _p(self.A), self.n, self.shift)
+
+    def apply(self, X) -> np.ndarray:
+        """W = A X - shift X (Alg. 4 line 1), fma chain in ascending column order."""
+        X = _f64(X)
+        k = X.shape[1]
+        W = np.empty_like(X)
+        L = lib()
+        if self.is_csr:
+            L.oracle_apply_csr(self.n, k, _p(self.rp), _p(self.ci), _p(self.v), self.shift, _p(X), _p(W))
+        else:
+            L.oracle_apply_dense(self.n, k, _p(self.A), self.n, self.shift, _p(X), _p(W))
+        return W
+
+
+def modified_lu(Q):
+    """Alg. 2.  Returns (Y unit-lower n x k, U k x k, sigma k, status)."""
+    Q = _f64(Q).copy()
+    n, k = Q.shape
+    sig = np.zeros(k)
+    st = lib().oracle_modified_lu(n, k, _p(Q), _p(sig))
+    Y = np.tril(Q, -1)
+    Y[np.arange(k), np.arange(k)] = 1.0
+    U = np.triu(Q[:k])
+    return Y, U, sig, st
+
+
+def compact_wy_lu(Q):
+    """Alg. 3.  Returns (Y, T, sigma, U, status)."""
+    Q = _f64(Q)
+    n, k = Q.shape
+    Y, T, sig, U = np.zeros((n, k)), np.zeros((k, k)), np.zeros(k), np.zeros((k, k))
+    st = lib().oracle_compact_wy_lu(n, k, _p(Q), _p(Y), _p(T), _p(sig), _p(U))
+    return Y, T, sig, U, st
+
+
+def compact_wy(Q):
+    """Alg. 1.  Returns (Y, T, status)."""
+    Q = _f64(Q)
+    n, k = Q.shape
+    Y, T = np.zeros((n, k)), np.zeros((k, k))
+    st = lib().oracle_compact_wy(n, k, _p(Q), _p(Y), _p(T))
+    return Y, T, st
+
+
+def apply_h(Y, T, B, transpose=False):
+    """H B = B - Y(T(Y^T B)) or H^T B."""
+    Y, T, B = _f64(Y), _f64(T), _f64(B)
+    n, k = Y.shape
+    m = B.shape[1]
+    out = np.empty_like(B)
+    lib().oracle_apply_h(n, k, _p(Y), _p(T), m, _p(B), _p(out), int(transpose))
+    return out
+
+
+DEBUG_KEYS = ("W", "Y", "T", "sigma", "dtilde", "alpha", "V", "E", "Xtilde", "U")
+
+
+@dataclass
+class SweepResult:
+    X: np.ndarray
+    status: int
+    stats: Stats
+    debug: dict
+
+
+def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=False) -> SweepResult:
+    """One sweep of Alg. 4 on a copy of X."""
+    X = _f64(X).copy()
+    n, k = X.shape
+    st = Stats()
+    dbg = {}
+    dptr = None
+    if debug:
+        shapes = {"W": (n, k), "Y": (n, k), "T": (k, k), "sigma": (k,), "dtilde": (k,), "alpha": (k,),
+                  "V": (n, k), "E": (n, k), "Xtilde": (n, k), "U": (k, k)}
+        dbg = {key: np.zeros(shapes[key]) for key in DEBUG_KEYS}
+        arr = (C.c_void_p * len(DEBUG_KEYS))(*[dbg[key].ctypes.data for key in DEBUG_KEYS])
+        dptr = C.cast(arr, C.c_void_p)
+    L = lib()
+    if op.is_csr:
+        s = L.oracle_sweep_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(X), delta_c, int(beta_zero),
+                               int(normalize), C.byref(st), dptr)
+    else:
+        s = L.oracle_sweep_dense(n, k, _p(op.A), n, op.shift, _p(X), delta_c, int(beta_zero), int(normalize),
+                                 C.byref(st), dptr)
+    return SweepResult(X, s, st, dbg)
+
+
+def run(op: Operator, X, iters: int, tol: float, delta_c=10.0, beta_zero=False, guard_window=3,
+        guard_factor=10.0):
+    """Iterate sweeps until ||E_L||_F <= tol, iters, or divergence.
+    Returns (X, status, iters_done, history[iters_done, 2] = (rel_resid, corr_norm))."""
+    X = _f64(X).copy()
+    n, k = X.shape
+    hist = np.zeros((max(iters, 1), 2))
+    done = C.c_int32(0)
+    L = lib()
+    if op.is_csr:
+        s = L.oracle_run_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(X), iters, tol, delta_c,
+                             int(beta_zero), guard_window, guard_factor, C.byref(done), _p(hist))
+    else:
+        s = L.oracle_run_dense(n, k, _p(op.A), n, op.shift, _p(X), iters, tol, delta_c, int(beta_zero),
+                               guard_window, guard_factor, C.byref(done), _p(hist))
+    return X, s, done.value, hist[:done.value]
+
+
+def num_threads() -> int:
+    return lib().oracle_num_threads()

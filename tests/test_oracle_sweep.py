@@ -1,0 +1,372 @@
+"""Pins for the oracle's refinement sweep (Alg. 4) against what
+the paper and the mathematics fix: eigenvectors from LAPACK (numpy.linalg.eigh) or a
+brute-force Jacobi, closed-form sine modes, the fixed point, the exact correction E_L of
+eq. (H-E-def) to first/second order, the linear rate of Thm. 3.7, the attainable
+accuracy, bitwise sign invariance, and the shift identity.  Nothing here re-types the
+oracle's formulas; each check goes through an independent route."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+U = 2.0 ** -53
+
+
+def sym_with_spectrum(n, lam, seed):
+    """Q diag(lam) Q^T with Q from numpy QR (independent of synth's reflectors)."""
+    rng = np.random.default_rng(seed)
+    q, r = np.linalg.qr(rng.standard_normal((n, n)))
+    q *= np.sign(np.diag(r))
+    A = (q * lam) @ q.T
+    return (A + A.T) / 2
+
+
+def align(Xh, X):
+    """Per-column sign alignment sign(x_j^T xh_j) (eigenvector signs are arbitrary)."""
+    s = np.sign(np.sum(Xh * X, axis=0))
+    s[s == 0] = 1.0
+    return Xh * s
+
+
+def jacobi_eig(A, sweeps=50):
+    """Brute-force cyclic Jacobi eigendecomposition (textbook, n <= 64)."""
+    A = np.array(A, dtype=np.float64)
+    n = A.shape[0]
+    V = np.eye(n)
+    for _ in range(sweeps):
+        off = np.sqrt(np.sum(np.tril(A, -1) ** 2))
+        if off < 1e-300:
+            break
+        for p in range(n - 1):
+            for q in range(p + 1, n):
+                if A[p, q] == 0.0:
+                    continue
+                theta = (A[q, q] - A[p, p]) / (2 * A[p, q])
+                t = np.sign(theta) / (abs(theta) + np.sqrt(theta * theta + 1)) if theta != 0 else 1.0
+                c = 1 / np.sqrt(t * t + 1); s = t * c
+                J = np.eye(n); J[p, p] = J[q, q] = c; J[p, q] = s; J[q, p] = -s
+                A = J.T @ A @ J
+                V = V @ J
+    return np.diag(A).copy(), V
+
+
+# ----------------------------------------------------------------------------- operator
+
+def test_apply_dense_and_csr_match_independent_products():
+    rng = np.random.default_rng(0)
+    A = sym_with_spectrum(70, rng.uniform(-3, 3, 70), 1)
+    X = rng.standard_normal((70, 5))
+    W = oracle.Operator(A=A, shift=0.7).apply(X)
+    ref = A @ X - 0.7 * X
+    bound = 4 * 71 * U * (np.abs(A) @ np.abs(X) + 0.7 * np.abs(X))
+    assert np.all(np.abs(W - ref) <= bound)
+    p = synth.small_laplacian((9, 7, 5), (1.0, 1.13, 1.29), 3)
+    M = sp.csr_matrix((p.val.numpy(), p.col_idx.numpy(), p.row_ptr.numpy()))
+    Xs = rng.standard_normal((p.n, 3))
+    Ws = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy()).apply(Xs)
+    assert np.allclose(Ws, M @ Xs, rtol=0, atol=1e-13)
+    assert abs(M - M.T).max() == 0.0                               # both triangles stored, symmetric
+
+
+def test_csr_fma_chain_order_is_literal():
+    """w_ij = fma chain over the CSR row in ascending column order (bitwise)."""
+    p = synth.small_laplacian((6, 5), (1.0, 1.37), 2)
+    rp, ci, v = p.row_ptr.numpy(), p.col_idx.numpy(), p.val.numpy()
+    X = np.random.default_rng(1).standard_normal((p.n, 2))
+    W = oracle.Operator(row_ptr=rp, col_idx=ci, val=v).apply(X)
+    from fractions import Fraction
+
+    def fma(a, b, c):   # exactly rounded a*b+c (Python int/int true division is correctly rounded)
+        return float(Fraction(a) * Fraction(b) + Fraction(c))
+    ref = np.zeros_like(X)
+    for i in range(p.n):
+        for j in range(2):
+            acc = 0.0
+            for t in range(rp[i], rp[i + 1]):
+                acc = fma(float(v[t]), float(X[ci[t], j]), acc)
+            ref[i, j] = acc
+    assert np.array_equal(W, ref)
+
+
+def test_sine_modes_are_eigenvectors_of_the_laplacian():
+    """Closed form (synth) vs the CSR operator: A' x = (sigma - mu) x to O(u)."""
+    p = synth.small_laplacian((12, 9, 7), (1.0, 1.13, 1.29), 6)
+    op = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy())
+    X = p.X.numpy()
+    R = op.apply(X) - X * p.lam_target
+    assert np.max(np.abs(R)) <= 50 * U * op.norm_inf()
+    assert np.linalg.norm(X.T @ X - np.eye(6)) <= 1e-14
+    Ad = sp.csr_matrix((p.val.numpy(), p.col_idx.numpy(), p.row_ptr.numpy())).toarray()
+    ev = np.linalg.eigvalsh(Ad)[::-1]
+    assert np.allclose(ev[:6], p.lam_target, atol=1e-12)           # the k largest of A'
+
+
+# ----------------------------------------------------------------------------- Rayleigh / Ediag
+
+def test_rayleigh_and_ediag_worked_examples():
+    g = json.load(open(os.path.join(GOLD, "rayleigh_examples.json")))
+    c = g["rayleigh"][0]
+    A = np.diag(c["A_diag"])
+    r = oracle.sweep(oracle.Operator(A=A), np.array(c["x"]).reshape(2, 1), debug=True)
+    assert r.status == oracle.OK
+    assert abs(r.debug["dtilde"][0] - c["d"]) <= 4 * U * c["d"]
+    # Ediag: alpha = 0.98 -> e_jj = 0.01 (exact eigenvector scaled by sqrt(0.98))
+    lam = np.array([5.0, 4.0, 1.0, 0.5, 0.25, -0.3])
+    A = sym_with_spectrum(6, lam, 3)
+    w, V = np.linalg.eigh(A)
+    x = V[:, [np.argmax(w)]] * np.sqrt(g["ediag"][0]["alpha"])
+    r = oracle.sweep(oracle.Operator(A=A), x, debug=True)
+    assert abs(r.debug["alpha"][0] - 0.98) <= 1e-15
+    assert abs(r.debug["E"][0, 0] - g["ediag"][0]["e"]) <= 1e-15
+    assert abs(r.debug["dtilde"][0] - 5.0) <= 4 * 6 * U * 5.0
+
+
+def test_rayleigh_scale_invariance():
+    A = sym_with_spectrum(30, np.linspace(-2, 9, 30), 4)
+    X = np.random.default_rng(5).standard_normal((30, 3))
+    d1 = oracle.sweep(oracle.Operator(A=A), X, debug=True).debug["dtilde"]
+    d2 = oracle.sweep(oracle.Operator(A=A), 2.0 * X, debug=True).debug["dtilde"]
+    assert np.array_equal(d1, d2)      # scaling by 2 is exact in binary floating point
+
+
+# ----------------------------------------------------------------------------- fixed point / E_L pins
+
+@pytest.mark.parametrize("n,k", [(40, 1), (64, 5), (120, 12)])
+def test_fixed_point(n, k):
+    """Exact eigenvectors (LAPACK) are a fixed point: E_L = O(u), X~ = X (eqs. Ediag, Eoffdiag)."""
+    rng = np.random.default_rng(n + k)
+    lam = np.concatenate([np.linspace(20, 10, k), rng.uniform(-5, 5, n - k)])
+    A = sym_with_spectrum(n, lam, n)
+    w, V = np.linalg.eigh(A)
+    X = V[:, np.argsort(-np.abs(w))[:k]]
+    r = oracle.sweep(oracle.Operator(A=A), X, debug=True)
+    assert r.status == oracle.OK
+    assert r.stats.corr_norm <= 200 * n * U
+    assert np.linalg.norm(align(r.X, X) - X) <= 200 * n * U
+
+
+@pytest.mark.parametrize("n,k,seed", [(50, 3, 0), (80, 6, 1), (60, 1, 2)])
+def test_correction_against_exact_EL(n, k, seed):
+    """E_L is defined by X = X^ + H^ E_L (eq. H-E-def).  Brute force:
+    E_L = H^T X' - I_{n,k} with H^ built from X^ (H^ orthogonal for orthonormal X^) and X'
+    the exact eigenvectors in X^'s sign frame.  From eqs. (HhatX-block)-(V-def): the top
+    block of E~_L agrees with E_11 to O(eps^2); the lower block satisfies
+    E~_21 = E_21 - D_2 E_21 D_1^{-1} + O(eps^2) with D_2 = (H^T A H)_22."""
+    rng = np.random.default_rng(seed)
+    lam = np.concatenate([np.linspace(10, 6, k), rng.uniform(-3, 3, n - k)])
+    A = sym_with_spectrum(n, lam, seed + 100)
+    w, V = np.linalg.eigh(A)
+    order = np.argsort(-np.abs(w))[:k]
+    Xt = V[:, order]
+    D1 = np.diag(w[order])
+    eps = 1e-5
+    Xh = Xt + eps * rng.standard_normal((n, k))
+    Xh, _ = np.linalg.qr(Xh)                     # orthonormal X^ so H^ is orthogonal
+    Xh = align(Xh, Xt)
+    r = oracle.sweep(oracle.Operator(A=A), Xh, debug=True, normalize=False)
+    assert r.status == oracle.OK
+    Y, T, sig = r.debug["Y"], r.debug["T"], r.debug["sigma"]
+    H = np.eye(n) - Y @ T @ Y.T
+    Xp = Xt * sig                                # exact eigenvectors in the flipped frame
+    EL = H.T @ Xp - np.eye(n, k)
+    Et = r.debug["E"]
+    e = np.linalg.norm(EL)
+    assert e > 1e-6
+    D1f = D1                                      # flipping signs does not change eigenvalues
+    D2 = (H.T @ A @ H)[k:, k:]
+    assert np.linalg.norm(Et[:k] - EL[:k]) <= 100 * e * e
+    pred = EL[k:] - D2 @ EL[k:] @ np.linalg.inv(D1f)
+    assert np.linalg.norm(Et[k:] - pred) <= 100 * e * e
+    # and X~ = X^' + H^ E~_L  (line 7) reproduced through the explicit H^
+    assert np.linalg.norm(r.debug["Xtilde"] - (Xh * sig + H @ Et)) <= 1e-13
+
+
+def test_V_is_HT_residual_with_explicit_H():
+    """Line 5 (eq. V-def): V = H^T (W - X D) -- compare the implicit WY application
+     with an explicit n x n H^."""
+    n, k = 70, 5
+    A = sym_with_spectrum(n, np.concatenate([np.linspace(9, 7, k), np.linspace(-4, 4, n - k)]), 9)
+    w, V = np.linalg.eigh(A)
+    Xh = V[:, np.argsort(-np.abs(w))[:k]] + 1e-4 * np.random.default_rng(3).standard_normal((n, k))
+    r = oracle.sweep(oracle.Operator(A=A), Xh, debug=True)
+    Y, T, sig, d = r.debug["Y"], r.debug["T"], r.debug["sigma"], r.debug["dtilde"]
+    H = np.eye(n) - Y @ T @ Y.T
+    Xf = Xh * sig
+    Vref = H.T @ (A @ Xf - Xf * d)
+    assert np.linalg.norm(r.debug["V"] - Vref) <= 1e-13 * max(1.0, np.linalg.norm(Vref)) + 1e-14
+    assert np.array_equal(r.debug["W"], r.debug["W"])
+    assert np.linalg.norm(r.debug["W"] - A @ Xf) <= 1e-13 * np.linalg.norm(A @ Xf)
+
+
+def test_diagonal_A_first_order():
+    """A = diag(lam), X^ = I_{n,k} + eps B: the lower block of X~ is eps D_2 B_2 D_1^{-1} + O(eps^2)
+    (first-order term of eq. V-def's lower block: V_2 = E_21 D_1, E_21 = -eps B_2 + D_2 ... )."""
+    n, k, eps = 40, 4, 1e-6
+    lam = np.concatenate([[9.0, 8.0, 7.0, 6.0], np.linspace(-2, 2, n - k)])
+    B = np.random.default_rng(2).standard_normal((n, k))
+    Xh = np.eye(n, k) + eps * B
+    r = oracle.sweep(oracle.Operator(A=np.diag(lam)), Xh, debug=True, normalize=False)
+    sig = r.debug["sigma"]
+    X2 = r.debug["Xtilde"][k:] * sig             # back to the unflipped frame
+    pred = eps * (lam[k:, None] * B[k:]) / lam[None, :k]
+    assert np.linalg.norm(X2 - pred) <= 50 * eps * eps * np.linalg.norm(B) ** 2
+    assert np.linalg.norm(X2 - pred) < 1e-3 * np.linalg.norm(pred)
+
+
+def test_sign_flip_invariance_bitwise():
+    """sweep(X S) == sweep(X) for any column signs S (the Sigma frame is canonical)."""
+    p = synth.small_dense(120, 6, signs=True)
+    A, X0 = p.A.numpy(), p.X0.numpy()
+    r1 = oracle.sweep(oracle.Operator(A=A), X0)
+    S = np.array([1, -1, -1, 1, -1, 1.0])
+    r2 = oracle.sweep(oracle.Operator(A=A), X0 * S)
+    assert np.array_equal(r1.X, r2.X)
+    assert r1.stats.rel_resid == r2.stats.rel_resid and r1.stats.corr_norm == r2.stats.corr_norm
+
+
+# ----------------------------------------------------------------------------- convergence
+
+def test_rate_law():
+    """Thm. 3.7 remark: per-column error ratio -> gamma_j =
+    max_{i>k}|lam_i| / |lam_j|."""
+    n, k = 160, 3
+    lam_t = np.array([10.0, 9.0, 8.0])
+    rest = np.linspace(-5.0, 5.0, n - k)
+    A = sym_with_spectrum(n, np.concatenate([lam_t, rest]), 21)
+    w, V = np.linalg.eigh(A)
+    Xt = V[:, np.argsort(-np.abs(w))[:k]]
+    X = Xt + 1e-4 * np.random.default_rng(4).standard_normal((n, k))
+    op = oracle.Operator(A=A)
+    errs = []
+    for _ in range(14):
+        r = oracle.sweep(op, X)
+        X = r.X
+        errs.append(np.linalg.norm(align(X, Xt) - Xt, axis=0))
+    errs = np.array(errs)
+    ratios = errs[6:12] / errs[5:11]
+    gm = np.exp(np.mean(np.log(ratios), axis=0))
+    gamma = 5.0 / lam_t
+    assert np.all(gm >= 0.5 * gamma) and np.all(gm <= 1.1 * gamma), (gm, gamma)
+
+
+def test_cfg1_converges_to_100nu_and_residual_floor():
+    """BASELINE cfg1 (n=256, k=4): converged error vs the known truth <= 100 n u
+    (north_star) and residual O(u)||A||."""
+    p = synth.make_config("cfg1")
+    op = oracle.Operator(A=p.A.numpy())
+    X, st, it, hist = oracle.run(op, p.X0.numpy(), iters=40, tol=1e-14)
+    Xt = p.X.numpy()
+    err = np.linalg.norm(align(X, Xt) - Xt, axis=0).max()
+    assert err <= 100 * p.n * U, err
+    r = oracle.sweep(op, X)
+    assert r.stats.rel_resid <= 50 * U * np.sqrt(p.k)
+    assert hist[0, 1] > 1e-7 and it <= 12         # gamma = 0.142: a handful of sweeps
+
+
+def test_jacobi_bruteforce_small():
+    """n <= 64: refined vectors equal the brute-force Jacobi eigenvectors."""
+    n, k = 24, 3
+    lam = np.concatenate([[6.0, -5.5, 5.0], np.linspace(-1.5, 1.5, n - k)])
+    A = sym_with_spectrum(n, lam, 31)
+    wj, Vj = jacobi_eig(A)
+    Xt = Vj[:, np.argsort(-np.abs(wj))[:k]]
+    X0 = Xt + 1e-5 * np.random.default_rng(6).standard_normal((n, k))
+    X, st, it, _ = oracle.run(oracle.Operator(A=A), X0, iters=60, tol=1e-15)
+    assert np.linalg.norm(align(X, Xt) - Xt, axis=0).max() <= 100 * n * U
+    assert np.allclose(np.sort(np.abs(wj))[::-1][:k], np.abs([6.0, -5.5, 5.0]), atol=1e-13)
+
+
+def test_laplacian_converges_to_sine_modes():
+    """Sparse path: shifted Laplacian A' = sigma I - L, k smallest-L modes (closed form)."""
+    p = synth.small_laplacian((7, 3), (1.0, 1.37), 3, noise=1e-6)     # gamma = 0.897
+    op = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy())
+    X, st, it, _ = oracle.run(op, p.X0.numpy(), iters=400, tol=1e-15)
+    Xt = p.X.numpy()
+    assert np.linalg.norm(align(X, Xt) - Xt, axis=0).max() <= 100 * p.n * U
+
+
+def test_shift_identity():
+    """Sec. 5.1: L with shift=sigma gives B = L - sigma I = -A'; the sweep is
+    invariant under A -> -A (d and V change sign together), so iterates agree to rounding."""
+    p = synth.small_laplacian((9, 8), (1.0, 1.37), 3)
+    rp, ci, v = p.row_ptr.numpy(), p.col_idx.numpy(), p.val.numpy()
+    sigma = p.meta["sigma"]
+    vL = np.where(ci == np.repeat(np.arange(p.n), np.diff(rp)), sigma - v, -v)   # L = sigma I - A'
+    r1 = oracle.sweep(oracle.Operator(row_ptr=rp, col_idx=ci, val=v), p.X0.numpy())
+    r2 = oracle.sweep(oracle.Operator(row_ptr=rp, col_idx=ci, val=vL, shift=sigma), p.X0.numpy())
+    assert r1.status == r2.status == oracle.OK
+    assert np.linalg.norm(r1.X - r2.X) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- statuses and branches
+
+def test_near_zero_rq_and_nan():
+    A = np.diag([0.0, 1.0, 2.0, 3.0])
+    X = np.eye(4, 1)
+    assert oracle.sweep(oracle.Operator(A=A), X).status == oracle.E_NEAR_ZERO_RQ
+    X = np.eye(4, 2) + 1e-3
+    X[2, 1] = np.nan
+    assert oracle.sweep(oracle.Operator(A=np.diag([5.0, 4, 1, 0.5])), X).status == oracle.DIVERGED
+
+
+def test_invalid_k():
+    assert oracle.sweep(oracle.Operator(A=np.eye(3)), np.ones((3, 3))).status == oracle.E_INVALID
+
+
+def test_delta_branch_beta():
+    """lam_1 = lam_2 inside the targets: |d_2 - d_1| <= delta takes beta_ij = -x_i^T x_j/2
+     or 0 (:460).  Parity unpinned beyond this construction."""
+    n = 20
+    A = np.diag(np.concatenate([[3.0, 3.0], np.linspace(-1, 1, n - 2)]))
+    X = np.eye(n, 2)
+    X[5, 0] = 1e-3; X[6, 1] = 2e-3; X[1, 0] = 1e-4; X[0, 1] = 3e-4
+    r = oracle.sweep(oracle.Operator(A=A), X, debug=True)
+    r0 = oracle.sweep(oracle.Operator(A=A), X, debug=True, beta_zero=True)
+    Xf = X * r.debug["sigma"]
+    G01 = Xf[:, 0] @ Xf[:, 1]
+    # Rayleigh quotients are 3 - O(1e-6) for both; their gap is << delta only if equal, so
+    # force equality by symmetric construction check
+    gap = abs(r.debug["dtilde"][1] - r.debug["dtilde"][0])
+    delta = 10 * 3.0 * U
+    if gap <= delta:
+        assert r.stats.delta_hits == 2
+        assert abs(r.debug["E"][0, 1] + G01 / 2) <= 1e-18 and r0.debug["E"][0, 1] == 0.0
+    else:
+        assert r.stats.delta_hits == 0
+
+
+def test_delta_branch_exact_tie():
+    """Exact tie of Rayleigh quotients: symmetric construction guarantees d_1 == d_2."""
+    n = 12
+    lam = np.concatenate([[4.0, 4.0], np.linspace(-1, 1, n - 2)])
+    A = np.diag(lam)
+    X = np.zeros((n, 2)); X[0, 0] = X[1, 1] = 1.0
+    X[4, 0] = X[4, 1] = 1e-3                    # identical perturbations -> identical RQs
+    r = oracle.sweep(oracle.Operator(A=A), X, debug=True)
+    assert r.debug["dtilde"][0] == r.debug["dtilde"][1]
+    assert r.stats.delta_hits == 2
+    Xf = X * r.debug["sigma"]
+    assert r.debug["E"][0, 1] == -(Xf[:, 0] @ Xf[:, 1]) / 2
+    r0 = oracle.sweep(oracle.Operator(A=A), X, debug=True, beta_zero=True)
+    assert r0.debug["E"][0, 1] == 0.0 and r0.debug["E"][1, 0] == 0.0
+
+
+def test_thread_count_invariance():
+    """Fixed-order reductions: 1 thread and all threads give bitwise equal sweeps."""
+    code = ("import numpy as np, oracle, synth, sys; p=synth.small_laplacian((40,30),(1.0,1.37),5);"
+            "r=oracle.sweep(oracle.Operator(row_ptr=p.row_ptr.numpy(),col_idx=p.col_idx.numpy(),val=p.val.numpy()),"
+            "p.X0.numpy()); sys.stdout.write(r.X.tobytes().hex()[:4000] + str(r.X.sum()))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for th in ("1", "4"):
+        env = dict(os.environ, OMP_NUM_THREADS=th, PYTHONPATH=root)
+        outs.append(subprocess.check_output([sys.executable, "-c", code], env=env, cwd=root))
+    assert outs[0] == outs[1]
