@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the refinement sweep (arXiv 2602.23778 Alg. 4) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+A "step" is one sweep (all SURVEY.md Sec. 8(a) steps) over the config's X^ (n x k).
+Headline workload: BASELINE.json configs[2] (cfg3: dense FP64 n=32768, k=64) -- the
+largest dense config, whose 8.6 GB A is larger than L2 (so no flush is needed between
+timed sweeps).  Metric: sweeps/s (BASELINE.json "refinement sweeps/s per config").
+Rank 0 prints ONE JSON line.  Other configs are reported under "per_config" (sweeps/s
+and roofline fraction each, smaller K).
+
+--impl reference times the oracle (oracle/, the plain CPU program the parity tests
+trust) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+METRIC = "refinement sweeps/s"
+
+
+def peaks():
+    hbm = 6547.5
+    try:
+        hbm = json.load(open(PEAKS_FILE))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        hbm_src = "fallback"
+    fp64 = json.load(open(FP64_FILE))["dmma_fp64_tflops"]
+    return hbm, hbm_src, fp64
+
+
+def alg_counts(p):
+    """Per-sweep algorithmic flops and bytes (Table 1, FMA = 2 flops)."""
+    n, k = p.n, p.k
+    if p.kind == "dense":
+        f = 2.0 * n * n * k + 8.0 * n * k * k
+        b = 8.0 * n * n + 16.0 * n * k
+    else:
+        f = 2.0 * p.nnz * k + 8.0 * n * k * k
+        b = 12.0 * p.nnz + 4.0 * (n + 1) + 16.0 * n * k
+    return f, b
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    elif args.impl != "reference":
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device="cuda"):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_problem(name, device):
+    import synth
+    return synth.make_config(name, device=device)
+
+
+def time_ours(p, steps, warmup, world, local, profile=True):
+    """Device-timed sweeps: CUDA events on the library's stream, barrier + sync on both sides."""
+    import torch
+    import paper_2602_23778_b200 as pkg
+    stream = torch.cuda.current_stream()
+    if p.kind == "dense":
+        R = pkg.Refiner.dense(p.A, p.k, shift=p.shift, stream=stream)
+    else:
+        R = pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, shift=p.shift, stream=stream)
+    X = p.X0.clone()
+    for _ in range(warmup):
+        R.refine_sweep(X)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if profile:
+        R.refine_profile_begin(steps)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        R.refine_sweep(X)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    kern = None
+    if profile:
+        kern, ns = R.refine_profile_end()
+        kern = {k_: v / max(ns, 1) for k_, v in kern.items()}       # ms per launch
+    s, st = R.refine_sweep(X, stats=True)
+    return ms / steps, kern, R, X, st, s
+
+
+def time_e2e(R, p, steps, warmup):
+    """Host buffers through the C ABI: H2D of X^, sweep, D2H of the result, each step."""
+    import torch
+    Xh = p.X0.cpu().pin_memory() if p.X0.is_cuda else p.X0.clone().pin_memory()
+    for _ in range(max(1, warmup)):
+        R.refine_sweep_host(Xh)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s, st = R.refine_sweep_host(Xh)
+    t1 = time.perf_counter()
+    nb = p.n * p.k * 8
+    return (t1 - t0) / steps, nb, nb + 40
+
+
+def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak):
+    """Dominant kernel: its algorithmic flops (bytes) per launch / its average launch time."""
+    if not kern:
+        return None
+    top = max(kern, key=kern.get)
+    n, k = p.n, p.k
+    traffic = None
+    try:
+        tr = json.load(open(TRAFFIC_FILE))
+        traffic = tr.get(p.name, {}).get(top)
+    except Exception:
+        pass
+    t = kern[top] * 1e-3
+    if top == "gemm_ax":
+        flops = 2.0 * n * n * k
+        ach = flops / t / 1e12
+        return {"kernel": top, "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": ach / fp64_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
+                "per_launch_alg": f"2*n*n*k = {flops:.4g} flop (FP64 DMMA)",
+                "peak_source": "DMMA FP64 microbenchmark on this pool's B200 (profiles/r01_fp64_peaks.json)"}
+    if top in ("passB", "passC"):
+        rows = n - k
+        fl = (4.0 if top == "passB" else 2.0) * rows * k * k
+        by = (16.0 if top == "passB" else 24.0) * rows * k
+        t_f, t_b = fl / (fp64_peak * 1e12), by / (hbm_peak * 1e9)
+        if t_f >= t_b:
+            ach = fl / t / 1e12
+            return {"kernel": top, "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": ach / fp64_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
+                    "per_launch_alg": f"{fl:.4g} flop", "peak_source": "DMMA FP64 microbenchmark"}
+        ach = by / t / 1e9
+        return {"kernel": top, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
+                "per_launch_alg": f"{by:.4g} bytes", "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    if top == "spmm_csr":
+        by = 12.0 * p.nnz + 4.0 * (n + 1) + 16.0 * n * k
+        ach = by / t / 1e9
+        return {"kernel": top, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
+                "per_launch_alg": f"A + X + W = {by:.4g} bytes", "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    return {"kernel": top, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
+            "traffic": traffic, "share_of_step": kern[top] / ms_step}
+
+
+def cpu_baseline(name, budget_s=25.0):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload.
+    Sample: the same config family at reduced n (dense: n scaled so one oracle sweep is
+    ~seconds; CSR: the full config if it fits the budget), converted to full-size sweeps/s
+    by the ratio of algorithmic flops (SURVEY.md 8(d) F_alg)."""
+    import numpy as np
+    import oracle
+    import synth
+    full = {"cfg1": (256, 4), "cfg2": (4096, 16), "cfg2b": (4096, 16), "cfg3": (32768, 64)}
+    if name in full:
+        n_full, k = full[name]
+        n_s = min(n_full, 8192)
+        p = synth.make_config(name, device="cuda" if n_s > 4096 else "cpu", n=n_s)
+        op = oracle.Operator(A=p.A.cpu().numpy())
+        X = p.X0.cpu().numpy()
+        f_full = 2.0 * n_full * n_full * k + 8.0 * n_full * k * k
+        f_s = 2.0 * n_s * n_s * k + 8.0 * n_s * k * k
+        sample = f"{name} family at n={n_s} (k={k}), oracle sweeps until {budget_s:.0f}s budget; scaled by F_alg ratio"
+    else:
+        p = synth.make_config(name, device="cpu")
+        op = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy())
+        X = p.X0.numpy()
+        f_full = f_s = 1.0
+        sample = f"{name} at full size, oracle sweeps until {budget_s:.0f}s budget"
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        r = oracle.sweep(op, X)
+        times.append(time.perf_counter() - t0)
+        X = r.X
+        if time.perf_counter() - t_start > budget_s or len(times) >= 20:
+            break
+    sec = statistics.median(times)
+    return {"value": (1.0 / sec) * (f_s / f_full), "unit": "sweeps/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "sample": sample, "oracle_s_per_sample_sweep": sec, "sample_sweeps": len(times)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle (plain CPU FP64 program) timed as it stands."""
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.config, budget_s=max(5.0, 150.0 / max(args.steps + args.warmup, 1)))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "sweeps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config}, "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip per_config and cpu_baseline")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    hbm, hbm_src, fp64 = peaks()
+    # Multi-GPU: this build runs N independent replicas; each rank
+    # refines its own copy, so the whole-job value is N x the per-replica rate (weak scaling).
+    p = make_problem(args.config, f"cuda:{local}")
+    with Clocks(local) as clk:
+        ms, kern, R, X, st, s = time_ours(p, args.steps, args.warmup, world, local)
+    ms_max = max_over_ranks(ms, world)
+    value = world * 1000.0 / ms_max
+    f, b = alg_counts(p)
+    line = {"metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n": p.n, "k": p.k, "kind": p.kind,
+                       "nnz": p.nnz, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (A = %.2f GB)" % (p.nnz * 8 / 1e9) if p.kind == "dense"
+                       else "A + X^ + W larger than L2"},
+            "clocks": clk.summary(),
+            "sweep": {"tflops_alg": f / (ms_max * 1e-3) / 1e12, "gbs_alg": b / (ms_max * 1e-3) / 1e9,
+                      "frac_of_sweep_roofline": max(f / (fp64 * 1e12), b / (hbm * 1e9)) / (ms_max * 1e-3),
+                      "F_alg": f, "B_alg": b, "status": s, "rel_resid": st.rel_resid, "corr_norm": st.corr_norm},
+            "kernels_ms": kern,
+            "roofline": roofline_for(p, kern, ms_max, fp64, hbm),
+            "gpu_launches": R.kernels_per_sweep() * args.steps}
+    # e2e through the host-buffer C ABI call
+    e2e_s, h2d, d2h = time_e2e(R, p, max(3, args.steps // 2), 1)
+    e2e_s = max_over_ranks(e2e_s, world)
+    line["e2e"] = {"value": world / e2e_s, "unit": "sweeps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    del R, X
+    if not args.no_extra:
+        per = {}
+        for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+            if name == args.config:
+                per[name] = {"sweeps_s": value / world, "roofline": line["roofline"],
+                             "frac_of_sweep_roofline": line["sweep"]["frac_of_sweep_roofline"]}
+                continue
+            q = make_problem(name, f"cuda:{local}")
+            qms, qk, QR, QX, qst, qs = time_ours(q, 5 if q.n > 10000 else 20, 3, 1, local)
+            qf, qb = alg_counts(q)
+            per[name] = {"sweeps_s": 1000.0 / qms, "ms_per_sweep": qms, "kernels_ms": qk,
+                         "roofline": roofline_for(q, qk, qms, fp64, hbm),
+                         "frac_of_sweep_roofline": max(qf / (fp64 * 1e12), qb / (hbm * 1e9)) / (qms * 1e-3)}
+            del QR, QX, q
+            torch.cuda.empty_cache()
+        line["per_config"] = per
+    if rank == 0 and not args.no_extra and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config)
+        except Exception as e:  # never fail the bench on the baseline leg
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * refine.h -- C ABI of the B200-native refinement sweep (paper_2602_23778_b200).
+ *
+ * One refinement sweep of arXiv 2602.23778, Algorithm 4:
+ * given k << n approximate eigenvectors X^ of a real symmetric n x n matrix A,
+ *   W = A X^                              (line 1; shifted A - shift I, Sec. 5.1)
+ *   Y^, T^ from X^ by CompactWY_LU        (line 2; Alg. 2, Alg. 3)
+ *   alpha_j = x_j^T x_j, d_j = x_j^T w_j / alpha_j        (lines 3-4, eq. Rayleigh)
+ *   V = H^T (W - X^ D)                    (line 5, eq. V-def; H = I - Y T Y^T)
+ *   E_L from V, d, alpha, delta, beta     (line 6, eqs. Ediag/Eoffdiag PAPER.md:395-426, 443-460)
+ *   X^ <- X^ + H E_L                      (line 7, eq. update-X)
+ * followed by column normalisation.  The sign transformation
+ * X^ <- X^ Sigma of PAPER.md:304-306 is applied inside every sweep (DESIGN.md
+ * reading R2), so column signs of X may flip (reported in stats.flipped).
+ *
+ * All arithmetic is FP64.  Every entry point is extern "C"
+ * and takes only plain pointers and sizes; nothing is thrown across the ABI.
+ *
+ * Memory:  pointers documented "device" are CUDA device pointers on the
+ * context's device; "host" pointers are ordinary (preferably pinned) host
+ * memory.  Blocks of size n x k are ROW-MAJOR with leading dimension k
+ * (entry (i, j) at [i*k + j]).
+ *
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  All work is enqueued on it; calls return without a host sync
+ * unless documented otherwise.  One context per stream; a context is not
+ * re-entrant.
+ *
+ * Errors: every call returns a refine_status.  CUDA and NCCL errors are sticky
+ * on the context (every later call returns the same error).  Device-side
+ * conditions (near-zero Rayleigh quotient, zero pivot, non-finite values) are
+ * detected on the device and reach the host when stats are requested, on
+ * refine_run's checks, or via refine_get_status().  When such a condition is
+ * detected the sweep leaves X unmodified.
+ */
+#ifndef PAPER_2602_23778_REFINE_H
+#define PAPER_2602_23778_REFINE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct refine_ctx refine_ctx;   /* opaque; owned by the library */
+
+typedef enum {
+  REFINE_OK = 0,               /* refine_run: ||E_L||_F <= tol; otherwise success          */
+  REFINE_MAXITER = 1,          /* refine_run: iteration budget exhausted                                  */
+  REFINE_DIVERGED = 2,         /* non-finite value, or ||E_L||_F grew >= guard_factor within guard_window
+                                  sweeps                                                  */
+  REFINE_E_INVALID = -1,       /* bad argument: k < 1, k >= n, lda < n, NULL, CSR out of range, alpha<=0  */
+  REFINE_E_NEAR_ZERO_RQ = -2,  /* |d_j| <= delta (PAPER.md:443-446 divides by d_j): shift A (Sec. 5)       */
+  REFINE_E_ZERO_PIVOT = -3,    /* modified-LU pivot exactly zero (Alg. 2 line 4; defensive)               */
+  REFINE_E_CUDA = -4,          /* CUDA runtime error (sticky)                                             */
+  REFINE_E_NCCL = -5,          /* NCCL error (sticky)                                                     */
+  REFINE_E_NOMEM = -6,         /* device allocation failed                                                */
+  REFINE_E_UNSUPPORTED = -7    /* k above the compiled maximum (128) or another unsupported shape         */
+} refine_status;
+
+/* Process group of the row partition (one process per GPU).  world == 1:
+ * everything local, nccl_id ignored.  world > 1: rank r owns rows
+ * [row_begin, row_end) of A and X^; rank 0 must own rows 0..k-1; nccl_id is
+ * the 128-byte ncclUniqueId produced by refine_nccl_id() on rank 0 and
+ * broadcast by the caller (e.g. torch.distributed). */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  const void* nccl_id;
+} refine_comm;
+
+/* Options (NULL = defaults). */
+typedef struct {
+  double delta_c;        /* delta = delta_c * ||A - shift I||_inf * 2^-53; default 10 */
+  int32_t beta_zero;     /* 0: beta_ij = -x_i^T x_j / 2; 1: beta_ij = 0      */
+  int32_t normalize;     /* 1: normalise columns after each update; default 1              */
+  int32_t guard_window;  /* refine_run divergence guard window; default 3                                 */
+  double guard_factor;   /* refine_run divergence guard growth factor; default 10                         */
+} refine_opts;
+
+/* Per-sweep diagnostics (host struct), for the sweep's input X^ (after the sign flip). */
+typedef struct {
+  double rel_resid;      /* ||A X^ - X^ D||_F / ||A - shift I||_inf                 */
+  double corr_norm;      /* ||E_L||_F                     */
+  double min_gap;        /* min_{i != j} |d_j - d_i| over the k Rayleigh quotients                       */
+  int32_t delta_hits;    /* ordered pairs (i, j), i != j, that took the beta branch        */
+  int32_t flipped;       /* 1 if any sigma_j = -1 this sweep (X^ <- X^ Sigma)           */
+} refine_sweep_stats;
+
+/* Dense symmetric A (both triangles), FP64, row-major, device pointer.
+ * A_rows points at row row_begin of A; rows [row_begin, row_end) are local,
+ * each of length n with leading dimension lda >= n.  A is BORROWED: keep it
+ * alive and unmodified until refine_destroy.  shift: operator is A - shift*I
+ * (PAPER.md:1203).  Allocates every workspace (O(n_loc k + k^2)); computes
+ * ||A - shift I||_inf once (one pass over A).  On success *out is a new
+ * context; on error *out is NULL. */
+refine_status refine_init_dense(refine_ctx** out, int64_t n, int32_t k,
+                                const double* A_rows, int64_t lda,
+                                int64_t row_begin, int64_t row_end, double shift,
+                                const refine_comm* comm, const refine_opts* opts, void* stream);
+
+/* CSR symmetric A (both triangles stored), device pointers: row_ptr has
+ * (row_end - row_begin + 1) int32 entries relative to val/col_idx (row_ptr[0]
+ * may be nonzero), col_idx are GLOBAL int32 column indices sorted ascending
+ * within each row, val FP64.  Borrowed like the dense A.  Within a row the
+ * product is an fma chain in ascending CSR order (bit-reproducible). */
+refine_status refine_init_csr(refine_ctx** out, int64_t n, int32_t k,
+                              const int32_t* row_ptr, const int32_t* col_idx, const double* val,
+                              int64_t row_begin, int64_t row_end, double shift,
+                              const refine_comm* comm, const refine_opts* opts, void* stream);
+
+/* One sweep on X (device, (row_end-row_begin) x k row-major), in place.
+ * stats == NULL: fully asynchronous.  stats != NULL: the call synchronises the
+ * stream and returns the device status of this sweep. */
+refine_status refine_sweep(refine_ctx* c, double* X, refine_sweep_stats* stats);
+
+/* Same sweep with HOST buffers (end-to-end entry point): copies X_host_in
+ * (n_loc x k) to the device, runs one sweep, copies the result to X_host_out
+ * (may equal X_host_in) and synchronises.  Pinned memory gives full PCIe rate. */
+refine_status refine_sweep_host(refine_ctx* c, const double* X_host_in, double* X_host_out,
+                                refine_sweep_stats* stats);
+
+/* Iterate sweeps on X (device) until ||E_L||_F <= tol (REFINE_OK), iters sweeps
+ * (REFINE_MAXITER), divergence (REFINE_DIVERGED) or a device error.  Synchronises.
+ * iters_done / last (nullable) report the sweeps executed and the last stats. */
+refine_status refine_run(refine_ctx* c, double* X, int32_t iters, double tol,
+                         int32_t* iters_done, refine_sweep_stats* last);
+
+/* Status of the last enqueued sweep (synchronises the stream). */
+refine_status refine_get_status(refine_ctx* c);
+
+/* Capture the sweep for X as a CUDA graph and replay it on later calls with the
+ * same X pointer (enable = 1), or launch kernels directly (enable = 0, default). */
+refine_status refine_set_graph(refine_ctx* c, int32_t enable);
+
+/* Number of CUDA kernel launches one sweep enqueues (for the bench's gpu_launches). */
+int32_t refine_kernels_per_sweep(const refine_ctx* c);
+
+/* Live per-kernel timing (bench.py's roofline): after refine_profile_begin, every sweep
+ * enqueued (without graphs) records a CUDA event at each kernel boundary on the context's
+ * stream; refine_profile_end synchronises and writes, for each of the
+ * refine_kernels_per_sweep() kernels, the summed milliseconds over the recorded sweeps
+ * (ms_sum must hold that many doubles).  refine_kernel_name(i) names kernel i. */
+refine_status refine_profile_begin(refine_ctx* c, int32_t max_sweeps);
+refine_status refine_profile_end(refine_ctx* c, double* ms_sum, int32_t* nkernels, int32_t* nsweeps);
+const char* refine_kernel_name(const refine_ctx* c, int32_t i);
+
+void refine_destroy(refine_ctx* c);
+const char* refine_status_string(refine_status s);
+
+/* 128-byte ncclUniqueId for world > 1 (call on rank 0, broadcast to all ranks). */
+refine_status refine_nccl_id(void* out128);
+
+/* Test hook: copy an intermediate of the LAST sweep to device buffer dst
+ * (synchronises).  what: 0 W = A X^ - shift X^ (n_loc x k, for the sweep's un-flipped input), 1 sigma (k), 2 U (k x k,
+ * un-flipped modified-LU factor), 3 Y_1 (k x k, unit lower), 4 T (k x k),
+ * 5 dtilde (k), 6 alpha (k), 7 E_11 (k x k), 8 Y (n_loc x k, materialised by
+ * the tall-skinny triangular apply Y_2 = X_2 U^{-1}; expects the sweep's input X
+ * in dst on entry), 9 status-independent stats vector (8 doubles). */
+refine_status refine_debug_get(refine_ctx* c, int32_t what, double* dst);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,101 @@
+// common.cuh -- device helpers shared by the sweep kernels (sm_100a, FP64).
+//
+//  * DMMA: the FP64 tensor-core instruction.  sm_100a has no tcgen05 FP64 kind;
+//    every f64 mma.sync shape lowers to SASS DMMA.8x8x4 (checked with cuobjdump),
+//    so m8n8k4 is used directly.  Measured on the B200 box: 37.1 TFLOP/s chip
+//    peak (tools/fp64_peak.cu, profiles/r01_fp64_peaks.json) vs 34.2 for DFMA.
+//  * double-double accumulation (error-free TwoSum / TwoProd) for the length-n
+//    reductions whose rounding is amplified by 1/gap in eq. (Eoffdiag)
+//    (alpha_j and x_j^T w_j).
+//  * cp.async (LDGSTS) staging.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define RF_DEV __device__ __forceinline__
+
+namespace rf {
+
+constexpr int KMAX = 128;       // largest k compiled (BASELINE configs use 4..128)
+
+// ---------------------------------------------------------------- DMMA m8n8k4
+// A (8x4, row): thread t holds A[t>>2][t&3];  B (4x8, col): thread t holds B[t&3][t>>2];
+// C (8x8): thread t holds C[t>>2][2*(t&3)], C[t>>2][2*(t&3)+1].
+RF_DEV void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- cp.async
+RF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+RF_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
+  // src-size 0 zero-fills the 16 bytes
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(pred ? 16 : 0));
+}
+RF_DEV void cp_async8(void* smem, const void* gmem, bool pred) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(pred ? 8 : 0));
+}
+RF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+RF_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------- double-double
+// Error-free transforms with explicit round-to-nearest intrinsics so that nvcc's
+// default fma contraction can never merge the products and sums below.
+struct dd { double hi, lo; };
+RF_DEV dd two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  double bb = __dadd_rn(s, -a);
+  double e = __dadd_rn(__dadd_rn(a, -__dadd_rn(s, -bb)), __dadd_rn(b, -bb));
+  return {s, e};
+}
+RF_DEV dd quick_two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  return {s, __dadd_rn(b, -__dadd_rn(s, -a))};
+}
+// acc += a*b exactly-rounded-to-dd
+RF_DEV void dd_add_prod(dd& acc, double a, double b) {
+  double p = __dmul_rn(a, b);
+  double pe = __fma_rn(a, b, -p);
+  dd s = two_sum(acc.hi, p);
+  double e = __dadd_rn(s.lo, __dadd_rn(acc.lo, pe));
+  acc = quick_two_sum(s.hi, e);
+}
+RF_DEV void dd_add(dd& acc, dd x) {
+  dd s = two_sum(acc.hi, x.hi);
+  double e = __dadd_rn(s.lo, __dadd_rn(acc.lo, x.lo));
+  acc = quick_two_sum(s.hi, e);
+}
+RF_DEV double dd_val(dd a) { return __dadd_rn(a.hi, a.lo); }
+
+// device status codes (same values as refine_status)
+enum : int { ST_OK = 0, ST_DIVERGED = 2, ST_E_INVALID = -1, ST_E_NEAR_ZERO_RQ = -2, ST_E_ZERO_PIVOT = -3 };
+
+// Everything the sweep keeps on the device; passed to kernels by value.
+struct Ws {
+  int64_t n_loc;     // local rows
+  int32_t k, kp;     // k and its padded power-of-two tile width (>= 8)
+  int32_t top;       // local rows [0, top) are the top k x k block (k on rank 0, else 0)
+  double shift, delta, normA;
+  int32_t beta_zero;
+  double* W;         // n_loc x k
+  double* Wpart;     // split-K partials (dense), S x n_loc x k
+  double* ag;        // alpha/g double-double slots: n_ag x k x 4 {a_hi, a_lo, g_hi, g_lo}
+  int32_t n_ag;
+  double* bpart;     // pass-B partials: n_chunk x tiles x (TA x TB), plus rr: n_chunk x kp
+  double* brr;
+  int32_t n_chunk;
+  double* M2;        // kp x kp  (X_2^T R_2, un-flipped)
+  double* G2;        // kp x kp  (X_2^T X_2)
+  double* rr2;       // kp       (sum_i r_ij^2 over rows >= top)
+  double* nslot;     // norm partial slots: n_nslot x kp
+  int32_t n_nslot;
+  // k x k state (row-major, ld = k)
+  double *alpha, *d, *rd, *sigma, *U, *L, *T, *E11, *Csig, *scal, *ntop, *invn, *stats;
+  double* scratch;   // 8 k x k scratch matrices for the k x k algebra
+  int* status;
+};
+
+}  // namespace rf

@@ -1,0 +1,187 @@
+// gemm_dense.cuh -- S1 for dense A: W = A X^ - shift X^ (Alg. 4 line 1, PAPER.md:434;
+// Sec. 5.1 shift) on the FP64 tensor cores (DMMA.8x8x4), plus the
+// S2 epilogue partials alpha_j = x_j^T x_j and g_j = x_j^T w_j (lines 3-4).
+//
+// Shape: M = n_loc rows of A (row-major, lda), N = k (padded to NT), K = n.
+// A is streamed from HBM exactly once; X^ (n x k, 16 MiB at cfg3) stays L2-resident.
+// CTA tile BM x NT, K step BK, STAGES-deep cp.async pipeline; warps tile the CTA
+// output in WM x WN blocks of m8n8 DMMA fragments.  Split-K over gridDim.y makes
+// 148 SMs busy at cfg3 (256 row tiles x 4 splits = 1024 CTAs = 6.9 waves); the
+// split partials are summed in fixed order by w_finish (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace rf {
+
+template <int NT, int BM, int WM, int WN, int BK, int STAGES>
+struct GemmCfg {
+  static constexpr int WARPS_M = BM / WM, WARPS_N = NT / WN, WARPS = WARPS_M * WARPS_N;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int LDA_S = BK + 4;                         // 8 rows x 4 cols frag reads: 2-way min
+  static constexpr int LDB_S = NT + ((NT % 16 == 8) ? 0 : 8);  // 4 rows x 8 cols frag reads: 2-way min
+  static constexpr int A_STAGE = BM * LDA_S, B_STAGE = BK * LDB_S;
+  static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * 8;
+  static constexpr int MI = WM / 8, NI = WN / 8;
+};
+
+// out[m][j] = sum_{l in [kb, ke)} A[m][l] X[l][j], m in [0, M), j in [0, k)
+template <int NT, int BM, int WM, int WN, int BK, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<NT, BM, WM, WN, BK, STAGES>::THREADS)
+gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ X, int32_t k,
+               int64_t M, int64_t K, int64_t kchunk, double* __restrict__ out, int64_t out_split_stride,
+               int a_vec16, int b_vec16, const int* __restrict__ status) {
+  using C = GemmCfg<NT, BM, WM, WN, BK, STAGES>;
+  if (*status != ST_OK) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * C::A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t ke = (kb + kchunk < K) ? kb + kchunk : K;
+  const int nk = (int)((ke - kb + BK - 1) / BK);
+  out += (int64_t)blockIdx.y * out_split_stride;
+
+  auto load_stage = [&](int stage, int it) {
+    const int64_t k0 = kb + (int64_t)it * BK;
+    double* as = As + stage * C::A_STAGE;
+    double* bs = Bs + stage * C::B_STAGE;
+    if (a_vec16) {
+      constexpr int CH = BM * BK / 2;          // 16-byte chunks
+      for (int c = tid; c < CH; c += C::THREADS) {
+        const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
+        const int64_t gr = m0 + r, gc = k0 + cc;
+        const bool ok = (gr < M) && (gc < ke);  // K and ke are even on this path
+        cp_async16(as + r * C::LDA_S + cc, ok ? (const void*)(A + gr * lda + gc) : (const void*)A, ok);
+      }
+    } else {
+      constexpr int CH = BM * BK;
+      for (int c = tid; c < CH; c += C::THREADS) {
+        const int r = c / BK, cc = c % BK;
+        const int64_t gr = m0 + r, gc = k0 + cc;
+        const bool ok = (gr < M) && (gc < ke);
+        cp_async8(as + r * C::LDA_S + cc, ok ? (const void*)(A + gr * lda + gc) : (const void*)A, ok);
+      }
+    }
+    if (b_vec16) {
+      constexpr int CH = BK * NT / 2;
+      for (int c = tid; c < CH; c += C::THREADS) {
+        const int r = c / (NT / 2), cc = (c % (NT / 2)) * 2;
+        const int64_t gr = k0 + r;
+        const bool ok = (gr < ke) && (cc < k);   // k even on this path
+        cp_async16(bs + r * C::LDB_S + cc, ok ? (const void*)(X + gr * k + cc) : (const void*)X, ok);
+      }
+    } else {
+      constexpr int CH = BK * NT;
+      for (int c = tid; c < CH; c += C::THREADS) {
+        const int r = c / NT, cc = c % NT;
+        const int64_t gr = k0 + r;
+        const bool ok = (gr < ke) && (cc < k);
+        cp_async8(bs + r * C::LDB_S + cc, ok ? (const void*)(X + gr * k + cc) : (const void*)X, ok);
+      }
+    }
+  };
+
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int ar = wm * WM + (lane >> 2), ac = lane & 3;   // A frag coords within the tile
+  const int br = lane & 3, bc = wn * WN + (lane >> 2);   // B frag coords
+  for (int it = 0; it < nk; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {  // prefetch stage it + STAGES - 1 (its buffer was consumed at iteration it - 1)
+      const int nx = it + STAGES - 1;
+      if (nx < nk) load_stage(nx % STAGES, nx);
+      cp_async_commit();
+    }
+    const double* as = As + (it % STAGES) * C::A_STAGE;
+    const double* bs = Bs + (it % STAGES) * C::B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[C::MI], b[C::NI];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) a[i] = as[(ar + i * 8) * C::LDA_S + kk + ac];
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) b[j] = bs[(kk + br) * C::LDB_S + bc + j * 8];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: fragment (i, j) -> rows m0 + wm*WM + i*8 + lane/4, cols wn*WN + j*8 + 2*(lane%4) + {0,1}
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int64_t r = m0 + wm * WM + i * 8 + (lane >> 2);
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) {
+      const int c = wn * WN + j * 8 + 2 * (lane & 3);
+      double* o = out + r * k + c;
+      if (b_vec16 && c < k) {   // k even: c, c+1 both valid
+        *reinterpret_cast<double2*>(o) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < k) o[0] = acc[i][j][0];
+        if (c + 1 < k) o[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+// Sum the S split partials in fixed order s = 0..S-1, apply the shift
+// (w = fma(-shift, x, w)), write W, and emit per-block double-double partials of
+// alpha_j = sum x_ij^2 and g_j = sum x_ij w_ij into Ws::ag.
+// Block b owns a fixed contiguous row range, so the result is deterministic.
+__global__ void __launch_bounds__(256) w_finish_kernel(Ws ws, const double* __restrict__ X, int nsplit,
+                                                      int64_t split_stride) {
+  __shared__ dd sa[256], sg[256];
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k;
+  const int R = 256 / k;                     // rows processed in parallel (k <= 128)
+  const int tid = threadIdx.x;
+  const int r = tid / k, j = tid % k;
+  const int64_t rows_per = (ws.n_loc + gridDim.x - 1) / gridDim.x;
+  const int64_t rb = (int64_t)blockIdx.x * rows_per;
+  const int64_t re = (rb + rows_per < ws.n_loc) ? rb + rows_per : ws.n_loc;
+  dd a = {0.0, 0.0}, g = {0.0, 0.0};
+  if (r < R) {
+    for (int64_t i = rb + r; i < re; i += R) {
+      const int64_t e = i * k + j;
+      double w;
+      if (nsplit == 1) {
+        w = ws.W[e];
+      } else {
+        w = ws.Wpart[e];
+        for (int s = 1; s < nsplit; ++s) w = __dadd_rn(w, ws.Wpart[s * split_stride + e]);
+      }
+      const double x = X[e];
+      if (ws.shift != 0.0) w = __fma_rn(-ws.shift, x, w);
+      ws.W[e] = w;
+      dd_add_prod(a, x, x);
+      dd_add_prod(g, x, w);
+    }
+  }
+  sa[tid] = a;
+  sg[tid] = g;
+  __syncthreads();
+  if (tid < k) {
+    dd ta = sa[tid], tg = sg[tid];
+    for (int q = 1; q < R; ++q) { dd_add(ta, sa[q * k + tid]); dd_add(tg, sg[q * k + tid]); }
+    double* slot = ws.ag + ((int64_t)blockIdx.x * k + tid) * 4;
+    slot[0] = ta.hi; slot[1] = ta.lo; slot[2] = tg.hi; slot[3] = tg.lo;
+  }
+}
+
+}  // namespace rf

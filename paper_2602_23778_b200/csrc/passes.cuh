@@ -1,0 +1,294 @@
+// passes.cuh -- the tall-skinny row passes of a sweep over rows i >= top (rows below the
+// k x k top block), on the FP64 tensor cores.
+//
+// pass B (S4 reductions): R = W - X^ D on the fly (Alg. 4 line 5 operand),
+//   [M_2 | G_2] = X^_2^T [R_2 | X^_2]   (k x 2k, reduction over rows)  and  rr_j = sum r_ij^2.
+//   A CTA owns one TA x TB output tile and one contiguous row chunk; partials go to fixed
+//   slots and are summed in chunk order by passB_reduce (deterministic).  Per row it reads
+//   x_i and w_i once (16 k bytes) for 2 k^2 FMAs.
+// pass C (S6 update): x~_i = (w_i Sigma D^{-1}) - x^_i Csig   (the lower block of
+//   X^ + H E_L, Alg. 4 line 7, via the identity in kxk.cuh), written in place, plus column
+//   sums of x~^2 for the normalisation.  Persistent CTAs keep Csig (k x k) in shared memory.
+// normalize (S7): x_ij *= 1/||x~_j||.
+#pragma once
+#include "common.cuh"
+
+namespace rf {
+
+template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
+struct PassBCfg {
+  static constexpr int THREADS = WARPS_A * WARPS_B * 32;
+  static constexpr int LDS = KP + ((KP % 16 == 8) ? 0 : 8);
+  static constexpr int STAGE = BR * LDS;
+  static constexpr int SMEM = 2 * 2 * STAGE * 8;       // X and R, double buffered
+  static constexpr int WTA = TA / WARPS_A, WTB = TB / WARPS_B;
+  static constexpr int MI = WTA / 8, NI = WTB / 8;
+  static constexpr int NTA = KP / TA, NTB = 2 * KP / TB, NTILES = NTA * NTB;
+};
+
+template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
+__global__ void __launch_bounds__(PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>::THREADS)
+passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
+  using C = PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double sd[KP];
+  __shared__ double srr[C::THREADS];
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wa = warp / WARPS_B, wb = warp % WARPS_B;
+  const int tile = blockIdx.x, ta = tile / C::NTB, tb = tile % C::NTB;
+  const int a0 = ta * TA, b0 = tb * TB;
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + gridDim.y - 1) / gridDim.y + BR - 1) / BR * BR;
+  const int64_t rb = ws.top + (int64_t)blockIdx.y * per;
+  const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
+  const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
+  for (int j = tid; j < KP; j += C::THREADS) sd[j] = (j < k) ? ws.d[j] : 0.0;
+  double* Xs = smem;
+  double* Rs = smem + 2 * C::STAGE;
+
+  auto load = [&](int buf, int it) {
+    const int64_t r0 = rb + (int64_t)it * BR;
+    double* xs = Xs + buf * C::STAGE;
+    double* rs = Rs + buf * C::STAGE;
+    if (vec16) {
+      for (int c = tid; c < BR * KP / 2; c += C::THREADS) {
+        const int r = c / (KP / 2), cc = (c % (KP / 2)) * 2;
+        const int64_t g = r0 + r;
+        const bool ok = (g < re) && (cc < k);
+        const int64_t off = ok ? g * k + cc : 0;
+        cp_async16(xs + r * C::LDS + cc, X + off, ok);
+        cp_async16(rs + r * C::LDS + cc, ws.W + off, ok);
+      }
+    } else {
+      for (int c = tid; c < BR * KP; c += C::THREADS) {
+        const int r = c / KP, cc = c % KP;
+        const int64_t g = r0 + r;
+        const bool ok = (g < re) && (cc < k);
+        const int64_t off = ok ? g * k + cc : 0;
+        cp_async8(xs + r * C::LDS + cc, X + off, ok);
+        cp_async8(rs + r * C::LDS + cc, ws.W + off, ok);
+      }
+    }
+  };
+
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double rr = 0.0;                       // column tid % KP (THREADS is a multiple of KP)
+  const bool do_rr = (tile == 0);
+  if (nit > 0) load(0, 0);
+  cp_async_commit();
+  for (int it = 0; it < nit; ++it) {
+    const int cur = it & 1;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (it + 1 < nit) load(cur ^ 1, it + 1);
+    cp_async_commit();
+    double* xs = Xs + cur * C::STAGE;
+    double* rs = Rs + cur * C::STAGE;
+    for (int e = tid; e < BR * KP; e += C::THREADS) {     // R = W - X D  (fma as in the oracle)
+      const int r = e / KP, c = e % KP;
+      const double v = __fma_rn(-xs[r * C::LDS + c], sd[c], rs[r * C::LDS + c]);
+      rs[r * C::LDS + c] = v;
+      rr = __fma_rn(v, v, rr);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BR; kk += 4) {
+      const int row = kk + (lane & 3);
+      double a[C::MI], b[C::NI];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) a[i] = xs[row * C::LDS + a0 + wa * C::WTA + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int col = b0 + wb * C::WTB + j * 8 + (lane >> 2);
+        b[j] = (col < KP) ? rs[row * C::LDS + col] : xs[row * C::LDS + col - KP];
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  double* out = ws.bpart + ((int64_t)blockIdx.y * C::NTILES + tile) * (TA * TB);
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) {
+      const int ra = wa * C::WTA + i * 8 + (lane >> 2);
+      const int cb = wb * C::WTB + j * 8 + 2 * (lane & 3);
+      out[ra * TB + cb] = acc[i][j][0];
+      out[ra * TB + cb + 1] = acc[i][j][1];
+    }
+  if (do_rr) {
+    srr[tid] = rr;
+    __syncthreads();
+    if (tid < KP) {
+      double s = srr[tid];
+      for (int q = 1; q < C::THREADS / KP; ++q) s += srr[q * KP + tid];
+      ws.brr[(int64_t)blockIdx.y * KP + tid] = s;
+    }
+  }
+}
+
+// Sum pass-B partials over chunks in fixed order -> M2 (k x k), G2 (k x k), rr2 (k).
+template <int KP, int TA, int TB>
+__global__ void passB_reduce_kernel(Ws ws, int nchunk) {
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k;
+  constexpr int NTB = 2 * KP / TB, NTILES = (KP / TA) * NTB;
+  const int total = k * 2 * k + k;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    if (e >= 2 * k * k) {
+      const int j = e - 2 * k * k;
+      double s = 0.0;
+      for (int c = 0; c < nchunk; ++c) s += ws.brr[(int64_t)c * KP + j];
+      ws.rr2[j] = s;
+      continue;
+    }
+    const int a = e / (2 * k), bb = e % (2 * k);
+    const int b = (bb < k) ? bb : KP + (bb - k);          // column in the padded [R | X] space
+    const int tile = (a / TA) * NTB + b / TB;
+    const int off = (a % TA) * TB + (b % TB);
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += ws.bpart[((int64_t)c * NTILES + tile) * (TA * TB) + off];
+    if (bb < k) ws.M2[a * k + bb] = s;
+    else ws.G2[a * k + (bb - k)] = s;
+  }
+}
+
+template <int KP, int BM, int WARPS_M, int WARPS_N>
+struct PassCCfg {
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int LDX = KP + 4;                               // A-frag reads (8 rows x 4)
+  static constexpr int LDC = KP + ((KP % 16 == 8) ? 0 : 8);        // B-frag reads (4 rows x 8)
+  static constexpr int XSTAGE = BM * LDX;
+  static constexpr int SMEM = (KP * LDC + 2 * XSTAGE) * 8;
+  static constexpr int WM = BM / WARPS_M, WN = KP / WARPS_N;
+  static constexpr int MI = WM / 8, NI = WN / 8;
+};
+
+template <int KP, int BM, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(PassCCfg<KP, BM, WARPS_M, WARPS_N>::THREADS)
+passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
+  using C = PassCCfg<KP, BM, WARPS_M, WARPS_N>;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double ssc[KP];
+  __shared__ double sred[WARPS_M * 8][KP];
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  double* Cs = smem;
+  double* Xs = smem + KP * C::LDC;
+  for (int e = tid; e < KP * KP; e += C::THREADS) {
+    const int l = e / KP, j = e % KP;
+    Cs[l * C::LDC + j] = (l < k && j < k) ? ws.Csig[l * k + j] : 0.0;
+  }
+  for (int j = tid; j < KP; j += C::THREADS) ssc[j] = (j < k) ? ws.scal[j] : 0.0;
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t ntile = (rows + BM - 1) / BM;
+
+  auto load = [&](int buf, int64_t t) {
+    const int64_t r0 = ws.top + t * BM;
+    double* xs = Xs + buf * C::XSTAGE;
+    if (vec16) {
+      for (int c = tid; c < BM * KP / 2; c += C::THREADS) {
+        const int r = c / (KP / 2), cc = (c % (KP / 2)) * 2;
+        const int64_t g = r0 + r;
+        const bool ok = (g < ws.n_loc) && (cc < k);
+        cp_async16(xs + r * C::LDX + cc, X + (ok ? g * k + cc : 0), ok);
+      }
+    } else {
+      for (int c = tid; c < BM * KP; c += C::THREADS) {
+        const int r = c / KP, cc = c % KP;
+        const int64_t g = r0 + r;
+        const bool ok = (g < ws.n_loc) && (cc < k);
+        cp_async8(xs + r * C::LDX + cc, X + (ok ? g * k + cc : 0), ok);
+      }
+    }
+  };
+
+  double nacc[C::NI][2];
+#pragma unroll
+  for (int j = 0; j < C::NI; ++j) nacc[j][0] = nacc[j][1] = 0.0;
+  int64_t t = blockIdx.x;
+  if (t < ntile) load(0, t);
+  cp_async_commit();
+  for (int buf = 0; t < ntile; t += gridDim.x, buf ^= 1) {
+    cp_async_wait<0>();
+    __syncthreads();
+    if (t + gridDim.x < ntile) load(buf ^ 1, t + gridDim.x);
+    cp_async_commit();
+    const int64_t r0 = ws.top + t * BM;
+    // prefetch this thread's W entries (independent of the MMA loop)
+    double w[C::MI][C::NI][2];
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int64_t g = r0 + wm * C::WM + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int c = wn * C::WN + j * 8 + 2 * (lane & 3);
+        const bool okr = g < ws.n_loc;
+        w[i][j][0] = (okr && c < k) ? ws.W[g * k + c] : 0.0;
+        w[i][j][1] = (okr && c + 1 < k) ? ws.W[g * k + c + 1] : 0.0;
+      }
+    }
+    double acc[C::MI][C::NI][2];
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* xs = Xs + buf * C::XSTAGE;
+#pragma unroll 4
+    for (int kk = 0; kk < KP; kk += 4) {
+      double a[C::MI], b[C::NI];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) a[i] = xs[(wm * C::WM + i * 8 + (lane >> 2)) * C::LDX + kk + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) b[j] = Cs[(kk + (lane & 3)) * C::LDC + wn * C::WN + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int64_t g = r0 + wm * C::WM + i * 8 + (lane >> 2);
+      if (g >= ws.n_loc) continue;
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int c = wn * C::WN + j * 8 + 2 * (lane & 3);
+        const double x0 = __fma_rn(w[i][j][0], ssc[c], -acc[i][j][0]);
+        const double x1 = __fma_rn(w[i][j][1], ssc[c + 1], -acc[i][j][1]);
+        if (c < k) { X[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
+        if (c + 1 < k) { X[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
+      }
+    }
+  }
+  // column norm partials: slot rows (wm, lane/4) reduced in fixed order
+#pragma unroll
+  for (int j = 0; j < C::NI; ++j) {
+    const int c = wn * C::WN + j * 8 + 2 * (lane & 3);
+    sred[wm * 8 + (lane >> 2)][c] = nacc[j][0];
+    sred[wm * 8 + (lane >> 2)][c + 1] = nacc[j][1];
+  }
+  __syncthreads();
+  for (int j = tid; j < KP; j += C::THREADS) {
+    double s = 0.0;
+    for (int q = 0; q < WARPS_M * 8; ++q) s += sred[q][j];
+    ws.nslot[(int64_t)blockIdx.x * KP + j] = s;
+  }
+}
+
+__global__ void normalize_kernel(Ws ws, double* __restrict__ X) {
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k;
+  const int64_t total = ws.n_loc * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    X[e] *= ws.invn[e % k];
+}
+
+}  // namespace rf

@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA sweep (through the C ABI) against the oracle, element by element.
+
+North_star bar: per-sweep relative Frobenius difference <= 1e-10 (one-step parity P1:
+the oracle consumes the GPU's own input X_t); converged eigenvector error <= 100 n u.
+Kernel-level (P3): CSR W bit-identical; dense W within gamma_n |A||X|; k x k factors
+<= 1e-13 relative.  Sizes span several tiles and ragged tails; the full BASELINE sizes
+run in test_gpu_fullsize.py."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2602_23778_b200 as p
+    from paper_2602_23778_b200 import build
+    build.build()
+    p.lib()
+    assert torch.cuda.is_available()
+    return p
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def op_of(p):
+    if p.kind == "dense":
+        return oracle.Operator(A=p.A.cpu().numpy(), shift=p.shift)
+    return oracle.Operator(row_ptr=p.row_ptr.cpu().numpy(), col_idx=p.col_idx.cpu().numpy(),
+                           val=p.val.cpu().numpy(), shift=p.shift)
+
+
+def refiner(pkg, p, **kw):
+    if p.kind == "dense":
+        return pkg.Refiner.dense(p.A.cuda(), p.k, shift=p.shift, **kw)
+    return pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k, shift=p.shift, **kw)
+
+
+def one_step(pkg, p, sweeps, R=None, op=None, stats_tol=1e-8):
+    """P1: at every sweep t run the oracle on the GPU's X_t and compare with X_{t+1}."""
+    R = R or refiner(pkg, p)
+    op = op or op_of(p)
+    X = p.X0.cuda().clone()
+    worst = 0.0
+    for t in range(sweeps):
+        xin = X.cpu().numpy()
+        s, st = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK, (t, s, ref.status)
+        e = rel(X.cpu().numpy(), ref.X)
+        worst = max(worst, e)
+        assert e <= TOL, f"sweep {t}: one-step rel diff {e:.3e}"
+        assert st.flipped == ref.stats.flipped and st.delta_hits == ref.stats.delta_hits
+        assert abs(st.rel_resid - ref.stats.rel_resid) <= stats_tol * max(ref.stats.rel_resid, 1e-300) + 1e-18
+        # ||E_L||_F carries the same 1/gap-amplified rounding as X~ (absolute floor 1e-9 ~ 1e-10 ||X||_F)
+        assert abs(st.corr_norm - ref.stats.corr_norm) <= 1e-6 * ref.stats.corr_norm + 1e-9
+    return worst, X
+
+
+# ------------------------------------------------------------------------------ dense
+
+def test_cfg1_one_step_parity(pkg):
+    p = synth.make_config("cfg1")
+    worst, _ = one_step(pkg, p, p.sweeps)
+    print(f"cfg1 worst one-step rel diff {worst:.3e}")
+
+
+def test_cfg1_trajectory_parity_and_convergence(pkg):
+    """P2 (independent trajectories) and the converged accuracy gate <= 100 n u."""
+    p = synth.make_config("cfg1")
+    R = refiner(pkg, p)
+    op = op_of(p)
+    X = p.X0.cuda().clone()
+    Xo = p.X0.numpy().copy()
+    for t in range(p.sweeps):
+        R.refine_sweep(X)
+        Xo = oracle.sweep(op, Xo).X
+        assert rel(X.cpu().numpy(), Xo) <= TOL, t
+    s, it, st = R.refine_run(X, 30, 1e-15)
+    Xt = p.X.numpy()
+    Xg = X.cpu().numpy()
+    sg = np.sign(np.sum(Xg * Xt, axis=0))
+    assert np.linalg.norm(Xg * sg - Xt, axis=0).max() <= 100 * p.n * U
+
+
+@pytest.mark.parametrize("n,k,shift", [(200, 1, 0.0), (300, 3, 0.0), (517, 5, 0.5), (1000, 12, 0.0),
+                                       (777, 16, 0.0), (1200, 33, 0.0), (900, 64, 0.0), (700, 100, 0.0),
+                                       (1100, 128, 0.0)])
+def test_dense_ragged_one_step(pkg, n, k, shift):
+    p = synth.small_dense(n, k, m=8, seed=n + k, signs=True)
+    p.shift = shift
+    one_step(pkg, p, 3)
+
+
+def test_cfg2_one_step_parity(pkg):
+    p = synth.make_config("cfg2", device="cuda")
+    worst, _ = one_step(pkg, p, 3)
+    print(f"cfg2 worst {worst:.3e}")
+
+
+def test_dense_intermediates(pkg):
+    """P3: W, alpha, d, sigma, U, L=Y_1, T, E_11 and the materialised Y vs the oracle."""
+    p = synth.small_dense(700, 24, m=8, seed=5, signs=True)
+    R = refiner(pkg, p)
+    X = p.X0.cuda().clone()
+    xin = X.clone()
+    s, _ = R.refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK
+    ref = oracle.sweep(op_of(p), xin.cpu().numpy(), debug=True)
+    D = ref.debug
+    sig = D["sigma"]
+    A = p.A.numpy()
+    Xn = xin.cpu().numpy()
+    Wg = R.debug(pkg.DBG_W).cpu().numpy()           # un-flipped A X
+    bound = 2 * p.n * U * (np.abs(A) @ np.abs(Xn))
+    assert np.all(np.abs(Wg * sig - D["W"]) <= bound)
+    assert np.array_equal(R.debug(pkg.DBG_SIGMA).cpu().numpy(), sig)
+    assert rel(R.debug(pkg.DBG_ALPHA).cpu().numpy(), D["alpha"]) <= 1e-15
+    assert rel(R.debug(pkg.DBG_D).cpu().numpy(), D["dtilde"]) <= 1e-14
+    assert rel(R.debug(pkg.DBG_U).cpu().numpy(), D["U"]) <= 1e-13
+    assert rel(R.debug(pkg.DBG_L).cpu().numpy(), D["Y"][:p.k]) <= 1e-13
+    assert rel(R.debug(pkg.DBG_T).cpu().numpy(), D["T"]) <= 1e-13
+    # E_11 = V_1/(d_j - d_i): rounding amplified by 1/gap; it enters X~ additively (|X| ~ 1)
+    assert np.max(np.abs(R.debug(pkg.DBG_E11).cpu().numpy() - D["E"][:p.k])) <= 1e-12
+    Y = R.debug(pkg.DBG_Y, xin).cpu().numpy()
+    assert rel(Y, D["Y"]) <= 1e-13
+
+
+def test_sign_flip_invariance_bitwise(pkg):
+    p = synth.small_dense(600, 8, seed=3, signs=True)
+    R = refiner(pkg, p)
+    X1 = p.X0.cuda().clone()
+    S = torch.tensor([1, -1, 1, -1, -1, 1, 1, -1], dtype=torch.float64, device="cuda")
+    X2 = X1 * S
+    R.refine_sweep(X1)
+    R.refine_sweep(X2)
+    assert torch.equal(X1, X2)
+
+
+def test_deterministic_and_graph_mode(pkg):
+    p = synth.small_dense(900, 16, seed=9)
+    R = refiner(pkg, p)
+    Xa, Xb, Xc = (p.X0.cuda().clone() for _ in range(3))
+    R.refine_sweep(Xa)
+    R.refine_sweep(Xb)
+    assert torch.equal(Xa, Xb)
+    R.refine_set_graph(True)
+    R.refine_sweep(Xc)
+    R.refine_sweep(Xc)           # replay
+    R.refine_set_graph(False)
+    R.refine_sweep(Xa)
+    assert torch.equal(Xa, Xc)
+
+
+def test_host_entry_point_matches_device(pkg):
+    p = synth.small_dense(400, 6, seed=4)
+    R = refiner(pkg, p)
+    Xd = p.X0.cuda().clone()
+    R.refine_sweep(Xd)
+    Xh = p.X0.numpy().copy()
+    s, st = R.refine_sweep_host(Xh)
+    assert s == pkg.REFINE_OK
+    assert np.array_equal(Xh, Xd.cpu().numpy())
+
+
+# ------------------------------------------------------------------------------ CSR
+
+@pytest.mark.parametrize("dims,coeffs,k", [((40, 37), (1.0, 1.37), 6), ((64, 61), (1.0, 1.37), 32),
+                                           ((17, 15, 13), (1.0, 1.13, 1.29), 20),
+                                           ((24, 22, 21), (1.0, 1.13, 1.29), 128)])
+def test_csr_one_step_and_bitwise_W(pkg, dims, coeffs, k):
+    p = synth.small_laplacian(dims, coeffs, k)
+    R = refiner(pkg, p)
+    op = op_of(p)
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, _ = R.refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK
+    ref = oracle.sweep(op, xin, debug=True)
+    assert rel(X.cpu().numpy(), ref.X) <= TOL
+    Wg = R.debug(pkg.DBG_W).cpu().numpy()
+    assert np.array_equal(Wg * ref.debug["sigma"], ref.debug["W"])      # P3: bit-identical fma chains
+    one_step(pkg, p, 3, R=R, op=op)
+
+
+def test_csr_shift(pkg):
+    """Sec. 5.1: L with shift = sigma (B = L - sigma I = -A') on the GPU vs the oracle."""
+    p = synth.small_laplacian((30, 29), (1.0, 1.37), 5)
+    rp, ci, v = p.row_ptr.numpy(), p.col_idx.numpy(), p.val.numpy()
+    diag = ci == np.repeat(np.arange(p.n), np.diff(rp))
+    p.val = torch.from_numpy(np.where(diag, p.meta["sigma"] - v, -v))
+    p.shift = p.meta["sigma"]
+    one_step(pkg, p, 2)
+
+
+# ------------------------------------------------------------------------------ statuses
+
+def test_near_zero_rq_leaves_X_unchanged(pkg):
+    A = torch.diag(torch.tensor([0.0, 1.0, 2.0, 3.0] + [0.1] * 60, dtype=torch.float64)).cuda()
+    R = pkg.Refiner.dense(A, 2)
+    X = torch.zeros(64, 2, dtype=torch.float64, device="cuda")
+    X[0, 0] = X[1, 1] = 1.0
+    X0 = X.clone()
+    s, _ = R.refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_E_NEAR_ZERO_RQ
+    assert torch.equal(X, X0)
+
+
+def test_nan_diverged(pkg):
+    p = synth.small_dense(300, 4, seed=2)
+    R = refiner(pkg, p)
+    X = p.X0.cuda().clone()
+    X[17, 2] = float("nan")
+    s, _ = R.refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_DIVERGED
+
+
+def test_run_statuses(pkg):
+    p = synth.make_config("cfg1")
+    R = refiner(pkg, p)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 2, 1e-30)
+    assert s == pkg.REFINE_MAXITER and it == 2
+    s, it, st = R.refine_run(X, 50, 1e-12)
+    assert s == pkg.REFINE_OK and st.corr_norm <= 1e-12 and it < 50
+    Xo, so, ito, _ = oracle.run(op_of(p), p.X0.numpy(), 50, 1e-12)
+    assert so == oracle.OK
