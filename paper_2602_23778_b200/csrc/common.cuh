@@ -93,8 +93,8 @@ struct Ws {
   double* nslot;     // norm partial slots: n_nslot x kp
   int32_t n_nslot;
   // k x k state (row-major, ld = k)
-  double *alpha, *d, *rd, *sigma, *U, *L, *T, *E11, *Csig, *scal, *ntop, *invn, *stats;
-  double* scratch;   // 8 k x k scratch matrices for the k x k algebra
+  double *alpha, *d, *rd, *sigma, *U, *L, *Uinv, *T, *E11, *Csig, *scal, *ntop, *invn, *stats;
+  double* scratch;   // 16 k x k scratch matrices for the k x k algebra
   int* status;
 };
 

@@ -6,7 +6,7 @@
 // A is streamed from HBM exactly once; X^ (n x k, 16 MiB at cfg3) stays L2-resident.
 // CTA tile BM x NT, K step BK, STAGES-deep cp.async pipeline; warps tile the CTA
 // output in WM x WN blocks of m8n8 DMMA fragments.  Split-K over gridDim.y makes
-// 148 SMs busy at cfg3 (256 row tiles x 4 splits = 1024 CTAs = 6.9 waves); the
+// 148 SMs busy at cfg3 (256 row tiles x 4 splits = 1024 CTAs, 2 resident per SM); the
 // split partials are summed in fixed order by w_finish (deterministic).
 #pragma once
 #include "common.cuh"
@@ -43,21 +43,26 @@ gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
   const int nk = (int)((ke - kb + BK - 1) / BK);
   out += (int64_t)blockIdx.y * out_split_stride;
 
+  // per-thread copy coordinates are the same for every stage: precompute them once
+  constexpr int ACH16 = BM * BK / 2, BCH16 = BK * NT / 2;
+  constexpr int AIT16 = (ACH16 + C::THREADS - 1) / C::THREADS, BIT16 = (BCH16 + C::THREADS - 1) / C::THREADS;
   auto load_stage = [&](int stage, int it) {
     const int64_t k0 = kb + (int64_t)it * BK;
     double* as = As + stage * C::A_STAGE;
     double* bs = Bs + stage * C::B_STAGE;
     if (a_vec16) {
-      constexpr int CH = BM * BK / 2;          // 16-byte chunks
-      for (int c = tid; c < CH; c += C::THREADS) {
-        const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
-        const int64_t gr = m0 + r, gc = k0 + cc;
-        const bool ok = (gr < M) && (gc < ke);  // K and ke are even on this path
-        cp_async16(as + r * C::LDA_S + cc, ok ? (const void*)(A + gr * lda + gc) : (const void*)A, ok);
+#pragma unroll
+      for (int q = 0; q < AIT16; ++q) {
+        const int c = tid + q * C::THREADS;
+        if (ACH16 % C::THREADS == 0 || c < ACH16) {
+          const int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
+          const int64_t gr = m0 + r, gc = k0 + cc;
+          const bool ok = (gr < M) && (gc < ke);  // K and ke are even on this path
+          cp_async16(as + r * C::LDA_S + cc, ok ? (const void*)(A + gr * lda + gc) : (const void*)A, ok);
+        }
       }
     } else {
-      constexpr int CH = BM * BK;
-      for (int c = tid; c < CH; c += C::THREADS) {
+      for (int c = tid; c < BM * BK; c += C::THREADS) {
         const int r = c / BK, cc = c % BK;
         const int64_t gr = m0 + r, gc = k0 + cc;
         const bool ok = (gr < M) && (gc < ke);
@@ -65,16 +70,18 @@ gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
       }
     }
     if (b_vec16) {
-      constexpr int CH = BK * NT / 2;
-      for (int c = tid; c < CH; c += C::THREADS) {
-        const int r = c / (NT / 2), cc = (c % (NT / 2)) * 2;
-        const int64_t gr = k0 + r;
-        const bool ok = (gr < ke) && (cc < k);   // k even on this path
-        cp_async16(bs + r * C::LDB_S + cc, ok ? (const void*)(X + gr * k + cc) : (const void*)X, ok);
+#pragma unroll
+      for (int q = 0; q < BIT16; ++q) {
+        const int c = tid + q * C::THREADS;
+        if (BCH16 % C::THREADS == 0 || c < BCH16) {
+          const int r = c / (NT / 2), cc = (c % (NT / 2)) * 2;
+          const int64_t gr = k0 + r;
+          const bool ok = (gr < ke) && (cc < k);   // k even on this path
+          cp_async16(bs + r * C::LDB_S + cc, ok ? (const void*)(X + gr * k + cc) : (const void*)X, ok);
+        }
       }
     } else {
-      constexpr int CH = BK * NT;
-      for (int c = tid; c < CH; c += C::THREADS) {
+      for (int c = tid; c < BK * NT; c += C::THREADS) {
         const int r = c / NT, cc = c % NT;
         const int64_t gr = k0 + r;
         const bool ok = (gr < ke) && (cc < k);

@@ -1,14 +1,16 @@
-// kxk.cuh -- the serial k x k stages of a sweep, each one CTA (k <= 128).
+// kxk.cuh -- the serial k x k stages of a sweep, each one CTA of 1024 threads (k <= 128).
 //
 // kxk_prep   (S2 + S3): fixed-order reduction of the alpha/g double-double partials
 //            -> alpha_j, d_j = g_j / alpha_j (eq. Rayleigh, Alg. 4
-//            lines 3-4); modified LU of the top k x k block X^_1 (Alg. 2, PAPER.md:
-//            271-284, sign(0) = +1) -> Sigma, U, Y_1 = L; T = -U Sigma Y_1^{-T}
+//            lines 3-4); modified LU of the top k x k block X^_1 in shared memory (Alg. 2,
+//            PAPER.md:271-284, sign(0) = +1) -> Sigma, U, Y_1 = L;  U^{-1} and L^{-1} by
+//            blocked triangular inversion;  T = -U Sigma Y_1^{-T} = -(U Sigma) (L^{-1})^T
 //            (Alg. 3).  Rows l > k of Alg. 2 only read U's rows, so
-//            Y_2 = X^_2 U^{-1} (the tall-skinny triangular apply) is never formed on
-//            the hot path: it is applied through k x k algebra.
+//            Y_2 = X^_2 U^{-1} (the tall-skinny triangular apply) is never formed on the
+//            hot path: it is applied through k x k algebra.
 // kxk_finish (S4-S6 top block + all k x k algebra): with the one-time flip
-//            X' = X^ Sigma, W' = W Sigma, U' = U Sigma (reading R2):
+//            X' = X^ Sigma, W' = W Sigma, U' = U Sigma (reading R2),
+//            U'^{-1} = Sigma U^{-1}:
 //              R_1  = W'_1 - X'_1 D                              (line 5 operand)
 //              Z    = Y^T R = L^T R_1 + U'^{-T} M'               M' = X'_2^T R_2 (pass B)
 //              P    = T^T Z,   V_1 = R_1 - L P                   (V = H^T R)
@@ -19,19 +21,149 @@
 //              X~_1 = X'_1 + (E_11 - L B)                        (top rows, written here)
 //              C'   = P~ D^{-1} + U'^{-1} B,  Csig = Sigma C'    (pass C: x~_i = w_i Sigma D^{-1} - x_i Csig)
 //            plus the sweep statistics.
-// norm_reduce: fixed-order column norms of X~ -> 1/||x~_j||.
+// All k x k products go through cta_gemm: operands live in global scratch (L2-resident),
+// 32-deep K panels are staged in shared memory and multiplied with DMMA m8n8k4 (one warp
+// per 8 x 8 output tile).  Triangular inverses use 16 x 16 diagonal blocks solved in registers and
+// recursive doubling with cta_gemm.
 #pragma once
 #include "common.cuh"
 
 namespace rf {
 
+constexpr int KXK_THREADS = 1024;
+constexpr int PANEL = 32;
+constexpr int LDA_P = PANEL + 4;                  // As[i][p]: A-fragment reads (8 rows x 4) conflict-free
+constexpr int LDB_P = KMAX + 8;                   // Bs[p][j]: B-fragment reads (4 rows x 8) conflict-free
+constexpr int PANEL_SMEM = KMAX * LDA_P + PANEL * LDB_P;   // doubles of shared memory cta_gemm needs
+
+// C (M x N, ldc) = alpha op(A) op(B) + beta C0 on the FP64 tensor cores (DMMA m8n8k4).
+// op(A) is M x K, op(B) is K x N, M, N <= 128.  K is consumed in 32-deep panels staged in
+// shared memory; warp w owns the 8 x 8 output tiles w, w + 32, ...  C0 may alias C (each
+// element is read then written by the same thread).  Starts and ends with a barrier.
+__device__ __noinline__ void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, bool ta, const double* B,
+                         int ldb, bool tb, double beta, const double* C0, int ldc0, double* C, int ldc,
+                         double* sm) {
+  double* As = sm;                      // [KMAX][LDA_P]  As[i][p] = op(A)(i, kk+p)
+  double* Bs = sm + KMAX * LDA_P;       // [PANEL][LDB_P] Bs[p][j] = op(B)(kk+p, j)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, ntile = tm * tn;
+  constexpr int MAXT = (KMAX / 8) * (KMAX / 8) / (KXK_THREADS / 32);   // tiles per warp at k = 128
+  double acc[MAXT][2];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int Mp = tm * 8, Np = tn * 8;
+  for (int kk = 0; kk < K; kk += PANEL) {
+    const int pk = min(PANEL, K - kk);
+    __syncthreads();
+    // stage op(A)(0:Mp, kk:kk+32) and op(B)(kk:kk+32, 0:Np), zero-padded
+    for (int e = tid; e < PANEL * Mp; e += KXK_THREADS) {
+      int i, p;
+      if (ta) { i = e % Mp; p = e / Mp; } else { p = e & (PANEL - 1); i = e >> 5; }
+      As[i * LDA_P + p] = (p < pk && i < M) ? (ta ? A[(kk + p) * lda + i] : A[i * lda + kk + p]) : 0.0;
+    }
+    for (int e = tid; e < PANEL * Np; e += KXK_THREADS) {
+      int j, p;
+      if (tb) { p = e & (PANEL - 1); j = e >> 5; } else { j = e % Np; p = e / Np; }
+      Bs[p * LDB_P + j] = (p < pk && j < N) ? (tb ? B[j * ldb + kk + p] : B[(kk + p) * ldb + j]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      const int tile = warp + 32 * t;
+      if (tile < ntile) {
+        const int i0 = (tile / tn) * 8, j0 = (tile % tn) * 8;
+#pragma unroll
+        for (int p = 0; p < PANEL; p += 4) {
+          const double a = As[(i0 + (lane >> 2)) * LDA_P + p + (lane & 3)];
+          const double b = Bs[(p + (lane & 3)) * LDB_P + j0 + (lane >> 2)];
+          dmma(acc[t][0], acc[t][1], a, b);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    const int tile = warp + 32 * t;
+    if (tile < ntile) {
+      const int i = (tile / tn) * 8 + (lane >> 2), j = (tile % tn) * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (i < M && j + h < N) {
+          const double v = alpha * acc[t][h];
+          C[i * ldc + j + h] = (beta != 0.0) ? fma(beta, C0[i * ldc0 + j + h], v) : v;
+        }
+    }
+  }
+  __syncthreads();
+}
+
+// Inverse of a k x k triangular matrix S (ld k) into R (ld k).  upper: S upper triangular;
+// else unit lower (diagonal taken as 1).  tmp: k x k scratch.  16 x 16 diagonal blocks are
+// inverted by substitution in registers (one thread per column), then off-diagonal blocks are
+// filled level by level: upper  R12 = -R11 S12 R22;  lower  R21 = -R22 S21 R11.
+__device__ void cta_trinv(int k, const double* S, bool upper, double* R, double* tmp, double* sm) {
+  constexpr int BS = 16;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < k * k; e += KXK_THREADS) R[e] = 0.0;
+  __syncthreads();
+  if (tid < k) {
+    const int c = tid, b0 = (c / BS) * BS, bn = min(BS, k - b0), cl = c - b0;
+    double x[BS];
+#pragma unroll
+    for (int i = 0; i < BS; ++i) x[i] = 0.0;
+    if (upper) {
+#pragma unroll
+      for (int i = BS - 1; i >= 0; --i) {
+        if (i < bn && i <= cl) {
+          double s = (i == cl) ? 1.0 : 0.0;
+#pragma unroll
+          for (int l = i + 1; l < BS; ++l)
+            if (l < bn && l <= cl) s = fma(-S[(b0 + i) * k + b0 + l], x[l], s);
+          x[i] = s / S[(b0 + i) * k + b0 + i];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < BS; ++i) {
+        if (i < bn && i >= cl) {
+          double s = (i == cl) ? 1.0 : 0.0;
+#pragma unroll
+          for (int l = 0; l < BS; ++l)
+            if (l < i && l >= cl) s = fma(-S[(b0 + i) * k + b0 + l], x[l], s);
+          x[i] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BS; ++i)
+      if (i < bn) R[(b0 + i) * k + c] = x[i];
+  }
+  __syncthreads();
+  for (int s = BS; s < k; s *= 2) {
+    for (int b0 = 0; b0 + s < k; b0 += 2 * s) {
+      const int b1 = b0 + s, n1 = s, n2 = min(s, k - b1);
+      if (upper) {   // R12 = -R11 (S12 R22)
+        cta_gemm(n1, n2, n2, 1.0, S + b0 * k + b1, k, false, R + b1 * k + b1, k, false, 0.0, nullptr, 0,
+                 tmp, k, sm);
+        cta_gemm(n1, n2, n1, -1.0, R + b0 * k + b0, k, false, tmp, k, false, 0.0, nullptr, 0, R + b0 * k + b1, k,
+                 sm);
+      } else {       // R21 = -R22 (S21 R11)
+        cta_gemm(n2, n1, n1, 1.0, S + b1 * k + b0, k, false, R + b0 * k + b0, k, false, 0.0, nullptr, 0,
+                 tmp, k, sm);
+        cta_gemm(n2, n1, n2, -1.0, R + b1 * k + b1, k, false, tmp, k, false, 0.0, nullptr, 0, R + b1 * k + b0, k,
+                 sm);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- kxk_prep
-__global__ void __launch_bounds__(1024) kxk_prep_kernel(Ws ws, const double* __restrict__ Xtop) {
-  extern __shared__ __align__(16) double Q[];     // k x k, in-place modified LU
-  __shared__ dd pa[1024], pg[1024];
+__global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const double* __restrict__ Xtop) {
+  extern __shared__ __align__(16) double Q[];     // k x k (in-place modified LU), then gemm panels
+  __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
   __shared__ int s_bad;
   if (*ws.status != ST_OK) return;
-  const int k = ws.k, tid = threadIdx.x, nt = blockDim.x;
+  const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
 
   // 1. alpha_j, g_j: P parts per column, each part a contiguous slot range, combined in order
   const int P = nt / k;
@@ -39,7 +171,17 @@ __global__ void __launch_bounds__(1024) kxk_prep_kernel(Ws ws, const double* __r
   dd a = {0.0, 0.0}, g = {0.0, 0.0};
   if (p < P) {
     const int s0 = (int)((int64_t)ws.n_ag * p / P), s1 = (int)((int64_t)ws.n_ag * (p + 1) / P);
-    for (int s = s0; s < s1; ++s) {
+    int s = s0;
+    for (; s + 4 <= s1; s += 4) {
+      double v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[u][q] = ws.ag[((int64_t)(s + u) * k + j) * 4 + q];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { dd_add(a, dd{v[u][0], v[u][1]}); dd_add(g, dd{v[u][2], v[u][3]}); }
+    }
+    for (; s < s1; ++s) {
       const double* slot = ws.ag + ((int64_t)s * k + j) * 4;
       dd_add(a, dd{slot[0], slot[1]});
       dd_add(g, dd{slot[2], slot[3]});
@@ -80,106 +222,72 @@ __global__ void __launch_bounds__(1024) kxk_prep_kernel(Ws ws, const double* __r
     if (tid == 0) { Q[jj * k + jj] = piv; ws.sigma[jj] = s; }
     for (int l = jj + 1 + tid; l < k; l += nt) Q[l * k + jj] = __ddiv_rn(Q[l * k + jj], piv);
     __syncthreads();
-    const int m = k - jj - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int l = jj + 1 + e / m, h = jj + 1 + e % m;
-      Q[l * k + h] = __dadd_rn(Q[l * k + h], -__dmul_rn(Q[l * k + jj], Q[jj * k + h]));
-    }
+    for (int l = jj + 1 + (tid >> 5); l < k; l += 32)
+      for (int h = jj + 1 + (tid & 31); h < k; h += 32)
+        Q[l * k + h] = __dadd_rn(Q[l * k + h], -__dmul_rn(Q[l * k + jj], Q[jj * k + h]));
     __syncthreads();
   }
   __syncthreads();
-  for (int e = tid; e < k * k; e += nt) {
-    const int r = e / k, c = e % k;
-    ws.U[e] = (c >= r) ? Q[e] : 0.0;
-    ws.L[e] = (c < r) ? Q[e] : (c == r ? 1.0 : 0.0);
+  if (s_bad == ST_E_ZERO_PIVOT) {
+    if (tid == 0) *ws.status = s_bad;
+    return;
+  }
+  double* Up = ws.scratch;                   // U Sigma
+  for (int r = tid >> 5; r < k; r += 32)
+    for (int c = tid & 31; c < k; c += 32) {
+    const int e = r * k + c;
+    const double qv = Q[e];
+    ws.U[e] = (c >= r) ? qv : 0.0;
+    ws.L[e] = (c < r) ? qv : (c == r ? 1.0 : 0.0);
   }
   __syncthreads();
-
-  // 3. T = -U Sigma L^{-T}: row i, ascending j >= i: t_ij = -u_ij sigma_j - sum_{i<=l<j} t_il L_jl
-  if (tid < k) {
-    const int i = tid;
-    double* Ti = ws.T + i * k;
-    for (int c = 0; c < i; ++c) Ti[c] = 0.0;
-    for (int c = i; c < k; ++c) {
-      double t = -(Q[i * k + c] * ws.sigma[c]);
-      for (int l = i; l < c; ++l) t = __dadd_rn(t, -__dmul_rn(Ti[l], Q[c * k + l]));
-      Ti[c] = t;
-    }
-  }
+  for (int r = tid >> 5; r < k; r += 32)
+    for (int c = tid & 31; c < k; c += 32) Up[r * k + c] = ws.U[r * k + c] * ws.sigma[c];
+  // 3. U^{-1}, L^{-1}; T = -(U Sigma) L^{-T}   (shared memory now holds gemm panels)
+  double* Linv = ws.scratch + k * k;
+  double* tmp = ws.scratch + 2 * k * k;
+  cta_trinv(k, ws.U, true, ws.Uinv, tmp, Q);
+  cta_trinv(k, ws.L, false, Linv, tmp, Q);
+  cta_gemm(k, k, k, -1.0, Up, k, false, Linv, k, true, 0.0, nullptr, 0, ws.T, k, Q);
   if (tid == 0 && s_bad != ST_OK) *ws.status = s_bad;
-}
-
-// ---------------------------------------------------------------- k x k helpers (block-wide)
-// C = op(A) op(B) (+ Cadd), all k x k, row-major ld k.  No aliasing of C with inputs.
-__device__ void blk_mm(int k, const double* A, bool ta, const double* B, bool tb, double* C,
-                       const double* Cadd = nullptr, double add_sign = 1.0) {
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int i = e / k, j = e % k;
-    double s = 0.0;
-    for (int l = 0; l < k; ++l) {
-      const double a = ta ? A[l * k + i] : A[i * k + l];
-      const double b = tb ? B[j * k + l] : B[l * k + j];
-      s = fma(a, b, s);
-    }
-    C[e] = Cadd ? fma(add_sign, s, Cadd[e]) : s;
-  }
-}
-// X = Up^{-T} M  (Up upper, so Up^T lower: forward substitution), one thread per column
-__device__ void blk_solve_upT(int k, const double* Up, const double* M, double* X) {
-  for (int c = threadIdx.x; c < k; c += blockDim.x)
-    for (int i = 0; i < k; ++i) {
-      double s = M[i * k + c];
-      for (int l = 0; l < i; ++l) s = fma(-Up[l * k + i], X[l * k + c], s);
-      X[i * k + c] = s / Up[i * k + i];
-    }
-}
-// X = Up^{-1} M (back substitution), one thread per column
-__device__ void blk_solve_up(int k, const double* Up, const double* M, double* X) {
-  for (int c = threadIdx.x; c < k; c += blockDim.x)
-    for (int i = k - 1; i >= 0; --i) {
-      double s = M[i * k + c];
-      for (int l = i + 1; l < k; ++l) s = fma(-Up[i * k + l], X[l * k + c], s);
-      X[i * k + c] = s / Up[i * k + i];
-    }
 }
 
 // ---------------------------------------------------------------- kxk_finish
 // Xtop/Wtop: the top k rows of X^ (in/out) and W (un-flipped), ld k.
-__global__ void __launch_bounds__(1024) kxk_finish_kernel(Ws ws, double* __restrict__ Xtop,
-                                                          const double* __restrict__ Wtop) {
-  if (*ws.status != ST_OK) return;
+__global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* __restrict__ Xtop,
+                                                                 const double* __restrict__ Wtop) {
+  extern __shared__ __align__(16) double sm[];
   __shared__ int s_hits;
   __shared__ double s_red[4][KMAX];
-  const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = blockDim.x;
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
   double* S = ws.scratch;
-  double *Xp = S, *R1 = S + kk, *Mp = S + 2 * kk, *Gp = S + 3 * kk, *Up = S + 4 * kk, *Z2 = S + 5 * kk,
-         *Z = S + 6 * kk, *P = S + 7 * kk, *V1 = S + 8 * kk, *Pt = S + 9 * kk, *GPt = S + 10 * kk,
-         *S2 = S + 11 * kk, *Y2E = S + 12 * kk, *Qm = S + 13 * kk, *B = S + 14 * kk, *UB = S + 15 * kk;
+  double *Xp = S, *R1 = S + kk, *Mp = S + 2 * kk, *Gp = S + 3 * kk, *Ui = S + 4 * kk, *Z = S + 5 * kk,
+         *P = S + 6 * kk, *V1 = S + 7 * kk, *Pt = S + 8 * kk, *GPt = S + 9 * kk, *S2 = S + 10 * kk,
+         *Qm = S + 11 * kk, *B = S + 12 * kk, *LB = S + 13 * kk, *UB = S + 14 * kk;
   const double* sig = ws.sigma;
   const double* d = ws.d;
   if (tid == 0) s_hits = 0;
-  for (int e = tid; e < kk; e += nt) {
-    const int i = e / k, j = e % k;
+  for (int i = tid >> 5; i < k; i += 32)
+    for (int j = tid & 31; j < k; j += 32) {
+    const int e = i * k + j;
     const double xp = Xtop[e] * sig[j];
     Xp[e] = xp;
     R1[e] = fma(-xp, d[j], Wtop[e] * sig[j]);
     Mp[e] = sig[i] * ws.M2[e] * sig[j];
     Gp[e] = sig[i] * ws.G2[e] * sig[j];
-    Up[e] = ws.U[e] * sig[j];
+    Ui[e] = sig[i] * ws.Uinv[e];                      // U'^{-1} = Sigma U^{-1}
   }
   __syncthreads();
-  blk_solve_upT(k, Up, Mp, Z2);                       // U'^{-T} M'
-  __syncthreads();
-  blk_mm(k, ws.L, true, R1, false, Z, Z2);            // Z = L^T R_1 + U'^{-T} M'
-  __syncthreads();
-  blk_mm(k, ws.T, true, Z, false, P);                 // P = T^T Z
-  __syncthreads();
-  blk_mm(k, ws.L, false, P, false, V1, R1, -1.0);     // V_1 = R_1 - L P
-  __syncthreads();
-  blk_solve_up(k, Up, P, Pt);                         // P~ = U'^{-1} P
+  cta_gemm(k, k, k, 1.0, ws.L, k, true, R1, k, false, 0.0, nullptr, 0, Z, k, sm);   // Z = L^T R_1
+  cta_gemm(k, k, k, 1.0, Ui, k, true, Mp, k, false, 1.0, Z, k, Z, k, sm);           //   + U'^{-T} M'
+  cta_gemm(k, k, k, 1.0, ws.T, k, true, Z, k, false, 0.0, nullptr, 0, P, k, sm);    // P = T^T Z
+  cta_gemm(k, k, k, -1.0, ws.L, k, false, P, k, false, 1.0, R1, k, V1, k, sm);      // V_1 = R_1 - L P
+  cta_gemm(k, k, k, 1.0, Ui, k, false, P, k, false, 0.0, nullptr, 0, Pt, k, sm);   // P~ = U'^{-1} P
   // E_11 (line 6): beta needs the Gram G = X'^T X' = X'_1^T X'_1 + G'
-  for (int e = tid; e < kk; e += nt) {
-    const int i = e / k, j = e % k;
+  for (int i = tid >> 5; i < k; i += 32)
+    for (int j = tid & 31; j < k; j += 32) {
+    const int e = i * k + j;
     double v;
     if (i == j) {
       v = (1.0 - ws.alpha[i]) / 2.0;
@@ -196,30 +304,22 @@ __global__ void __launch_bounds__(1024) kxk_finish_kernel(Ws ws, double* __restr
     }
     ws.E11[e] = v;
   }
+  cta_gemm(k, k, k, 1.0, Gp, k, false, Pt, k, false, 0.0, nullptr, 0, GPt, k, sm);  // G' P~ (barrier inside)
+  for (int i = tid >> 5; i < k; i += 32)
+    for (int j = tid & 31; j < k; j += 32) S2[i * k + j] = (Mp[i * k + j] - GPt[i * k + j]) / d[j];
   __syncthreads();
-  blk_mm(k, Gp, false, Pt, false, GPt);               // G' P~
-  __syncthreads();
-  for (int e = tid; e < kk; e += nt) S2[e] = (Mp[e] - GPt[e]) / d[e % k];
-  __syncthreads();
-  blk_solve_upT(k, Up, S2, Y2E);                      // Y_2^T E_2
-  __syncthreads();
-  blk_mm(k, ws.L, true, ws.E11, false, Qm, Y2E);      // Qm = L^T E_11 + Y_2^T E_2
-  __syncthreads();
-  blk_mm(k, ws.T, false, Qm, false, B);               // B = T Qm
-  __syncthreads();
-  blk_solve_up(k, Up, B, UB);                         // U'^{-1} B
-  // X~_1 = X'_1 + (E_11 - L B)
-  for (int e = tid; e < kk; e += nt) {
-    const int i = e / k, j = e % k;
-    double s = 0.0;
-    for (int l = 0; l < k; ++l) s = fma(ws.L[i * k + l], B[l * k + j], s);
-    Xtop[e] = Xp[e] + (ws.E11[e] - s);
+  cta_gemm(k, k, k, 1.0, ws.L, k, true, ws.E11, k, false, 0.0, nullptr, 0, Qm, k, sm);  // Qm = L^T E_11
+  cta_gemm(k, k, k, 1.0, Ui, k, true, S2, k, false, 1.0, Qm, k, Qm, k, sm);             //   + U'^{-T} S2
+  cta_gemm(k, k, k, 1.0, ws.T, k, false, Qm, k, false, 0.0, nullptr, 0, B, k, sm);      // B = T Qm
+  cta_gemm(k, k, k, 1.0, ws.L, k, false, B, k, false, 0.0, nullptr, 0, LB, k, sm);      // L B
+  cta_gemm(k, k, k, 1.0, Ui, k, false, B, k, false, 0.0, nullptr, 0, UB, k, sm);        // U'^{-1} B
+  for (int l = tid >> 5; l < k; l += 32)
+    for (int j = tid & 31; j < k; j += 32) {
+    const int e = l * k + j;
+    Xtop[e] = Xp[e] + (ws.E11[e] - LB[e]);             // X~_1 = X'_1 + (E_11 - L B)
+    ws.Csig[e] = sig[l] * (Pt[e] / d[j] + UB[e]);      // Csig = Sigma (P~ D^{-1} + U'^{-1} B)
   }
   __syncthreads();
-  for (int e = tid; e < kk; e += nt) {
-    const int l = e / k, j = e % k;
-    ws.Csig[e] = sig[l] * (Pt[e] / d[j] + UB[e]);
-  }
   // per-column quantities and statistics
   if (tid < k) {
     const int j = tid;
@@ -262,7 +362,15 @@ __global__ void __launch_bounds__(128) norm_reduce_kernel(Ws ws) {
   const int j = threadIdx.x;
   if (j >= ws.k) return;
   double s = ws.ntop[j];
-  for (int q = 0; q < ws.n_nslot; ++q) s += ws.nslot[(int64_t)q * ws.kp + j];
+  int q = 0;
+  for (; q + 8 <= ws.n_nslot; q += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ws.nslot[(int64_t)(q + u) * ws.kp + j];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; q < ws.n_nslot; ++q) s += ws.nslot[(int64_t)q * ws.kp + j];
   const double nrm = sqrt(s);
   ws.invn[j] = 1.0 / nrm;
   if (!isfinite(ws.invn[j]) || !(nrm > 0.0)) atomicCAS(ws.status, ST_OK, ST_DIVERGED);

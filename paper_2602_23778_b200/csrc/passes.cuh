@@ -134,60 +134,92 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   }
 }
 
+// sum_{c < n} p[c * stride] in ascending c (loads batched 8 at a time so they overlap)
+__device__ __forceinline__ double sum_strided(const double* __restrict__ p, int64_t stride, int n) {
+  double s = 0.0;
+  int c = 0;
+  for (; c + 8 <= n; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(c + u) * stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; c < n; ++c) s += p[(int64_t)c * stride];
+  return s;
+}
+
 // Sum pass-B partials over chunks in fixed order -> M2 (k x k), G2 (k x k), rr2 (k).
+// Block = 32 elements x 8 contiguous chunk ranges; the 8 range sums are combined in order.
 template <int KP, int TA, int TB>
-__global__ void passB_reduce_kernel(Ws ws, int nchunk) {
+__global__ void __launch_bounds__(256) passB_reduce_kernel(Ws ws, int nchunk) {
+  __shared__ double part[8][33];
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   constexpr int NTB = 2 * KP / TB, NTILES = (KP / TA) * NTB;
   const int total = k * 2 * k + k;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+  const int el = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + el;
+  const int c0 = (int)((int64_t)nchunk * rg / 8), c1 = (int)((int64_t)nchunk * (rg + 1) / 8);
+  double s = 0.0;
+  if (e < total) {
     if (e >= 2 * k * k) {
       const int j = e - 2 * k * k;
-      double s = 0.0;
-      for (int c = 0; c < nchunk; ++c) s += ws.brr[(int64_t)c * KP + j];
-      ws.rr2[j] = s;
-      continue;
+      s = sum_strided(ws.brr + (int64_t)c0 * KP + j, KP, c1 - c0);
+    } else {
+      const int a = e / (2 * k), bb = e % (2 * k);
+      const int b = (bb < k) ? bb : KP + (bb - k);        // column in the padded [R | X] space
+      const int tile = (a / TA) * NTB + b / TB;
+      const int off = (a % TA) * TB + (b % TB);
+      s = sum_strided(ws.bpart + ((int64_t)c0 * NTILES + tile) * (TA * TB) + off, (int64_t)NTILES * TA * TB,
+                      c1 - c0);
     }
-    const int a = e / (2 * k), bb = e % (2 * k);
-    const int b = (bb < k) ? bb : KP + (bb - k);          // column in the padded [R | X] space
-    const int tile = (a / TA) * NTB + b / TB;
-    const int off = (a % TA) * TB + (b % TB);
-    double s = 0.0;
-    for (int c = 0; c < nchunk; ++c) s += ws.bpart[((int64_t)c * NTILES + tile) * (TA * TB) + off];
-    if (bb < k) ws.M2[a * k + bb] = s;
-    else ws.G2[a * k + (bb - k)] = s;
+  }
+  part[rg][el] = s;
+  __syncthreads();
+  if (rg == 0 && e < total) {
+    for (int q = 1; q < 8; ++q) s += part[q][el];
+    if (e >= 2 * k * k) {
+      ws.rr2[e - 2 * k * k] = s;
+    } else {
+      const int a = e / (2 * k), bb = e % (2 * k);
+      if (bb < k) ws.M2[a * k + bb] = s;
+      else ws.G2[a * k + (bb - k)] = s;
+    }
   }
 }
 
-template <int KP, int BM, int WARPS_M, int WARPS_N>
+// pass C CTA: BM rows x NC output columns (blockIdx.y selects the column block), Csig[:, cols]
+// resident in shared memory for the CTA's lifetime (persistent over row tiles).
+template <int KP, int NC, int BM, int WARPS_M, int WARPS_N>
 struct PassCCfg {
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int LDX = KP + 4;                               // A-frag reads (8 rows x 4)
-  static constexpr int LDC = KP + ((KP % 16 == 8) ? 0 : 8);        // B-frag reads (4 rows x 8)
+  static constexpr int LDC = NC + ((NC % 16 == 8) ? 0 : 8);        // B-frag reads (4 rows x 8)
   static constexpr int XSTAGE = BM * LDX;
   static constexpr int SMEM = (KP * LDC + 2 * XSTAGE) * 8;
-  static constexpr int WM = BM / WARPS_M, WN = KP / WARPS_N;
+  static constexpr int WM = BM / WARPS_M, WN = NC / WARPS_N;
   static constexpr int MI = WM / 8, NI = WN / 8;
 };
 
-template <int KP, int BM, int WARPS_M, int WARPS_N>
-__global__ void __launch_bounds__(PassCCfg<KP, BM, WARPS_M, WARPS_N>::THREADS)
+template <int KP, int NC, int BM, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(PassCCfg<KP, NC, BM, WARPS_M, WARPS_N>::THREADS)
 passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
-  using C = PassCCfg<KP, BM, WARPS_M, WARPS_N>;
+  using C = PassCCfg<KP, NC, BM, WARPS_M, WARPS_N>;
   extern __shared__ __align__(16) double smem[];
-  __shared__ double ssc[KP];
-  __shared__ double sred[WARPS_M * 8][KP];
+  __shared__ double ssc[NC];
+  __shared__ double sred[WARPS_M * 8][NC];
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int n0 = blockIdx.y * NC;                  // first output column of this CTA
   double* Cs = smem;
   double* Xs = smem + KP * C::LDC;
-  for (int e = tid; e < KP * KP; e += C::THREADS) {
-    const int l = e / KP, j = e % KP;
-    Cs[l * C::LDC + j] = (l < k && j < k) ? ws.Csig[l * k + j] : 0.0;
+  for (int l = tid / NC; l < KP; l += C::THREADS / NC) {
+    const int j = tid % NC;
+    Cs[l * C::LDC + j] = (l < k && n0 + j < k) ? ws.Csig[l * k + n0 + j] : 0.0;
   }
-  for (int j = tid; j < KP; j += C::THREADS) ssc[j] = (j < k) ? ws.scal[j] : 0.0;
+  for (int j = tid; j < NC; j += C::THREADS) ssc[j] = (n0 + j < k) ? ws.scal[n0 + j] : 0.0;
   const int64_t rows = ws.n_loc - ws.top;
   const int64_t ntile = (rows + BM - 1) / BM;
 
@@ -230,10 +262,15 @@ passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
       const int64_t g = r0 + wm * C::WM + i * 8 + (lane >> 2);
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
-        const int c = wn * C::WN + j * 8 + 2 * (lane & 3);
+        const int c = n0 + wn * C::WN + j * 8 + 2 * (lane & 3);
         const bool okr = g < ws.n_loc;
-        w[i][j][0] = (okr && c < k) ? ws.W[g * k + c] : 0.0;
-        w[i][j][1] = (okr && c + 1 < k) ? ws.W[g * k + c + 1] : 0.0;
+        if (vec16 && okr && c < k) {
+          const double2 v = *reinterpret_cast<const double2*>(ws.W + g * k + c);
+          w[i][j][0] = v.x; w[i][j][1] = v.y;
+        } else {
+          w[i][j][0] = (okr && c < k) ? ws.W[g * k + c] : 0.0;
+          w[i][j][1] = (okr && c + 1 < k) ? ws.W[g * k + c + 1] : 0.0;
+        }
       }
     }
     double acc[C::MI][C::NI][2];
@@ -260,11 +297,17 @@ passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
       if (g >= ws.n_loc) continue;
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
-        const int c = wn * C::WN + j * 8 + 2 * (lane & 3);
-        const double x0 = __fma_rn(w[i][j][0], ssc[c], -acc[i][j][0]);
-        const double x1 = __fma_rn(w[i][j][1], ssc[c + 1], -acc[i][j][1]);
-        if (c < k) { X[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
-        if (c + 1 < k) { X[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
+        const int cl = wn * C::WN + j * 8 + 2 * (lane & 3), c = n0 + cl;
+        const double x0 = __fma_rn(w[i][j][0], ssc[cl], -acc[i][j][0]);
+        const double x1 = __fma_rn(w[i][j][1], ssc[cl + 1], -acc[i][j][1]);
+        if (vec16 && c < k) {
+          *reinterpret_cast<double2*>(X + g * k + c) = make_double2(x0, x1);
+          nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]);
+          nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]);
+        } else {
+          if (c < k) { X[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
+          if (c + 1 < k) { X[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
+        }
       }
     }
   }
@@ -276,19 +319,33 @@ passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
     sred[wm * 8 + (lane >> 2)][c + 1] = nacc[j][1];
   }
   __syncthreads();
-  for (int j = tid; j < KP; j += C::THREADS) {
+  for (int j = tid; j < NC; j += C::THREADS) {
     double s = 0.0;
     for (int q = 0; q < WARPS_M * 8; ++q) s += sred[q][j];
-    ws.nslot[(int64_t)blockIdx.x * KP + j] = s;
+    ws.nslot[(int64_t)blockIdx.x * KP + n0 + j] = s;
   }
 }
 
-__global__ void normalize_kernel(Ws ws, double* __restrict__ X) {
+// x_ij *= 1/||x~_j||.  The thread count is a multiple of k/2 on the vector path, so every
+// thread always scales the same column pair (no per-element index arithmetic).
+__global__ void __launch_bounds__(256) normalize_kernel(Ws ws, double* __restrict__ X) {
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
-  const int64_t total = ws.n_loc * k;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
-    X[e] *= ws.invn[e % k];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  if ((k & 1) == 0 && (256 % (k / 2)) == 0) {
+    const int64_t total2 = ws.n_loc * (k / 2);
+    const int j = (int)(tid % (k / 2)) * 2;
+    const double s0 = ws.invn[j], s1 = ws.invn[j + 1];
+    double2* X2 = reinterpret_cast<double2*>(X);
+    for (int64_t e = tid; e < total2; e += nthr) {
+      double2 v = X2[e];
+      v.x *= s0; v.y *= s1;
+      X2[e] = v;
+    }
+  } else {
+    const int64_t total = ws.n_loc * k;
+    for (int64_t e = tid; e < total; e += nthr) X[e] *= ws.invn[e % k];
+  }
 }
 
 }  // namespace rf

@@ -153,26 +153,26 @@ static refine_status cuda_fail(refine_ctx* c, cudaError_t e, const char* what) {
 
 // ---------------------------------------------------------------- per-KP kernel tables
 template <int KP> struct Tiles;
-//                 GEMM: BM  WM  WN  BK  ST | passB: TA  TB  WA WB  BR | passC: BM WM WN
-template <> struct Tiles<8>   { static constexpr int G[5] = {64, 16, 8, 32, 4};   static constexpr int B[5] = {8, 16, 1, 2, 32};   static constexpr int C[3] = {64, 8, 1}; };
-template <> struct Tiles<16>  { static constexpr int G[5] = {64, 16, 16, 32, 4};  static constexpr int B[5] = {16, 32, 2, 4, 32};  static constexpr int C[3] = {64, 8, 1}; };
-template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 3}; static constexpr int B[5] = {32, 64, 2, 4, 32};  static constexpr int C[3] = {64, 4, 2}; };
-template <> struct Tiles<64>  { static constexpr int G[5] = {128, 32, 32, 32, 3}; static constexpr int B[5] = {64, 128, 2, 4, 32}; static constexpr int C[3] = {64, 2, 4}; };
-template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 3};  static constexpr int B[5] = {64, 128, 2, 4, 32}; static constexpr int C[3] = {32, 2, 4}; };
+//                 GEMM: BM  WM  WN  BK  ST | passB: TA  TB  WA WB  BR | passC: NC BM WM WN
+template <> struct Tiles<8>   { static constexpr int G[5] = {64, 16, 8, 32, 4};   static constexpr int B[5] = {8, 16, 1, 2, 32};   static constexpr int C[4] = {8, 64, 8, 1}; };
+template <> struct Tiles<16>  { static constexpr int G[5] = {64, 16, 16, 32, 4};  static constexpr int B[5] = {16, 32, 2, 4, 32};  static constexpr int C[4] = {16, 64, 8, 1}; };
+template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}; static constexpr int B[5] = {32, 64, 2, 4, 32};  static constexpr int C[4] = {32, 64, 4, 2}; };
+template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
+template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 16, 1, 8}; };
 
 template <int KP>
 struct Kern {
   using TT = Tiles<KP>;
   static constexpr int GBM = TT::G[0], GWM = TT::G[1], GWN = TT::G[2], GBK = TT::G[3], GST = TT::G[4];
   static constexpr int BTA = TT::B[0], BTB = TT::B[1], BWA = TT::B[2], BWB = TT::B[3], BBR = TT::B[4];
-  static constexpr int CBM = TT::C[0], CWM = TT::C[1], CWN = TT::C[2];
+  static constexpr int CNC = TT::C[0], CBM = TT::C[1], CWM = TT::C[2], CWN = TT::C[3];
   using GC = GemmCfg<KP, GBM, GWM, GWN, GBK, GST>;
   using BC = PassBCfg<KP, BTA, BTB, BWA, BWB, BBR>;
-  using CC = PassCCfg<KP, CBM, CWM, CWN>;
+  using CC = PassCCfg<KP, CNC, CBM, CWM, CWN>;
   static constexpr auto gemm = gemm_ax_kernel<KP, GBM, GWM, GWN, GBK, GST>;
   static constexpr auto passB = passB_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
   static constexpr auto passBred = passB_reduce_kernel<KP, BTA, BTB>;
-  static constexpr auto passC = passC_kernel<KP, CBM, CWM, CWN>;
+  static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN>;
 
   static cudaError_t setup(refine_ctx* c) {
     cudaError_t e;
@@ -188,14 +188,17 @@ struct Kern {
       c->gemm_bm = GBM;
       c->gemm_gx = (int)((c->n_loc + GBM - 1) / GBM);
       const int64_t kiters = (c->n + GBK - 1) / GBK;
+      // split-K: smallest split whose grid fills >= 3 waves of resident CTAs at >= 90% wave
+      // efficiency (each extra split adds 2 x n_loc x k x 8 bytes of partial traffic)
       int best = 1;
       double best_eff = -1.0;
       for (int s = 1; s <= 16 && s <= kiters; ++s) {
         const int64_t ctas = (int64_t)c->gemm_gx * s;
         const double waves = std::ceil((double)ctas / slots);
         double eff = (double)ctas / (waves * slots);
-        if (ctas < 2 * slots) eff *= (double)ctas / (2.0 * slots);   // prefer >= 2 waves in flight
+        if (ctas < 3 * slots) eff *= (double)ctas / (3.0 * slots);
         if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
+        if (eff >= 0.9 && ctas >= 3 * slots) break;
       }
       c->nsplit = best;
       const int64_t kit = (kiters + best - 1) / best;
@@ -205,12 +208,12 @@ struct Kern {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passB, BC::THREADS, BC::SMEM))) return e;
     occ = std::max(occ, 1);
     const int64_t rows = std::max<int64_t>(c->n_loc - c->ws.top, 1);
-    const int64_t max_chunks = std::max<int64_t>((rows + BBR - 1) / BBR, 1);
-    c->passb_grid_y = (int)std::min<int64_t>(std::max(2 * c->sms * occ / BC::NTILES, 1), max_chunks);
+    const int64_t max_chunks = std::max<int64_t>((rows + 255) / 256, 1);   // >= 256 rows per chunk
+    c->passb_grid_y = (int)std::min<int64_t>(std::max(c->sms * occ / BC::NTILES, 1), max_chunks);
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passC, CC::THREADS, CC::SMEM))) return e;
     occ = std::max(occ, 1);
     const int64_t ctiles = std::max<int64_t>((rows + CBM - 1) / CBM, 1);
-    c->passc_grid = (int)std::min<int64_t>(c->sms * occ, ctiles);
+    c->passc_grid = (int)std::min<int64_t>(std::max(c->sms * occ / (KP / CNC), 1), ctiles);
     return cudaSuccess;
   }
 
@@ -235,31 +238,44 @@ struct Kern {
       w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(ws, X, c->nsplit, c->n_loc * c->k);
       n += 2;
     } else {
-      const int cpl = (c->k + 31) / 32;
       c->mark();
-      switch (cpl) {
-        case 1: spmm_csr_kernel<1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-        case 2: spmm_csr_kernel<2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-        case 3: spmm_csr_kernel<3><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-        default: spmm_csr_kernel<4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2;
+      auto* Xg = X;
+      if (vec) {
+        switch (c->k) {
+          case 2: spmm_csr_vec_kernel<1, 1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 4: spmm_csr_vec_kernel<1, 2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 8: spmm_csr_vec_kernel<1, 4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 16: spmm_csr_vec_kernel<1, 8><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 32: spmm_csr_vec_kernel<1, 16><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 64: spmm_csr_vec_kernel<1, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          default: spmm_csr_vec_kernel<2, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+        }
+      } else {
+        switch ((c->k + 31) / 32) {
+          case 1: spmm_csr_kernel<1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 2: spmm_csr_kernel<2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          case 3: spmm_csr_kernel<3><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+          default: spmm_csr_kernel<4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+        }
       }
       n += 1;
     }
     c->mark();
-    kxk_prep_kernel<<<1, 1024, c->k * c->k * 8, s>>>(ws, X);
+    kxk_prep_kernel<<<1, KXK_THREADS, std::max(c->k * c->k, PANEL_SMEM) * 8, s>>>(ws, X);
     c->mark();
     passB<<<dim3(BC::NTILES, c->passb_grid_y), BC::THREADS, BC::SMEM, s>>>(ws, X, xv16);
     c->mark();
-    passBred<<<64, 256, 0, s>>>(ws, c->passb_grid_y);
+    passBred<<<(2 * c->k * c->k + c->k + 31) / 32, 256, 0, s>>>(ws, c->passb_grid_y);
     c->mark();
-    kxk_finish_kernel<<<1, 1024, 0, s>>>(ws, X, ws.W);
+    kxk_finish_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
     c->mark();
-    passC<<<c->passc_grid, CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
+    passC<<<dim3(c->passc_grid, KP / CNC), CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
     c->mark();
     norm_reduce_kernel<<<1, 128, 0, s>>>(ws);
     if (c->opts.normalize) {
       c->mark();
-      normalize_kernel<<<c->sms * 4, 256, 0, s>>>(ws, X);
+      normalize_kernel<<<c->sms * 8, 256, 0, s>>>(ws, X);
       ++n;
     }
     c->mark();
@@ -303,6 +319,7 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   refine_status st = REFINE_OK;
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
   RF_CK(c, cudaFuncSetAttribute(kxk_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KMAX * KMAX * 8));
+  RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
   // workspace sizes (doubles)
   size_t bpart = 0, brr = 0, nslot = 0;
   dispatch(c->kp, [&](auto K) { decltype(K)::sizes(c, bpart, brr, nslot); return 0; });
@@ -316,7 +333,7 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   const size_t oW = take(nk), oWp = take(wpart), oAg = take((size_t)c->n_ag * k * 4), oBp = take(bpart),
                oBrr = take(brr), oM2 = take(kk), oG2 = take(kk), oRr = take(k), oNs = take(nslot),
                oAl = take(k), oD = take(k), oRd = take(k), oSg = take(k), oU = take(kk), oL = take(kk),
-               oT = take(kk), oE = take(kk), oCs = take(kk), oSc = take(k), oNt = take(k), oIn = take(k),
+               oT = take(kk), oUi = take(kk), oE = take(kk), oCs = take(kk), oSc = take(k), oNt = take(k), oIn = take(k),
                oSt = take(8), oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
@@ -327,7 +344,7 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   ws.bpart = b + oBp; ws.brr = b + oBrr; ws.n_chunk = c->passb_grid_y;
   ws.M2 = b + oM2; ws.G2 = b + oG2; ws.rr2 = b + oRr; ws.nslot = b + oNs; ws.n_nslot = c->passc_grid;
   ws.alpha = b + oAl; ws.d = b + oD; ws.rd = b + oRd; ws.sigma = b + oSg; ws.U = b + oU; ws.L = b + oL;
-  ws.T = b + oT; ws.E11 = b + oE; ws.Csig = b + oCs; ws.scal = b + oSc; ws.ntop = b + oNt; ws.invn = b + oIn;
+  ws.T = b + oT; ws.Uinv = b + oUi; ws.E11 = b + oE; ws.Csig = b + oCs; ws.scal = b + oSc; ws.ntop = b + oNt; ws.invn = b + oIn;
   ws.stats = b + oSt; ws.scratch = b + oScr;
   c->run = reinterpret_cast<RunState*>(b + oRun);
   ws.status = reinterpret_cast<int*>(b + off);     // after all arrays (64 spare bytes)
