@@ -20,24 +20,59 @@ struct PassBCfg {
   static constexpr int THREADS = WARPS_A * WARPS_B * 32;
   static constexpr int LDS = KP + ((KP % 16 == 8) ? 0 : 8);
   static constexpr int STAGE = BR * LDS;
-  static constexpr int SMEM = 2 * 2 * STAGE * 8;       // X and R, double buffered
+  static constexpr int SMEM = 2 * 2 * STAGE * 8;       // X and W, double buffered
   static constexpr int WTA = TA / WARPS_A, WTB = TB / WARPS_B;
   static constexpr int MI = WTA / 8, NI = WTB / 8;
-  static constexpr int NTA = KP / TA, NTB = 2 * KP / TB, NTILES = NTA * NTB;
+  static constexpr int NTA = KP / TA, NTB = 2 * KP / TB;
+  // G = X^T X is symmetric: tiles of the G half lying strictly below its diagonal are skipped
+  // (the reduction mirrors them), so tile ids enumerate only the kept (ta, tb) pairs.
+  static constexpr __host__ __device__ bool kept(int ta, int tb) {
+    return !(tb * TB >= KP && (tb * TB - KP) + TB <= ta * TA);
+  }
+  static constexpr __host__ __device__ int count() {
+    int n = 0;
+    for (int a = 0; a < NTA; ++a)
+      for (int b = 0; b < NTB; ++b) n += kept(a, b) ? 1 : 0;
+    return n;
+  }
+  static constexpr int NTILES = count();
+  static __host__ __device__ int tile_id(int ta, int tb) {   // -1 if skipped
+    int n = 0;
+    for (int a = 0; a < NTA; ++a)
+      for (int b = 0; b < NTB; ++b) {
+        if (!kept(a, b)) continue;
+        if (a == ta && b == tb) return n;
+        ++n;
+      }
+    return -1;
+  }
 };
 
+// R = W - X D is formed on the fly while loading the B fragments of the M half (no shared
+// memory write-back, one barrier per stage); rr_j = sum r_ij^2 is accumulated by the warps of
+// tile 0 in the first a-row of warps, which see every (row, column) of R exactly once.
 template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
 __global__ void __launch_bounds__(PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>::THREADS)
 passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   using C = PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>;
   extern __shared__ __align__(16) double smem[];
   __shared__ double sd[KP];
-  __shared__ double srr[C::THREADS];
+  __shared__ double srr[WARPS_B * 4][TB];
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wa = warp / WARPS_B, wb = warp % WARPS_B;
-  const int tile = blockIdx.x, ta = tile / C::NTB, tb = tile % C::NTB;
+  int ta = 0, tb = 0;
+  {   // decode the kept-tile index
+    int n = 0;
+    for (int a = 0; a < C::NTA; ++a)
+      for (int b = 0; b < C::NTB; ++b) {
+        if (!C::kept(a, b)) continue;
+        if (n == (int)blockIdx.x) { ta = a; tb = b; }
+        ++n;
+      }
+  }
   const int a0 = ta * TA, b0 = tb * TB;
+  const bool rpart = b0 < KP;                            // the tile has R columns (it may also have X)
   const int64_t rows = ws.n_loc - ws.top;
   const int64_t per = ((rows + gridDim.y - 1) / gridDim.y + BR - 1) / BR * BR;
   const int64_t rb = ws.top + (int64_t)blockIdx.y * per;
@@ -45,12 +80,12 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
   for (int j = tid; j < KP; j += C::THREADS) sd[j] = (j < k) ? ws.d[j] : 0.0;
   double* Xs = smem;
-  double* Rs = smem + 2 * C::STAGE;
+  double* Ws_ = smem + 2 * C::STAGE;
 
   auto load = [&](int buf, int it) {
     const int64_t r0 = rb + (int64_t)it * BR;
     double* xs = Xs + buf * C::STAGE;
-    double* rs = Rs + buf * C::STAGE;
+    double* wsb = Ws_ + buf * C::STAGE;
     if (vec16) {
       for (int c = tid; c < BR * KP / 2; c += C::THREADS) {
         const int r = c / (KP / 2), cc = (c % (KP / 2)) * 2;
@@ -58,7 +93,7 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
         const bool ok = (g < re) && (cc < k);
         const int64_t off = ok ? g * k + cc : 0;
         cp_async16(xs + r * C::LDS + cc, X + off, ok);
-        cp_async16(rs + r * C::LDS + cc, ws.W + off, ok);
+        if (rpart) cp_async16(wsb + r * C::LDS + cc, ws.W + off, ok);
       }
     } else {
       for (int c = tid; c < BR * KP; c += C::THREADS) {
@@ -67,7 +102,7 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
         const bool ok = (g < re) && (cc < k);
         const int64_t off = ok ? g * k + cc : 0;
         cp_async8(xs + r * C::LDS + cc, X + off, ok);
-        cp_async8(rs + r * C::LDS + cc, ws.W + off, ok);
+        if (rpart) cp_async8(wsb + r * C::LDS + cc, ws.W + off, ok);
       }
     }
   };
@@ -77,8 +112,10 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   for (int i = 0; i < C::MI; ++i)
 #pragma unroll
     for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  double rr = 0.0;                       // column tid % KP (THREADS is a multiple of KP)
-  const bool do_rr = (tile == 0);
+  double rr[C::NI];
+#pragma unroll
+  for (int j = 0; j < C::NI; ++j) rr[j] = 0.0;
+  const bool do_rr = (ta == 0) && rpart && (wa == 0);    // the R tiles of the first a-block
   if (nit > 0) load(0, 0);
   cp_async_commit();
   for (int it = 0; it < nit; ++it) {
@@ -87,15 +124,8 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
     __syncthreads();
     if (it + 1 < nit) load(cur ^ 1, it + 1);
     cp_async_commit();
-    double* xs = Xs + cur * C::STAGE;
-    double* rs = Rs + cur * C::STAGE;
-    for (int e = tid; e < BR * KP; e += C::THREADS) {     // R = W - X D  (fma as in the oracle)
-      const int r = e / KP, c = e % KP;
-      const double v = __fma_rn(-xs[r * C::LDS + c], sd[c], rs[r * C::LDS + c]);
-      rs[r * C::LDS + c] = v;
-      rr = __fma_rn(v, v, rr);
-    }
-    __syncthreads();
+    const double* xs = Xs + cur * C::STAGE;
+    const double* wsb = Ws_ + cur * C::STAGE;
 #pragma unroll
     for (int kk = 0; kk < BR; kk += 4) {
       const int row = kk + (lane & 3);
@@ -104,8 +134,15 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
       for (int i = 0; i < C::MI; ++i) a[i] = xs[row * C::LDS + a0 + wa * C::WTA + i * 8 + (lane >> 2)];
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
-        const int col = b0 + wb * C::WTB + j * 8 + (lane >> 2);
-        b[j] = (col < KP) ? rs[row * C::LDS + col] : xs[row * C::LDS + col - KP];
+        const int cb8 = b0 + wb * C::WTB + j * 8;          // 8-column block: all R or all X (warp-uniform)
+        const int col = cb8 + (lane >> 2);
+        if (cb8 < KP) {
+          const double r = __fma_rn(-xs[row * C::LDS + col], sd[col], wsb[row * C::LDS + col]);
+          b[j] = r;
+          if (do_rr) rr[j] = __fma_rn(r, r, rr[j]);
+        } else {
+          b[j] = xs[row * C::LDS + col - KP];
+        }
       }
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
@@ -113,7 +150,7 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
         for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
-  double* out = ws.bpart + ((int64_t)blockIdx.y * C::NTILES + tile) * (TA * TB);
+  double* out = ws.bpart + ((int64_t)blockIdx.y * C::NTILES + blockIdx.x) * (TA * TB);
 #pragma unroll
   for (int i = 0; i < C::MI; ++i)
 #pragma unroll
@@ -123,13 +160,18 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
       out[ra * TB + cb] = acc[i][j][0];
       out[ra * TB + cb + 1] = acc[i][j][1];
     }
-  if (do_rr) {
-    srr[tid] = rr;
+  if (ta == 0 && rpart) {
+    // rr: lane (wb, j, lane>>2) holds column b0 + wb*WTB + j*8 + lane/4 summed over its rows (lane&3)
+    if (wa == 0) {
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) srr[wb * 4 + (lane & 3)][wb * C::WTB + j * 8 + (lane >> 2)] = rr[j];
+    }
     __syncthreads();
-    if (tid < KP) {
-      double s = srr[tid];
-      for (int q = 1; q < C::THREADS / KP; ++q) s += srr[q * KP + tid];
-      ws.brr[(int64_t)blockIdx.y * KP + tid] = s;
+    for (int j = tid; j < TB && b0 + j < KP; j += C::THREADS) {
+      const int q0 = (j / C::WTB) * 4;
+      double s = 0.0;
+      for (int q = 0; q < 4; ++q) s += srr[q0 + q][j];
+      ws.brr[(int64_t)blockIdx.y * KP + b0 + j] = s;
     }
   }
 }
@@ -151,12 +193,12 @@ __device__ __forceinline__ double sum_strided(const double* __restrict__ p, int6
 
 // Sum pass-B partials over chunks in fixed order -> M2 (k x k), G2 (k x k), rr2 (k).
 // Block = 32 elements x 8 contiguous chunk ranges; the 8 range sums are combined in order.
-template <int KP, int TA, int TB>
+template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
 __global__ void __launch_bounds__(256) passB_reduce_kernel(Ws ws, int nchunk) {
+  using C = PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>;
   __shared__ double part[8][33];
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
-  constexpr int NTB = 2 * KP / TB, NTILES = (KP / TA) * NTB;
   const int total = k * 2 * k + k;
   const int el = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + el;
@@ -167,12 +209,16 @@ __global__ void __launch_bounds__(256) passB_reduce_kernel(Ws ws, int nchunk) {
       const int j = e - 2 * k * k;
       s = sum_strided(ws.brr + (int64_t)c0 * KP + j, KP, c1 - c0);
     } else {
-      const int a = e / (2 * k), bb = e % (2 * k);
-      const int b = (bb < k) ? bb : KP + (bb - k);        // column in the padded [R | X] space
-      const int tile = (a / TA) * NTB + b / TB;
+      int a = e / (2 * k), bb = e % (2 * k);
+      if (bb >= k) {                                   // G half: mirror skipped (lower) tiles
+        const int gb = bb - k;
+        if (C::tile_id(a / TA, (KP + gb) / TB) < 0) { const int t = a; a = gb; bb = k + t; }
+      }
+      const int b = (bb < k) ? bb : KP + (bb - k);     // column in the padded [R | X] space
+      const int tile = C::tile_id(a / TA, b / TB);
       const int off = (a % TA) * TB + (b % TB);
-      s = sum_strided(ws.bpart + ((int64_t)c0 * NTILES + tile) * (TA * TB) + off, (int64_t)NTILES * TA * TB,
-                      c1 - c0);
+      s = sum_strided(ws.bpart + ((int64_t)c0 * C::NTILES + tile) * (TA * TB) + off,
+                      (int64_t)C::NTILES * TA * TB, c1 - c0);
     }
   }
   part[rg][el] = s;

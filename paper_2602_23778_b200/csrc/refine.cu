@@ -158,7 +158,7 @@ template <> struct Tiles<8>   { static constexpr int G[5] = {64, 16, 8, 32, 4}; 
 template <> struct Tiles<16>  { static constexpr int G[5] = {64, 16, 16, 32, 4};  static constexpr int B[5] = {16, 32, 2, 4, 32};  static constexpr int C[4] = {16, 64, 8, 1}; };
 template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}; static constexpr int B[5] = {32, 64, 2, 4, 32};  static constexpr int C[4] = {32, 64, 4, 2}; };
 template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
-template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 16, 1, 8}; };
+template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 4, 16};  static constexpr int C[4] = {64, 16, 1, 8}; };
 
 template <int KP>
 struct Kern {
@@ -171,7 +171,7 @@ struct Kern {
   using CC = PassCCfg<KP, CNC, CBM, CWM, CWN>;
   static constexpr auto gemm = gemm_ax_kernel<KP, GBM, GWM, GWN, GBK, GST>;
   static constexpr auto passB = passB_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
-  static constexpr auto passBred = passB_reduce_kernel<KP, BTA, BTB>;
+  static constexpr auto passBred = passB_reduce_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
   static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN>;
 
   static cudaError_t setup(refine_ctx* c) {
