@@ -96,6 +96,12 @@ struct Ws {
   double *alpha, *d, *rd, *sigma, *U, *L, *Uinv, *T, *E11, *Csig, *scal, *ntop, *invn, *stats;
   double* scratch;   // 16 k x k scratch matrices for the k x k algebra
   int* status;
+  long long* tlog;   // optional clock64() phase log of the k x k kernels (REFINE_KXK_TIMING=1)
 };
+
+#define RF_TSTAMP(ws, i)                                                   \
+  do {                                                                     \
+    if ((ws).tlog && threadIdx.x == 0) (ws).tlog[i] = clock64();          \
+  } while (0)
 
 }  // namespace rf

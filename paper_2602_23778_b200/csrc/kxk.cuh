@@ -158,44 +158,56 @@ __device__ void cta_trinv(int k, const double* S, bool upper, double* R, double*
 }
 
 // ---------------------------------------------------------------- kxk_prep
+// Shared memory: Q (k x k, the in-place modified LU); for k <= 64 also Ls, Ts, Us (L, T, U^{-1}).
 __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const double* __restrict__ Xtop) {
-  extern __shared__ __align__(16) double Q[];     // k x k (in-place modified LU), then gemm panels
+  extern __shared__ __align__(16) double Q[];
   __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
   __shared__ int s_bad;
   if (*ws.status != ST_OK) return;
+  RF_TSTAMP(ws, 0);
   const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
 
-  // 1. alpha_j, g_j: P parts per column, each part a contiguous slot range, combined in order
+  // 1. alpha_j, g_j: P parts per column (contiguous slot ranges, 4 interleaved accumulators
+  //    each), then a fixed pairwise tree over the parts -- deterministic for a given launch shape
   const int P = nt / k;
   const int j = tid % k, p = tid / k;
   dd a = {0.0, 0.0}, g = {0.0, 0.0};
   if (p < P) {
     const int s0 = (int)((int64_t)ws.n_ag * p / P), s1 = (int)((int64_t)ws.n_ag * (p + 1) / P);
+    dd a4[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}}, g4[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
     int s = s0;
-    for (; s + 4 <= s1; s += 4) {
-      double v[4][4];
+    for (; s + 8 <= s1; s += 8) {
+      double v[8][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int q = 0; q < 4; ++q) v[u][q] = ws.ag[((int64_t)(s + u) * k + j) * 4 + q];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { dd_add(a, dd{v[u][0], v[u][1]}); dd_add(g, dd{v[u][2], v[u][3]}); }
+      for (int u = 0; u < 8; ++u) { dd_add(a4[u & 3], dd{v[u][0], v[u][1]}); dd_add(g4[u & 3], dd{v[u][2], v[u][3]}); }
     }
     for (; s < s1; ++s) {
       const double* slot = ws.ag + ((int64_t)s * k + j) * 4;
-      dd_add(a, dd{slot[0], slot[1]});
-      dd_add(g, dd{slot[2], slot[3]});
+      dd_add(a4[0], dd{slot[0], slot[1]});
+      dd_add(g4[0], dd{slot[2], slot[3]});
     }
+    a = a4[0]; g = g4[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) { dd_add(a, a4[u]); dd_add(g, g4[u]); }
   }
   pa[tid] = a;
   pg[tid] = g;
   for (int e = tid; e < k * k; e += nt) Q[e] = Xtop[e];
   if (tid == 0) s_bad = ST_OK;
   __syncthreads();
+  for (int st = 1; st < P; st *= 2) {
+    if (p < P && (p % (2 * st)) == 0 && p + st < P) {
+      dd_add(pa[tid], pa[tid + st * k]);
+      dd_add(pg[tid], pg[tid + st * k]);
+    }
+    __syncthreads();
+  }
   if (tid < k) {
-    dd ta = pa[tid], tg = pg[tid];
-    for (int q = 1; q < P; ++q) { dd_add(ta, pa[q * k + tid]); dd_add(tg, pg[q * k + tid]); }
-    const double al = dd_val(ta), gv = dd_val(tg);
+    const double al = dd_val(pa[tid]), gv = dd_val(pg[tid]);
     const double dj = gv / al;
     ws.alpha[tid] = al;
     ws.d[tid] = dj;
@@ -206,10 +218,17 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
     else if (fabs(dj) <= ws.delta) bad = ST_E_NEAR_ZERO_RQ;
     if (bad != ST_OK) atomicCAS(&s_bad, ST_OK, bad);
   }
-  __syncthreads();
+  RF_TSTAMP(ws, 1);
 
-  // 2. Alg. 2 on the top block, literal order: sigma_j = -sign(q_jj) (sign(0)=+1),
-  //    q_jj -= sigma_j, scale the column below, rank-1 update of the trailing block.
+  // 2. Alg. 2 on the top block, literal arithmetic: sigma_j = -sign(q_jj) (sign(0)=+1),
+  //    q_jj -= sigma_j, q_lj /= q_jj, q_lh -= q_lj q_jh.  One barrier per step: thread (l, h)
+  //    forms q_lj / pivot itself, column j of Y goes straight to L (never re-read here), and
+  //    only q_lh with l, h > j are written, which no other thread reads during the step.
+  const bool small = (k <= 64);
+  double* Ls = Q + k * k;          // small k: L, T, U^{-1} also in shared memory
+  double* Ts = Q + 2 * k * k;
+  double* Us = Q + 3 * k * k;
+  __syncthreads();
   for (int jj = 0; jj < k; ++jj) {
     const double q = Q[jj * k + jj];
     const double s = (q >= 0.0) ? -1.0 : 1.0;
@@ -218,13 +237,18 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
       if (tid == 0) atomicCAS(&s_bad, ST_OK, ST_E_ZERO_PIVOT);
       break;
     }
-    __syncthreads();                         // everyone has read q before it is overwritten
-    if (tid == 0) { Q[jj * k + jj] = piv; ws.sigma[jj] = s; }
-    for (int l = jj + 1 + tid; l < k; l += nt) Q[l * k + jj] = __ddiv_rn(Q[l * k + jj], piv);
-    __syncthreads();
-    for (int l = jj + 1 + (tid >> 5); l < k; l += 32)
-      for (int h = jj + 1 + (tid & 31); h < k; h += 32)
-        Q[l * k + h] = __dadd_rn(Q[l * k + h], -__dmul_rn(Q[l * k + jj], Q[jj * k + h]));
+    if (tid == 0) ws.sigma[jj] = s;
+    for (int l = jj + 1 + (tid >> 5); l < k; l += 32) {
+      const double ql = __ddiv_rn(Q[l * k + jj], piv);
+      for (int h = jj + (tid & 31); h < k; h += 32) {
+        if (h == jj) {
+          ws.L[l * k + jj] = ql;
+          if (small) Ls[l * k + jj] = ql;
+        } else {
+          Q[l * k + h] = __dadd_rn(Q[l * k + h], -__dmul_rn(ql, Q[jj * k + h]));
+        }
+      }
+    }
     __syncthreads();
   }
   __syncthreads();
@@ -232,23 +256,56 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
     if (tid == 0) *ws.status = s_bad;
     return;
   }
-  double* Up = ws.scratch;                   // U Sigma
+  // U = upper(Q) with the shifted diagonal; L unit lower (strict part written above)
   for (int r = tid >> 5; r < k; r += 32)
     for (int c = tid & 31; c < k; c += 32) {
-    const int e = r * k + c;
-    const double qv = Q[e];
-    ws.U[e] = (c >= r) ? qv : 0.0;
-    ws.L[e] = (c < r) ? qv : (c == r ? 1.0 : 0.0);
-  }
+      const double qv = Q[r * k + c];
+      const double sg = ws.sigma[r];
+      const double u = (c > r) ? qv : (c == r ? __dadd_rn(qv, -sg) : 0.0);
+      Q[r * k + c] = u;                                    // Q now holds U
+      ws.U[r * k + c] = u;
+      if (c >= r) {
+        ws.L[r * k + c] = (c == r) ? 1.0 : 0.0;
+        if (small) Ls[r * k + c] = (c == r) ? 1.0 : 0.0;
+      }
+    }
   __syncthreads();
-  for (int r = tid >> 5; r < k; r += 32)
-    for (int c = tid & 31; c < k; c += 32) Up[r * k + c] = ws.U[r * k + c] * ws.sigma[c];
-  // 3. U^{-1}, L^{-1}; T = -(U Sigma) L^{-T}   (shared memory now holds gemm panels)
-  double* Linv = ws.scratch + k * k;
-  double* tmp = ws.scratch + 2 * k * k;
-  cta_trinv(k, ws.U, true, ws.Uinv, tmp, Q);
-  cta_trinv(k, ws.L, false, Linv, tmp, Q);
-  cta_gemm(k, k, k, -1.0, Up, k, false, Linv, k, true, 0.0, nullptr, 0, ws.T, k, Q);
+  RF_TSTAMP(ws, 2);
+  if (small) {
+    // 3a. T = -U Sigma L^{-T}: thread i < k owns row i (t_ic = -u_ic s_c - sum_{i<=l<c} t_il L_cl);
+    //     thread k + c owns column c of U^{-1} (back substitution).  All operands in shared memory.
+    if (tid < k) {
+      const int i = tid;
+      for (int c = 0; c < i; ++c) Ts[i * k + c] = 0.0;
+      for (int c = i; c < k; ++c) {
+        double t = -(Q[i * k + c] * ws.sigma[c]);
+        for (int l = i; l < c; ++l) t = fma(-Ts[i * k + l], Ls[c * k + l], t);
+        Ts[i * k + c] = t;
+      }
+    } else if (tid < 2 * k) {
+      const int c = tid - k;
+      for (int i = k - 1; i > c; --i) Us[i * k + c] = 0.0;
+      for (int i = c; i >= 0; --i) {
+        double x = (i == c) ? 1.0 : 0.0;
+        for (int l = i + 1; l <= c; ++l) x = fma(-Q[i * k + l], Us[l * k + c], x);
+        Us[i * k + c] = x / Q[i * k + i];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < k * k; e += nt) { ws.T[e] = Ts[e]; ws.Uinv[e] = Us[e]; }
+  } else {
+    // 3b. large k: blocked triangular inversion and a DMMA product through L2-resident scratch
+    double* Up = ws.scratch;                   // U Sigma
+    for (int r = tid >> 5; r < k; r += 32)
+      for (int c = tid & 31; c < k; c += 32) Up[r * k + c] = Q[r * k + c] * ws.sigma[c];
+    double* Linv = ws.scratch + k * k;
+    double* tmp = ws.scratch + 2 * k * k;
+    __syncthreads();
+    cta_trinv(k, ws.U, true, ws.Uinv, tmp, Q);
+    cta_trinv(k, ws.L, false, Linv, tmp, Q);
+    cta_gemm(k, k, k, -1.0, Up, k, false, Linv, k, true, 0.0, nullptr, 0, ws.T, k, Q);
+  }
+  RF_TSTAMP(ws, 5);
   if (tid == 0 && s_bad != ST_OK) *ws.status = s_bad;
 }
 

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "../../include/refine.h"
@@ -262,7 +263,7 @@ struct Kern {
       n += 1;
     }
     c->mark();
-    kxk_prep_kernel<<<1, KXK_THREADS, std::max(c->k * c->k, PANEL_SMEM) * 8, s>>>(ws, X);
+    kxk_prep_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8, s>>>(ws, X);
     c->mark();
     passB<<<dim3(BC::NTILES, c->passb_grid_y), BC::THREADS, BC::SMEM, s>>>(ws, X, xv16);
     c->mark();
@@ -318,7 +319,7 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   ws.beta_zero = c->opts.beta_zero;
   refine_status st = REFINE_OK;
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
-  RF_CK(c, cudaFuncSetAttribute(kxk_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KMAX * KMAX * 8));
+  RF_CK(c, cudaFuncSetAttribute(kxk_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
   RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
   // workspace sizes (doubles)
   size_t bpart = 0, brr = 0, nslot = 0;
@@ -348,6 +349,8 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   ws.stats = b + oSt; ws.scratch = b + oScr;
   c->run = reinterpret_cast<RunState*>(b + oRun);
   ws.status = reinterpret_cast<int*>(b + off);     // after all arrays (64 spare bytes)
+  ws.tlog = nullptr;
+  if (getenv("REFINE_KXK_TIMING")) RF_CK(c, cudaMalloc(&ws.tlog, 64 * sizeof(long long)));
   // ||A - shift I||_inf (one pass over A) -> delta = c ||A|| u
   double* rows = b + oRows;
   if (!c->csr)
@@ -572,6 +575,7 @@ extern "C" void refine_destroy(refine_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->pool) cudaFree(c->pool);
+  if (c->ws.tlog) cudaFree(c->ws.tlog);
   if (c->dX) cudaFree(c->dX);
   delete c;
 }
@@ -620,6 +624,9 @@ extern "C" refine_status refine_debug_get(refine_ctx* c, int32_t what, double* d
       RF_CK(c, cudaStreamSynchronize(c->stream));
       return REFINE_OK;
     case 9: src = ws.stats; cnt = 8; break;
+    case 10:   // clock64 phase log (REFINE_KXK_TIMING=1), raw int64 bits
+      if (!ws.tlog) return REFINE_E_UNSUPPORTED;
+      src = reinterpret_cast<const double*>(ws.tlog); cnt = 64; break;
     default: return REFINE_E_INVALID;
   }
   RF_CK(c, cudaMemcpyAsync(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
