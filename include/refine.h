@@ -59,10 +59,20 @@ typedef enum {
 } refine_status;
 
 /* Process group of the row partition (one process per GPU).  world == 1:
- * everything local, nccl_id ignored.  world > 1: rank r owns rows
- * [row_begin, row_end) of A and X^; rank 0 must own rows 0..k-1; nccl_id is
- * the 128-byte ncclUniqueId produced by refine_nccl_id() on rank 0 and
- * broadcast by the caller (e.g. torch.distributed). */
+ * everything local, nccl_id ignored.  world > 1 with nccl_id != NULL: rank r owns
+ * rows [row_begin, row_end) of A and X^ (the ranks' ranges must tile [0, n) in
+ * rank order; rank 0 must own rows 0..k-1); nccl_id is the 128-byte
+ * ncclUniqueId produced by refine_nccl_id() on rank 0 and broadcast by the
+ * caller (e.g. torch.distributed); the caller has selected the rank's device.
+ * Per sweep the ranks exchange X (dense: every block to every rank; CSR: only
+ * the halo rows the local rows reference) and gather small per-rank partials
+ * (2k, 2k^2 + k and k doubles) and one broadcast of k^2 + k + 9 doubles from
+ * rank 0; every cross-rank sum is taken in rank order, so the k x k state is
+ * bit-identical on all ranks.
+ * world > 1 with nccl_id == NULL: LOOPBACK emulation for tests -- one process,
+ * one device, the FULL problem is passed (row_begin = 0, row_end = n) and split
+ * into `world` row blocks that run the multi-rank code path with device copies
+ * in place of NCCL. */
 typedef struct {
   int32_t rank;
   int32_t world;
@@ -100,9 +110,10 @@ refine_status refine_init_dense(refine_ctx** out, int64_t n, int32_t k,
                                 const refine_comm* comm, const refine_opts* opts, void* stream);
 
 /* CSR symmetric A (both triangles stored), device pointers: row_ptr has
- * (row_end - row_begin + 1) int32 entries relative to val/col_idx (row_ptr[0]
- * may be nonzero), col_idx are GLOBAL int32 column indices sorted ascending
- * within each row, val FP64.  Borrowed like the dense A.  Within a row the
+ * (row_end - row_begin + 1) int32 entries that index col_idx / val directly
+ * (absolute offsets; row_ptr[0] may be nonzero, e.g. a row slice of a global
+ * CSR), col_idx are GLOBAL int32 column indices sorted ascending within each
+ * row, val FP64.  Borrowed like the dense A.  Within a row the
  * product is an fma chain in ascending CSR order (bit-reproducible). */
 refine_status refine_init_csr(refine_ctx** out, int64_t n, int32_t k,
                               const int32_t* row_ptr, const int32_t* col_idx, const double* val,
@@ -148,8 +159,20 @@ const char* refine_kernel_name(const refine_ctx* c, int32_t i);
 void refine_destroy(refine_ctx* c);
 const char* refine_status_string(refine_status s);
 
-/* 128-byte ncclUniqueId for world > 1 (call on rank 0, broadcast to all ranks). */
+/* 128-byte ncclUniqueId for world > 1 (call on rank 0, broadcast to all ranks).
+ * NCCL is resolved at run time (dlopen); REFINE_E_NCCL if it is unavailable. */
 refine_status refine_nccl_id(void* out128);
+
+/* Host-only: the CSR halo plan of `rank` (no GPU needed; the multi-rank init uses
+ * the same routine).  row_begin/row_end/col_lo/col_hi: every rank's rows and the
+ * smallest/largest column its rows reference (world entries each).  A rank
+ * receives the X rows [col_lo, row_begin) and [row_end, col_hi] it does not own,
+ * stored in its halo buffer in that order.  send/recv: up to cap segments of 4
+ * int64 {peer, first global row, row count, offset} (offset: local row for send,
+ * halo row for recv); *nsend, *nrecv: segment counts; *halo_rows: halo size. */
+int32_t refine_halo_plan(int32_t world, int32_t rank, const int64_t* row_begin, const int64_t* row_end,
+                         const int64_t* col_lo, const int64_t* col_hi, int64_t* send, int32_t* nsend,
+                         int64_t* recv, int32_t* nrecv, int64_t* halo_rows, int32_t cap);
 
 /* Test hook: copy an intermediate of the LAST sweep to device buffer dst
  * (synchronises).  what: 0 W = A X^ - shift X^ (n_loc x k, for the sweep's un-flipped input), 1 sigma (k), 2 U (k x k,

@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
         L.refine_profile_end.argtypes = [P, C.POINTER(C.c_double), C.POINTER(i32), C.POINTER(i32)]
         L.refine_kernel_name.argtypes = [P, i32]
         L.refine_kernel_name.restype = C.c_char_p
+        L.refine_halo_plan.argtypes = [i32, i32, P, P, P, P, P, C.POINTER(i32), P, C.POINTER(i32), C.POINTER(i64), i32]
+        L.refine_halo_plan.restype = i32
         for f in ("refine_init_dense", "refine_init_csr", "refine_sweep", "refine_sweep_host", "refine_run",
                   "refine_get_status", "refine_set_graph", "refine_nccl_id", "refine_debug_get",
                   "refine_profile_begin", "refine_profile_end"):
@@ -270,4 +272,19 @@ def refine_nccl_id() -> bytes:
 EXPORTED = ("refine_init_dense", "refine_init_csr", "refine_sweep", "refine_sweep_host", "refine_run",
             "refine_get_status", "refine_set_graph", "refine_kernels_per_sweep", "refine_destroy",
             "refine_status_string", "refine_nccl_id", "refine_debug_get", "refine_profile_begin",
-            "refine_profile_end", "refine_kernel_name")
+            "refine_profile_end", "refine_kernel_name", "refine_halo_plan")
+
+
+def refine_halo_plan(world: int, rank: int, row_begin, row_end, col_lo, col_hi, cap: int = 64):
+    """Host-only CSR halo plan of `rank` (see refine.h).  Returns (send, recv, halo_rows) with
+    send/recv lists of (peer, first_row, count, offset)."""
+    import numpy as np
+    arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.int64)) for a in (row_begin, row_end, col_lo, col_hi)]
+    send = np.zeros((cap, 4), dtype=np.int64)
+    recv = np.zeros((cap, 4), dtype=np.int64)
+    ns, nr, hr = C.c_int32(0), C.c_int32(0), C.c_int64(0)
+    s = lib().refine_halo_plan(int(world), int(rank), *[a.ctypes.data for a in arrs], send.ctypes.data, C.byref(ns),
+                               recv.ctypes.data, C.byref(nr), C.byref(hr), int(cap))
+    if s != REFINE_OK:
+        raise RefineError(s, "refine_halo_plan")
+    return [tuple(map(int, r)) for r in send[:ns.value]], [tuple(map(int, r)) for r in recv[:nr.value]], hr.value

@@ -81,6 +81,7 @@ struct Ws {
   double shift, delta, normA;
   int32_t beta_zero;
   double* W;         // n_loc x k
+  double* Xt;        // n_loc x k: X~ (written by kxk_finish / passC, read by normalize)
   double* Wpart;     // split-K partials (dense), S x n_loc x k
   double* ag;        // alpha/g double-double slots: n_ag x k x 4 {a_hi, a_lo, g_hi, g_lo}
   int32_t n_ag;
@@ -96,8 +97,24 @@ struct Ws {
   double *alpha, *d, *rd, *sigma, *U, *L, *Uinv, *T, *E11, *Csig, *scal, *ntop, *invn, *stats;
   double* scratch;   // 16 k x k scratch matrices for the k x k algebra
   int* status;
+  // row partition (world > 1; world == 1: row0 = 0, row1 = n_loc, halo = nullptr)
+  int32_t world, rank;
+  int32_t multi;          // 1: the multi-rank code path (gathered partials), even at world == 1 (NCCL test)
+  int64_t row0, row1;     // global rows [row0, row1) are local
+  double* halo;           // CSR: X rows [halo_lo, row0) then [row1, halo_hi) gathered from other ranks
+  int64_t halo_lo;
+  double *ag_send, *ag_all;    // alpha/g dd vectors: local (4k) / all ranks in rank order (world x 4k)
+  double* mg_all;              // [M2 | G2 | rr2] of all ranks (world x (2k^2 + k))
+  double *nrm_send, *nrm_all;  // column sums of x~^2: local (k) / all ranks (world x k)
   long long* tlog;   // optional clock64() phase log of the k x k kernels (REFINE_KXK_TIMING=1)
 };
+
+// X row of global index col: local rows first, else the halo (CSR row partition)
+RF_DEV const double* xrow(const Ws& ws, const double* Xloc, int64_t col, int k) {
+  if (ws.halo == nullptr || (col >= ws.row0 && col < ws.row1)) return Xloc + (col - ws.row0) * k;
+  const int64_t h = (col < ws.row0) ? col - ws.halo_lo : (ws.row0 - ws.halo_lo) + (col - ws.row1);
+  return ws.halo + h * k;
+}
 
 #define RF_TSTAMP(ws, i)                                                   \
   do {                                                                     \

@@ -157,18 +157,11 @@ __device__ void cta_trinv(int k, const double* S, bool upper, double* R, double*
   }
 }
 
-// ---------------------------------------------------------------- kxk_prep
-// Shared memory: Q (k x k, the in-place modified LU); for k <= 64 also Ls, Ts, Us (L, T, U^{-1}).
-__global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const double* __restrict__ Xtop) {
-  extern __shared__ __align__(16) double Q[];
-  __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
-  __shared__ int s_bad;
-  if (*ws.status != ST_OK) return;
-  RF_TSTAMP(ws, 0);
+// alpha/g slot reduction: P parts per column (contiguous slot ranges, 4 interleaved accumulators
+// each), then a fixed pairwise tree over the parts.  On return pa[j], pg[j] (j < k) hold the
+// column sums.  Called by the whole block.
+__device__ void reduce_ag_slots(const Ws& ws, dd* pa, dd* pg) {
   const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
-
-  // 1. alpha_j, g_j: P parts per column (contiguous slot ranges, 4 interleaved accumulators
-  //    each), then a fixed pairwise tree over the parts -- deterministic for a given launch shape
   const int P = nt / k;
   const int j = tid % k, p = tid / k;
   dd a = {0.0, 0.0}, g = {0.0, 0.0};
@@ -196,8 +189,6 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
   }
   pa[tid] = a;
   pg[tid] = g;
-  for (int e = tid; e < k * k; e += nt) Q[e] = Xtop[e];
-  if (tid == 0) s_bad = ST_OK;
   __syncthreads();
   for (int st = 1; st < P; st *= 2) {
     if (p < P && (p % (2 * st)) == 0 && p + st < P) {
@@ -205,6 +196,48 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
       dd_add(pg[tid], pg[tid + st * k]);
     }
     __syncthreads();
+  }
+}
+
+// world > 1: this rank's alpha/g double-double vector (4 doubles per column) for the all-gather
+__global__ void __launch_bounds__(KXK_THREADS) ag_local_kernel(Ws ws) {
+  __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
+  if (*ws.status != ST_OK) return;
+  reduce_ag_slots(ws, pa, pg);
+  if (threadIdx.x < ws.k) {
+    double* v = ws.ag_send + 4 * threadIdx.x;
+    v[0] = pa[threadIdx.x].hi; v[1] = pa[threadIdx.x].lo; v[2] = pg[threadIdx.x].hi; v[3] = pg[threadIdx.x].lo;
+  }
+}
+
+// ---------------------------------------------------------------- kxk_prep
+// Shared memory: Q (k x k, the in-place modified LU); for k <= 64 also Ls, Ts, Us (L, T, U^{-1}).
+__global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const double* __restrict__ Xtop) {
+  extern __shared__ __align__(16) double Q[];
+  __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
+  __shared__ int s_bad;
+  if (*ws.status != ST_OK) return;
+  RF_TSTAMP(ws, 0);
+  const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
+
+  // 1. alpha_j, g_j: this rank's slots, or (world > 1) the gathered per-rank
+  //    double-double vectors combined in rank order -- identical on every rank
+  for (int e = tid; e < k * k; e += nt) Q[e] = (ws.top > 0) ? Xtop[e] : 0.0;
+  if (tid == 0) s_bad = ST_OK;
+  if (ws.multi) {
+    if (tid < k) {
+      dd ta = {ws.ag_all[4 * tid], ws.ag_all[4 * tid + 1]}, tg = {ws.ag_all[4 * tid + 2], ws.ag_all[4 * tid + 3]};
+      for (int r = 1; r < ws.world; ++r) {
+        const double* v = ws.ag_all + (int64_t)r * 4 * k + 4 * tid;
+        dd_add(ta, dd{v[0], v[1]});
+        dd_add(tg, dd{v[2], v[3]});
+      }
+      pa[tid] = ta;
+      pg[tid] = tg;
+    }
+    __syncthreads();
+  } else {
+    reduce_ag_slots(ws, pa, pg);
   }
   if (tid < k) {
     const double al = dd_val(pa[tid]), gv = dd_val(pg[tid]);
@@ -219,6 +252,11 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
     if (bad != ST_OK) atomicCAS(&s_bad, ST_OK, bad);
   }
   RF_TSTAMP(ws, 1);
+  if (ws.top == 0) {                          // ranks without the top block only need alpha, d
+    __syncthreads();
+    if (tid == 0 && s_bad != ST_OK) *ws.status = s_bad;
+    return;
+  }
 
   // 2. Alg. 2 on the top block, literal arithmetic: sigma_j = -sign(q_jj) (sign(0)=+1),
   //    q_jj -= sigma_j, q_lj /= q_jj, q_lh -= q_lj q_jh.  One barrier per step: thread (l, h)
@@ -325,6 +363,15 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   const double* sig = ws.sigma;
   const double* d = ws.d;
   if (tid == 0) s_hits = 0;
+  if (ws.multi) {   // [M2 | G2 | rr2] of every rank, summed in rank order (M2, G2, rr2 are contiguous)
+    const int64_t cnt = 2 * kk + k;
+    for (int64_t e = tid; e < cnt; e += nt) {
+      double sum = ws.mg_all[e];
+      for (int r = 1; r < ws.world; ++r) sum += ws.mg_all[(int64_t)r * cnt + e];
+      ws.M2[e] = sum;
+    }
+    __syncthreads();
+  }
   for (int i = tid >> 5; i < k; i += 32)
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
@@ -373,7 +420,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   for (int l = tid >> 5; l < k; l += 32)
     for (int j = tid & 31; j < k; j += 32) {
     const int e = l * k + j;
-    Xtop[e] = Xp[e] + (ws.E11[e] - LB[e]);             // X~_1 = X'_1 + (E_11 - L B)
+    ws.Xt[e] = Xp[e] + (ws.E11[e] - LB[e]);            // X~_1 = X'_1 + (E_11 - L B)  (top rows of X~)
     ws.Csig[e] = sig[l] * (Pt[e] / d[j] + UB[e]);      // Csig = Sigma (P~ D^{-1} + U'^{-1} B)
   }
   __syncthreads();
@@ -382,7 +429,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     const int j = tid;
     double nt2 = 0.0, r1 = 0.0, e1 = 0.0, pm = 0.0, pgp = 0.0;
     for (int i = 0; i < k; ++i) {
-      const double x = Xtop[i * k + j];
+      const double x = ws.Xt[i * k + j];
       nt2 = fma(x, x, nt2);
       r1 = fma(R1[i * k + j], R1[i * k + j], r1);
       e1 = fma(ws.E11[i * k + j], ws.E11[i * k + j], e1);
@@ -428,6 +475,10 @@ __global__ void __launch_bounds__(128) norm_reduce_kernel(Ws ws) {
     for (int u = 0; u < 8; ++u) s += v[u];
   }
   for (; q < ws.n_nslot; ++q) s += ws.nslot[(int64_t)q * ws.kp + j];
+  if (ws.multi) {          // partial for the all-gather; normalize_kernel combines in rank order
+    ws.nrm_send[j] = s;
+    return;
+  }
   const double nrm = sqrt(s);
   ws.invn[j] = 1.0 / nrm;
   if (!isfinite(ws.invn[j]) || !(nrm > 0.0)) atomicCAS(ws.status, ST_OK, ST_DIVERGED);

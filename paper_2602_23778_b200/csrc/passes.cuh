@@ -7,9 +7,10 @@
 //   slots and are summed in chunk order by passB_reduce (deterministic).  Per row it reads
 //   x_i and w_i once (16 k bytes) for 2 k^2 FMAs.
 // pass C (S6 update): x~_i = (w_i Sigma D^{-1}) - x^_i Csig   (the lower block of
-//   X^ + H E_L, Alg. 4 line 7, via the identity in kxk.cuh), written in place, plus column
-//   sums of x~^2 for the normalisation.  Persistent CTAs keep Csig (k x k) in shared memory.
-// normalize (S7): x_ij *= 1/||x~_j||.
+//   X^ + H E_L, Alg. 4 line 7, via the identity in kxk.cuh), written to the X~ buffer (not in
+//   place: CTAs of other column blocks still read the x^_i rows), plus column sums of x~^2 for
+//   the normalisation.  Persistent CTAs keep a column block of Csig in shared memory.
+// normalize (S7): x_ij = x~_ij / ||x~_j||, X~ buffer -> X.
 #pragma once
 #include "common.cuh"
 
@@ -347,12 +348,12 @@ passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
         const double x0 = __fma_rn(w[i][j][0], ssc[cl], -acc[i][j][0]);
         const double x1 = __fma_rn(w[i][j][1], ssc[cl + 1], -acc[i][j][1]);
         if (vec16 && c < k) {
-          *reinterpret_cast<double2*>(X + g * k + c) = make_double2(x0, x1);
+          *reinterpret_cast<double2*>(ws.Xt + g * k + c) = make_double2(x0, x1);
           nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]);
           nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]);
         } else {
-          if (c < k) { X[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
-          if (c + 1 < k) { X[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
+          if (c < k) { ws.Xt[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
+          if (c + 1 < k) { ws.Xt[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
         }
       }
     }
@@ -375,22 +376,43 @@ passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
 // x_ij *= 1/||x~_j||.  The thread count is a multiple of k/2 on the vector path, so every
 // thread always scales the same column pair (no per-element index arithmetic).
 __global__ void __launch_bounds__(256) normalize_kernel(Ws ws, double* __restrict__ X) {
+  __shared__ double sinv[KMAX];
+  __shared__ int sbad;
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
+  if (ws.multi) {         // combine the gathered per-rank column sums in rank order
+    if (threadIdx.x == 0) sbad = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      double sum = ws.nrm_all[j];
+      for (int r = 1; r < ws.world; ++r) sum += ws.nrm_all[(int64_t)r * k + j];
+      const double nrm = sqrt(sum);
+      sinv[j] = 1.0 / nrm;
+      if (!isfinite(sinv[j]) || !(nrm > 0.0)) sbad = 1;
+      if (blockIdx.x == 0) ws.invn[j] = sinv[j];
+    }
+    __syncthreads();
+    if (sbad) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(ws.status, ST_OK, ST_DIVERGED);
+      return;
+    }
+  }
+  const double* invn = ws.multi ? sinv : ws.invn;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
   if ((k & 1) == 0 && (256 % (k / 2)) == 0) {
     const int64_t total2 = ws.n_loc * (k / 2);
     const int j = (int)(tid % (k / 2)) * 2;
-    const double s0 = ws.invn[j], s1 = ws.invn[j + 1];
+    const double s0 = invn[j], s1 = invn[j + 1];
     double2* X2 = reinterpret_cast<double2*>(X);
+    const double2* T2 = reinterpret_cast<const double2*>(ws.Xt);
     for (int64_t e = tid; e < total2; e += nthr) {
-      double2 v = X2[e];
+      double2 v = T2[e];
       v.x *= s0; v.y *= s1;
       X2[e] = v;
     }
   } else {
     const int64_t total = ws.n_loc * k;
-    for (int64_t e = tid; e < total; e += nthr) X[e] *= ws.invn[e % k];
+    for (int64_t e = tid; e < total; e += nthr) X[e] = ws.Xt[e] * invn[e % k];
   }
 }
 

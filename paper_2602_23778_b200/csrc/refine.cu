@@ -5,9 +5,20 @@
 //   kxk_prep -> passB -> passB_reduce -> kxk_finish -> passC -> norm_reduce -> normalize
 // Device-side conditions are carried by a status word every kernel checks first, so a
 // failed or halted sweep leaves X untouched and refine_run needs no per-sweep host sync.
+//
+// Row partition (world > 1): rank r owns rows [rb_r, re_r), rank 0 the
+// top k x k block.  Per sweep: X exchange (dense: all-gather of X; CSR: halo rows) -> S1 ->
+// all-gather of the alpha/g double-double vectors -> kxk_prep (identical d on every rank; LU on
+// rank 0) -> passB -> all-gather of [M2 | G2 | rr2] -> kxk_finish on rank 0 -> broadcast of
+// [Csig | scal | stats | status] -> passC -> all-gather of the column norm partials ->
+// normalize.  Every cross-rank sum is formed from gathered per-rank values in rank order, so
+// all ranks hold bit-identical k x k state.  Collectives are NCCL (one process per GPU) or, for
+// tests on one device, device copies between emulated ranks ("loopback": world > 1 with
+// nccl_id == NULL).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +31,7 @@
 #include "kxk.cuh"
 #include "passes.cuh"
 #include "spmm_csr.cuh"
+#include "nccl_dl.h"
 
 using namespace rf;
 
@@ -69,7 +81,7 @@ __global__ void absrow_max_csr_kernel(const int32_t* rp, const int32_t* ci, cons
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_loc; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     bool diag = false;
-    for (int32_t p = rp[i] - rp[0]; p < rp[i + 1] - rp[0]; ++p) {
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
       double a = v[p];
       if (ci[p] == row0 + i) { a -= shift; diag = true; }
       s += fabs(a);
@@ -89,6 +101,18 @@ __global__ void max_kernel(const double* x, int64_t n, double* out) {
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = s[0];
+}
+
+__global__ void col_range_kernel(const int32_t* rp, const int32_t* ci, int64_t n_loc, unsigned long long* out) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  const int64_t p0 = rp[0], p1 = rp[n_loc];
+  for (int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long c = (unsigned long long)ci[p];
+    lo = c < lo ? c : lo;
+    hi = c > hi ? c : hi;
+  }
+  atomicMin(out, lo);
+  atomicMax(out + 1, hi);
 }
 
 int pad_kp(int k) {
@@ -135,6 +159,19 @@ struct refine_ctx {
   // live per-kernel timing (refine_profile_begin/end): events at every kernel boundary
   cudaEvent_t* prof_ev = nullptr;
   int prof_cap = 0, prof_used = 0, prof_per_sweep = 0, prof_sweeps = 0, prof_max_sweeps = 0;
+  // row partition
+  bool loopback = false;                      // parent of `world` emulated ranks on one device
+  bool loopback_kid = false;                  // one emulated rank (its X rows alias the parent's X)
+  bool multi = false;                         // multi-rank code path (world > 1, or NCCL forced at world 1)
+  std::vector<refine_ctx*> kids;
+  ncclComm_t comm = nullptr;
+  std::vector<int64_t> rb_all, re_all;        // every rank's rows
+  double* Xfull = nullptr;                    // dense world > 1: gathered X (n x k)
+  bool own_xfull = false;
+  struct Seg { int peer; int64_t row, cnt, off; };   // rows [row, row + cnt); off = local / halo row
+  std::vector<Seg> hsend, hrecv;
+  double* bc = nullptr;                       // [Csig | scal | stats(8) | status] broadcast from rank 0
+  size_t bc_cnt = 0;
   void mark() {
     if (prof_ev && prof_used < prof_cap) cudaEventRecord(prof_ev[prof_used++], stream);
   }
@@ -224,63 +261,92 @@ struct Kern {
     nslot = (size_t)c->passc_grid * KP;
   }
 
-  static int enqueue(refine_ctx* c, double* X) {
+  // phase ph of one sweep on this rank (see the file header); returns kernels launched
+  static int phase(refine_ctx* c, int ph, double* X) {
     Ws& ws = c->ws;
     cudaStream_t s = c->stream;
     int n = 0;
     const bool xv16 = (c->k % 2 == 0) && ((uintptr_t)X % 16 == 0);
-    if (!c->csr) {
-      const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
-      double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
-      c->mark();
-      gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
-          c->A, c->lda, X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, xv16, ws.status);
-      c->mark();
-      w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(ws, X, c->nsplit, c->n_loc * c->k);
-      n += 2;
-    } else {
-      c->mark();
-      const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2;
-      auto* Xg = X;
-      if (vec) {
-        switch (c->k) {
-          case 2: spmm_csr_vec_kernel<1, 1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 4: spmm_csr_vec_kernel<1, 2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 8: spmm_csr_vec_kernel<1, 4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 16: spmm_csr_vec_kernel<1, 8><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 32: spmm_csr_vec_kernel<1, 16><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 64: spmm_csr_vec_kernel<1, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          default: spmm_csr_vec_kernel<2, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+    switch (ph) {
+      case 0:  // S1 (+ S2 partials)
+        if (!c->csr) {
+          const double* Xb = c->multi ? c->Xfull : X;            // B operand: all n rows of X
+          const bool bv16 = xv16 && ((uintptr_t)Xb % 16 == 0);
+          const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
+          double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
+          c->mark();
+          gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
+              c->A, c->lda, Xb, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
+          c->mark();
+          w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(ws, X, c->nsplit, c->n_loc * c->k);
+          n += 2;
+        } else {
+          c->mark();
+          const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2 &&
+                           (ws.halo == nullptr || (uintptr_t)ws.halo % 16 == 0);
+          if (vec) {
+            switch (c->k) {
+              case 2: spmm_csr_vec_kernel<1, 1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 4: spmm_csr_vec_kernel<1, 2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 8: spmm_csr_vec_kernel<1, 4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 16: spmm_csr_vec_kernel<1, 8><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 32: spmm_csr_vec_kernel<1, 16><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 64: spmm_csr_vec_kernel<1, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              default: spmm_csr_vec_kernel<2, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+            }
+          } else {
+            switch ((c->k + 31) / 32) {
+              case 1: spmm_csr_kernel<1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 2: spmm_csr_kernel<2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              case 3: spmm_csr_kernel<3><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+              default: spmm_csr_kernel<4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+            }
+          }
+          n += 1;
         }
-      } else {
-        switch ((c->k + 31) / 32) {
-          case 1: spmm_csr_kernel<1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 2: spmm_csr_kernel<2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          case 3: spmm_csr_kernel<3><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
-          default: spmm_csr_kernel<4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xg, X); break;
+        if (c->multi) {
+          ag_local_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
+          ++n;
         }
-      }
-      n += 1;
+        break;
+      case 1:  // S2 + S3
+        c->mark();
+        kxk_prep_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8, s>>>(ws, X);
+        n += 1;
+        break;
+      case 2:  // S4 reductions
+        c->mark();
+        passB<<<dim3(BC::NTILES, c->passb_grid_y), BC::THREADS, BC::SMEM, s>>>(ws, X, xv16);
+        c->mark();
+        passBred<<<(2 * c->k * c->k + c->k + 31) / 32, 256, 0, s>>>(ws, c->passb_grid_y);
+        n += 2;
+        break;
+      case 3:  // k x k algebra (rank 0)
+        c->mark();
+        if (c->rank == 0) {
+          kxk_finish_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
+          n += 1;
+        }
+        break;
+      case 4:  // S6
+        c->mark();
+        passC<<<dim3(c->passc_grid, KP / CNC), CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
+        c->mark();
+        norm_reduce_kernel<<<1, 128, 0, s>>>(ws);
+        n += 2;
+        break;
+      case 5:  // S7
+        if (c->opts.normalize) {
+          c->mark();
+          normalize_kernel<<<c->sms * 8, 256, 0, s>>>(ws, X);
+          ++n;
+        } else {
+          cudaMemcpyAsync(X, ws.Xt, (size_t)c->n_loc * c->k * sizeof(double), cudaMemcpyDeviceToDevice, s);
+        }
+        c->mark();
+        break;
     }
-    c->mark();
-    kxk_prep_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8, s>>>(ws, X);
-    c->mark();
-    passB<<<dim3(BC::NTILES, c->passb_grid_y), BC::THREADS, BC::SMEM, s>>>(ws, X, xv16);
-    c->mark();
-    passBred<<<(2 * c->k * c->k + c->k + 31) / 32, 256, 0, s>>>(ws, c->passb_grid_y);
-    c->mark();
-    kxk_finish_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
-    c->mark();
-    passC<<<dim3(c->passc_grid, KP / CNC), CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
-    c->mark();
-    norm_reduce_kernel<<<1, 128, 0, s>>>(ws);
-    if (c->opts.normalize) {
-      c->mark();
-      normalize_kernel<<<c->sms * 8, 256, 0, s>>>(ws, X);
-      ++n;
-    }
-    c->mark();
-    return n + 6;
+    return n;
   }
 };
 
@@ -296,13 +362,17 @@ static auto dispatch(int kp, F&& f) {
 }
 
 // ---------------------------------------------------------------- init
-static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t row_begin, int64_t row_end,
-                                 double shift, const refine_comm* comm, const refine_opts* opts, void* stream) {
+static refine_ctx* ctx0(refine_ctx* c) { return c->loopback ? c->kids[0] : c; }
+
+// Per-rank setup: launch geometry, workspace pool, local ||A - shift I||_inf row maxima and (CSR)
+// the range of referenced columns.  Cross-rank quantities are settled by finalize_partition.
+static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_begin, int64_t row_end,
+                               double shift, int rank, int world, const refine_opts* opts, void* stream,
+                               double* local_norm, int64_t* col_lo, int64_t* col_hi) {
   if (k < 1 || (int64_t)k >= n || row_begin < 0 || row_end > n || row_end <= row_begin) return REFINE_E_INVALID;
   if (k > KMAX) return REFINE_E_UNSUPPORTED;
-  c->rank = comm ? comm->rank : 0;
-  c->world = comm ? comm->world : 1;
-  if (c->world != 1) return REFINE_E_UNSUPPORTED;      // multi-GPU row partition: see DESIGN.md
+  c->rank = rank;
+  c->world = world;
   if (c->rank == 0 && (row_begin != 0 || row_end - row_begin < k)) return REFINE_E_INVALID;
   c->n = n; c->k = k; c->kp = pad_kp(k);
   c->row_begin = row_begin; c->row_end = row_end; c->n_loc = row_end - row_begin;
@@ -317,7 +387,10 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   ws.top = (c->rank == 0) ? k : 0;
   ws.shift = shift;
   ws.beta_zero = c->opts.beta_zero;
-  refine_status st = REFINE_OK;
+  ws.world = world; ws.rank = rank;
+  ws.multi = c->multi ? 1 : 0;
+  ws.row0 = row_begin; ws.row1 = row_end;
+  ws.halo = nullptr; ws.halo_lo = row_begin;
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
   RF_CK(c, cudaFuncSetAttribute(kxk_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
   RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
@@ -327,44 +400,190 @@ static refine_status init_common(refine_ctx* c, int64_t n, int32_t k, int64_t ro
   c->w_fin_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 4, c->n_loc / 2));
   c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 8, (c->n_loc + 7) / 8));
   c->n_ag = c->csr ? c->spmm_grid : c->w_fin_grid;
-  const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k;
+  const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k, P = (size_t)world;
   const size_t wpart = (!c->csr && c->nsplit > 1) ? (size_t)c->nsplit * nk : 0;
+  c->bc_cnt = kk + k + 8 + 1;
   size_t off = 0;
   auto take = [&](size_t cnt) { size_t o = off; off += (cnt + 31) & ~size_t(31); return o; };
-  const size_t oW = take(nk), oWp = take(wpart), oAg = take((size_t)c->n_ag * k * 4), oBp = take(bpart),
-               oBrr = take(brr), oM2 = take(kk), oG2 = take(kk), oRr = take(k), oNs = take(nslot),
+  const size_t oW = take(nk), oXt = take(nk), oWp = take(wpart), oAg = take((size_t)c->n_ag * k * 4), oBp = take(bpart),
+               oBrr = take(brr), oMg = take(2 * kk + k), oNs = take(nslot),
                oAl = take(k), oD = take(k), oRd = take(k), oSg = take(k), oU = take(kk), oL = take(kk),
-               oT = take(kk), oUi = take(kk), oE = take(kk), oCs = take(kk), oSc = take(k), oNt = take(k), oIn = take(k),
-               oSt = take(8), oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8);
+               oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
+               oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8),
+               oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
+               oNrS = take(k), oNrA = take(P * k), oCol = take(2);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
   c->pool_bytes = bytes;
   RF_CK(c, cudaMemsetAsync(c->pool, 0, bytes, c->stream));
   double* b = (double*)c->pool;
-  ws.W = b + oW; ws.Wpart = wpart ? b + oWp : nullptr; ws.ag = b + oAg; ws.n_ag = c->n_ag;
+  ws.W = b + oW; ws.Xt = b + oXt; ws.Wpart = wpart ? b + oWp : nullptr; ws.ag = b + oAg; ws.n_ag = c->n_ag;
   ws.bpart = b + oBp; ws.brr = b + oBrr; ws.n_chunk = c->passb_grid_y;
-  ws.M2 = b + oM2; ws.G2 = b + oG2; ws.rr2 = b + oRr; ws.nslot = b + oNs; ws.n_nslot = c->passc_grid;
+  ws.M2 = b + oMg; ws.G2 = ws.M2 + kk; ws.rr2 = ws.M2 + 2 * kk;        // contiguous [M2 | G2 | rr2]
+  ws.nslot = b + oNs; ws.n_nslot = c->passc_grid;
   ws.alpha = b + oAl; ws.d = b + oD; ws.rd = b + oRd; ws.sigma = b + oSg; ws.U = b + oU; ws.L = b + oL;
-  ws.T = b + oT; ws.Uinv = b + oUi; ws.E11 = b + oE; ws.Csig = b + oCs; ws.scal = b + oSc; ws.ntop = b + oNt; ws.invn = b + oIn;
-  ws.stats = b + oSt; ws.scratch = b + oScr;
+  ws.T = b + oT; ws.Uinv = b + oUi; ws.E11 = b + oE; ws.ntop = b + oNt; ws.invn = b + oIn;
+  c->bc = b + oBc;                                                   // [Csig | scal | stats(8) | status]
+  ws.Csig = c->bc; ws.scal = c->bc + kk; ws.stats = c->bc + kk + k;
+  ws.status = reinterpret_cast<int*>(c->bc + kk + k + 8);
+  ws.scratch = b + oScr;
+  ws.ag_send = b + oAgS; ws.ag_all = b + oAgA; ws.mg_all = c->multi ? b + oMgA : nullptr;
+  ws.nrm_send = b + oNrS; ws.nrm_all = b + oNrA;
   c->run = reinterpret_cast<RunState*>(b + oRun);
-  ws.status = reinterpret_cast<int*>(b + off);     // after all arrays (64 spare bytes)
   ws.tlog = nullptr;
   if (getenv("REFINE_KXK_TIMING")) RF_CK(c, cudaMalloc(&ws.tlog, 64 * sizeof(long long)));
-  // ||A - shift I||_inf (one pass over A) -> delta = c ||A|| u
+  // local rows of ||A - shift I||_inf (one pass over A) -> delta = c ||A|| u
   double* rows = b + oRows;
   if (!c->csr)
     absrow_max_dense_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->A, c->lda, c->n_loc, c->n, c->row_begin, shift, rows);
   else
     absrow_max_csr_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, c->n_loc, c->row_begin, shift, rows);
   max_kernel<<<1, 1024, 0, c->stream>>>(rows, c->n_loc, ws.stats + 7);
+  unsigned long long* colr = reinterpret_cast<unsigned long long*>(b + oCol);
+  if (c->csr && c->multi) {
+    const unsigned long long init[2] = {~0ull, 0ull};
+    RF_CK(c, cudaMemcpyAsync(colr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    col_range_kernel<<<c->sms * 4, 256, 0, c->stream>>>(c->rp, c->ci, c->n_loc, colr);
+  }
   RF_CK(c, cudaGetLastError());
-  double normA = 0.0;
-  RF_CK(c, cudaMemcpyAsync(&normA, ws.stats + 7, 8, cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long cr[2] = {0, 0};
+  RF_CK(c, cudaMemcpyAsync(local_norm, ws.stats + 7, 8, cudaMemcpyDeviceToHost, c->stream));
+  if (c->csr && c->multi) RF_CK(c, cudaMemcpyAsync(cr, colr, sizeof(cr), cudaMemcpyDeviceToHost, c->stream));
   RF_CK(c, cudaStreamSynchronize(c->stream));
-  ws.normA = normA;
-  ws.delta = c->opts.delta_c * normA * std::ldexp(1.0, -53);
-  return st;
+  *col_lo = (c->csr && c->multi) ? (int64_t)cr[0] : row_begin;
+  *col_hi = (c->csr && c->multi) ? (int64_t)cr[1] : row_end - 1;
+  if (*col_lo > row_begin) *col_lo = row_begin;
+  if (*col_hi < row_end - 1) *col_hi = row_end - 1;
+  return REFINE_OK;
+}
+
+// Halo plan of `rank` (see refine.h, refine_halo_plan): which X rows it receives from / sends to
+// each other rank, with halo offsets (rows [lo, rb) first, then [re, hi]) and local offsets.
+static void halo_plan(int world, int rank, const int64_t* rb, const int64_t* re, const int64_t* lo,
+                      const int64_t* hi, std::vector<refine_ctx::Seg>& send, std::vector<refine_ctx::Seg>& recv,
+                      int64_t* hrows) {
+  send.clear();
+  recv.clear();
+  auto needs = [&](int r, int64_t out[4]) {
+    out[0] = lo[r]; out[1] = rb[r];                       // [lo, rb)
+    out[2] = re[r]; out[3] = hi[r] + 1;                   // [re, hi]
+  };
+  auto hidx = [&](int64_t g) { return g < rb[rank] ? g - lo[rank] : (rb[rank] - lo[rank]) + (g - re[rank]); };
+  int64_t me[4];
+  needs(rank, me);
+  for (int s = 0; s < world; ++s) {
+    if (s == rank) continue;
+    for (int h = 0; h < 2; ++h) {                         // what I receive from s
+      const int64_t a = std::max(me[2 * h], rb[s]), e = std::min(me[2 * h + 1], re[s]);
+      if (e > a) recv.push_back({s, a, e - a, hidx(a)});
+    }
+    int64_t ns[4];
+    needs(s, ns);
+    for (int h = 0; h < 2; ++h) {                         // what s receives from me
+      const int64_t a = std::max(ns[2 * h], rb[rank]), e = std::min(ns[2 * h + 1], re[rank]);
+      if (e > a) send.push_back({s, a, e - a, a - rb[rank]});
+    }
+  }
+  *hrows = std::max<int64_t>(rb[rank] - lo[rank], 0) + std::max<int64_t>(hi[rank] + 1 - re[rank], 0);
+}
+
+// Settle the cross-rank state of rank context c given every rank's rows, row maxima and column range.
+static refine_status finalize_rank(refine_ctx* c, const std::vector<int64_t>& rb, const std::vector<int64_t>& re,
+                                   const std::vector<double>& nrm, const std::vector<int64_t>& lo,
+                                   const std::vector<int64_t>& hi) {
+  const int P = c->world;
+  if (rb[0] != 0 || re[P - 1] != c->n) return REFINE_E_INVALID;
+  for (int r = 0; r + 1 < P; ++r)
+    if (re[r] != rb[r + 1]) return REFINE_E_INVALID;       // ranks must tile [0, n) in rank order
+  c->rb_all = rb;
+  c->re_all = re;
+  double normA = 0.0;
+  for (double v : nrm) normA = std::max(normA, v);
+  c->ws.normA = normA;
+  c->ws.delta = c->opts.delta_c * normA * std::ldexp(1.0, -53);
+  if (c->multi && c->csr) {
+    int64_t hrows = 0;
+    halo_plan(P, c->rank, rb.data(), re.data(), lo.data(), hi.data(), c->hsend, c->hrecv, &hrows);
+    RF_CK(c, cudaMalloc(&c->ws.halo, std::max<int64_t>(hrows, 1) * c->k * sizeof(double)));
+    c->ws.halo_lo = std::min(lo[c->rank], rb[c->rank]);
+  }
+  if (c->multi && !c->csr && !c->loopback_kid) {
+    RF_CK(c, cudaMalloc(&c->Xfull, (size_t)c->n * c->k * sizeof(double)));
+    c->own_xfull = true;
+  }
+  return REFINE_OK;
+}
+
+template <typename MakeRank>
+static refine_status init_any(refine_ctx* c, int64_t n, int32_t k, int64_t row_begin, int64_t row_end, double shift,
+                              const refine_comm* comm, const refine_opts* opts, void* stream, MakeRank make_rank) {
+  const int world = comm ? comm->world : 1;
+  const int rank = comm ? comm->rank : 0;
+  if (world < 1 || rank < 0 || rank >= world) return REFINE_E_INVALID;
+  if (world > 1 && comm->nccl_id == nullptr) {
+    // loopback: `world` emulated ranks on this device, equal row blocks (rank 0 gets the rest)
+    if (row_begin != 0 || row_end != n) return REFINE_E_INVALID;
+    c->loopback = true;
+    c->world = world;
+    c->n = n; c->k = k; c->n_loc = n; c->row_begin = 0; c->row_end = n;
+    c->stream = (cudaStream_t)stream;
+    c->opts = refine_opts{10.0, 0, 1, 3, 10.0};
+    if (opts) c->opts = *opts;
+    std::vector<int64_t> rb(world), re(world), lo(world), hi(world);
+    std::vector<double> nrm(world);
+    const int64_t blk = n / world;
+    for (int r = 0; r < world; ++r) { rb[r] = r == 0 ? 0 : (n - blk * (world - r)); re[r] = n - blk * (world - r - 1); }
+    c->multi = true;
+    for (int r = 0; r < world; ++r) {
+      refine_ctx* kid = new (std::nothrow) refine_ctx();
+      if (!kid) return REFINE_E_NOMEM;
+      c->kids.push_back(kid);
+      kid->loopback_kid = true;
+      kid->multi = true;
+      make_rank(kid, rb[r]);
+      refine_status st = init_rank(kid, n, k, rb[r], re[r], shift, r, world, opts, stream, &nrm[r], &lo[r], &hi[r]);
+      if (st != REFINE_OK) return st;
+    }
+    for (auto* kid : c->kids) {
+      refine_status st = finalize_rank(kid, rb, re, nrm, lo, hi);
+      if (st != REFINE_OK) return st;
+    }
+    c->csr = c->kids[0]->csr;
+    c->kp = c->kids[0]->kp;
+    return REFINE_OK;
+  }
+  make_rank(c, row_begin);
+  // NCCL path for world > 1; REFINE_FORCE_NCCL=1 also takes it at world == 1 (tests of the NCCL calls)
+  c->multi = world > 1 || (comm && comm->nccl_id && getenv("REFINE_FORCE_NCCL"));
+  double nrm = 0.0;
+  int64_t lo = 0, hi = 0;
+  refine_status st = init_rank(c, n, k, row_begin, row_end, shift, rank, world, opts, stream, &nrm, &lo, &hi);
+  if (st != REFINE_OK) return st;
+  if (!c->multi) {
+    return finalize_rank(c, {row_begin}, {row_end}, {nrm}, {lo}, {hi});
+  }
+  // NCCL: one process per GPU; gather every rank's (rb, re, ||.||_inf rows, lo, hi)
+  Nccl& N = nccl();
+  if (!N.ok) return REFINE_E_NCCL;
+  ncclUniqueId id;
+  memcpy(&id, comm->nccl_id, sizeof(id));
+  if (N.CommInitRank(&c->comm, world, id, rank) != ncclSuccess) return REFINE_E_NCCL;
+  double* dv = nullptr;
+  RF_CK(c, cudaMalloc(&dv, sizeof(double) * 5 * (world + 1)));
+  const double mine[5] = {(double)row_begin, (double)row_end, nrm, (double)lo, (double)hi};
+  RF_CK(c, cudaMemcpyAsync(dv, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+  if (N.AllGather(dv, dv + 5, 5, ncclDouble, c->comm, c->stream) != ncclSuccess) { cudaFree(dv); return REFINE_E_NCCL; }
+  std::vector<double> all(5 * world);
+  RF_CK(c, cudaMemcpyAsync(all.data(), dv + 5, sizeof(double) * 5 * world, cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(dv);
+  std::vector<int64_t> rb(world), re(world), lov(world), hiv(world);
+  std::vector<double> nv(world);
+  for (int r = 0; r < world; ++r) {
+    rb[r] = (int64_t)all[5 * r]; re[r] = (int64_t)all[5 * r + 1]; nv[r] = all[5 * r + 2];
+    lov[r] = (int64_t)all[5 * r + 3]; hiv[r] = (int64_t)all[5 * r + 4];
+  }
+  return finalize_rank(c, rb, re, nv, lov, hiv);
 }
 
 extern "C" refine_status refine_init_dense(refine_ctx** out, int64_t n, int32_t k, const double* A_rows, int64_t lda,
@@ -375,8 +594,12 @@ extern "C" refine_status refine_init_dense(refine_ctx** out, int64_t n, int32_t 
   if (!A_rows || lda < n) return REFINE_E_INVALID;
   refine_ctx* c = new (std::nothrow) refine_ctx();
   if (!c) return REFINE_E_NOMEM;
-  c->csr = false; c->A = A_rows; c->lda = lda;
-  refine_status st = init_common(c, n, k, row_begin, row_end, shift, comm, opts, stream);
+  c->csr = false;
+  refine_status st = init_any(c, n, k, row_begin, row_end, shift, comm, opts, stream, [&](refine_ctx* r, int64_t rb) {
+    r->csr = false;
+    r->lda = lda;
+    r->A = (r == c || !c->loopback) ? A_rows : A_rows + rb * lda;   // loopback: rank r's row block
+  });
   if (st != REFINE_OK) { refine_destroy(c); return st; }
   *out = c;
   return REFINE_OK;
@@ -391,19 +614,133 @@ extern "C" refine_status refine_init_csr(refine_ctx** out, int64_t n, int32_t k,
   if (!row_ptr || !col_idx || !val) return REFINE_E_INVALID;
   refine_ctx* c = new (std::nothrow) refine_ctx();
   if (!c) return REFINE_E_NOMEM;
-  c->csr = true; c->rp = row_ptr; c->ci = col_idx; c->val = val;
-  refine_status st = init_common(c, n, k, row_begin, row_end, shift, comm, opts, stream);
+  c->csr = true;
+  refine_status st = init_any(c, n, k, row_begin, row_end, shift, comm, opts, stream, [&](refine_ctx* r, int64_t rb) {
+    r->csr = true;
+    r->rp = (r == c || !c->loopback) ? row_ptr : row_ptr + rb;          // loopback: rank r's rows
+    r->ci = col_idx;
+    r->val = val;
+  });
   if (st != REFINE_OK) { refine_destroy(c); return st; }
   *out = c;
   return REFINE_OK;
 }
 
 // ---------------------------------------------------------------- sweeps
-static refine_status enqueue_sweep(refine_ctx* c, double* X) {
-  RF_CK(c, cudaMemsetAsync(c->ws.status, 0, sizeof(int), c->stream));
-  c->launches = dispatch(c->kp, [&](auto K) { return decltype(K)::enqueue(c, X); });
+enum { C_X = 0, C_AG, C_MG, C_BC, C_NRM };
+
+static refine_status nccl_fail(refine_ctx* c, int r, const char* what) {
+  Nccl& N = nccl();
+  fprintf(stderr, "[refine] NCCL error in %s: %s\n", what, N.GetErrorString ? N.GetErrorString((ncclResult_t)r) : "?");
+  c->sticky = REFINE_E_NCCL;
+  return REFINE_E_NCCL;
+}
+#define RF_NC(c, expr)                                       \
+  do {                                                       \
+    int r_ = (int)(expr);                                    \
+    if (r_ != 0) return nccl_fail((c), r_, #expr);           \
+  } while (0)
+
+// The cross-rank step `which` of one sweep.  c is the rank context (NCCL) or the loopback parent.
+static refine_status collective(refine_ctx* c, int which, double* X) {
+  const int64_t k = c->k;
+  const cudaMemcpyKind D2D = cudaMemcpyDeviceToDevice;
+  if (c->loopback) {
+    auto& K = c->kids;
+    const int P = (int)K.size();
+    cudaStream_t s = c->stream;
+    switch (which) {
+      case C_X:
+        for (auto* kid : K) {
+          if (!kid->csr) { kid->Xfull = X; continue; }             // X already holds all n rows
+          for (auto& g : kid->hrecv)
+            RF_CK(c, cudaMemcpyAsync(kid->ws.halo + g.off * k, X + g.row * k, g.cnt * k * 8, D2D, s));
+        }
+        break;
+      case C_AG:
+        for (auto* kid : K)
+          for (int r = 0; r < P; ++r)
+            RF_CK(c, cudaMemcpyAsync(kid->ws.ag_all + r * 4 * k, K[r]->ws.ag_send, 4 * k * 8, D2D, s));
+        break;
+      case C_MG: {
+        const int64_t cnt = 2 * k * k + k;
+        for (int r = 0; r < P; ++r)
+          RF_CK(c, cudaMemcpyAsync(K[0]->ws.mg_all + r * cnt, K[r]->ws.M2, cnt * 8, D2D, s));
+        break;
+      }
+      case C_BC:
+        for (int r = 1; r < P; ++r) RF_CK(c, cudaMemcpyAsync(K[r]->bc, K[0]->bc, K[0]->bc_cnt * 8, D2D, s));
+        break;
+      case C_NRM:
+        for (auto* kid : K)
+          for (int r = 0; r < P; ++r)
+            RF_CK(c, cudaMemcpyAsync(kid->ws.nrm_all + r * k, K[r]->ws.nrm_send, k * 8, D2D, s));
+        break;
+    }
+    return REFINE_OK;
+  }
+  Nccl& N = nccl();
+  cudaStream_t s = c->stream;
+  switch (which) {
+    case C_X:
+      RF_NC(c, N.GroupStart());
+      if (!c->csr) {              // dense: every rank's block of X into the full copy
+        for (int r = 0; r < c->world; ++r) {
+          double* dst = c->Xfull + c->rb_all[r] * k;
+          RF_NC(c, N.Broadcast(r == c->rank ? X : dst, dst, (c->re_all[r] - c->rb_all[r]) * k, ncclDouble, r,
+                               c->comm, s));
+        }
+      } else {                    // CSR: halo rows only
+        for (auto& g : c->hsend) RF_NC(c, N.Send(X + g.off * k, g.cnt * k, ncclDouble, g.peer, c->comm, s));
+        for (auto& g : c->hrecv) RF_NC(c, N.Recv(c->ws.halo + g.off * k, g.cnt * k, ncclDouble, g.peer, c->comm, s));
+      }
+      RF_NC(c, N.GroupEnd());
+      break;
+    case C_AG:
+      RF_NC(c, N.AllGather(c->ws.ag_send, c->ws.ag_all, 4 * k, ncclDouble, c->comm, s));
+      break;
+    case C_MG:
+      RF_NC(c, N.AllGather(c->ws.M2, c->ws.mg_all, 2 * k * k + k, ncclDouble, c->comm, s));
+      break;
+    case C_BC:
+      RF_NC(c, N.Broadcast(c->bc, c->bc, c->bc_cnt, ncclDouble, 0, c->comm, s));
+      break;
+    case C_NRM:
+      RF_NC(c, N.AllGather(c->ws.nrm_send, c->ws.nrm_all, k, ncclDouble, c->comm, s));
+      break;
+  }
+  return REFINE_OK;
+}
+
+// One sweep's kernels and collectives (no status reset), every rank of c (loopback) or c itself.
+static refine_status enqueue_phases(refine_ctx* c, double* X) {
+  const bool multi = c->multi;
+  refine_ctx* one[1] = {c};
+  refine_ctx** ranks = c->loopback ? c->kids.data() : one;
+  const int nr = c->loopback ? (int)c->kids.size() : 1;
+  static const int after[6] = {C_AG, -1, C_MG, C_BC, C_NRM, -1};
+  refine_status st;
+  if (multi && (st = collective(c, C_X, X)) != REFINE_OK) return st;
+  int launches = 0;
+  for (int ph = 0; ph < 6; ++ph) {
+    for (int i = 0; i < nr; ++i) {
+      refine_ctx* r = ranks[i];
+      double* Xr = c->loopback ? X + r->row_begin * c->k : X;
+      launches += dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, ph, Xr); });
+    }
+    if (multi && after[ph] >= 0 && (st = collective(c, after[ph], X)) != REFINE_OK) return st;
+  }
+  c->launches = launches;
   RF_CK(c, cudaGetLastError());
   return REFINE_OK;
+}
+
+static refine_status enqueue_sweep(refine_ctx* c, double* X) {
+  if (c->loopback)
+    for (auto* kid : c->kids) RF_CK(c, cudaMemsetAsync(kid->ws.status, 0, sizeof(int), c->stream));
+  else
+    RF_CK(c, cudaMemsetAsync(c->ws.status, 0, sizeof(int), c->stream));
+  return enqueue_phases(c, X);
 }
 
 static refine_status launch_sweep(refine_ctx* c, double* X) {
@@ -442,8 +779,9 @@ static refine_status map_status(int s) {
 static refine_status read_stats(refine_ctx* c, refine_sweep_stats* stats, int* dev_status) {
   double h[8];
   int st = 0;
-  RF_CK(c, cudaMemcpyAsync(h, c->ws.stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-  RF_CK(c, cudaMemcpyAsync(&st, c->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  const Ws& ws = ctx0(c)->ws;
+  RF_CK(c, cudaMemcpyAsync(h, ws.stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaMemcpyAsync(&st, ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   RF_CK(c, cudaStreamSynchronize(c->stream));
   if (stats) {
     stats->rel_resid = h[0]; stats->corr_norm = h[1]; stats->min_gap = h[2];
@@ -482,16 +820,21 @@ extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, dou
                                     refine_sweep_stats* last) {
   if (!c || !X || iters < 0) return REFINE_E_INVALID;
   if (c->sticky != REFINE_OK) return c->sticky;
-  RF_CK(c, cudaMemsetAsync(c->run, 0, sizeof(RunState), c->stream));
-  RF_CK(c, cudaMemsetAsync(c->ws.status, 0, sizeof(int), c->stream));
+  std::vector<refine_ctx*> ranks = c->loopback ? c->kids : std::vector<refine_ctx*>{c};
+  for (auto* r : ranks) {
+    RF_CK(c, cudaMemsetAsync(r->run, 0, sizeof(RunState), c->stream));
+    RF_CK(c, cudaMemsetAsync(r->ws.status, 0, sizeof(int), c->stream));
+  }
   for (int t = 0; t < iters; ++t) {
-    c->launches = dispatch(c->kp, [&](auto K) { return decltype(K)::enqueue(c, X); });
-    run_check_kernel<<<1, 1, 0, c->stream>>>(c->ws.status, c->run, c->ws.stats, tol, c->opts.guard_window,
-                                             c->opts.guard_factor);
+    refine_status st = enqueue_phases(c, X);
+    if (st != REFINE_OK) return st;
+    for (auto* r : ranks)      // every rank holds the same stats after the broadcast: same decision
+      run_check_kernel<<<1, 1, 0, c->stream>>>(r->ws.status, r->run, r->ws.stats, tol, c->opts.guard_window,
+                                               c->opts.guard_factor);
     RF_CK(c, cudaGetLastError());
   }
   RunState rs;
-  RF_CK(c, cudaMemcpyAsync(&rs, c->run, sizeof(rs), cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaMemcpyAsync(&rs, ctx0(c)->run, sizeof(rs), cudaMemcpyDeviceToHost, c->stream));
   int ds = 0;
   refine_sweep_stats st{};
   refine_status r = read_stats(c, &st, &ds);
@@ -507,13 +850,14 @@ extern "C" refine_status refine_get_status(refine_ctx* c) {
   if (!c) return REFINE_E_INVALID;
   if (c->sticky != REFINE_OK) return c->sticky;
   int ds = 0;
-  RF_CK(c, cudaMemcpyAsync(&ds, c->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaMemcpyAsync(&ds, ctx0(c)->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   RF_CK(c, cudaStreamSynchronize(c->stream));
   return map_status(ds == ST_HALT_CONVERGED ? ST_OK : ds);
 }
 
 extern "C" refine_status refine_set_graph(refine_ctx* c, int32_t enable) {
   if (!c) return REFINE_E_INVALID;
+  if (c->loopback && enable) return REFINE_E_UNSUPPORTED;
   c->use_graph = enable != 0;
   if (!c->use_graph && c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; c->gX = nullptr; }
   return REFINE_OK;
@@ -521,7 +865,14 @@ extern "C" refine_status refine_set_graph(refine_ctx* c, int32_t enable) {
 
 extern "C" int32_t refine_kernels_per_sweep(const refine_ctx* c) {
   if (!c) return 0;
-  return (c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0);
+  if (c->loopback) {
+    int n = 0;
+    for (auto* kid : c->kids) n += refine_kernels_per_sweep(kid);
+    return n;
+  }
+  const int per = (c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0);
+  if (!c->multi) return per;
+  return per + 1 - (c->rank == 0 ? 0 : 1);   // + ag_local; kxk_finish on rank 0 only
 }
 
 static const char* kernel_names_dense[] = {"gemm_ax", "w_finish", "kxk_prep", "passB", "passB_reduce",
@@ -530,15 +881,16 @@ static const char* kernel_names_csr[] = {"spmm_csr", "kxk_prep", "passB", "passB
                                          "kxk_finish", "passC", "norm_reduce", "normalize"};
 
 extern "C" const char* refine_kernel_name(const refine_ctx* c, int32_t i) {
-  if (!c || i < 0 || i >= refine_kernels_per_sweep(c)) return "";
+  if (!c || i < 0 || i >= (c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0)) return "";
   return c->csr ? kernel_names_csr[i] : kernel_names_dense[i];
 }
 
 extern "C" refine_status refine_profile_begin(refine_ctx* c, int32_t max_sweeps) {
   if (!c || max_sweeps < 1) return REFINE_E_INVALID;
+  if (c->loopback) return REFINE_E_UNSUPPORTED;
   if (c->use_graph) return REFINE_E_UNSUPPORTED;      // events are recorded at enqueue time
   if (c->prof_ev) return REFINE_E_INVALID;
-  c->prof_per_sweep = refine_kernels_per_sweep(c) + 1;
+  c->prof_per_sweep = ((c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0)) + 1;   // kernel slots (mark() positions)
   c->prof_cap = c->prof_per_sweep * max_sweeps;
   c->prof_ev = new (std::nothrow) cudaEvent_t[c->prof_cap];
   if (!c->prof_ev) return REFINE_E_NOMEM;
@@ -572,6 +924,11 @@ extern "C" refine_status refine_profile_end(refine_ctx* c, double* ms_sum, int32
 extern "C" void refine_destroy(refine_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto* kid : c->kids) refine_destroy(kid);
+  c->kids.clear();
+  if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+  if (c->own_xfull && c->Xfull) cudaFree(c->Xfull);
+  if (c->ws.halo) cudaFree(c->ws.halo);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->pool) cudaFree(c->pool);
@@ -598,12 +955,38 @@ extern "C" const char* refine_status_string(refine_status s) {
 
 extern "C" refine_status refine_nccl_id(void* out128) {
   if (!out128) return REFINE_E_INVALID;
-  return REFINE_E_UNSUPPORTED;   // multi-GPU path not in this build
+  Nccl& N = nccl();
+  if (!N.ok) return REFINE_E_NCCL;
+  ncclUniqueId id;
+  if (N.GetUniqueId(&id) != ncclSuccess) return REFINE_E_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return REFINE_OK;
+}
+
+extern "C" int32_t refine_halo_plan(int32_t world, int32_t rank, const int64_t* row_begin, const int64_t* row_end,
+                                    const int64_t* col_lo, const int64_t* col_hi, int64_t* send, int32_t* nsend,
+                                    int64_t* recv, int32_t* nrecv, int64_t* halo_rows, int32_t cap) {
+  if (world < 1 || rank < 0 || rank >= world || !row_begin || !row_end || !col_lo || !col_hi) return REFINE_E_INVALID;
+  std::vector<refine_ctx::Seg> sv, rv;
+  int64_t hr = 0;
+  halo_plan(world, rank, row_begin, row_end, col_lo, col_hi, sv, rv, &hr);
+  if ((int)sv.size() > cap || (int)rv.size() > cap) return REFINE_E_INVALID;
+  for (size_t i = 0; i < sv.size(); ++i) {
+    send[4 * i] = sv[i].peer; send[4 * i + 1] = sv[i].row; send[4 * i + 2] = sv[i].cnt; send[4 * i + 3] = sv[i].off;
+  }
+  for (size_t i = 0; i < rv.size(); ++i) {
+    recv[4 * i] = rv[i].peer; recv[4 * i + 1] = rv[i].row; recv[4 * i + 2] = rv[i].cnt; recv[4 * i + 3] = rv[i].off;
+  }
+  *nsend = (int32_t)sv.size();
+  *nrecv = (int32_t)rv.size();
+  if (halo_rows) *halo_rows = hr;
+  return REFINE_OK;
 }
 
 extern "C" refine_status refine_debug_get(refine_ctx* c, int32_t what, double* dst) {
   if (!c || !dst) return REFINE_E_INVALID;
   if (c->sticky != REFINE_OK) return c->sticky;
+  if (c->loopback) return refine_debug_get(c->kids[0], what, dst);   // rank 0 holds the k x k state
   const int k = c->k;
   const size_t kk = (size_t)k * k, nk = (size_t)c->n_loc * k;
   const Ws& ws = c->ws;

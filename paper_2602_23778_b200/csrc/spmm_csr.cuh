@@ -17,20 +17,19 @@ template <int CPL>   // columns per lane = ceil(k / 32)
 __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx,
                                                        const double* __restrict__ val,
-                                                       const double* __restrict__ X,   // gathered (global rows)
+                                                       const double* __restrict__ X,      // unused (see xrow)
                                                        const double* __restrict__ Xloc) {  // local rows
   __shared__ dd sa[8][KMAX], sg[8][KMAX];
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t base = row_ptr[0];
   dd a[CPL], g[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) a[c] = g[c] = dd{0.0, 0.0};
   // block-cyclic rows: all CTAs sweep the matrix together, so the rows a stencil gathers
   // (+-1 grid line / plane) were touched recently and are still in L2
   for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < ws.n_loc; i += (int64_t)gridDim.x * 8) {
-    const int32_t p0 = row_ptr[i] - base, p1 = row_ptr[i + 1] - base;
+    const int32_t p0 = row_ptr[i], p1 = row_ptr[i + 1];   // absolute offsets into col_idx / val
     double acc[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
@@ -42,7 +41,7 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __r
       for (int t = 0; t < cnt; ++t) {
         const int32_t col = __shfl_sync(0xffffffffu, mycol, t);
         const double v = __shfl_sync(0xffffffffu, myval, t);
-        const double* xr = X + (int64_t)col * k;
+        const double* xr = xrow(ws, Xloc, col, k);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int j = lane + 32 * c;
@@ -94,12 +93,11 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
   if (*ws.status != ST_OK) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, l = lane % LPR, slot = warp * RPW + sub;
-  const int32_t base = row_ptr[0];
   dd a[2 * VPL], g[2 * VPL];
 #pragma unroll
   for (int c = 0; c < 2 * VPL; ++c) a[c] = g[c] = dd{0.0, 0.0};
   for (int64_t i = (int64_t)blockIdx.x * SLOTS + slot; i < ws.n_loc; i += (int64_t)gridDim.x * SLOTS) {
-    const int32_t p0 = row_ptr[i] - base, p1 = row_ptr[i + 1] - base;
+    const int32_t p0 = row_ptr[i], p1 = row_ptr[i + 1];   // absolute offsets into col_idx / val
     double acc[2 * VPL];
 #pragma unroll
     for (int c = 0; c < 2 * VPL; ++c) acc[c] = 0.0;
@@ -116,7 +114,7 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
         if (t < cnt)
 #pragma unroll
           for (int v = 0; v < VPL; ++v)
-            xs[t][v] = __ldg(reinterpret_cast<const double2*>(X + (int64_t)cols[t] * K) + l + LPR * v);
+            xs[t][v] = __ldg(reinterpret_cast<const double2*>(xrow(ws, Xloc, cols[t], K)) + l + LPR * v);
 #pragma unroll
       for (int t = 0; t < MAXNZ; ++t)
         if (t < cnt)

@@ -234,3 +234,76 @@ def test_run_statuses(pkg):
     assert s == pkg.REFINE_OK and st.corr_norm <= 1e-12 and it < 50
     Xo, so, ito, _ = oracle.run(op_of(p), p.X0.numpy(), 50, 1e-12)
     assert so == oracle.OK
+
+
+# ------------------------------------------------------------------------------ row partition (loopback)
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_loopback_dense_row_partition(pkg, world):
+    """The multi-rank code path (partitioned S1, gathered alpha/g, rank-0 k x k stage, broadcast,
+    gathered norms) emulated on one device: one-step parity with the oracle and agreement with
+    the single-rank run."""
+    p = synth.small_dense(1003, 16, m=8, seed=17, signs=True)
+    R = pkg.Refiner.dense(p.A.cuda(), p.k, world=world)
+    one_step(pkg, p, 3, R=R)
+    X1, Xp = p.X0.cuda().clone(), p.X0.cuda().clone()
+    refiner(pkg, p).refine_sweep(X1)
+    R.refine_sweep(Xp)
+    assert rel(Xp.cpu().numpy(), X1.cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,k,world", [((40, 37), 6, 2), ((64, 8), 6, 16), ((17, 15, 13), 20, 3),
+                                          ((24, 22, 21), 128, 4)])
+def test_loopback_csr_halo(pkg, dims, k, world):
+    """CSR row partition with halo exchange (incl. halos spanning several ranks at world=16)."""
+    coeffs = (1.0, 1.37) if len(dims) == 2 else (1.0, 1.13, 1.29)
+    p = synth.small_laplacian(dims, coeffs, k)
+    R = pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k, world=world)
+    one_step(pkg, p, 2, R=R)
+    X1, Xp = p.X0.cuda().clone(), p.X0.cuda().clone()
+    refiner(pkg, p).refine_sweep(X1)
+    R.refine_sweep(Xp)
+    assert rel(Xp.cpu().numpy(), X1.cpu().numpy()) <= 1e-13
+
+
+def test_loopback_run_converges(pkg):
+    p = synth.make_config("cfg1")
+    R = pkg.Refiner.dense(p.A.cuda(), p.k, world=2)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 40, 1e-14)
+    assert s == pkg.REFINE_OK
+    Xt = p.X.numpy()
+    Xg = X.cpu().numpy()
+    sg = np.sign(np.sum(Xg * Xt, axis=0))
+    assert np.linalg.norm(Xg * sg - Xt, axis=0).max() <= 100 * p.n * U
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_nccl_path_single_rank(pkg, kind, monkeypatch):
+    """The NCCL code path (all-gathers, broadcast, group send/recv) on a 1-rank communicator:
+    REFINE_FORCE_NCCL=1 makes world == 1 take it.  One-step parity with the oracle."""
+    monkeypatch.setenv("REFINE_FORCE_NCCL", "1")
+    try:
+        nid = pkg.refine_nccl_id()
+    except pkg.RefineError:
+        pytest.skip("NCCL not loadable")
+    if kind == "dense":
+        p = synth.small_dense(777, 12, m=8, seed=23, signs=True)
+        R = pkg.Refiner.dense(p.A.cuda(), p.k, world=1, rank=0, nccl_id=nid)
+    else:
+        p = synth.small_laplacian((30, 21), (1.0, 1.37), 8)
+        R = pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k, world=1, rank=0, nccl_id=nid)
+    assert R.kernels_per_sweep() == (10 if kind == "dense" else 9)      # + ag_local
+    one_step(pkg, p, 2, R=R)
+
+
+def test_repeat_bitwise_k128(pkg):
+    """Run-to-run determinism at the largest k (guards against races between CTAs)."""
+    p = synth.small_dense(1100, 128, m=8, seed=1228, signs=True)
+    R = refiner(pkg, p)
+    outs = []
+    for _ in range(4):
+        X = p.X0.cuda().clone()
+        R.refine_sweep(X)
+        outs.append(X.cpu().numpy())
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
