@@ -139,16 +139,40 @@ def make_problem(name, device):
     return synth.make_config(name, device=device)
 
 
-def time_ours(p, steps, warmup, world, local, profile=True):
-    """Device-timed sweeps: CUDA events on the library's stream, barrier + sync on both sides."""
+def partition(n, world, rank):
+    """Row blocks of the multi-GPU path (rank 0 takes the remainder; it must own rows 0..k-1)."""
+    blk = n // world
+    rb = 0 if rank == 0 else n - blk * (world - rank)
+    return rb, n - blk * (world - rank - 1)
+
+
+def make_refiner(p, world, rank):
+    """Refiner for this rank: world == 1 -> whole problem; world > 1 -> row partition over NCCL
+    (ncclUniqueId from rank 0, broadcast over torch.distributed).  Returns (Refiner, X_local)."""
     import torch
     import paper_2602_23778_b200 as pkg
     stream = torch.cuda.current_stream()
+    if world == 1:
+        if p.kind == "dense":
+            return pkg.Refiner.dense(p.A, p.k, shift=p.shift, stream=stream), p.X0.clone()
+        return pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, shift=p.shift, stream=stream), p.X0.clone()
+    import torch.distributed as dist
+    obj = [pkg.refine_nccl_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    rb, re = partition(p.n, world, rank)
+    kw = dict(shift=p.shift, stream=stream, row_begin=rb, row_end=re, rank=rank, world=world, nccl_id=obj[0])
     if p.kind == "dense":
-        R = pkg.Refiner.dense(p.A, p.k, shift=p.shift, stream=stream)
+        R = pkg.Refiner.dense(p.A[rb:re], p.k, n=p.n, **kw)
     else:
-        R = pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, shift=p.shift, stream=stream)
-    X = p.X0.clone()
+        R = pkg.Refiner.csr(p.row_ptr[rb:re + 1].contiguous(), p.col_idx, p.val, p.n, p.k, **kw)
+    return R, p.X0[rb:re].clone()
+
+
+def time_ours(p, steps, warmup, world, local, profile=True, rank=0):
+    """Device-timed sweeps: CUDA events on the library's stream, barrier + sync on both sides."""
+    import torch
+    stream = torch.cuda.current_stream()
+    R, X = make_refiner(p, world, rank)
     for _ in range(warmup):
         R.refine_sweep(X)
     torch.cuda.synchronize()
@@ -172,10 +196,11 @@ def time_ours(p, steps, warmup, world, local, profile=True):
     return ms / steps, kern, R, X, st, s
 
 
-def time_e2e(R, p, steps, warmup):
+def time_e2e(R, p, steps, warmup, world=1, rank=0):
     """Host buffers through the C ABI: H2D of X^, sweep, D2H of the result, each step."""
     import torch
-    Xh = p.X0.cpu().pin_memory() if p.X0.is_cuda else p.X0.clone().pin_memory()
+    rb, re = partition(p.n, world, rank)
+    Xh = p.X0[rb:re].cpu().pin_memory()
     for _ in range(max(1, warmup)):
         R.refine_sweep_host(Xh)
     torch.cuda.synchronize()
@@ -183,16 +208,18 @@ def time_e2e(R, p, steps, warmup):
     for _ in range(steps):
         s, st = R.refine_sweep_host(Xh)
     t1 = time.perf_counter()
-    nb = p.n * p.k * 8
+    nb = (re - rb) * p.k * 8
     return (t1 - t0) / steps, nb, nb + 40
 
 
-def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak):
-    """Dominant kernel: its algorithmic flops (bytes) per launch / its average launch time."""
+def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak, n_loc=None):
+    """Dominant kernel: its algorithmic flops (bytes) per launch / its average launch time
+    (per rank: n_loc local rows of the row partition)."""
     if not kern:
         return None
     top = max(kern, key=kern.get)
     n, k = p.n, p.k
+    nl = n if n_loc is None else n_loc
     traffic = None
     try:
         tr = json.load(open(TRAFFIC_FILE))
@@ -201,14 +228,14 @@ def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak):
         pass
     t = kern[top] * 1e-3
     if top == "gemm_ax":
-        flops = 2.0 * n * n * k
+        flops = 2.0 * nl * n * k
         ach = flops / t / 1e12
         return {"kernel": top, "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": ach / fp64_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
                 "per_launch_alg": f"2*n*n*k = {flops:.4g} flop (FP64 DMMA)",
                 "peak_source": "DMMA FP64 microbenchmark on this pool's B200 (profiles/r01_fp64_peaks.json)"}
     if top in ("passB", "passC"):
-        rows = n - k
+        rows = nl - k
         fl = (4.0 if top == "passB" else 2.0) * rows * k * k
         by = (16.0 if top == "passB" else 24.0) * rows * k
         t_f, t_b = fl / (fp64_peak * 1e12), by / (hbm_peak * 1e9)
@@ -299,19 +326,20 @@ def main():
         return
     import torch
     hbm, hbm_src, fp64 = peaks()
-    # Multi-GPU: this build runs N independent replicas; each rank
-    # refines its own copy, so the whole-job value is N x the per-replica rate (weak scaling).
+    # Multi-GPU: A and X^ row-partitioned over the N ranks (NCCL over NVLink, DESIGN.md
+    # "Multi-GPU"); one step = one sweep of the whole problem, so value = 1 / max-over-ranks time
+    # (strong scaling).
     p = make_problem(args.config, f"cuda:{local}")
     with Clocks(local) as clk:
-        ms, kern, R, X, st, s = time_ours(p, args.steps, args.warmup, world, local)
+        ms, kern, R, X, st, s = time_ours(p, args.steps, args.warmup, world, local, rank=rank)
     ms_max = max_over_ranks(ms, world)
-    value = world * 1000.0 / ms_max
+    value = 1000.0 / ms_max
     f, b = alg_counts(p)
     line = {"metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n": p.n, "k": p.k, "kind": p.kind,
-                       "nnz": p.nnz, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "nnz": p.nnz, "parallelism": f"rows{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (A = %.2f GB)" % (p.nnz * 8 / 1e9) if p.kind == "dense"
                        else "A + X^ + W larger than L2"},
             "clocks": clk.summary(),
@@ -319,14 +347,15 @@ def main():
                       "frac_of_sweep_roofline": max(f / (fp64 * 1e12), b / (hbm * 1e9)) / (ms_max * 1e-3),
                       "F_alg": f, "B_alg": b, "status": s, "rel_resid": st.rel_resid, "corr_norm": st.corr_norm},
             "kernels_ms": kern,
-            "roofline": roofline_for(p, kern, ms_max, fp64, hbm),
+            "roofline": roofline_for(p, kern, ms_max, fp64, hbm, n_loc=partition(p.n, world, rank)[1] - partition(p.n, world, rank)[0]),
             "gpu_launches": R.kernels_per_sweep() * args.steps}
     # e2e through the host-buffer C ABI call
-    e2e_s, h2d, d2h = time_e2e(R, p, max(3, args.steps // 2), 1)
+    e2e_s, h2d, d2h = time_e2e(R, p, max(3, args.steps // 2), 1, world, rank)
     e2e_s = max_over_ranks(e2e_s, world)
-    line["e2e"] = {"value": world / e2e_s, "unit": "sweeps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    line["e2e"] = {"value": 1.0 / e2e_s, "unit": "sweeps/s", "h2d_bytes_per_step": h2d * world,
+                   "d2h_bytes_per_step": d2h * world}
     del R, X
-    if not args.no_extra:
+    if not args.no_extra and world == 1:
         per = {}
         for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
             if name == args.config:
@@ -342,7 +371,7 @@ def main():
             del QR, QX, q
             torch.cuda.empty_cache()
         line["per_config"] = per
-    if rank == 0 and not args.no_extra and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_extra and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config)
         except Exception as e:  # never fail the bench on the baseline leg

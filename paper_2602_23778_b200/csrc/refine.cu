@@ -198,6 +198,31 @@ template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}
 template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
 template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 4, 16};  static constexpr int C[4] = {64, 16, 1, 8}; };
 
+template <bool HALO>
+static void launch_spmm(refine_ctx* c, bool vec, double* X) {
+  const Ws& ws = c->ws;
+  cudaStream_t s = c->stream;
+  const int g = c->spmm_grid;
+  if (vec) {
+    switch (c->k) {
+      case 2: spmm_csr_vec_kernel<1, 1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 4: spmm_csr_vec_kernel<1, 2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 8: spmm_csr_vec_kernel<1, 4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 16: spmm_csr_vec_kernel<1, 8, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 32: spmm_csr_vec_kernel<1, 16, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 64: spmm_csr_vec_kernel<1, 32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      default: spmm_csr_vec_kernel<2, 32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+    }
+  } else {
+    switch ((c->k + 31) / 32) {
+      case 1: spmm_csr_kernel<1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 2: spmm_csr_kernel<2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 3: spmm_csr_kernel<3, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      default: spmm_csr_kernel<4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+    }
+  }
+}
+
 template <int KP>
 struct Kern {
   using TT = Tiles<KP>;
@@ -284,24 +309,8 @@ struct Kern {
           c->mark();
           const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2 &&
                            (ws.halo == nullptr || (uintptr_t)ws.halo % 16 == 0);
-          if (vec) {
-            switch (c->k) {
-              case 2: spmm_csr_vec_kernel<1, 1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 4: spmm_csr_vec_kernel<1, 2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 8: spmm_csr_vec_kernel<1, 4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 16: spmm_csr_vec_kernel<1, 8><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 32: spmm_csr_vec_kernel<1, 16><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 64: spmm_csr_vec_kernel<1, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              default: spmm_csr_vec_kernel<2, 32><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-            }
-          } else {
-            switch ((c->k + 31) / 32) {
-              case 1: spmm_csr_kernel<1><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 2: spmm_csr_kernel<2><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              case 3: spmm_csr_kernel<3><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-              default: spmm_csr_kernel<4><<<c->spmm_grid, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-            }
-          }
+          if (ws.halo) launch_spmm<true>(c, vec, X);
+          else launch_spmm<false>(c, vec, X);
           n += 1;
         }
         if (c->multi) {

@@ -13,7 +13,7 @@
 
 namespace rf {
 
-template <int CPL>   // columns per lane = ceil(k / 32)
+template <int CPL, bool HALO>   // columns per lane = ceil(k / 32); HALO: row-partitioned X
 __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx,
                                                        const double* __restrict__ val,
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __r
       for (int t = 0; t < cnt; ++t) {
         const int32_t col = __shfl_sync(0xffffffffu, mycol, t);
         const double v = __shfl_sync(0xffffffffu, myval, t);
-        const double* xr = xrow(ws, Xloc, col, k);
+        const double* xr = HALO ? xrow(ws, Xloc, col, k) : Xloc + (int64_t)col * k;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int j = lane + 32 * c;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __r
 // double2 column pairs (LPR = 32 / rows-per-warp), so small k still issues full 256-byte
 // warp transactions.  Up to MAXNZ gathers of a row are issued before the (in-order) fma chain
 // consumes them, which keeps ~MAXNZ x 256 bytes in flight per row.
-template <int VPL, int LPR>
+template <int VPL, int LPR, bool HALO>
 __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32_t* __restrict__ row_ptr,
                                                            const int32_t* __restrict__ col_idx,
                                                            const double* __restrict__ val,
@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
         if (t < cnt)
 #pragma unroll
           for (int v = 0; v < VPL; ++v)
-            xs[t][v] = __ldg(reinterpret_cast<const double2*>(xrow(ws, Xloc, cols[t], K)) + l + LPR * v);
+            xs[t][v] = __ldg(reinterpret_cast<const double2*>(HALO ? xrow(ws, Xloc, cols[t], K)
+                                                                   : Xloc + (int64_t)cols[t] * K) + l + LPR * v);
 #pragma unroll
       for (int t = 0; t < MAXNZ; ++t)
         if (t < cnt)
