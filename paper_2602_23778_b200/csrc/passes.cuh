@@ -49,16 +49,17 @@ struct PassBCfg {
   }
 };
 
-// R = W - X D is formed on the fly while loading the B fragments of the M half (no shared
-// memory write-back, one barrier per stage); rr_j = sum r_ij^2 is accumulated by the warps of
-// tile 0 in the first a-row of warps, which see every (row, column) of R exactly once.
+// R = W - X D is formed in place in the staged W rows for this tile's R columns (one fma per
+// element, once per CTA), so the MMA loop reads one shared operand per fragment.  The tiles of
+// the first a-block cover every R column exactly once; they also accumulate rr_j = sum r_ij^2.
 template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
 __global__ void __launch_bounds__(PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>::THREADS)
 passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   using C = PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>;
+  constexpr int THREADS = C::THREADS;
   extern __shared__ __align__(16) double smem[];
   __shared__ double sd[KP];
-  __shared__ double srr[WARPS_B * 4][TB];
+  __shared__ double srr[THREADS];
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wa = warp / WARPS_B, wb = warp % WARPS_B;
@@ -73,13 +74,13 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
       }
   }
   const int a0 = ta * TA, b0 = tb * TB;
-  const bool rpart = b0 < KP;                            // the tile has R columns (it may also have X)
+  const int rw = (b0 < KP) ? min(TB, KP - b0) : 0;      // R columns [b0, b0 + rw) of this tile
   const int64_t rows = ws.n_loc - ws.top;
   const int64_t per = ((rows + gridDim.y - 1) / gridDim.y + BR - 1) / BR * BR;
   const int64_t rb = ws.top + (int64_t)blockIdx.y * per;
   const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
   const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
-  for (int j = tid; j < KP; j += C::THREADS) sd[j] = (j < k) ? ws.d[j] : 0.0;
+  for (int j = tid; j < KP; j += THREADS) sd[j] = (j < k) ? ws.d[j] : 0.0;
   double* Xs = smem;
   double* Ws_ = smem + 2 * C::STAGE;
 
@@ -88,22 +89,22 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
     double* xs = Xs + buf * C::STAGE;
     double* wsb = Ws_ + buf * C::STAGE;
     if (vec16) {
-      for (int c = tid; c < BR * KP / 2; c += C::THREADS) {
+      for (int c = tid; c < BR * KP / 2; c += THREADS) {
         const int r = c / (KP / 2), cc = (c % (KP / 2)) * 2;
         const int64_t g = r0 + r;
         const bool ok = (g < re) && (cc < k);
         const int64_t off = ok ? g * k + cc : 0;
         cp_async16(xs + r * C::LDS + cc, X + off, ok);
-        if (rpart) cp_async16(wsb + r * C::LDS + cc, ws.W + off, ok);
+        if (cc >= b0 && cc < b0 + rw) cp_async16(wsb + r * C::LDS + cc, ws.W + off, ok);
       }
     } else {
-      for (int c = tid; c < BR * KP; c += C::THREADS) {
+      for (int c = tid; c < BR * KP; c += THREADS) {
         const int r = c / KP, cc = c % KP;
         const int64_t g = r0 + r;
         const bool ok = (g < re) && (cc < k);
         const int64_t off = ok ? g * k + cc : 0;
         cp_async8(xs + r * C::LDS + cc, X + off, ok);
-        if (rpart) cp_async8(wsb + r * C::LDS + cc, ws.W + off, ok);
+        if (cc >= b0 && cc < b0 + rw) cp_async8(wsb + r * C::LDS + cc, ws.W + off, ok);
       }
     }
   };
@@ -113,10 +114,8 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   for (int i = 0; i < C::MI; ++i)
 #pragma unroll
     for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  double rr[C::NI];
-#pragma unroll
-  for (int j = 0; j < C::NI; ++j) rr[j] = 0.0;
-  const bool do_rr = (ta == 0) && rpart && (wa == 0);    // the R tiles of the first a-block
+  double rr = 0.0;                                        // column b0 + tid % rw
+  const bool do_rr = (ta == 0) && (rw > 0);
   if (nit > 0) load(0, 0);
   cp_async_commit();
   for (int it = 0; it < nit; ++it) {
@@ -126,7 +125,16 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
     if (it + 1 < nit) load(cur ^ 1, it + 1);
     cp_async_commit();
     const double* xs = Xs + cur * C::STAGE;
-    const double* wsb = Ws_ + cur * C::STAGE;
+    double* wsb = Ws_ + cur * C::STAGE;
+    if (rw > 0) {
+      for (int e = tid; e < BR * rw; e += THREADS) {     // R = W - X D  (fma as in the oracle)
+        const int r = e / rw, c = b0 + e % rw;
+        const double v = __fma_rn(-xs[r * C::LDS + c], sd[c], wsb[r * C::LDS + c]);
+        wsb[r * C::LDS + c] = v;
+        if (do_rr) rr = __fma_rn(v, v, rr);
+      }
+      __syncthreads();
+    }
 #pragma unroll
     for (int kk = 0; kk < BR; kk += 4) {
       const int row = kk + (lane & 3);
@@ -137,13 +145,7 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
       for (int j = 0; j < C::NI; ++j) {
         const int cb8 = b0 + wb * C::WTB + j * 8;          // 8-column block: all R or all X (warp-uniform)
         const int col = cb8 + (lane >> 2);
-        if (cb8 < KP) {
-          const double r = __fma_rn(-xs[row * C::LDS + col], sd[col], wsb[row * C::LDS + col]);
-          b[j] = r;
-          if (do_rr) rr[j] = __fma_rn(r, r, rr[j]);
-        } else {
-          b[j] = xs[row * C::LDS + col - KP];
-        }
+        b[j] = (cb8 < KP) ? wsb[row * C::LDS + col] : xs[row * C::LDS + col - KP];
       }
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
@@ -161,18 +163,13 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
       out[ra * TB + cb] = acc[i][j][0];
       out[ra * TB + cb + 1] = acc[i][j][1];
     }
-  if (ta == 0 && rpart) {
-    // rr: lane (wb, j, lane>>2) holds column b0 + wb*WTB + j*8 + lane/4 summed over its rows (lane&3)
-    if (wa == 0) {
-#pragma unroll
-      for (int j = 0; j < C::NI; ++j) srr[wb * 4 + (lane & 3)][wb * C::WTB + j * 8 + (lane >> 2)] = rr[j];
-    }
+  if (do_rr) {   // threads t, t + rw, ... share column b0 + t % rw (THREADS is a multiple of rw)
+    srr[tid] = rr;
     __syncthreads();
-    for (int j = tid; j < TB && b0 + j < KP; j += C::THREADS) {
-      const int q0 = (j / C::WTB) * 4;
-      double s = 0.0;
-      for (int q = 0; q < 4; ++q) s += srr[q0 + q][j];
-      ws.brr[(int64_t)blockIdx.y * KP + b0 + j] = s;
+    if (tid < rw) {
+      double sum = srr[tid];
+      for (int q = 1; q < THREADS / rw; ++q) sum += srr[q * rw + tid];
+      ws.brr[(int64_t)blockIdx.y * KP + b0 + tid] = sum;
     }
   }
 }
