@@ -31,6 +31,7 @@
 namespace rf {
 
 constexpr int KXK_THREADS = 1024;
+__device__ long long* g_gemm_tlog = nullptr;   // optional phase log of one cta_gemm call (timing builds)
 constexpr int PANEL = 32;
 constexpr int LDA_P = PANEL + 4;                  // As[i][p]: A-fragment reads (8 rows x 4) conflict-free
 constexpr int LDB_P = KMAX + 8;                   // Bs[p][j]: B-fragment reads (4 rows x 8) conflict-free
@@ -40,21 +41,27 @@ constexpr int PANEL_SMEM = KMAX * LDA_P + PANEL * LDB_P;   // doubles of shared 
 // op(A) is M x K, op(B) is K x N, M, N <= 128.  K is consumed in 32-deep panels staged in
 // shared memory; warp w owns the 8 x 8 output tiles w, w + 32, ...  C0 may alias C (each
 // element is read then written by the same thread).  Starts and ends with a barrier.
-__device__ __noinline__ void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, bool ta, const double* B,
-                         int ldb, bool tb, double beta, const double* C0, int ldc0, double* C, int ldc,
-                         double* sm) {
+template <int MAXT>
+__device__ __noinline__ void cta_gemm_t(int M, int N, int K, double alpha, const double* A, int lda, bool ta,
+                                        const double* B, int ldb, bool tb, double beta, const double* C0, int ldc0,
+                                        double* C, int ldc, double* sm) {
   double* As = sm;                      // [KMAX][LDA_P]  As[i][p] = op(A)(i, kk+p)
   double* Bs = sm + KMAX * LDA_P;       // [PANEL][LDB_P] Bs[p][j] = op(B)(kk+p, j)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, ntile = tm * tn;
-  constexpr int MAXT = (KMAX / 8) * (KMAX / 8) / (KXK_THREADS / 32);   // tiles per warp at k = 128
   double acc[MAXT][2];
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) acc[t][0] = acc[t][1] = 0.0;
   const int Mp = tm * 8, Np = tn * 8;
+  long long* tl = g_gemm_tlog;
+  int ts = 0;
+  if (tl && tid == 0) tl[ts] = clock64();
+  ++ts;
   for (int kk = 0; kk < K; kk += PANEL) {
     const int pk = min(PANEL, K - kk);
     __syncthreads();
+    if (tl && tid == 0 && ts < 14) tl[ts] = clock64();
+    ++ts;
     // stage op(A)(0:Mp, kk:kk+32) and op(B)(kk:kk+32, 0:Np), zero-padded
     for (int e = tid; e < PANEL * Mp; e += KXK_THREADS) {
       int i, p;
@@ -67,6 +74,8 @@ __device__ __noinline__ void cta_gemm(int M, int N, int K, double alpha, const d
       Bs[p * LDB_P + j] = (p < pk && j < N) ? (tb ? B[j * ldb + kk + p] : B[(kk + p) * ldb + j]) : 0.0;
     }
     __syncthreads();
+    if (tl && tid == 0 && ts < 14) tl[ts] = clock64();
+    ++ts;
 #pragma unroll
     for (int t = 0; t < MAXT; ++t) {
       const int tile = warp + 32 * t;
@@ -94,7 +103,22 @@ __device__ __noinline__ void cta_gemm(int M, int N, int K, double alpha, const d
         }
     }
   }
+  if (tl && tid == 0 && ts < 14) tl[ts] = clock64();
   __syncthreads();
+  if (tl && tid == 0 && ts < 15) { tl[ts + 1] = clock64(); tl[15] = ts + 2; }
+  if (tl && tid == 0) g_gemm_tlog = nullptr;       // log only the first call
+}
+
+// tiles per warp: 1 (<= 32 output tiles, k <= 44), 2 (k <= 64), 8 (k <= 128).  Instantiating
+// by tile count keeps the unrolled MMA body small, so it stays in the instruction cache of the
+// single SM that runs the k x k chain.
+__device__ __forceinline__ void cta_gemm(int M, int N, int K, double alpha, const double* A, int lda, bool ta,
+                                         const double* B, int ldb, bool tb, double beta, const double* C0, int ldc0,
+                                         double* C, int ldc, double* sm) {
+  const int nt = ((M + 7) >> 3) * ((N + 7) >> 3);
+  if (nt <= 32) cta_gemm_t<1>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C0, ldc0, C, ldc, sm);
+  else if (nt <= 64) cta_gemm_t<2>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C0, ldc0, C, ldc, sm);
+  else cta_gemm_t<8>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C0, ldc0, C, ldc, sm);
 }
 
 // Inverse of a k x k triangular matrix S (ld k) into R (ld k).  upper: S upper triangular;
@@ -363,6 +387,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   const double* sig = ws.sigma;
   const double* d = ws.d;
   if (tid == 0) s_hits = 0;
+  if (ws.tlog && tid == 0) g_gemm_tlog = ws.tlog + 40;
   if (ws.multi) {   // [M2 | G2 | rr2] of every rank, summed in rank order (M2, G2, rr2 are contiguous)
     const int64_t cnt = 2 * kk + k;
     for (int64_t e = tid; e < cnt; e += nt) {
