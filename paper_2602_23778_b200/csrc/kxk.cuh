@@ -1,6 +1,6 @@
 // kxk.cuh -- the serial k x k stages of a sweep, each one CTA of 1024 threads (k <= 128).
 //
-// kxk_prep   (S2 + S3): fixed-order reduction of the alpha/g double-double partials
+// kxk_rq + kxk_lu (S2 + S3): fixed-order reduction of the alpha/g double-double partials
 //            -> alpha_j, d_j = g_j / alpha_j (eq. Rayleigh, Alg. 4
 //            lines 3-4); modified LU of the top k x k block X^_1 in shared memory (Alg. 2,
 //            PAPER.md:271-284, sign(0) = +1) -> Sigma, U, Y_1 = L;  U^{-1} and L^{-1} by
@@ -234,10 +234,8 @@ __global__ void __launch_bounds__(KXK_THREADS) ag_local_kernel(Ws ws) {
   }
 }
 
-// ---------------------------------------------------------------- kxk_prep
-// Shared memory: Q (k x k, the in-place modified LU); for k <= 64 also Ls, Ts, Us (L, T, U^{-1}).
-__global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const double* __restrict__ Xtop) {
-  extern __shared__ __align__(16) double Q[];
+// ---------------------------------------------------------------- kxk_rq (S2: alpha, Rayleigh quotients)
+__global__ void __launch_bounds__(KXK_THREADS) kxk_rq_kernel(Ws ws) {
   __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
   __shared__ int s_bad;
   if (*ws.status != ST_OK) return;
@@ -246,7 +244,6 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
 
   // 1. alpha_j, g_j: this rank's slots, or (world > 1) the gathered per-rank
   //    double-double vectors combined in rank order -- identical on every rank
-  for (int e = tid; e < k * k; e += nt) Q[e] = (ws.top > 0) ? Xtop[e] : 0.0;
   if (tid == 0) s_bad = ST_OK;
   if (ws.multi) {
     if (tid < k) {
@@ -276,11 +273,21 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
     if (bad != ST_OK) atomicCAS(&s_bad, ST_OK, bad);
   }
   RF_TSTAMP(ws, 1);
-  if (ws.top == 0) {                          // ranks without the top block only need alpha, d
-    __syncthreads();
-    if (tid == 0 && s_bad != ST_OK) *ws.status = s_bad;
-    return;
-  }
+  __syncthreads();
+  if (tid == 0 && s_bad != ST_OK) atomicCAS(ws.status, ST_OK, s_bad);
+}
+
+// ---------------------------------------------------------------- kxk_lu
+// S3 on the top k x k block: needs only X^_1, so it runs on a side stream concurrently with
+// S1 / S2 / passB (joined before kxk_finish).  Rank 0 only.
+// Shared memory: Q (k x k, the in-place modified LU); for k <= 64 also Ls, Ts, Us (L, T, U^{-1}).
+__global__ void __launch_bounds__(KXK_THREADS) kxk_lu_kernel(Ws ws, const double* __restrict__ Xtop) {
+  extern __shared__ __align__(16) double Q[];
+  __shared__ int s_bad;
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
+  for (int e = tid; e < k * k; e += nt) Q[e] = Xtop[e];
+  if (tid == 0) s_bad = ST_OK;
 
   // 2. Alg. 2 on the top block, literal arithmetic: sigma_j = -sign(q_jj) (sign(0)=+1),
   //    q_jj -= sigma_j, q_lj /= q_jj, q_lh -= q_lj q_jh.  One barrier per step: thread (l, h)
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
   }
   __syncthreads();
   if (s_bad == ST_E_ZERO_PIVOT) {
-    if (tid == 0) *ws.status = s_bad;
+    if (tid == 0) atomicCAS(ws.status, ST_OK, s_bad);
     return;
   }
   // U = upper(Q) with the shifted diagonal; L unit lower (strict part written above)
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_prep_kernel(Ws ws, const doub
     cta_gemm(k, k, k, -1.0, Up, k, false, Linv, k, true, 0.0, nullptr, 0, ws.T, k, Q);
   }
   RF_TSTAMP(ws, 5);
-  if (tid == 0 && s_bad != ST_OK) *ws.status = s_bad;
+  if (tid == 0 && s_bad != ST_OK) atomicCAS(ws.status, ST_OK, s_bad);
 }
 
 // ---------------------------------------------------------------- kxk_finish

@@ -2,13 +2,14 @@
 //
 // One sweep = the launch sequence below on the caller's stream:
 //   dense: gemm_ax (DMMA, split-K) -> w_finish            | CSR: spmm_csr (fma chain, fused)
-//   kxk_prep -> passB -> passB_reduce -> kxk_finish -> passC -> norm_reduce -> normalize
+//   kxk_rq -> passB -> passB_reduce -> [join kxk_lu] kxk_finish -> passC -> norm_reduce -> normalize
+//   (kxk_lu -- modified LU, T, U^{-1} of the top block -- needs only X^_1 and runs on a side stream)
 // Device-side conditions are carried by a status word every kernel checks first, so a
 // failed or halted sweep leaves X untouched and refine_run needs no per-sweep host sync.
 //
 // Row partition (world > 1): rank r owns rows [rb_r, re_r), rank 0 the
 // top k x k block.  Per sweep: X exchange (dense: all-gather of X; CSR: halo rows) -> S1 ->
-// all-gather of the alpha/g double-double vectors -> kxk_prep (identical d on every rank; LU on
+// all-gather of the alpha/g double-double vectors -> kxk_rq (identical d on every rank; kxk_lu on
 // rank 0) -> passB -> all-gather of [M2 | G2 | rr2] -> kxk_finish on rank 0 -> broadcast of
 // [Csig | scal | stats | status] -> passC -> all-gather of the column norm partials ->
 // normalize.  Every cross-rank sum is formed from gathered per-rank values in rank order, so
@@ -153,6 +154,8 @@ struct refine_ctx {
   cudaGraphExec_t gexec = nullptr;
   double* gX = nullptr;
   cudaStream_t cap_stream = nullptr;   // graphs are captured on a private stream (the caller's may be legacy)
+  cudaStream_t side = nullptr;         // kxk_lu (depends on X only) overlaps S1 / S2 / passB here
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // host-buffer entry point
   double* dX = nullptr;
   int launches = 0;
@@ -293,7 +296,15 @@ struct Kern {
     int n = 0;
     const bool xv16 = (c->k % 2 == 0) && ((uintptr_t)X % 16 == 0);
     switch (ph) {
-      case 0:  // S1 (+ S2 partials)
+      case 0:  // S1 (+ S2 partials); S3 (kxk_lu, X^_1 only) forked onto the side stream
+        if (ws.top > 0) {
+          cudaEventRecord(c->ev_fork, s);
+          cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+          kxk_lu_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8,
+                          c->side>>>(ws, X);
+          cudaEventRecord(c->ev_join, c->side);
+          ++n;
+        }
         if (!c->csr) {
           const double* Xb = c->multi ? c->Xfull : X;            // B operand: all n rows of X
           const bool bv16 = xv16 && ((uintptr_t)Xb % 16 == 0);
@@ -318,9 +329,9 @@ struct Kern {
           ++n;
         }
         break;
-      case 1:  // S2 + S3
+      case 1:  // S2: alpha, Rayleigh quotients
         c->mark();
-        kxk_prep_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8, s>>>(ws, X);
+        kxk_rq_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
         n += 1;
         break;
       case 2:  // S4 reductions
@@ -330,9 +341,10 @@ struct Kern {
         passBred<<<(2 * c->k * c->k + c->k + 31) / 32, 256, 0, s>>>(ws, c->passb_grid_y);
         n += 2;
         break;
-      case 3:  // k x k algebra (rank 0)
+      case 3:  // k x k algebra (rank 0), after the side-stream S3 joins
         c->mark();
         if (c->rank == 0) {
+          cudaStreamWaitEvent(s, c->ev_join, 0);
           kxk_finish_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
           n += 1;
         }
@@ -401,7 +413,10 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.row0 = row_begin; ws.row1 = row_end;
   ws.halo = nullptr; ws.halo_lo = row_begin;
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
-  RF_CK(c, cudaFuncSetAttribute(kxk_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
+  RF_CK(c, cudaFuncSetAttribute(kxk_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
+  RF_CK(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  RF_CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  RF_CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
   // workspace sizes (doubles)
   size_t bpart = 0, brr = 0, nslot = 0;
@@ -879,14 +894,14 @@ extern "C" int32_t refine_kernels_per_sweep(const refine_ctx* c) {
     for (auto* kid : c->kids) n += refine_kernels_per_sweep(kid);
     return n;
   }
-  const int per = (c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0);
+  const int per = (c->csr ? 8 : 9) + (c->opts.normalize ? 1 : 0);   // incl. kxk_lu (side stream)
   if (!c->multi) return per;
-  return per + 1 - (c->rank == 0 ? 0 : 1);   // + ag_local; kxk_finish on rank 0 only
+  return per + 1 - (c->rank == 0 ? 0 : 2);   // + ag_local; kxk_lu / kxk_finish on rank 0 only
 }
 
-static const char* kernel_names_dense[] = {"gemm_ax", "w_finish", "kxk_prep", "passB", "passB_reduce",
+static const char* kernel_names_dense[] = {"gemm_ax", "w_finish", "kxk_rq", "passB", "passB_reduce",
                                            "kxk_finish", "passC", "norm_reduce", "normalize"};
-static const char* kernel_names_csr[] = {"spmm_csr", "kxk_prep", "passB", "passB_reduce",
+static const char* kernel_names_csr[] = {"spmm_csr", "kxk_rq", "passB", "passB_reduce",
                                          "kxk_finish", "passC", "norm_reduce", "normalize"};
 
 extern "C" const char* refine_kernel_name(const refine_ctx* c, int32_t i) {
@@ -940,6 +955,9 @@ extern "C" void refine_destroy(refine_ctx* c) {
   if (c->ws.halo) cudaFree(c->ws.halo);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->pool) cudaFree(c->pool);
   if (c->ws.tlog) cudaFree(c->ws.tlog);
   if (c->dX) cudaFree(c->dX);
