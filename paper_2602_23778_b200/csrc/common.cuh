@@ -69,6 +69,11 @@ RF_DEV void dd_add(dd& acc, dd x) {
   acc = quick_two_sum(s.hi, e);
 }
 RF_DEV double dd_val(dd a) { return __dadd_rn(a.hi, a.lo); }
+// acc += x (x a plain double)
+RF_DEV void dd_add1(dd& acc, double x) {
+  dd s = two_sum(acc.hi, x);
+  acc = quick_two_sum(s.hi, __dadd_rn(s.lo, acc.lo));
+}
 
 // device status codes (same values as refine_status)
 enum : int { ST_OK = 0, ST_DIVERGED = 2, ST_E_INVALID = -1, ST_E_NEAR_ZERO_RQ = -2, ST_E_ZERO_PIVOT = -3 };

@@ -93,9 +93,15 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
   if (*ws.status != ST_OK) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, l = lane % LPR, slot = warp * RPW + sub;
+  // alpha / g: plain FP64 fma sums over blocks of ABLK rows, merged into double-double
+  // accumulators (relative error <= ABLK u for the same-sign terms of x^2 and x w, against
+  // ~u^2 for a full double-double chain at a quarter of its FP64 instructions)
+  constexpr int ABLK = 8;
   dd a[2 * VPL], g[2 * VPL];
+  double ba[2 * VPL], bg[2 * VPL];
 #pragma unroll
-  for (int c = 0; c < 2 * VPL; ++c) a[c] = g[c] = dd{0.0, 0.0};
+  for (int c = 0; c < 2 * VPL; ++c) { a[c] = g[c] = dd{0.0, 0.0}; ba[c] = bg[c] = 0.0; }
+  int nb = 0;
   for (int64_t i = (int64_t)blockIdx.x * SLOTS + slot; i < ws.n_loc; i += (int64_t)gridDim.x * SLOTS) {
     const int32_t p0 = row_ptr[i], p1 = row_ptr[i + 1];   // absolute offsets into col_idx / val
     double acc[2 * VPL];
@@ -131,12 +137,22 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
       double w0 = acc[2 * v], w1 = acc[2 * v + 1];
       if (ws.shift != 0.0) { w0 = __fma_rn(-ws.shift, x.x, w0); w1 = __fma_rn(-ws.shift, x.y, w1); }
       reinterpret_cast<double2*>(ws.W + i * K)[l + LPR * v] = make_double2(w0, w1);
-      dd_add_prod(a[2 * v], x.x, x.x);
-      dd_add_prod(a[2 * v + 1], x.y, x.y);
-      dd_add_prod(g[2 * v], x.x, w0);
-      dd_add_prod(g[2 * v + 1], x.y, w1);
+      ba[2 * v] = __fma_rn(x.x, x.x, ba[2 * v]);
+      ba[2 * v + 1] = __fma_rn(x.y, x.y, ba[2 * v + 1]);
+      bg[2 * v] = __fma_rn(x.x, w0, bg[2 * v]);
+      bg[2 * v + 1] = __fma_rn(x.y, w1, bg[2 * v + 1]);
+    }
+    if (++nb == ABLK) {
+      nb = 0;
+#pragma unroll
+      for (int c = 0; c < 2 * VPL; ++c) {
+        dd_add1(a[c], ba[c]); dd_add1(g[c], bg[c]);
+        ba[c] = bg[c] = 0.0;
+      }
     }
   }
+#pragma unroll
+  for (int c = 0; c < 2 * VPL; ++c) { dd_add1(a[c], ba[c]); dd_add1(g[c], bg[c]); }
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int j = 2 * (l + LPR * v);
