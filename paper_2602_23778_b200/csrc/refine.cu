@@ -135,6 +135,11 @@ struct refine_ctx {
   int64_t lda = 0;
   const int32_t *rp = nullptr, *ci = nullptr;
   const double* val = nullptr;
+  // CSR gather kernel (spmm_gather_kernel): rows per chunk (0 = not eligible -> vec / generic
+  // kernel) and the precomputed gather offsets (owned; indexed by absolute CSR position)
+  int gather_R = 0;
+  int32_t* xoff_buf = nullptr;
+  const int32_t* xoff = nullptr;
   double shift = 0.0;
   refine_opts opts{};
   int rank = 0, world = 1;
@@ -206,6 +211,19 @@ static void launch_spmm(refine_ctx* c, bool vec, double* X) {
   const Ws& ws = c->ws;
   cudaStream_t s = c->stream;
   const int g = c->spmm_grid;
+  if (vec && c->gather_R > 0) {   // vec: 16-byte aligned X / halo rows
+    const int R = c->gather_R;
+    switch (c->k) {
+      case 2: spmm_gather_kernel<2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      case 4: spmm_gather_kernel<4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      case 8: spmm_gather_kernel<8, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      case 16: spmm_gather_kernel<16, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      case 32: spmm_gather_kernel<32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      case 64: spmm_gather_kernel<64, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      default: spmm_gather_kernel<128, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+    }
+    return;
+  }
   if (vec) {
     switch (c->k) {
       case 2: spmm_csr_vec_kernel<1, 1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
@@ -385,6 +403,69 @@ static auto dispatch(int kp, F&& f) {
 // ---------------------------------------------------------------- init
 static refine_ctx* ctx0(refine_ctx* c) { return c->loopback ? c->kids[0] : c; }
 
+// spmm_gather_kernel eligibility and geometry (k a power of two <= 128, 32-bit gather offsets):
+// resident grid and the largest rows-per-chunk R whose chunks all fit the staged nonzero buffer.
+template <int K>
+static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp) {
+  using G = GatherCfg<K>;
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_gather_kernel<K, false>, 256, 0);
+  if (e != cudaSuccess) return e;
+  int occ2 = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, spmm_gather_kernel<K, true>, 256, 0);
+  if (e != cudaSuccess) return e;
+  occ = std::max(1, std::min(occ, occ2));
+  const int64_t n = c->n_loc;
+  int R = 0;
+  for (int r = G::RMAX; r >= 1 && R == 0; r = (r > G::RG) ? r - G::RG : r / 2) {
+    int64_t worst = 0;
+    for (int64_t i = 0; i < n; i += r) worst = std::max<int64_t>(worst, (int64_t)rp[std::min<int64_t>(i + r, n)] - rp[i]);
+    if (worst <= G::NZCAP) R = r;
+  }
+  c->gather_R = R;
+  if (R > 0) {
+    const int64_t chunks = (n + R - 1) / R;
+    c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sms * occ, chunks));
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t gather_setup(refine_ctx* c) {
+  c->gather_R = 0;
+  const int k = c->k;
+  if (getenv("REFINE_NO_GATHER") || (k & (k - 1)) != 0 || k < 2 || k > 128) return cudaSuccess;
+  if ((int64_t)(c->n - 0) * (k / 2) >= (int64_t(1) << 31)) return cudaSuccess;   // local + halo offsets in int32
+  std::vector<int32_t> rp(c->n_loc + 1);
+  cudaError_t e = cudaMemcpy(rp.data(), c->rp, rp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  switch (k) {
+    case 2: return gather_geometry<2>(c, rp);
+    case 4: return gather_geometry<4>(c, rp);
+    case 8: return gather_geometry<8>(c, rp);
+    case 16: return gather_geometry<16>(c, rp);
+    case 32: return gather_geometry<32>(c, rp);
+    case 64: return gather_geometry<64>(c, rp);
+    default: return gather_geometry<128>(c, rp);
+  }
+}
+
+// gather offsets of the local nonzeros (after the halo layout is known)
+static cudaError_t gather_offsets(refine_ctx* c) {
+  if (c->gather_R <= 0) return cudaSuccess;
+  int32_t p[2];
+  cudaError_t e = cudaMemcpy(&p[0], c->rp, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&p[1], c->rp + c->n_loc, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  const int64_t nnz = (int64_t)p[1] - p[0];
+  if ((e = cudaMalloc(&c->xoff_buf, std::max<int64_t>(nnz, 1) * sizeof(int32_t))) != cudaSuccess) return e;
+  c->xoff = c->xoff_buf - p[0];                    // indexed by absolute CSR position, like col_idx
+  if (nnz > 0)
+    spmm_xoff_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->ci + p[0], nnz, c->ws.row0, c->ws.row1,
+                                                        c->ws.halo ? c->ws.halo_lo : c->ws.row0, c->k / 2,
+                                                        c->xoff_buf);
+  return cudaGetLastError();
+}
+
 // Per-rank setup: launch geometry, workspace pool, local ||A - shift I||_inf row maxima and (CSR)
 // the range of referenced columns.  Cross-rank quantities are settled by finalize_partition.
 static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_begin, int64_t row_end,
@@ -423,6 +504,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   dispatch(c->kp, [&](auto K) { decltype(K)::sizes(c, bpart, brr, nslot); return 0; });
   c->w_fin_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 4, c->n_loc / 2));
   c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 8, (c->n_loc + 7) / 8));
+  if (c->csr) RF_CK(c, gather_setup(c));
   c->n_ag = c->csr ? c->spmm_grid : c->w_fin_grid;
   const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k, P = (size_t)world;
   const size_t wpart = (!c->csr && c->nsplit > 1) ? (size_t)c->nsplit * nk : 0;
@@ -535,6 +617,7 @@ static refine_status finalize_rank(refine_ctx* c, const std::vector<int64_t>& rb
     RF_CK(c, cudaMalloc(&c->Xfull, (size_t)c->n * c->k * sizeof(double)));
     c->own_xfull = true;
   }
+  if (c->csr) RF_CK(c, gather_offsets(c));
   return REFINE_OK;
 }
 
@@ -953,6 +1036,7 @@ extern "C" void refine_destroy(refine_ctx* c) {
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   if (c->own_xfull && c->Xfull) cudaFree(c->Xfull);
   if (c->ws.halo) cudaFree(c->ws.halo);
+  if (c->xoff_buf) cudaFree(c->xoff_buf);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->side) cudaStreamDestroy(c->side);

@@ -168,4 +168,182 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
   }
 }
 
+
+// ---------------------------------------------------------------- spmm_gather (production CSR S1)
+// For k in {2, 4, ..., 128}.  The vec kernel above is latency bound: each row is a chain of three
+// dependent global round trips (row_ptr -> col/val -> the gathered X rows) with ~16 rows in flight
+// per SM (cfg5: 1.9 TB/s).  Here
+//   * work item = a chunk of R consecutive rows; chunks are dealt block-cyclically over the
+//     persistent grid, so the whole grid sweeps A together: the X rows a banded matrix gathers
+//     again (the +-y / +-z stencil neighbours) are still in L2, and consecutive rows of a chunk,
+//     processed side by side by the CTA's row groups, share their x-neighbour rows through L1;
+//   * the chunk's row_ptr and (gather offset, val) are staged in shared memory by cp.async two
+//     and one chunks ahead, so only the X gathers are left on a row's critical path (R <= RMAX
+//     is chosen at init so that every chunk's nonzeros fit NZCAP);
+//   * a row group (LPR lanes x VPL double2 = the K columns) issues all gathers of its row (up to
+//     8 per batch) and its own x_i before the fma chain;
+//   * xoff = gather offsets precomputed at init in double2 units -- local row * K/2 (>= 0), or
+//     -1 - halo row * K/2 for halo rows (row partition) -- so a gather is one IMAD.WIDE + LDG.128;
+//   * W is written with streaming stores (evict-first) so it does not push X out of L2.
+// Each output w_ij is the fma chain over the row's nonzeros in ascending CSR order -- the oracle's
+// chain, so W is bit-identical to the oracle given identical X (P3).  alpha / g: 8-row
+// FP64 blocks merged into double-double accumulators in shared memory; fixed-order CTA reduction,
+// one slot per CTA: ws.ag[(blockIdx.x * K + j) * 4 + {a_hi, a_lo, g_hi, g_lo}].
+template <int K>
+struct GatherCfg {
+  static constexpr int LPR = K / 2 < 32 ? K / 2 : 32;   // lanes per row
+  static constexpr int VPL = K / (2 * LPR);              // double2 per lane
+  static constexpr int RG = 256 / LPR;                   // rows in flight per CTA
+  static constexpr int RMAX = VPL > 1 ? RG * 4 : (RG * 8 > 256 ? 256 : RG * 8);   // measured best at cfg4 / cfg5
+  static constexpr int NZCAP = RMAX * 8 < 1024 ? RMAX * 8 : 1024;
+  static constexpr int MINB = K >= 128 ? 2 : 3;
+};
+
+RF_DEV double2 ldg2_at(const char* base, uint32_t idx2) {   // base + idx2 double2s (one IMAD.WIDE.U32)
+  return __ldg(reinterpret_cast<const double2*>(base + (uint64_t)idx2 * 16u));
+}
+
+// requires n_loc * K / 2 < 2^31 and halo rows * K / 2 < 2^31 (checked at init)
+template <int K, bool HALO>
+__global__ void __launch_bounds__(256, GatherCfg<K>::MINB) spmm_gather_kernel(
+    Ws ws, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ xoff, const double* __restrict__ val,
+    const double* __restrict__ Xloc, const int R) {
+  using C = GatherCfg<K>;
+  constexpr int LPR = C::LPR, VPL = C::VPL, RG = C::RG, RMAX = C::RMAX, NZCAP = C::NZCAP, UN = 8, K2 = K / 2;
+  __shared__ int32_t s_rp[3][RMAX + 1];
+  __shared__ int32_t s_off[2][NZCAP];
+  __shared__ double s_v[2][NZCAP];
+  __shared__ dd s_acc[4 * VPL][256];
+  if (*ws.status != ST_OK) return;
+  const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
+  const int64_t n = ws.n_loc, G = gridDim.x;
+  const int64_t nchunk = (n + R - 1) / R;
+  const int T = (int)((nchunk - blockIdx.x + G - 1) / G);
+  const char* Xb = reinterpret_cast<const char*>(Xloc);
+  const char* Hb = reinterpret_cast<const char*>(ws.halo);
+  char* Wb = reinterpret_cast<char*>(ws.W);
+  auto r0_of = [=](int t) { return ((int64_t)t * G + blockIdx.x) * R; };
+  auto nr_of = [=](int t) { return (int)min((int64_t)R, n - r0_of(t)); };
+  auto stage_rp = [&](int t) {
+    if (t >= T) return;
+    const int nr = nr_of(t);
+    const int32_t* g = row_ptr + r0_of(t);
+    int32_t* d = s_rp[t % 3];
+    for (int i = tid; i <= nr; i += 256)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(d + i)), "l"(g + i));
+  };
+  auto stage_nz = [&](int t) {   // needs s_rp[t % 3]
+    if (t >= T) return;
+    const int32_t* r = s_rp[t % 3];
+    const int32_t p0 = r[0], cnt = r[nr_of(t)] - p0;
+    for (int i = tid; i < cnt; i += 256) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&s_off[t & 1][i])), "l"(xoff + p0 + i));
+      cp_async8(&s_v[t & 1][i], val + p0 + i, true);
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < 4 * VPL; ++q) s_acc[q][tid] = dd{0.0, 0.0};
+  stage_rp(0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  stage_nz(0);
+  stage_rp(1);
+  cp_async_commit();
+  double ba[2 * VPL], bg[2 * VPL];
+#pragma unroll
+  for (int u = 0; u < 2 * VPL; ++u) ba[u] = bg[u] = 0.0;
+  int nb8 = 0;
+  const double shift = ws.shift;
+  for (int t = 0; t < T; ++t) {
+    cp_async_wait<0>();
+    __syncthreads();
+    stage_nz(t + 1);   // row_ptr of chunk t+1 arrived with the previous group
+    stage_rp(t + 2);
+    cp_async_commit();
+    const int32_t* r = s_rp[t % 3];
+    const int nr = nr_of(t);
+    const int32_t p0 = r[0];
+    const uint32_t rb2 = (uint32_t)r0_of(t) * K2 + l;   // double2 index of (chunk row 0, this lane)
+    const int32_t* so = s_off[t & 1];
+    const double* sv = s_v[t & 1];
+    for (int rl = grp; rl < nr; rl += RG) {
+      const int q0 = r[rl] - p0, q1 = r[rl + 1] - p0;
+      const uint32_t i2 = rb2 + (uint32_t)rl * K2;
+      double2 xi[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) xi[v] = ldg2_at(Xb + 16 * LPR * v, i2);
+      double acc[2 * VPL];
+#pragma unroll
+      for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;
+      for (int qb = q0; qb < q1; qb += UN) {   // all gathers of a batch issued before its fma chain
+        const int cnt = q1 - qb;
+        double2 x[UN][VPL];
+#pragma unroll
+        for (int u = 0; u < UN; ++u)
+          if (u < cnt) {
+            const int32_t off = so[qb + u];
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+              x[u][v] = (!HALO || off >= 0) ? ldg2_at(Xb + 16 * LPR * v, (uint32_t)off + l)
+                                            : ldg2_at(Hb + 16 * LPR * v, (uint32_t)(-1 - off) + l);
+          }
+#pragma unroll
+        for (int u = 0; u < UN; ++u)
+          if (u < cnt) {
+            const double vv = sv[qb + u];
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              acc[2 * v] = __fma_rn(vv, x[u][v].x, acc[2 * v]);
+              acc[2 * v + 1] = __fma_rn(vv, x[u][v].y, acc[2 * v + 1]);
+            }
+          }
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        double w0 = acc[2 * v], w1 = acc[2 * v + 1];
+        if (shift != 0.0) { w0 = __fma_rn(-shift, xi[v].x, w0); w1 = __fma_rn(-shift, xi[v].y, w1); }
+        __stcs(reinterpret_cast<double2*>(Wb + 16 * LPR * v + (uint64_t)i2 * 16u), make_double2(w0, w1));
+        ba[2 * v] = __fma_rn(xi[v].x, xi[v].x, ba[2 * v]);
+        ba[2 * v + 1] = __fma_rn(xi[v].y, xi[v].y, ba[2 * v + 1]);
+        bg[2 * v] = __fma_rn(xi[v].x, w0, bg[2 * v]);
+        bg[2 * v + 1] = __fma_rn(xi[v].y, w1, bg[2 * v + 1]);
+      }
+      if (++nb8 == 8) {   // 8-row FP64 blocks merged into double-double
+        nb8 = 0;
+#pragma unroll
+        for (int u = 0; u < 2 * VPL; ++u) {
+          dd_add1(s_acc[u][tid], ba[u]); dd_add1(s_acc[2 * VPL + u][tid], bg[u]);
+          ba[u] = bg[u] = 0.0;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int u = 0; u < 2 * VPL; ++u) { dd_add1(s_acc[u][tid], ba[u]); dd_add1(s_acc[2 * VPL + u][tid], bg[u]); }
+  __syncthreads();
+  // fixed-order reduction over the RG row groups; thread grp * LPR + l owns columns 2 (l + LPR v) + {0, 1}
+  for (int j = tid; j < K; j += 256) {
+    const int pair = j >> 1, e = j & 1, v = pair / LPR, lj = pair % LPR;
+    const int ua = 2 * v + e, ug = 2 * VPL + 2 * v + e;
+    dd ta = s_acc[ua][lj], tg = s_acc[ug][lj];
+    for (int g = 1; g < RG; ++g) { dd_add(ta, s_acc[ua][g * LPR + lj]); dd_add(tg, s_acc[ug][g * LPR + lj]); }
+    double* slot = ws.ag + ((int64_t)blockIdx.x * K + j) * 4;
+    slot[0] = ta.hi; slot[1] = ta.lo; slot[2] = tg.hi; slot[3] = tg.lo;
+  }
+}
+
+// xoff for spmm_gather_kernel: gather offset of every local nonzero in double2 units
+__global__ void spmm_xoff_kernel(const int32_t* __restrict__ col_idx, int64_t nnz, int64_t row0, int64_t row1,
+                                 int64_t halo_lo, int k2, int32_t* __restrict__ xoff) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = col_idx[q];
+    int64_t o;
+    if (col >= row0 && col < row1) o = (col - row0) * k2;
+    else o = -1 - ((col < row0) ? col - halo_lo : (row0 - halo_lo) + (col - row1)) * k2;
+    xoff[q] = (int32_t)o;
+  }
+}
+
 }  // namespace rf

@@ -307,3 +307,63 @@ def test_repeat_bitwise_k128(pkg):
         R.refine_sweep(X)
         outs.append(X.cpu().numpy())
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+# ------------------------------------------------------------------------------ CSR gather kernel
+
+@pytest.mark.parametrize("k", [2, 4, 8, 16, 64])
+def test_csr_gather_every_k(pkg, k):
+    """spmm_gather_kernel instantiations (k a power of two): bit-identical W, one-step parity."""
+    p = synth.small_laplacian((41, 37), (1.0, 1.37), k)
+    R = refiner(pkg, p)
+    op = op_of(p)
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    assert R.refine_sweep(X) == pkg.REFINE_OK
+    ref = oracle.sweep(op, xin, debug=True)
+    assert rel(X.cpu().numpy(), ref.X) <= TOL
+    assert np.array_equal(R.debug(pkg.DBG_W).cpu().numpy() * ref.debug["sigma"], ref.debug["W"])
+
+
+def _arrow(p, width, eps=1e-3):
+    """Laplacian plus a symmetric 'arrow' coupling row/column 0 to columns 1..width-1 (long rows)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix((p.val.numpy(), p.col_idx.numpy(), p.row_ptr.numpy()), shape=(p.n, p.n))
+    B = sp.lil_matrix((p.n, p.n))
+    for j in range(1, width):
+        B[0, j] = B[j, 0] = eps * (1.0 + (j % 7) / 7.0)
+    C = (A + B.tocsr()).tocsr()
+    C.sort_indices()
+    import dataclasses
+    return dataclasses.replace(p, row_ptr=torch.from_numpy(C.indptr.astype(np.int32)),
+                               col_idx=torch.from_numpy(C.indices.astype(np.int32)),
+                               val=torch.from_numpy(C.data.astype(np.float64)))
+
+
+@pytest.mark.parametrize("width,k", [(700, 32), (3000, 32), (300, 128)])
+def test_csr_gather_long_rows(pkg, width, k):
+    """Rows with many nonzeros shrink the rows-per-chunk R (or fall back to the vec kernel when one
+    chunk cannot be staged at all); the fma chains stay bit-identical to the oracle's."""
+    q = _arrow(synth.small_laplacian((64, 61), (1.0, 1.37), k), width)
+    R = refiner(pkg, q)
+    op = op_of(q)
+    X = q.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    assert R.refine_sweep(X) == pkg.REFINE_OK
+    ref = oracle.sweep(op, xin, debug=True)
+    assert rel(X.cpu().numpy(), ref.X) <= TOL
+    assert np.array_equal(R.debug(pkg.DBG_W).cpu().numpy() * ref.debug["sigma"], ref.debug["W"])
+
+
+def test_csr_gather_matches_vec_kernel(pkg, monkeypatch):
+    """The gather kernel and the previous vec kernel (REFINE_NO_GATHER=1) produce identical W
+    (same fma chains); X agrees to rounding of the alpha / g partial-sum order."""
+    p = synth.small_laplacian((24, 22, 21), (1.0, 1.13, 1.29), 64)
+    Xa, Xb = p.X0.cuda().clone(), p.X0.cuda().clone()
+    Ra = refiner(pkg, p)
+    Ra.refine_sweep(Xa)
+    monkeypatch.setenv("REFINE_NO_GATHER", "1")
+    Rb = refiner(pkg, p)
+    Rb.refine_sweep(Xb)
+    assert torch.equal(Ra.debug(pkg.DBG_W), Rb.debug(pkg.DBG_W))
+    assert rel(Xa.cpu().numpy(), Xb.cpu().numpy()) <= 1e-13
