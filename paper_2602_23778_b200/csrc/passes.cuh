@@ -233,6 +233,242 @@ __global__ void __launch_bounds__(256) passB_reduce_kernel(Ws ws, int nchunk) {
   }
 }
 
+// ---------------------------------------------------------------- pass B, k >= 32
+// CTA tile = all KP output rows a (the X^ columns) x one 64-wide block tb of the [R | X^] column
+// space, so every staged row is read by the CTA's MMAs TA x 64 / (KP + R width) times and the
+// CTA count per row chunk is 2 KP / 64.  BR = 32 rows per stage, one barrier per stage (8 k-steps
+// of DMMA).  The symmetric G half: warp tiles lying strictly below G's diagonal issue no MMAs (the
+// reduction mirrors them), so no flops are spent on them.  R = W - X D is formed in place in the
+// staged W columns of R tiles (one fma per element, exactly once per element over the grid) by
+// the thread that copied both operands, right after its own copies of the NEXT stage land --
+// so the R formation needs no barrier of its own and overlaps the other warps' MMAs; the R tiles
+// also accumulate rr_j = sum r_ij^2.
+template <int KP, int WA_ = 2, int WB_ = 4, int BR_ = 32>
+struct PassB2Cfg {
+  static constexpr int TA = KP, TB = 64, NT = 2 * KP / TB;
+  static constexpr int WA = WA_, WB = WB_;                     // default 8 warps
+  static constexpr int THREADS = WA * WB * 32;
+  static constexpr int WTA = TA / WA, WTB = TB / WB;           // warp tile (KP=128: 64 x 16)
+  static constexpr int MI = WTA / 8, NI = WTB / 8;
+  static constexpr int BR = BR_;
+  static constexpr int LDX = KP + ((KP % 16 == 8) ? 0 : 8);
+  static constexpr int LDW = (KP < TB ? KP : TB) + 8;          // staged R columns of a tile
+  static constexpr int XST = BR * LDX, WST = BR * LDW;
+  static constexpr int SMEM = 2 * (XST + WST) * 8;
+  static constexpr bool PAIRED = (KP == 128 && WA == 2);       // balanced 7-unit grid (see passB2_kernel)
+  static constexpr int MINB = (2 * (XST + WST) * 8 <= 113 * 1024) ? 2 : 1;   // 2 CTAs / SM when smem allows
+};
+
+template <int KP, int WA_ = 2, int WB_ = 4, int BR_ = 32>
+__global__ void __launch_bounds__(PassB2Cfg<KP, WA_, WB_, BR_>::THREADS, PassB2Cfg<KP, WA_, WB_, BR_>::MINB)
+passB2_kernel(Ws ws, const double* __restrict__ X, int vec16) {
+  using C = PassB2Cfg<KP, WA_, WB_, BR_>;
+  constexpr int THREADS = C::THREADS, BR = C::BR, TB = C::TB;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double sd[KP];
+  __shared__ double srr[2][THREADS];
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wa = warp / C::WB, wb = warp % C::WB;
+  // KP = 128: the X0 tile does half the MMAs of the others (G10 skipped), so the grid is made of
+  // balanced work units -- per pair of row chunks: R0, R1, X1 for each chunk (6 units) plus one
+  // X0 unit spanning both chunks (gridDim.x = 7 x pairs).  Otherwise gridDim = (NT, chunks).
+  int tb, span = 1;
+  int64_t cidx, nchunk;
+  if (C::PAIRED) {
+    const int u = blockIdx.x, pair = u / 7, w = u % 7;
+    nchunk = 2 * (int64_t)(gridDim.x / 7);
+    if (w < 6) { tb = (w % 3 == 2) ? 3 : (w % 3); cidx = 2 * pair + w / 3; }
+    else { tb = 2; cidx = 2 * pair; span = 2; }
+  } else {
+    tb = blockIdx.x; cidx = blockIdx.y; nchunk = gridDim.y;
+  }
+  const int b0 = tb * TB;                                     // [R | X] columns [b0, b0 + 64)
+  const int rw = (b0 < KP) ? min(TB, KP - b0) : 0;           // R columns of this tile: [b0, b0 + rw)
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + nchunk - 1) / nchunk + BR - 1) / BR * BR;
+  const int64_t rb = ws.top + cidx * per;
+  const int64_t re = (rb + span * per < ws.n_loc) ? rb + span * per : ws.n_loc;
+  const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
+  for (int j = tid; j < KP; j += THREADS) sd[j] = (j < k) ? ws.d[j] : 0.0;
+  double* Xs = smem;
+  double* Wsm = smem + 2 * C::XST;
+  // this warp's MMAs: skipped when its block lies strictly below the diagonal of G = X^T X
+  const int a_lo = wa * C::WTA, bw = b0 + wb * C::WTB;       // first a row, first [R|X] column
+  const bool active = !(bw >= KP && a_lo >= (bw - KP) + C::WTB);
+  // R chunks: the thread that copies W[r][b0+c..] also copies X[r][b0+c..], so it can form those
+  // R entries as soon as its own copies land (no barrier).  Its R columns are fixed.
+  const int rpair = vec16 ? 2 : 1;
+  const int rcpr = (rw > 0) ? rw / rpair : 1;                 // R chunks per row
+  const int rcol = (tid % rcpr) * rpair;                      // this thread's R column(s) b0 + rcol (+1)
+
+  auto load = [&](int buf, int it) {
+    const int64_t r0 = rb + (int64_t)it * BR;
+    double* xs = Xs + buf * C::XST;
+    double* wsb = Wsm + buf * C::WST;
+    if (vec16) {
+      for (int c = tid; c < BR * rw / 2; c += THREADS) {     // paired W / X chunks of the R columns
+        const int r = c / (rw / 2), cc = (c % (rw / 2)) * 2;
+        const int64_t g = r0 + r;
+        const bool ok = (g < re) && (b0 + cc < k);
+        cp_async16(wsb + r * C::LDW + cc, ws.W + (ok ? g * k + b0 + cc : 0), ok);
+        cp_async16(xs + r * C::LDX + b0 + cc, X + (ok ? g * k + b0 + cc : 0), ok);
+      }
+      constexpr int H = KP / 2;
+      for (int c = tid; c < BR * H; c += THREADS) {           // the other X columns
+        const int r = c / H, cc = (c % H) * 2;
+        if (cc >= b0 && cc < b0 + rw) continue;
+        const int64_t g = r0 + r;
+        const bool ok = (g < re) && (cc < k);
+        cp_async16(xs + r * C::LDX + cc, X + (ok ? g * k + cc : 0), ok);
+      }
+    } else {
+      for (int c = tid; c < BR * rw; c += THREADS) {
+        const int r = c / rw, cc = c % rw;
+        const int64_t g = r0 + r;
+        const bool ok = (g < re) && (b0 + cc < k);
+        cp_async8(wsb + r * C::LDW + cc, ws.W + (ok ? g * k + b0 + cc : 0), ok);
+        cp_async8(xs + r * C::LDX + b0 + cc, X + (ok ? g * k + b0 + cc : 0), ok);
+      }
+      for (int c = tid; c < BR * KP; c += THREADS) {
+        const int r = c / KP, cc = c % KP;
+        if (cc >= b0 && cc < b0 + rw) continue;
+        const int64_t g = r0 + r;
+        const bool ok = (g < re) && (cc < k);
+        cp_async8(xs + r * C::LDX + cc, X + (ok ? g * k + cc : 0), ok);
+      }
+    }
+  };
+  double rr0 = 0.0, rr1 = 0.0;
+  // R = W - X D for this thread's own (landed) chunks of stage buffer buf, in place (fma as in the oracle)
+  auto form_r = [&](int buf) {
+    const double* xs = Xs + buf * C::XST;
+    double* wsb = Wsm + buf * C::WST;
+    const double d0 = sd[b0 + rcol], d1 = sd[b0 + rcol + (rpair - 1)];
+    for (int c = tid; c < BR * rcpr; c += THREADS) {
+      const int r = c / rcpr;
+      const double v0 = __fma_rn(-xs[r * C::LDX + b0 + rcol], d0, wsb[r * C::LDW + rcol]);
+      wsb[r * C::LDW + rcol] = v0;
+      rr0 = __fma_rn(v0, v0, rr0);
+      if (rpair == 2) {
+        const double v1 = __fma_rn(-xs[r * C::LDX + b0 + rcol + 1], d1, wsb[r * C::LDW + rcol + 1]);
+        wsb[r * C::LDW + rcol + 1] = v1;
+        rr1 = __fma_rn(v1, v1, rr1);
+      }
+    }
+  };
+
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (nit > 0) load(0, 0);
+  cp_async_commit();
+  __syncthreads();                                            // sd visible to form_r
+  cp_async_wait<0>();
+  if (rw > 0 && nit > 0) form_r(0);
+  // iteration it: [barrier] issue stage it+1 -> MMAs of stage it -> wait own copies of it+1 -> R(it+1)
+  for (int it = 0; it < nit; ++it) {
+    const int cur = it & 1;
+    __syncthreads();
+    if (it + 1 < nit) load(cur ^ 1, it + 1);
+    cp_async_commit();
+    const double* xs = Xs + cur * C::XST;
+    const double* wsb = Wsm + cur * C::WST;
+    if (active) {
+#pragma unroll
+      for (int kk = 0; kk < BR; kk += 4) {
+        const int row = kk + (lane & 3);
+        double a[C::MI], b[C::NI];
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i) a[i] = xs[row * C::LDX + a_lo + i * 8 + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int cb8 = bw + j * 8;                         // 8-column block: all R or all X (warp-uniform)
+          b[j] = (cb8 < KP) ? wsb[row * C::LDW + (cb8 - b0) + (lane >> 2)] : xs[row * C::LDX + cb8 - KP + (lane >> 2)];
+        }
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    cp_async_wait<0>();
+    if (rw > 0 && it + 1 < nit) form_r(cur ^ 1);
+  }
+  if (active) {
+    for (int q = 0; q < span; ++q) {          // a two-chunk unit stores its sum in the first slot, 0 in the second
+      double* out = ws.bpart + ((cidx + q) * C::NT + tb) * (C::TA * TB);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int ra = a_lo + i * 8 + (lane >> 2);
+          const int cb = wb * C::WTB + j * 8 + 2 * (lane & 3);
+          out[ra * TB + cb] = q ? 0.0 : acc[i][j][0];
+          out[ra * TB + cb + 1] = q ? 0.0 : acc[i][j][1];
+        }
+    }
+  }
+  if (rw > 0) {   // threads t, t + rcpr, ... share the R column(s) b0 + rcol (+1): fixed-order sum
+    srr[0][tid] = rr0;
+    srr[1][tid] = rr1;
+    __syncthreads();
+    if (tid < rcpr) {
+      double s0 = srr[0][tid], s1 = srr[1][tid];
+      for (int q = 1; q < THREADS / rcpr; ++q) { s0 += srr[0][q * rcpr + tid]; s1 += srr[1][q * rcpr + tid]; }
+      ws.brr[cidx * KP + b0 + rcol] = s0;
+      if (rpair == 2) ws.brr[cidx * KP + b0 + rcol + 1] = s1;
+    }
+  }
+}
+
+// Sum pass-B2 partials over chunks in fixed order -> M2, G2 (mirrored from its upper triangle), rr2.
+template <int KP>
+__global__ void __launch_bounds__(256) passB2_reduce_kernel(Ws ws, int nchunk) {
+  using C = PassB2Cfg<KP>;
+  __shared__ double part[8][33];
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k;
+  const int total = k * 2 * k + k;
+  const int el = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + el;
+  const int c0 = (int)((int64_t)nchunk * rg / 8), c1 = (int)((int64_t)nchunk * (rg + 1) / 8);
+  double s = 0.0;
+  if (e < total) {
+    if (e >= 2 * k * k) {
+      const int j = e - 2 * k * k;
+      s = sum_strided(ws.brr + (int64_t)c0 * KP + j, KP, c1 - c0);
+    } else {
+      int a = e / (2 * k), bb = e % (2 * k);
+      int col;                                           // column in the padded [R | X] space
+      if (bb < k) {
+        col = bb;
+      } else {                                           // G[a][g] = G[min][max] (upper triangle)
+        const int g = bb - k, lo = a < g ? a : g, hi = a < g ? g : a;
+        a = lo;
+        col = KP + hi;
+      }
+      const int tile = col / C::TB, off = a * C::TB + (col % C::TB);
+      s = sum_strided(ws.bpart + ((int64_t)c0 * C::NT + tile) * (C::TA * C::TB) + off,
+                      (int64_t)C::NT * C::TA * C::TB, c1 - c0);
+    }
+  }
+  part[rg][el] = s;
+  __syncthreads();
+  if (rg == 0 && e < total) {
+    for (int q = 1; q < 8; ++q) s += part[q][el];
+    if (e >= 2 * k * k) {
+      ws.rr2[e - 2 * k * k] = s;
+    } else {
+      const int a = e / (2 * k), bb = e % (2 * k);
+      if (bb < k) ws.M2[a * k + bb] = s;
+      else ws.G2[a * k + (bb - k)] = s;
+    }
+  }
+}
+
 // pass C CTA: BM rows x NC output columns (blockIdx.y selects the column block), Csig[:, cols]
 // resident in shared memory for the CTA's lifetime (persistent over row tiles).
 template <int KP, int NC, int BM, int WARPS_M, int WARPS_N>

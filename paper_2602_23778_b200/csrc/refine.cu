@@ -254,14 +254,24 @@ struct Kern {
   using BC = PassBCfg<KP, BTA, BTB, BWA, BWB, BBR>;
   using CC = PassCCfg<KP, CNC, CBM, CWM, CWN>;
   static constexpr auto gemm = gemm_ax_kernel<KP, GBM, GWM, GWN, GBK, GST>;
-  static constexpr auto passB = passB_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
-  static constexpr auto passBred = passB_reduce_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
+  // k = 128: pass B2 (all-a CTA tiles, balanced 7-unit grid); smaller k: the 2-D tiled pass B
+  // (measured faster there: cfg4 0.19 vs 0.22 ms, cfg3 0.034 vs 0.039 ms)
+  static constexpr bool B2 = KP >= 128;
+  using B2C = PassB2Cfg<(KP >= 32 ? KP : 32)>;
+  static constexpr auto passB = B2 ? (decltype(&passB_kernel<KP, BTA, BTB, BWA, BWB, BBR>))passB2_kernel<(KP >= 32 ? KP : 32)>
+                                   : passB_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
+  static constexpr auto passBred = B2 ? (decltype(&passB_reduce_kernel<KP, BTA, BTB, BWA, BWB, BBR>))passB2_reduce_kernel<(KP >= 32 ? KP : 32)>
+                                      : passB_reduce_kernel<KP, BTA, BTB, BWA, BWB, BBR>;
+  static constexpr int B_THREADS = B2 ? B2C::THREADS : BC::THREADS;
+  static constexpr int B_SMEM = B2 ? B2C::SMEM : BC::SMEM;
+  static constexpr int B_NT = B2 ? B2C::NT : BC::NTILES;
+  static constexpr size_t B_TILE = B2 ? (size_t)B2C::TA * B2C::TB : (size_t)BTA * BTB;
   static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN>;
 
   static cudaError_t setup(refine_ctx* c) {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM))) return e;
-    if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, BC::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passC, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
     int occ = 1;
     // dense GEMM: split-K so the grid fills whole waves of resident CTAs
@@ -289,11 +299,15 @@ struct Kern {
       c->kchunk = kit * GBK;
       c->nsplit = (int)((c->n + c->kchunk - 1) / c->kchunk);
     }
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passB, BC::THREADS, BC::SMEM))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passB, B_THREADS, B_SMEM))) return e;
     occ = std::max(occ, 1);
     const int64_t rows = std::max<int64_t>(c->n_loc - c->ws.top, 1);
     const int64_t max_chunks = std::max<int64_t>((rows + 255) / 256, 1);   // >= 256 rows per chunk
-    c->passb_grid_y = (int)std::min<int64_t>(std::max(c->sms * occ / BC::NTILES, 1), max_chunks);
+    c->passb_grid_y = (int)std::min<int64_t>(std::max(c->sms * occ / B_NT, 1), max_chunks);
+    if (B2 && B2C::PAIRED) {   // 7 balanced units per pair of chunks (passB2_kernel)
+      const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * occ / 7, std::max<int64_t>(max_chunks / 2, 1)));
+      c->passb_grid_y = 2 * pairs;
+    }
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passC, CC::THREADS, CC::SMEM))) return e;
     occ = std::max(occ, 1);
     const int64_t ctiles = std::max<int64_t>((rows + CBM - 1) / CBM, 1);
@@ -302,7 +316,7 @@ struct Kern {
   }
 
   static void sizes(refine_ctx* c, size_t& bpart, size_t& brr, size_t& nslot) {
-    bpart = (size_t)c->passb_grid_y * BC::NTILES * BTA * BTB;
+    bpart = (size_t)c->passb_grid_y * B_NT * B_TILE;
     brr = (size_t)c->passb_grid_y * KP;
     nslot = (size_t)c->passc_grid * KP;
   }
@@ -354,7 +368,10 @@ struct Kern {
         break;
       case 2:  // S4 reductions
         c->mark();
-        passB<<<dim3(BC::NTILES, c->passb_grid_y), BC::THREADS, BC::SMEM, s>>>(ws, X, xv16);
+        if (B2 && B2C::PAIRED)
+          passB<<<dim3(7 * (c->passb_grid_y / 2)), B_THREADS, B_SMEM, s>>>(ws, X, xv16);
+        else
+          passB<<<dim3(B_NT, c->passb_grid_y), B_THREADS, B_SMEM, s>>>(ws, X, xv16);
         c->mark();
         passBred<<<(2 * c->k * c->k + c->k + 31) / 32, 256, 0, s>>>(ws, c->passb_grid_y);
         n += 2;
