@@ -137,7 +137,7 @@ struct refine_ctx {
   const double* val = nullptr;
   // CSR gather kernel (spmm_gather_kernel): rows per chunk (0 = not eligible -> vec / generic
   // kernel) and the precomputed gather offsets (owned; indexed by absolute CSR position)
-  int gather_R = 0;
+  int gather_R = 0, gather_un = 8;
   int32_t* xoff_buf = nullptr;
   const int32_t* xoff = nullptr;
   double shift = 0.0;
@@ -213,15 +213,23 @@ static void launch_spmm(refine_ctx* c, bool vec, double* X) {
   const int g = c->spmm_grid;
   if (vec && c->gather_R > 0) {   // vec: 16-byte aligned X / halo rows
     const int R = c->gather_R;
+    auto go = [&](auto kern) { kern<<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); };
+#define RF_GATHER_K(KK)                                                          \
+  case KK:                                                                       \
+    if (c->gather_un == 5) go(spmm_gather_kernel<KK, HALO, 5>);                  \
+    else if (c->gather_un == 7) go(spmm_gather_kernel<KK, HALO, 7>);             \
+    else go(spmm_gather_kernel<KK, HALO, 8>);                                    \
+    break;
     switch (c->k) {
-      case 2: spmm_gather_kernel<2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
-      case 4: spmm_gather_kernel<4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
-      case 8: spmm_gather_kernel<8, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
-      case 16: spmm_gather_kernel<16, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
-      case 32: spmm_gather_kernel<32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
-      case 64: spmm_gather_kernel<64, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
-      default: spmm_gather_kernel<128, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); break;
+      RF_GATHER_K(2)
+      RF_GATHER_K(4)
+      RF_GATHER_K(8)
+      RF_GATHER_K(16)
+      RF_GATHER_K(32)
+      RF_GATHER_K(64)
+      default: RF_GATHER_K(128)
     }
+#undef RF_GATHER_K
     return;
   }
   if (vec) {
@@ -422,14 +430,14 @@ static refine_ctx* ctx0(refine_ctx* c) { return c->loopback ? c->kids[0] : c; }
 
 // spmm_gather_kernel eligibility and geometry (k a power of two <= 128, 32-bit gather offsets):
 // resident grid and the largest rows-per-chunk R whose chunks all fit the staged nonzero buffer.
-template <int K>
-static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp) {
-  using G = GatherCfg<K>;
+template <int K, int UN>
+static cudaError_t gather_geometry_un(refine_ctx* c, const std::vector<int32_t>& rp) {
+  using G = GatherCfg<K, UN>;
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_gather_kernel<K, false>, 256, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_gather_kernel<K, false, UN>, 256, 0);
   if (e != cudaSuccess) return e;
   int occ2 = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, spmm_gather_kernel<K, true>, 256, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, spmm_gather_kernel<K, true, UN>, 256, 0);
   if (e != cudaSuccess) return e;
   occ = std::max(1, std::min(occ, occ2));
   const int64_t n = c->n_loc;
@@ -440,11 +448,29 @@ static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp
     if (worst <= G::NZCAP) R = r;
   }
   c->gather_R = R;
+  c->gather_un = UN;
   if (R > 0) {
     const int64_t chunks = (n + R - 1) / R;
     c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sms * occ, chunks));
   }
   return cudaSuccess;
+}
+
+// batch size UN: the smallest of {5, 7, 8} covering 95% of the rows (the stencils' 5 / 7)
+template <int K>
+static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp) {
+  const int64_t n = c->n_loc;
+  int64_t cnt[10] = {0};
+  for (int64_t i = 0; i < n; ++i) cnt[std::min<int64_t>(rp[i + 1] - rp[i], 9)]++;
+  int64_t acc = 0;
+  int p95 = 9;
+  for (int v = 0; v <= 9; ++v) {
+    acc += cnt[v];
+    if (acc * 100 >= n * 95) { p95 = v; break; }
+  }
+  if (p95 <= 5) return gather_geometry_un<K, 5>(c, rp);
+  if (p95 <= 7) return gather_geometry_un<K, 7>(c, rp);
+  return gather_geometry_un<K, 8>(c, rp);
 }
 
 static cudaError_t gather_setup(refine_ctx* c) {

@@ -189,27 +189,35 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
 // chain, so W is bit-identical to the oracle given identical X (P3).  alpha / g: 8-row
 // FP64 blocks merged into double-double accumulators in shared memory; fixed-order CTA reduction,
 // one slot per CTA: ws.ag[(blockIdx.x * K + j) * 4 + {a_hi, a_lo, g_hi, g_lo}].
-template <int K>
+// UN = gathers per batch = the matrix's typical row length (chosen at init from {5, 7, 8}): a batch
+// sized to the row keeps every register of x[UN] useful (cfg4 5-point rows: UN=5, 0.142 vs 0.188 ms
+// at UN=8; cfg5 7-point rows: UN=7, 2.34 vs 2.75 ms), which is what lets 4 CTAs / SM fit at k <= 64.
+template <int K, int UN_ = 8, int LPR_ = 0, int MINB_ = 0>
 struct GatherCfg {
-  static constexpr int LPR = K / 2 < 32 ? K / 2 : 32;   // lanes per row
+  static constexpr int LPR = LPR_ ? LPR_ : (K / 2 < 32 ? K / 2 : 32);   // lanes per row
   static constexpr int VPL = K / (2 * LPR);              // double2 per lane
   static constexpr int RG = 256 / LPR;                   // rows in flight per CTA
-  static constexpr int RMAX = VPL > 1 ? RG * 4 : (RG * 8 > 256 ? 256 : RG * 8);   // measured best at cfg4 / cfg5
+  static constexpr int RMAX = VPL > 1 ? (RG * 4 < 64 ? RG * 4 : 64) : (RG * 8 > 256 ? 256 : RG * 8);   // measured best at cfg4 / cfg5
   static constexpr int NZCAP = RMAX * 8 < 1024 ? RMAX * 8 : 1024;
-  static constexpr int MINB = K >= 128 ? 2 : 3;
+  static constexpr int UN = UN_;                         // gathers per batch
+  static constexpr int MINB = MINB_ ? MINB_ : (K >= 128 ? 2 : (UN <= 5 ? 4 : 3));
 };
 
 RF_DEV double2 ldg2_at(const char* base, uint32_t idx2) {   // base + idx2 double2s (one IMAD.WIDE.U32)
   return __ldg(reinterpret_cast<const double2*>(base + (uint64_t)idx2 * 16u));
 }
 
+RF_DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p)); }
+
 // requires n_loc * K / 2 < 2^31 and halo rows * K / 2 < 2^31 (checked at init)
-template <int K, bool HALO>
-__global__ void __launch_bounds__(256, GatherCfg<K>::MINB) spmm_gather_kernel(
+// PF = 1: before a row's fma chain, prefetch (into L1, no registers held) the X rows the group's
+// NEXT row gathers, so two rows' gathers are in flight per group.
+template <int K, bool HALO, int UN_ = 8, int PF = 0, int LPR_ = 0, int MINB_ = 0>
+__global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spmm_gather_kernel(
     Ws ws, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ xoff, const double* __restrict__ val,
     const double* __restrict__ Xloc, const int R) {
-  using C = GatherCfg<K>;
-  constexpr int LPR = C::LPR, VPL = C::VPL, RG = C::RG, RMAX = C::RMAX, NZCAP = C::NZCAP, UN = 8, K2 = K / 2;
+  using C = GatherCfg<K, UN_, LPR_, MINB_>;
+  constexpr int LPR = C::LPR, VPL = C::VPL, RG = C::RG, RMAX = C::RMAX, NZCAP = C::NZCAP, UN = C::UN, K2 = K / 2;
   __shared__ int32_t s_rp[3][RMAX + 1];
   __shared__ int32_t s_off[2][NZCAP];
   __shared__ double s_v[2][NZCAP];
@@ -273,6 +281,16 @@ __global__ void __launch_bounds__(256, GatherCfg<K>::MINB) spmm_gather_kernel(
       double2 xi[VPL];
 #pragma unroll
       for (int v = 0; v < VPL; ++v) xi[v] = ldg2_at(Xb + 16 * LPR * v, i2);
+      if (PF && rl + RG < nr) {
+        const int n0 = r[rl + RG] - p0, n1 = r[rl + RG + 1] - p0;
+        for (int q = n0; q < n1; ++q) {
+          const int32_t off = so[q];
+          const char* base = (!HALO || off >= 0) ? Xb + (uint64_t)((uint32_t)off + l) * 16u
+                                                 : Hb + (uint64_t)((uint32_t)(-1 - off) + l) * 16u;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) prefetch_l1(base + 16 * LPR * v);
+        }
+      }
       double acc[2 * VPL];
 #pragma unroll
       for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;

@@ -74,9 +74,9 @@ struct Prob {
 
 
 
-template <int K>
+template <int K, int PF = 0, int LPR = 0, int MINB = 0, int UN = 8>
 static void gather_case(const char* name, const Prob& p, int sms, const double* Wref, int R, int occ_override = 0) {
-  auto kern = spmm_gather_kernel<K, false>;
+  auto kern = spmm_gather_kernel<K, false, UN, PF, LPR, MINB>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ_override) occ = occ_override;
@@ -91,7 +91,7 @@ static void gather_case(const char* name, const Prob& p, int sms, const double* 
   cudaMemcpy(b.data(), Wref, b.size() * 8, cudaMemcpyDeviceToHost);
   int64_t bad = 0;
   for (size_t i = 0; i < a.size(); ++i) bad += (a[i] != b[i]);
-  printf("%s gather K=%d R=%d occ=%d grid=%d: %.3f ms %6.0f GB/s  mismatches %lld\n", name, K, R, occ, gx, ms,
+  printf("%s gather PF=%d LPR=%d MINB=%d UN=%d K=%d R=%d occ=%d grid=%d: %.3f ms %6.0f GB/s  mismatches %lld\n", name, PF, LPR, MINB, UN, K, R, occ, gx, ms,
          p.bytes / ms / 1e6, (long long)bad);
 }
 
@@ -153,15 +153,18 @@ int main(int argc, char** argv) {
     Prob p = make(1024, 1021, 1, 32);
     double* Wref = prod_case<1, 16>("cfg4", p, sms);
     gather_case<32>("cfg4", p, sms, Wref, 128);
-    gather_case<32>("cfg4", p, sms, Wref, 64);
-    gather_case<32>("cfg4", p, sms, Wref, 128, 2);
+    gather_case<32, 0, 0, 4, 7>("cfg4", p, sms, Wref, 128);
+    gather_case<32, 0, 0, 4, 5>("cfg4", p, sms, Wref, 128);
+    gather_case<32, 0, 0, 4, 6>("cfg4", p, sms, Wref, 128);
+    gather_case<32, 0, 0, 3, 7>("cfg4", p, sms, Wref, 128);
   }
   if (which == 0 || which == 5) {
     Prob p = make(160, 160, 160, 128);
     double* Wref = prod_case<2, 32>("cfg5", p, sms);
-    gather_case<128>("cfg5", p, sms, Wref, 64);
-    gather_case<128>("cfg5", p, sms, Wref, 32);
-    gather_case<128>("cfg5", p, sms, Wref, 16);
+    gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32);
+    gather_case<128, 0, 0, 2, 8>("cfg5", p, sms, Wref, 32);
+    gather_case<128, 0, 0, 2, 6>("cfg5", p, sms, Wref, 32);
+    gather_case<128, 0, 0, 2, 4>("cfg5", p, sms, Wref, 32);
   }
   return 0;
 }
