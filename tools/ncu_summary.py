@@ -27,15 +27,16 @@ def launches(path, out):
             scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(
                 d["Metric Unit"], 1.0)
             agg.setdefault(name, []).append(v * scale)
-    ours = {k: v for k, v in agg.items() if k.split("<")[0].split("::")[-1] in (
-        "gemm_ax_kernel", "w_finish_kernel", "kxk_prep_kernel", "passB_kernel", "passB_reduce_kernel",
-        "kxk_finish_kernel", "passC_kernel", "norm_reduce_kernel", "normalize_kernel", "spmm_csr_kernel",
-        "spmm_csr_vec_kernel", "absrow_max_dense_kernel", "absrow_max_csr_kernel", "max_kernel")}
-    tot = sum(sum(v) / len(v) for k, v in ours.items() if "absrow" not in k and "max_kernel" not in k)
+    skip = ("absrow_max_dense_kernel", "absrow_max_csr_kernel", "max_kernel", "col_range_kernel", "spmm_xoff_kernel")
+    mine = ("gemm_ax", "w_finish", "kxk_", "passB", "passC", "norm_reduce", "normalize", "spmm_", "ag_local",
+            "absrow_max", "max_kernel", "col_range")
+    ours = {k: v for k, v in agg.items() if any(m in k.split("<")[0] for m in mine)}
+    init = lambda k: any(x in k for x in skip)
+    tot = sum(sum(v) / len(v) for k, v in ours.items() if not init(k))
     res = {"source": path, "note": "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised); "
                                   "per-kernel mean us per launch and share of the per-sweep kernel time",
            "kernels": {k: {"launches": len(v), "mean_us": sum(v) / len(v),
-                           "share_of_sweep": (sum(v) / len(v)) / tot if "absrow" not in k and "max_kernel" not in k else None}
+                           "share_of_sweep": (sum(v) / len(v)) / tot if not init(k) else None}
                        for k, v in ours.items()},
            "sweep_kernel_time_us": tot}
     json.dump(res, open(out, "w"), indent=1)
