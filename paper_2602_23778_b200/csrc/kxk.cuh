@@ -493,20 +493,35 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
 }
 
 // ---------------------------------------------------------------- norm_reduce
-__global__ void __launch_bounds__(128) norm_reduce_kernel(Ws ws) {
+// Column sums of x~^2 over pass C's slots: P = 1024 / k contiguous slot ranges per column summed
+// in parallel (loads batched 8 at a time), then a fixed pairwise tree over the ranges, plus the
+// top block (deterministic; was one thread per column, latency bound at ~40 us for 444 slots).
+__global__ void __launch_bounds__(KXK_THREADS) norm_reduce_kernel(Ws ws) {
+  __shared__ double part[KXK_THREADS];
   if (*ws.status != ST_OK) return;
-  const int j = threadIdx.x;
-  if (j >= ws.k) return;
-  double s = ws.ntop[j];
-  int q = 0;
-  for (; q + 8 <= ws.n_nslot; q += 8) {
-    double v[8];
+  const int k = ws.k, tid = threadIdx.x;
+  const int P = KXK_THREADS / k, j = tid % k, p = tid / k;
+  double s = 0.0;
+  if (p < P) {
+    const int q0 = (int)((int64_t)ws.n_nslot * p / P), q1 = (int)((int64_t)ws.n_nslot * (p + 1) / P);
+    int q = q0;
+    for (; q + 8 <= q1; q += 8) {
+      double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = ws.nslot[(int64_t)(q + u) * ws.kp + j];
+      for (int u = 0; u < 8; ++u) v[u] = ws.nslot[(int64_t)(q + u) * ws.kp + j];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s += v[u];
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; q < q1; ++q) s += ws.nslot[(int64_t)q * ws.kp + j];
   }
-  for (; q < ws.n_nslot; ++q) s += ws.nslot[(int64_t)q * ws.kp + j];
+  part[tid] = s;
+  __syncthreads();
+  for (int st = 1; st < P; st *= 2) {
+    if (p < P && (p % (2 * st)) == 0 && p + st < P) part[tid] += part[tid + st * k];
+    __syncthreads();
+  }
+  if (tid >= k) return;
+  s = ws.ntop[j] + part[j];
   if (ws.multi) {          // partial for the all-gather; normalize_kernel combines in rank order
     ws.nrm_send[j] = s;
     return;

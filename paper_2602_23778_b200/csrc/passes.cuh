@@ -16,6 +16,8 @@
 
 namespace rf {
 
+constexpr int PB_RED_THREADS = 512;   // pass-B partial reduction: 32 elements x 16 chunk ranges per block
+
 template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
 struct PassBCfg {
   static constexpr int THREADS = WARPS_A * WARPS_B * 32;
@@ -190,17 +192,18 @@ __device__ __forceinline__ double sum_strided(const double* __restrict__ p, int6
 }
 
 // Sum pass-B partials over chunks in fixed order -> M2 (k x k), G2 (k x k), rr2 (k).
-// Block = 32 elements x 8 contiguous chunk ranges; the 8 range sums are combined in order.
+// Block = 32 elements x NR contiguous chunk ranges; the NR range sums are combined in order.
 template <int KP, int TA, int TB, int WARPS_A, int WARPS_B, int BR>
-__global__ void __launch_bounds__(256) passB_reduce_kernel(Ws ws, int nchunk) {
+__global__ void __launch_bounds__(PB_RED_THREADS) passB_reduce_kernel(Ws ws, int nchunk) {
   using C = PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>;
-  __shared__ double part[8][33];
+  constexpr int NR = PB_RED_THREADS / 32;              // contiguous chunk ranges per element
+  __shared__ double part[NR][33];
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int total = k * 2 * k + k;
   const int el = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + el;
-  const int c0 = (int)((int64_t)nchunk * rg / 8), c1 = (int)((int64_t)nchunk * (rg + 1) / 8);
+  const int c0 = (int)((int64_t)nchunk * rg / NR), c1 = (int)((int64_t)nchunk * (rg + 1) / NR);
   double s = 0.0;
   if (e < total) {
     if (e >= 2 * k * k) {
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(256) passB_reduce_kernel(Ws ws, int nchunk) {
   part[rg][el] = s;
   __syncthreads();
   if (rg == 0 && e < total) {
-    for (int q = 1; q < 8; ++q) s += part[q][el];
+    for (int q = 1; q < NR; ++q) s += part[q][el];
     if (e >= 2 * k * k) {
       ws.rr2[e - 2 * k * k] = s;
     } else {
@@ -426,15 +429,16 @@ passB2_kernel(Ws ws, const double* __restrict__ X, int vec16) {
 
 // Sum pass-B2 partials over chunks in fixed order -> M2, G2 (mirrored from its upper triangle), rr2.
 template <int KP>
-__global__ void __launch_bounds__(256) passB2_reduce_kernel(Ws ws, int nchunk) {
+__global__ void __launch_bounds__(PB_RED_THREADS) passB2_reduce_kernel(Ws ws, int nchunk) {
   using C = PassB2Cfg<KP>;
-  __shared__ double part[8][33];
+  constexpr int NR = PB_RED_THREADS / 32;              // contiguous chunk ranges per element
+  __shared__ double part[NR][33];
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int total = k * 2 * k + k;
   const int el = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + el;
-  const int c0 = (int)((int64_t)nchunk * rg / 8), c1 = (int)((int64_t)nchunk * (rg + 1) / 8);
+  const int c0 = (int)((int64_t)nchunk * rg / NR), c1 = (int)((int64_t)nchunk * (rg + 1) / NR);
   double s = 0.0;
   if (e < total) {
     if (e >= 2 * k * k) {
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(256) passB2_reduce_kernel(Ws ws, int nchunk) {
   part[rg][el] = s;
   __syncthreads();
   if (rg == 0 && e < total) {
-    for (int q = 1; q < 8; ++q) s += part[q][el];
+    for (int q = 1; q < NR; ++q) s += part[q][el];
     if (e >= 2 * k * k) {
       ws.rr2[e - 2 * k * k] = s;
     } else {

@@ -381,7 +381,7 @@ struct Kern {
         else
           passB<<<dim3(B_NT, c->passb_grid_y), B_THREADS, B_SMEM, s>>>(ws, X, xv16);
         c->mark();
-        passBred<<<(2 * c->k * c->k + c->k + 31) / 32, 256, 0, s>>>(ws, c->passb_grid_y);
+        passBred<<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(ws, c->passb_grid_y);
         n += 2;
         break;
       case 3:  // k x k algebra (rank 0), after the side-stream S3 joins
@@ -396,7 +396,7 @@ struct Kern {
         c->mark();
         passC<<<dim3(c->passc_grid, KP / CNC), CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
         c->mark();
-        norm_reduce_kernel<<<1, 128, 0, s>>>(ws);
+        norm_reduce_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
         n += 2;
         break;
       case 5:  // S7

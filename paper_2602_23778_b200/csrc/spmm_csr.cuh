@@ -207,12 +207,9 @@ RF_DEV double2 ldg2_at(const char* base, uint32_t idx2) {   // base + idx2 doubl
   return __ldg(reinterpret_cast<const double2*>(base + (uint64_t)idx2 * 16u));
 }
 
-RF_DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p)); }
-
-// requires n_loc * K / 2 < 2^31 and halo rows * K / 2 < 2^31 (checked at init)
-// PF = 1: before a row's fma chain, prefetch (into L1, no registers held) the X rows the group's
-// NEXT row gathers, so two rows' gathers are in flight per group.
-template <int K, bool HALO, int UN_ = 8, int PF = 0, int LPR_ = 0, int MINB_ = 0>
+// requires n_loc * K / 2 < 2^31 and halo rows * K / 2 < 2^31 (checked at init).  (Measured and
+// dropped: L1 prefetch of the next row's gathers, two rows per group in flight -- both slower.)
+template <int K, bool HALO, int UN_ = 8, int LPR_ = 0, int MINB_ = 0>
 __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spmm_gather_kernel(
     Ws ws, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ xoff, const double* __restrict__ val,
     const double* __restrict__ Xloc, const int R) {
@@ -275,48 +272,12 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
     const uint32_t rb2 = (uint32_t)r0_of(t) * K2 + l;   // double2 index of (chunk row 0, this lane)
     const int32_t* so = s_off[t & 1];
     const double* sv = s_v[t & 1];
-    for (int rl = grp; rl < nr; rl += RG) {
-      const int q0 = r[rl] - p0, q1 = r[rl + 1] - p0;
-      const uint32_t i2 = rb2 + (uint32_t)rl * K2;
-      double2 xi[VPL];
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) xi[v] = ldg2_at(Xb + 16 * LPR * v, i2);
-      if (PF && rl + RG < nr) {
-        const int n0 = r[rl + RG] - p0, n1 = r[rl + RG + 1] - p0;
-        for (int q = n0; q < n1; ++q) {
-          const int32_t off = so[q];
-          const char* base = (!HALO || off >= 0) ? Xb + (uint64_t)((uint32_t)off + l) * 16u
-                                                 : Hb + (uint64_t)((uint32_t)(-1 - off) + l) * 16u;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) prefetch_l1(base + 16 * LPR * v);
-        }
-      }
-      double acc[2 * VPL];
-#pragma unroll
-      for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;
-      for (int qb = q0; qb < q1; qb += UN) {   // all gathers of a batch issued before its fma chain
-        const int cnt = q1 - qb;
-        double2 x[UN][VPL];
-#pragma unroll
-        for (int u = 0; u < UN; ++u)
-          if (u < cnt) {
-            const int32_t off = so[qb + u];
-#pragma unroll
-            for (int v = 0; v < VPL; ++v)
-              x[u][v] = (!HALO || off >= 0) ? ldg2_at(Xb + 16 * LPR * v, (uint32_t)off + l)
-                                            : ldg2_at(Hb + 16 * LPR * v, (uint32_t)(-1 - off) + l);
-          }
-#pragma unroll
-        for (int u = 0; u < UN; ++u)
-          if (u < cnt) {
-            const double vv = sv[qb + u];
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-              acc[2 * v] = __fma_rn(vv, x[u][v].x, acc[2 * v]);
-              acc[2 * v + 1] = __fma_rn(vv, x[u][v].y, acc[2 * v + 1]);
-            }
-          }
-      }
+    auto gather = [&](int32_t off, int v) -> double2 {
+      return (!HALO || off >= 0) ? ldg2_at(Xb + 16 * LPR * v, (uint32_t)off + l)
+                                 : ldg2_at(Hb + 16 * LPR * v, (uint32_t)(-1 - off) + l);
+    };
+    // epilogue of one row: shift, streaming store of w_i, alpha / g block partials
+    auto finish_row = [&](uint32_t i2, const double2 (&xi)[VPL], const double (&acc)[2 * VPL]) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         double w0 = acc[2 * v], w1 = acc[2 * v + 1];
@@ -334,6 +295,41 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
           dd_add1(s_acc[u][tid], ba[u]); dd_add1(s_acc[2 * VPL + u][tid], bg[u]);
           ba[u] = bg[u] = 0.0;
         }
+      }
+    };
+    for (int rl = grp; rl < nr; rl += RG) {
+      {
+        const int rr = rl;
+        const int q0 = r[rr] - p0, q1 = r[rr + 1] - p0;
+        const uint32_t i2 = rb2 + (uint32_t)rr * K2;
+        double2 xi[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) xi[v] = ldg2_at(Xb + 16 * LPR * v, i2);
+        double acc[2 * VPL];
+#pragma unroll
+        for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;
+        for (int qb = q0; qb < q1; qb += UN) {   // all gathers of a batch issued before its fma chain
+          const int cnt = q1 - qb;
+          double2 x[UN][VPL];
+#pragma unroll
+          for (int u = 0; u < UN; ++u)
+            if (u < cnt) {
+              const int32_t off = so[qb + u];
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) x[u][v] = gather(off, v);
+            }
+#pragma unroll
+          for (int u = 0; u < UN; ++u)
+            if (u < cnt) {
+              const double vv = sv[qb + u];
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) {
+                acc[2 * v] = __fma_rn(vv, x[u][v].x, acc[2 * v]);
+                acc[2 * v + 1] = __fma_rn(vv, x[u][v].y, acc[2 * v + 1]);
+              }
+            }
+        }
+        finish_row(i2, xi, acc);
       }
     }
   }

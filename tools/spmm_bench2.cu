@@ -76,7 +76,7 @@ struct Prob {
 
 template <int K, int PF = 0, int LPR = 0, int MINB = 0, int UN = 8>
 static void gather_case(const char* name, const Prob& p, int sms, const double* Wref, int R, int occ_override = 0) {
-  auto kern = spmm_gather_kernel<K, false, UN, PF, LPR, MINB>;
+  auto kern = spmm_gather_kernel<K, false, UN, LPR, MINB>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
   if (occ_override) occ = occ_override;
@@ -152,19 +152,12 @@ int main(int argc, char** argv) {
   if (which == 0 || which == 4) {
     Prob p = make(1024, 1021, 1, 32);
     double* Wref = prod_case<1, 16>("cfg4", p, sms);
-    gather_case<32>("cfg4", p, sms, Wref, 128);
-    gather_case<32, 0, 0, 4, 7>("cfg4", p, sms, Wref, 128);
     gather_case<32, 0, 0, 4, 5>("cfg4", p, sms, Wref, 128);
-    gather_case<32, 0, 0, 4, 6>("cfg4", p, sms, Wref, 128);
-    gather_case<32, 0, 0, 3, 7>("cfg4", p, sms, Wref, 128);
   }
   if (which == 0 || which == 5) {
     Prob p = make(160, 160, 160, 128);
     double* Wref = prod_case<2, 32>("cfg5", p, sms);
     gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32);
-    gather_case<128, 0, 0, 2, 8>("cfg5", p, sms, Wref, 32);
-    gather_case<128, 0, 0, 2, 6>("cfg5", p, sms, Wref, 32);
-    gather_case<128, 0, 0, 2, 4>("cfg5", p, sms, Wref, 32);
   }
   return 0;
 }
