@@ -63,6 +63,11 @@ def lib():
         L.oracle_sweep_csr.argtypes = [i64, i32, P, P, P, d, P, d, i32, i32, C.POINTER(Stats), P]
         L.oracle_run_dense.argtypes = [i64, i32, P, i64, d, P, i32, d, d, i32, i32, d, C.POINTER(i32), P]
         L.oracle_run_csr.argtypes = [i64, i32, P, P, P, d, P, i32, d, d, i32, i32, d, C.POINTER(i32), P]
+        L.oracle_rr_dense.argtypes = [i64, i32, P, i64, d, P, P]
+        L.oracle_rr_csr.argtypes = [i64, i32, P, P, P, d, P, P]
+        L.oracle_jacobi_eig.argtypes = [i32, P, P, P]
+        L.oracle_sweep_tz_dense.argtypes = [i64, i32, P, i64, d, P, d, C.POINTER(Stats)]
+        L.oracle_sweep_tz_csr.argtypes = [i64, i32, P, P, P, d, P, d, C.POINTER(Stats)]
         L.oracle_num_threads.restype = C.c_int
         for f in ("oracle_apply_dense", "oracle_apply_csr", "oracle_modified_lu", "oracle_compact_wy_lu",
                   "oracle_compact_wy", "oracle_apply_h", "oracle_sweep_dense", "oracle_sweep_csr",
@@ -207,6 +212,45 @@ def run(op: Operator, X, iters: int, tol: float, delta_c=10.0, beta_zero=False, 
         s = L.oracle_run_dense(n, k, _p(op.A), n, op.shift, _p(X), iters, tol, delta_c, int(beta_zero),
                                guard_window, guard_factor, C.byref(done), _p(hist))
     return X, s, done.value, hist[:done.value]
+
+
+def rayleigh_ritz(op: Operator, X):
+    """Rayleigh-Ritz preprocessing (Sec. 3.4): returns (status, Z, ritz) with
+    Z = X S, (X^T A X) S = (X^T X) S diag(ritz); ritz descending (readings RR1-RR3 in oracle.c)."""
+    Z = np.array(X, dtype=np.float64, order="C", copy=True)
+    n, k = Z.shape
+    ritz = np.zeros(k)
+    if not op.is_csr:
+        s = lib().oracle_rr_dense(n, k, _p(op.A), op.n, op.shift, _p(Z), _p(ritz))
+    else:
+        s = lib().oracle_rr_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(Z), _p(ritz))
+    return s, Z, ritz
+
+
+def sweep_rr(op: Operator, X, delta_c=10.0):
+    """Rayleigh-Ritz (Sec. 3.4) followed by one sweep with the top block of E_L zero and beta = 0
+    (PAPER.md:460, 921-926): one iteration of the preprocessed refinement.  Returns
+    (SweepResult, ritz); the result's status is the RR status if RR fails."""
+    s, Z, ritz = rayleigh_ritz(op, X)
+    st = Stats()
+    if s != OK:
+        return SweepResult(Z, s, st, {}), ritz
+    n, k = Z.shape
+    L = lib()
+    if op.is_csr:
+        s = L.oracle_sweep_tz_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(Z), delta_c, C.byref(st))
+    else:
+        s = L.oracle_sweep_tz_dense(n, k, _p(op.A), n, op.shift, _p(Z), delta_c, C.byref(st))
+    return SweepResult(Z, s, st, {}), ritz
+
+
+def jacobi_eig(Cm):
+    """k x k symmetric eigen-decomposition by cyclic Jacobi (oracle.c jacobi_eig): (Q, d), unsorted."""
+    Cw = np.array(Cm, dtype=np.float64, order="C", copy=True)
+    k = Cw.shape[0]
+    Q, dv = np.zeros((k, k)), np.zeros(k)
+    lib().oracle_jacobi_eig(k, _p(Cw), _p(Q), _p(dv))
+    return Q, dv
 
 
 def num_threads() -> int:

@@ -21,6 +21,7 @@
  *   normalisation
  *   delta = c ||A|| u, c = 10
  *   shift B = A - alpha I       PAPER.md:1194-1209 (Sec. 5.1)
+ *   Rayleigh-Ritz preprocessing PAPER.md:904-930 (Sec. 3.4), beta = 0 after it
  *
  * Readings where the paper is silent or misprinted are listed in DESIGN.md
  * ("Readings of the paper"); the ones that change arithmetic here:
@@ -346,6 +347,7 @@ typedef struct {
   double delta_c;      /* c in delta = c ||A|| u, default 10 */
   int32_t beta_zero;   /* 0: beta_ij = -x_i^T x_j / 2; 1: beta = 0 (:460) */
   int32_t normalize;   /* 1: normalise columns after the update */
+  int32_t top_zero;    /* 1: E_11 = 0 -- the sweep follows Rayleigh-Ritz (reading RR4) */
 } oracle_opts;
 
 typedef struct {
@@ -461,6 +463,11 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   double min_gap = INFINITY;
   for (int32_t i = 0; i < k; ++i)
     for (int32_t j = 0; j < k; ++j) {
+      if (o->top_zero) {   /* after Rayleigh-Ritz: e_ij = 0 for i, j <= k */
+        if (i != j && fabs(d[j] - d[i]) < min_gap) min_gap = fabs(d[j] - d[i]);
+        W[IDX(i, j, k)] = 0.0;
+        continue;
+      }
       if (i == j) { W[IDX(i, j, k)] = (1.0 - alpha[i]) / 2.0; continue; }
       const double gap = d[j] - d[i];
       if (fabs(gap) < min_gap) min_gap = fabs(gap);
@@ -541,7 +548,7 @@ done:
 }
 
 static void fill_opts(oracle_opts* o, double delta_c, int32_t beta_zero, int32_t normalize) {
-  o->delta_c = delta_c; o->beta_zero = beta_zero; o->normalize = normalize;
+  o->delta_c = delta_c; o->beta_zero = beta_zero; o->normalize = normalize; o->top_zero = 0;
 }
 
 int oracle_sweep_dense(int64_t n, int32_t k, const double* A, int64_t lda, double shift,
@@ -558,6 +565,20 @@ int oracle_sweep_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci,
   op_t op = {1, n, NULL, 0, rp, ci, v, shift};
   oracle_opts o; fill_opts(&o, delta_c, beta_zero, normalize);
   return sweep(&op, k, X, op_norm_inf(&op), &o, st, dbg);
+}
+
+/* one sweep after Rayleigh-Ritz (top block of E_L zero, beta = 0) */
+int oracle_sweep_tz_dense(int64_t n, int32_t k, const double* A, int64_t lda, double shift, double* X,
+                          double delta_c, oracle_stats* st) {
+  op_t op = {0, n, A, lda, NULL, NULL, NULL, shift};
+  oracle_opts o; fill_opts(&o, delta_c, 1, 1); o.top_zero = 1;
+  return sweep(&op, k, X, op_norm_inf(&op), &o, st, NULL);
+}
+int oracle_sweep_tz_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci, const double* v, double shift,
+                        double* X, double delta_c, oracle_stats* st) {
+  op_t op = {1, n, NULL, 0, rp, ci, v, shift};
+  oracle_opts o; fill_opts(&o, delta_c, 1, 1); o.top_zero = 1;
+  return sweep(&op, k, X, op_norm_inf(&op), &o, st, NULL);
 }
 
 /* =========================================================================
@@ -604,6 +625,176 @@ int oracle_run_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci, c
   op_t op = {1, n, NULL, 0, rp, ci, v, shift};
   return run(&op, k, X, iters, tol, delta_c, beta_zero, guard_window, guard_factor, iters_done, history);
 }
+
+/* =========================================================================
+ * Rayleigh-Ritz preprocessing for clustered targets (Sec. 3.4):
+ *   solve (X^T A X) S = (X^T X) S D~  and set  X <- Z = X S,  so Z^T Z = I and
+ *   Z^T A Z = D~; the refinement that follows uses beta = 0
+ *   (PAPER.md:460).  The paper does not say how the k x k pencil is solved; the
+ *   readings:
+ *     RR1  M = X^T (A - shift I) X is symmetrised, M <- (M + M^T)/2.
+ *     RR2  the pencil is reduced with the Cholesky factor G = X^T X = L L^T to the
+ *          symmetric C = L^{-1} M L^{-T}, whose eigen-decomposition C = Q diag(d) Q^T
+ *          is taken by cyclic Jacobi rotations (row-cyclic order, until the
+ *          off-diagonal Frobenius mass <= (u ||C||_F)^2, at most 60 sweeps); S = L^{-T} Q.
+ *     RR3  Ritz pairs are ordered by descending Ritz value; each column of Q is signed
+ *          so that its entry of largest magnitude (first on ties) is positive.
+ *   G and M are Neumaier-compensated length-n sums; k x k arithmetic is plain FP64.
+ * Returns OR_E_INVALID if G is not positive definite (X rank deficient).
+ * ========================================================================= */
+static int jacobi_eig(int32_t k, double* C, double* Q, double* d) {
+  for (int32_t i = 0; i < k; ++i)
+    for (int32_t j = 0; j < k; ++j) Q[IDX(i, j, k)] = (i == j) ? 1.0 : 0.0;
+  const double u = ldexp(1.0, -53);
+  double fro = 0.0;
+  for (int64_t t = 0; t < (int64_t)k * k; ++t) fro += C[t] * C[t];
+  for (int sweep_ = 0; sweep_ < 60; ++sweep_) {
+    double off = 0.0;
+    for (int32_t i = 0; i < k; ++i)
+      for (int32_t j = 0; j < k; ++j)
+        if (i != j) off += C[IDX(i, j, k)] * C[IDX(i, j, k)];
+    if (off <= u * u * fro) break;
+    for (int32_t p = 0; p < k - 1; ++p)
+      for (int32_t q = p + 1; q < k; ++q) {
+        const double apq = C[IDX(p, q, k)];
+        if (apq == 0.0) continue;
+        const double theta = (C[IDX(q, q, k)] - C[IDX(p, p, k)]) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        for (int32_t r = 0; r < k; ++r) {            /* C <- C J (columns p, q) */
+          const double cp = C[IDX(r, p, k)], cq = C[IDX(r, q, k)];
+          C[IDX(r, p, k)] = c * cp - sn * cq;
+          C[IDX(r, q, k)] = sn * cp + c * cq;
+        }
+        for (int32_t r = 0; r < k; ++r) {            /* C <- J^T C (rows p, q) */
+          const double cp = C[IDX(p, r, k)], cq = C[IDX(q, r, k)];
+          C[IDX(p, r, k)] = c * cp - sn * cq;
+          C[IDX(q, r, k)] = sn * cp + c * cq;
+        }
+        for (int32_t r = 0; r < k; ++r) {            /* Q <- Q J */
+          const double qp = Q[IDX(r, p, k)], qq = Q[IDX(r, q, k)];
+          Q[IDX(r, p, k)] = c * qp - sn * qq;
+          Q[IDX(r, q, k)] = sn * qp + c * qq;
+        }
+      }
+  }
+  for (int32_t j = 0; j < k; ++j) d[j] = C[IDX(j, j, k)];
+  return OR_OK;
+}
+
+static int rayleigh_ritz(const op_t* op, int32_t k, double* X, double* ritz) {
+  const int64_t n = op->n;
+  if (k < 1 || (int64_t)k >= n) return OR_E_INVALID;
+  const size_t nk = (size_t)n * (size_t)k, kk = (size_t)k * (size_t)k;
+  double* W = (double*)malloc(sizeof(double) * nk);
+  double* Z = (double*)malloc(sizeof(double) * nk);
+  double* G = (double*)malloc(sizeof(double) * kk);
+  double* M = (double*)malloc(sizeof(double) * kk);
+  double* Cm = (double*)malloc(sizeof(double) * kk);
+  double* Q = (double*)malloc(sizeof(double) * kk);
+  double* S = (double*)malloc(sizeof(double) * kk);
+  double* d = (double*)malloc(sizeof(double) * (size_t)k);
+  int32_t* ord = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);
+  int status = OR_OK;
+  if (!W || !Z || !G || !M || !Cm || !Q || !S || !d || !ord) { status = OR_E_NOMEM; goto done; }
+  op_apply(op, k, X, W);                                   /* W = (A - shift I) X */
+  #pragma omp parallel for schedule(static)
+  for (int32_t a = 0; a < k; ++a)                          /* G = X^T X, M = X^T W */
+    for (int32_t b = 0; b < k; ++b) {
+      nsum sg = {0, 0}, sm = {0, 0};
+      for (int64_t i = 0; i < n; ++i) {
+        nsum_add(&sg, X[IDX(i, a, k)] * X[IDX(i, b, k)]);
+        nsum_add(&sm, X[IDX(i, a, k)] * W[IDX(i, b, k)]);
+      }
+      G[IDX(a, b, k)] = nsum_val(&sg);
+      M[IDX(a, b, k)] = nsum_val(&sm);
+    }
+  for (int32_t a = 0; a < k; ++a)                          /* RR1: symmetrise M */
+    for (int32_t b = a + 1; b < k; ++b) {
+      const double m = (M[IDX(a, b, k)] + M[IDX(b, a, k)]) / 2.0;
+      M[IDX(a, b, k)] = m; M[IDX(b, a, k)] = m;
+    }
+  for (int32_t j = 0; j < k; ++j) {                        /* RR2: G = L L^T (L in G's lower part) */
+    double s = G[IDX(j, j, k)];
+    for (int32_t l = 0; l < j; ++l) s -= G[IDX(j, l, k)] * G[IDX(j, l, k)];
+    if (!(s > 0.0)) { status = OR_E_INVALID; goto done; }
+    const double ljj = sqrt(s);
+    G[IDX(j, j, k)] = ljj;
+    for (int32_t i = j + 1; i < k; ++i) {
+      double t = G[IDX(i, j, k)];
+      for (int32_t l = 0; l < j; ++l) t -= G[IDX(i, l, k)] * G[IDX(j, l, k)];
+      G[IDX(i, j, k)] = t / ljj;
+    }
+  }
+  /* C = L^{-1} M L^{-T}: B = L^{-1} M (forward substitution per column), C = L^{-1} B^T */
+  for (int32_t c = 0; c < k; ++c)
+    for (int32_t i = 0; i < k; ++i) {
+      double t = M[IDX(i, c, k)];
+      for (int32_t l = 0; l < i; ++l) t -= G[IDX(i, l, k)] * Cm[IDX(l, c, k)];
+      Cm[IDX(i, c, k)] = t / G[IDX(i, i, k)];
+    }
+  for (int32_t c = 0; c < k; ++c)                          /* S <- (L^{-1} M)^T, scratch */
+    for (int32_t i = 0; i < k; ++i) S[IDX(i, c, k)] = Cm[IDX(c, i, k)];
+  for (int32_t c = 0; c < k; ++c)
+    for (int32_t i = 0; i < k; ++i) {
+      double t = S[IDX(i, c, k)];
+      for (int32_t l = 0; l < i; ++l) t -= G[IDX(i, l, k)] * Cm[IDX(l, c, k)];
+      Cm[IDX(i, c, k)] = t / G[IDX(i, i, k)];
+    }
+  for (int32_t a = 0; a < k; ++a)                          /* symmetrise C */
+    for (int32_t b = a + 1; b < k; ++b) {
+      const double m = (Cm[IDX(a, b, k)] + Cm[IDX(b, a, k)]) / 2.0;
+      Cm[IDX(a, b, k)] = m; Cm[IDX(b, a, k)] = m;
+    }
+  jacobi_eig(k, Cm, Q, d);
+  for (int32_t j = 0; j < k; ++j) ord[j] = j;              /* RR3: descending Ritz values */
+  for (int32_t a = 1; a < k; ++a) {                        /* insertion sort, stable */
+    const int32_t v = ord[a];
+    int32_t b = a - 1;
+    while (b >= 0 && d[ord[b]] < d[v]) { ord[b + 1] = ord[b]; --b; }
+    ord[b + 1] = v;
+  }
+  for (int32_t j = 0; j < k; ++j) {                        /* permuted, signed Q into Cm */
+    const int32_t o = ord[j];
+    int32_t im = 0;
+    for (int32_t i = 1; i < k; ++i)
+      if (fabs(Q[IDX(i, o, k)]) > fabs(Q[IDX(im, o, k)])) im = i;
+    const double sg = (Q[IDX(im, o, k)] < 0.0) ? -1.0 : 1.0;
+    for (int32_t i = 0; i < k; ++i) Cm[IDX(i, j, k)] = sg * Q[IDX(i, o, k)];
+    ritz[j] = d[o];
+  }
+  for (int32_t c = 0; c < k; ++c)                          /* S = L^{-T} Q (back substitution) */
+    for (int32_t i = k - 1; i >= 0; --i) {
+      double t = Cm[IDX(i, c, k)];
+      for (int32_t l = i + 1; l < k; ++l) t -= G[IDX(l, i, k)] * S[IDX(l, c, k)];
+      S[IDX(i, c, k)] = t / G[IDX(i, i, k)];
+    }
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)                          /* Z = X S */
+    for (int32_t c = 0; c < k; ++c) {
+      double t = 0.0;
+      for (int32_t l = 0; l < k; ++l) t += X[IDX(i, l, k)] * S[IDX(l, c, k)];
+      Z[IDX(i, c, k)] = t;
+    }
+  memcpy(X, Z, sizeof(double) * nk);
+  for (size_t t = 0; t < nk; ++t)
+    if (!isfinite(X[t])) { status = OR_DIVERGED; break; }
+done:
+  free(W); free(Z); free(G); free(M); free(Cm); free(Q); free(S); free(d); free(ord);
+  return status;
+}
+
+int oracle_rr_dense(int64_t n, int32_t k, const double* A, int64_t lda, double shift, double* X, double* ritz) {
+  op_t op = {0, n, A, lda, NULL, NULL, NULL, shift};
+  return rayleigh_ritz(&op, k, X, ritz);
+}
+int oracle_rr_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci, const double* v, double shift,
+                  double* X, double* ritz) {
+  op_t op = {1, n, NULL, 0, rp, ci, v, shift};
+  return rayleigh_ritz(&op, k, X, ritz);
+}
+/* k x k symmetric eigen-decomposition alone (tests): C (in, destroyed) -> Q, d (unsorted) */
+int oracle_jacobi_eig(int32_t k, double* C, double* Q, double* d) { return jacobi_eig(k, C, Q, d); }
 
 int oracle_num_threads(void) {
 #ifdef _OPENMP
