@@ -209,6 +209,21 @@ def time_ours(p, steps, warmup, world, local, profile=True, rank=0):
     return ms, kern, R, X, st, s, ms_prof
 
 
+def time_rr(R, X, reps=3):
+    """Rayleigh-Ritz preprocessing (NEXT-1, Sec. 3.4): device time of refine_rayleigh_ritz."""
+    import torch
+    X = X.clone()
+    R.refine_rayleigh_ritz(X)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        s, _ = R.refine_rayleigh_ritz(X)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, s
+
+
 def time_e2e(R, p, steps, warmup, world=1, rank=0):
     """Host buffers through the C ABI: H2D of X^, sweep, D2H of the result, each step."""
     import torch
@@ -366,6 +381,10 @@ def main():
             "kernels_ms": kern,
             "roofline": roofline_for(p, kern, ms_prof or ms_max, fp64, hbm, n_loc=partition(p.n, world, rank)[1] - partition(p.n, world, rank)[0]),
             "gpu_launches": R.kernels_per_sweep() * args.steps}
+    if world == 1:
+        rr_ms, rr_s = time_rr(R, X)
+        line["rayleigh_ritz"] = {"ms": rr_ms, "status": rr_s, "what": "refine_rayleigh_ritz (NEXT-1, Sec. 3.4): "
+                                 "S1 + pass B (D = 0) + k x k Cholesky/Jacobi + pass C + normalise"}
     # e2e through the host-buffer C ABI call
     e2e_s, h2d, d2h = time_e2e(R, p, max(3, args.steps // 2), 1, world, rank)
     e2e_s = max_over_ranks(e2e_s, world)
@@ -382,7 +401,9 @@ def main():
             q = make_problem(name, f"cuda:{local}")
             qms, qk, QR, QX, qst, qs, qprof = time_ours(q, 5 if q.n > 10000 else 20, 3, 1, local)
             qf, qb = alg_counts(q)
+            qrr, _ = time_rr(QR, QX)
             per[name] = {"sweeps_s": 1000.0 / qms, "ms_per_sweep": qms, "ms_per_sweep_instrumented": qprof,
+                         "rayleigh_ritz_ms": qrr,
                          "kernels_ms": qk, "roofline": roofline_for(q, qk, qprof or qms, fp64, hbm),
                          "frac_of_sweep_roofline": max(qf / (fp64 * 1e12), qb / (hbm * 1e9)) / (qms * 1e-3)}
             del QR, QX, q

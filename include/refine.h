@@ -137,6 +137,22 @@ refine_status refine_sweep_host(refine_ctx* c, const double* X_host_in, double* 
 refine_status refine_run(refine_ctx* c, double* X, int32_t iters, double tol,
                          int32_t* iters_done, refine_sweep_stats* last);
 
+/* Rayleigh-Ritz preprocessing for clustered targets (Sec. 3.4):
+ * solves (X^T A' X) S = (X^T X) S D~ (A' = A - shift I) and replaces X (device,
+ * n_loc x k row-major, in place) by Z = X S, so Z^T Z = I and Z^T A' Z = D~
+ * (PAPER.md:915-919).  The k x k pencil is reduced by the Cholesky factor of X^T X
+ * and solved by parallel Jacobi rotations on one CTA; Ritz pairs are ordered by
+ * descending Ritz value, each eigenvector column signed so its largest entry is
+ * positive (readings RR1-RR3).  ritz (host, k doubles, nullable) receives
+ * D~.  Synchronises.  REFINE_E_INVALID if X^T X is not positive definite (X rank
+ * deficient); X is then unchanged. */
+refine_status refine_rayleigh_ritz(refine_ctx* c, double* X, double* ritz);
+
+/* One iteration of the preprocessed refinement: refine_rayleigh_ritz, then one sweep
+ * whose E_L top block is set to its exact-arithmetic value 0 (beta = 0,
+ * PAPER.md:460).  Stats / ritz as for refine_sweep / refine_rayleigh_ritz.  Synchronises. */
+refine_status refine_sweep_rr(refine_ctx* c, double* X, refine_sweep_stats* stats, double* ritz);
+
 /* Status of the last enqueued sweep (synchronises the stream). */
 refine_status refine_get_status(refine_ctx* c);
 

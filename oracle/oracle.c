@@ -640,7 +640,8 @@ int oracle_run_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci, c
  *     RR3  Ritz pairs are ordered by descending Ritz value; each column of Q is signed
  *          so that its entry of largest magnitude (first on ties) is positive.
  *   G and M are Neumaier-compensated length-n sums; k x k arithmetic is plain FP64.
- * Returns OR_E_INVALID if G is not positive definite (X rank deficient).
+ * Returns OR_E_INVALID if G is numerically singular: a Cholesky pivot <= 4 k u G_jj
+ * (X rank deficient; reading RR2).
  * ========================================================================= */
 static int jacobi_eig(int32_t k, double* C, double* Q, double* d) {
   for (int32_t i = 0; i < k; ++i)
@@ -716,8 +717,10 @@ static int rayleigh_ritz(const op_t* op, int32_t k, double* X, double* ritz) {
     }
   for (int32_t j = 0; j < k; ++j) {                        /* RR2: G = L L^T (L in G's lower part) */
     double s = G[IDX(j, j, k)];
+    const double g0 = s;
     for (int32_t l = 0; l < j; ++l) s -= G[IDX(j, l, k)] * G[IDX(j, l, k)];
-    if (!(s > 0.0)) { status = OR_E_INVALID; goto done; }
+    /* numerically singular (X rank deficient): pivot <= 4 k u G_jj */
+    if (!(s > 4.0 * k * ldexp(1.0, -53) * g0)) { status = OR_E_INVALID; goto done; }
     const double ljj = sqrt(s);
     G[IDX(j, j, k)] = ljj;
     for (int32_t i = j + 1; i < k; ++i) {

@@ -85,9 +85,11 @@ def lib() -> C.CDLL:
         L.refine_kernel_name.restype = C.c_char_p
         L.refine_halo_plan.argtypes = [i32, i32, P, P, P, P, P, C.POINTER(i32), P, C.POINTER(i32), C.POINTER(i64), i32]
         L.refine_halo_plan.restype = i32
+        L.refine_rayleigh_ritz.argtypes = [P, P, P]
+        L.refine_sweep_rr.argtypes = [P, P, C.POINTER(refine_sweep_stats), P]
         for f in ("refine_init_dense", "refine_init_csr", "refine_sweep", "refine_sweep_host", "refine_run",
                   "refine_get_status", "refine_set_graph", "refine_nccl_id", "refine_debug_get",
-                  "refine_profile_begin", "refine_profile_end"):
+                  "refine_profile_begin", "refine_profile_end", "refine_rayleigh_ritz", "refine_sweep_rr"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -205,6 +207,27 @@ class Refiner:
         s = lib().refine_run(self._h, _ptr(X), int(iters), float(tol), C.byref(done), C.byref(st))
         return s, done.value, st
 
+    def refine_rayleigh_ritz(self, X):
+        """Rayleigh-Ritz preprocessing (Sec. 3.4) on X in place: X <- X S with
+        (X^T A X) S = (X^T X) S diag(ritz).  Returns (status, ritz as a numpy array, descending)."""
+        import numpy as np
+        import torch
+        _check_dev(X, torch.float64, "X")
+        ritz = np.zeros(self.k)
+        s = lib().refine_rayleigh_ritz(self._h, _ptr(X), C.c_void_p(ritz.ctypes.data))
+        return s, ritz
+
+    def refine_sweep_rr(self, X):
+        """Rayleigh-Ritz, then one sweep with the E_L top block zero.
+        Returns (status, refine_sweep_stats, ritz)."""
+        import numpy as np
+        import torch
+        _check_dev(X, torch.float64, "X")
+        ritz = np.zeros(self.k)
+        st = refine_sweep_stats()
+        s = lib().refine_sweep_rr(self._h, _ptr(X), C.byref(st), C.c_void_p(ritz.ctypes.data))
+        return s, st, ritz
+
     def refine_get_status(self) -> int:
         return lib().refine_get_status(self._h)
 
@@ -272,7 +295,8 @@ def refine_nccl_id() -> bytes:
 EXPORTED = ("refine_init_dense", "refine_init_csr", "refine_sweep", "refine_sweep_host", "refine_run",
             "refine_get_status", "refine_set_graph", "refine_kernels_per_sweep", "refine_destroy",
             "refine_status_string", "refine_nccl_id", "refine_debug_get", "refine_profile_begin",
-            "refine_profile_end", "refine_kernel_name", "refine_halo_plan")
+            "refine_profile_end", "refine_kernel_name", "refine_halo_plan", "refine_rayleigh_ritz",
+            "refine_sweep_rr")
 
 
 def refine_halo_plan(world: int, rank: int, row_begin, row_end, col_lo, col_hi, cap: int = 64):

@@ -112,6 +112,10 @@ struct Ws {
   double* mg_all;              // [M2 | G2 | rr2] of all ranks (world x (2k^2 + k))
   double *nrm_send, *nrm_all;  // column sums of x~^2: local (k) / all ranks (world x k)
   long long* tlog;   // optional clock64() phase log of the k x k kernels (REFINE_KXK_TIMING=1)
+  // Rayleigh-Ritz preprocessing (Sec. 3.4): ritz values (k, descending), a zero k-vector (pass B
+  // with D = 0 gives [X^T W | X^T X]), and the top-zero flag of the sweep that follows RR
+  double *ritz, *zerod;
+  int32_t top_zero;
 };
 
 // X row of global index col: local rows first, else the halo (CSR row partition)

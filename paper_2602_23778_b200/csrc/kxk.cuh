@@ -425,7 +425,9 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     double v;
-    if (i == j) {
+    if (ws.top_zero) {                                 // after Rayleigh-Ritz
+      v = 0.0;
+    } else if (i == j) {
       v = (1.0 - ws.alpha[i]) / 2.0;
     } else {
       const double gap = d[j] - d[i];
@@ -489,6 +491,183 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     ws.stats[3] = (double)s_hits;
     ws.stats[4] = (fl > 0.0) ? 1.0 : 0.0;
     ws.stats[5] = rr;
+  }
+}
+
+// ---------------------------------------------------------------- rr_kxk (Rayleigh-Ritz, Sec. 3.4)
+// (X^T A X) S = (X^T X) S D~,  Z = X S  (Z^T Z = I, Z^T A Z = D~).  Inputs: the
+// pass-B sums over rows >= top with D = 0, M2 = X_2^T W_2 and G2 = X_2^T X_2, plus the top rows.
+//   M = M2 + X_1^T W_1, G = G2 + X_1^T X_1;  M <- (M + M^T)/2                      (reading RR1)
+//   G = L L^T (Cholesky);  Ui = L^{-T};  C = Ui^T M Ui;  C = Q diag(d) Q^T by parallel Jacobi
+//   (round-robin pairs, k/2 disjoint rotations per step, until off(C) <= (u ||C||_F)^2)   (RR2)
+//   Ritz pairs by descending d; each Q column signed so its largest |entry| is positive  (RR3)
+//   S = Ui Q;  top rows Z_1 = X_1 S -> X~;  Csig = -S, scal = 0 so that pass C forms Z_2 = X_2 S.
+__device__ void rr_rotate(int k, double* C, double* Q, int m, int round, double* cs, double* sn, int* pp,
+                          int* qq) {
+  const int tid = threadIdx.x, npair = m / 2;
+  if (tid < npair) {   // round-robin pairing of players 0..m-1 (player 0 fixed)
+    auto player = [&](int j) { return j == 0 ? 0 : 1 + (j - 1 + round) % (m - 1); };
+    int p = player(tid), q = player(m - 1 - tid);
+    if (p > q) { const int t = p; p = q; q = t; }
+    double c = 1.0, s = 0.0;
+    if (q < k) {
+      const double apq = C[p * k + q];
+      if (apq != 0.0) {
+        const double theta = (C[q * k + q] - C[p * k + p]) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        c = 1.0 / sqrt(t * t + 1.0);
+        s = t * c;
+      }
+    }
+    cs[tid] = c; sn[tid] = s; pp[tid] = p; qq[tid] = q;
+  }
+  __syncthreads();
+  for (int e = tid; e < k * npair; e += KXK_THREADS) {   // C <- C J, Q <- Q J (columns p, q)
+    const int t = e % npair, r = e / npair, p = pp[t], q = qq[t];
+    if (q >= k) continue;
+    const double c = cs[t], s = sn[t];
+    const double cp = C[r * k + p], cq = C[r * k + q];
+    C[r * k + p] = c * cp - s * cq;
+    C[r * k + q] = s * cp + c * cq;
+    const double qp = Q[r * k + p], qv = Q[r * k + q];
+    Q[r * k + p] = c * qp - s * qv;
+    Q[r * k + q] = s * qp + c * qv;
+  }
+  __syncthreads();
+  for (int e = tid; e < k * npair; e += KXK_THREADS) {   // C <- J^T C (rows p, q)
+    const int t = e % npair, r = e / npair, p = pp[t], q = qq[t];
+    if (q >= k) continue;
+    const double c = cs[t], s = sn[t];
+    const double cp = C[p * k + r], cq = C[q * k + r];
+    C[p * k + r] = c * cp - s * cq;
+    C[q * k + r] = s * cp + c * cq;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(KXK_THREADS) rr_kxk_kernel(Ws ws, const double* __restrict__ Xtop,
+                                                             const double* __restrict__ Wtop) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double s_cs[KMAX / 2 + 1], s_sn[KMAX / 2 + 1], s_red[KXK_THREADS / 32];
+  __shared__ int s_p[KMAX / 2 + 1], s_q[KMAX / 2 + 1], s_ord[KMAX], s_bad;
+  __shared__ double s_d[KMAX];
+  if (*ws.status != ST_OK) return;
+  const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
+  double* S = ws.scratch;
+  double *M = S, *G = S + kk, *Lt = S + 2 * kk, *Ui = S + 3 * kk, *T1 = S + 4 * kk, *Cm = S + 5 * kk,
+         *Q = S + 6 * kk, *Qs = S + 7 * kk, *Sm = S + 8 * kk, *tmp = S + 9 * kk, *X1 = S + 10 * kk;
+  if (tid == 0) s_bad = 0;
+  if (ws.multi) {   // [M2 | G2 | rr2] of every rank, summed in rank order
+    const int64_t cnt = 2 * kk + k;
+    for (int64_t e = tid; e < cnt; e += nt) {
+      double sum = ws.mg_all[e];
+      for (int r = 1; r < ws.world; ++r) sum += ws.mg_all[(int64_t)r * cnt + e];
+      ws.M2[e] = sum;
+    }
+  }
+  for (int e = tid; e < kk; e += nt) X1[e] = Xtop[e];
+  __syncthreads();
+  cta_gemm(k, k, k, 1.0, X1, k, true, Wtop, k, false, 1.0, ws.M2, k, M, k, sm);   // M = M2 + X_1^T W_1
+  cta_gemm(k, k, k, 1.0, X1, k, true, X1, k, false, 1.0, ws.G2, k, G, k, sm);      // G = G2 + X_1^T X_1
+  for (int e = tid; e < kk; e += nt) {                                              // RR1
+    const int i = e / k, j = e % k;
+    if (i < j) { const double m = (M[e] + M[j * k + i]) / 2.0; M[e] = m; M[j * k + i] = m; }
+  }
+  __syncthreads();
+  // Cholesky G = L L^T, right-looking, L in G's lower triangle
+  if (tid < k) s_d[tid] = G[tid * k + tid];   // original diagonal (singularity threshold)
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const double g = G[j * k + j];
+      if (!(g > 4.0 * k * 1.1102230246251565e-16 * s_d[j])) s_bad = 1;   // X rank deficient (RR2)
+      G[j * k + j] = sqrt(fmax(g, 0.0));
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const double ljj = G[j * k + j];
+    for (int i = j + 1 + tid; i < k; i += nt) G[i * k + j] /= ljj;
+    __syncthreads();
+    for (int e = tid; e < (k - j - 1) * (k - j - 1); e += nt) {
+      const int a = j + 1 + e / (k - j - 1), b = j + 1 + e % (k - j - 1);
+      if (b <= a) G[a * k + b] -= G[a * k + j] * G[b * k + j];
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) atomicCAS(ws.status, ST_OK, ST_E_INVALID);   // X^T X not positive definite
+    return;
+  }
+  for (int e = tid; e < kk; e += nt) {   // Lt = L^T (upper, non-unit)
+    const int i = e / k, j = e % k;
+    Lt[e] = (j >= i) ? G[j * k + i] : 0.0;
+  }
+  __syncthreads();
+  cta_trinv(k, Lt, true, Ui, tmp, sm);                                            // Ui = L^{-T}
+  cta_gemm(k, k, k, 1.0, Ui, k, true, M, k, false, 0.0, nullptr, 0, T1, k, sm);   // Ui^T M
+  cta_gemm(k, k, k, 1.0, T1, k, false, Ui, k, false, 0.0, nullptr, 0, Cm, k, sm); // C = Ui^T M Ui
+  for (int e = tid; e < kk; e += nt) {
+    const int i = e / k, j = e % k;
+    Q[e] = (i == j) ? 1.0 : 0.0;
+    if (i < j) { const double m = (Cm[e] + Cm[j * k + i]) / 2.0; Cm[e] = m; Cm[j * k + i] = m; }
+  }
+  __syncthreads();
+  // parallel Jacobi sweeps (RR2)
+  const int m = (k + 1) & ~1;
+  const double u = 1.1102230246251565e-16;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, fro = 0.0;
+    for (int e = tid; e < kk; e += nt) {
+      const double v = Cm[e];
+      fro += v * v;
+      if (e / k != e % k) off += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) { off += __shfl_xor_sync(0xffffffffu, off, o); fro += __shfl_xor_sync(0xffffffffu, fro, o); }
+    __shared__ double s_off[KXK_THREADS / 32];
+    if ((tid & 31) == 0) { s_off[tid >> 5] = off; s_red[tid >> 5] = fro; }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < nt / 32; ++w) { a += s_off[w]; b += s_red[w]; }
+      s_off[0] = a; s_red[0] = b;
+    }
+    __syncthreads();
+    const bool done = s_off[0] <= u * u * s_red[0];
+    __syncthreads();
+    if (done || k == 1) break;
+    for (int round = 0; round < m - 1; ++round) rr_rotate(k, Cm, Q, m, round, s_cs, s_sn, s_p, s_q);
+  }
+  // RR3: descending Ritz values (stable), columns signed by their largest |entry|
+  if (tid < k) s_d[tid] = Cm[tid * k + tid];
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < k; ++j) s_ord[j] = j;
+    for (int a = 1; a < k; ++a) {
+      const int v = s_ord[a];
+      int b = a - 1;
+      while (b >= 0 && s_d[s_ord[b]] < s_d[v]) { s_ord[b + 1] = s_ord[b]; --b; }
+      s_ord[b + 1] = v;
+    }
+  }
+  __syncthreads();
+  if (tid < k) {
+    const int j = tid, o = s_ord[j];
+    int im = 0;
+    for (int i = 1; i < k; ++i)
+      if (fabs(Q[i * k + o]) > fabs(Q[im * k + o])) im = i;
+    const double sg = (Q[im * k + o] < 0.0) ? -1.0 : 1.0;
+    for (int i = 0; i < k; ++i) Qs[i * k + j] = sg * Q[i * k + o];
+    ws.ritz[j] = s_d[o];
+  }
+  __syncthreads();
+  cta_gemm(k, k, k, 1.0, Ui, k, false, Qs, k, false, 0.0, nullptr, 0, Sm, k, sm);   // S = Ui Q
+  cta_gemm(k, k, k, 1.0, X1, k, false, Sm, k, false, 0.0, nullptr, 0, ws.Xt, k, sm);  // Z_1 = X_1 S
+  for (int e = tid; e < kk; e += nt) ws.Csig[e] = -Sm[e];                         // pass C: Z_2 = X_2 S
+  if (tid < k) {
+    ws.scal[tid] = 0.0;
+    double nt2 = 0.0;
+    for (int i = 0; i < k; ++i) nt2 = fma(ws.Xt[i * k + tid], ws.Xt[i * k + tid], nt2);
+    ws.ntop[tid] = nt2;
   }
 }
 

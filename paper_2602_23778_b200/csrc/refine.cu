@@ -336,8 +336,9 @@ struct Kern {
     int n = 0;
     const bool xv16 = (c->k % 2 == 0) && ((uintptr_t)X % 16 == 0);
     switch (ph) {
-      case 0:  // S1 (+ S2 partials); S3 (kxk_lu, X^_1 only) forked onto the side stream
-        if (ws.top > 0) {
+      case 0:    // S1 (+ S2 partials); S3 (kxk_lu, X^_1 only) forked onto the side stream
+      case 10:   // Rayleigh-Ritz: S1 only (W = (A - shift I) X)
+        if (ph == 0 && ws.top > 0) {
           cudaEventRecord(c->ev_fork, s);
           cudaStreamWaitEvent(c->side, c->ev_fork, 0);
           kxk_lu_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8,
@@ -364,9 +365,26 @@ struct Kern {
           else launch_spmm<false>(c, vec, X);
           n += 1;
         }
-        if (c->multi) {
+        if (ph == 0 && c->multi) {
           ag_local_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
           ++n;
+        }
+        break;
+      case 11: {  // Rayleigh-Ritz: pass B with D = 0 -> M2 = X_2^T W_2, G2 = X_2^T X_2
+        Ws wz = ws;
+        wz.d = ws.zerod;
+        if (B2 && B2C::PAIRED)
+          passB<<<dim3(7 * (c->passb_grid_y / 2)), B_THREADS, B_SMEM, s>>>(wz, X, xv16);
+        else
+          passB<<<dim3(B_NT, c->passb_grid_y), B_THREADS, B_SMEM, s>>>(wz, X, xv16);
+        passBred<<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(ws, c->passb_grid_y);
+        n += 2;
+        break;
+      }
+      case 12:  // Rayleigh-Ritz k x k stage (rank 0)
+        if (c->rank == 0) {
+          rr_kxk_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
+          n += 1;
         }
         break;
       case 1:  // S2: alpha, Rayleigh quotients
@@ -542,6 +560,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   RF_CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RF_CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
+  RF_CK(c, cudaFuncSetAttribute(rr_kxk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
   // workspace sizes (doubles)
   size_t bpart = 0, brr = 0, nslot = 0;
   dispatch(c->kp, [&](auto K) { decltype(K)::sizes(c, bpart, brr, nslot); return 0; });
@@ -560,7 +579,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
                oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
-               oNrS = take(k), oNrA = take(P * k), oCol = take(2);
+               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
   c->pool_bytes = bytes;
@@ -578,6 +597,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.scratch = b + oScr;
   ws.ag_send = b + oAgS; ws.ag_all = b + oAgA; ws.mg_all = c->multi ? b + oMgA : nullptr;
   ws.nrm_send = b + oNrS; ws.nrm_all = b + oNrA;
+  ws.ritz = b + oRitz; ws.zerod = b + oZd; ws.top_zero = 0;   // (the pool is zeroed below)
   c->run = reinterpret_cast<RunState*>(b + oRun);
   ws.tlog = nullptr;
   if (getenv("REFINE_KXK_TIMING")) RF_CK(c, cudaMalloc(&ws.tlog, 64 * sizeof(long long)));
@@ -915,6 +935,35 @@ static refine_status launch_sweep(refine_ctx* c, double* X) {
   return REFINE_OK;
 }
 
+// Rayleigh-Ritz preprocessing (Sec. 3.4): S1 -> pass B with D = 0 -> [gather]
+// -> rr_kxk (rank 0) -> [broadcast Csig = -S, scal = 0] -> pass C (Z_2 = X_2 S) -> norms -> X = Z.
+static refine_status enqueue_rr(refine_ctx* c, double* X) {
+  refine_ctx* one[1] = {c};
+  refine_ctx** ranks = c->loopback ? c->kids.data() : one;
+  const int nr = c->loopback ? (int)c->kids.size() : 1;
+  for (int i = 0; i < nr; ++i) RF_CK(c, cudaMemsetAsync(ranks[i]->ws.status, 0, sizeof(int), c->stream));
+  refine_status st;
+  if (c->multi && (st = collective(c, C_X, X)) != REFINE_OK) return st;
+  static const int phases[5] = {10, 11, 12, 4, 5};
+  static const int after[5] = {-1, C_MG, C_BC, C_NRM, -1};
+  for (int q = 0; q < 5; ++q) {
+    for (int i = 0; i < nr; ++i) {
+      refine_ctx* r = ranks[i];
+      double* Xr = c->loopback ? X + r->row_begin * c->k : X;
+      dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, phases[q], Xr); });
+    }
+    if (c->multi && after[q] >= 0 && (st = collective(c, after[q], X)) != REFINE_OK) return st;
+  }
+  RF_CK(c, cudaGetLastError());
+  return REFINE_OK;
+}
+
+static void set_top_zero(refine_ctx* c, int v) {
+  if (c->loopback)
+    for (auto* kid : c->kids) kid->ws.top_zero = v;
+  c->ws.top_zero = v;
+}
+
 static refine_status map_status(int s) {
   switch (s) {
     case ST_OK: return REFINE_OK;
@@ -939,6 +988,36 @@ static refine_status read_stats(refine_ctx* c, refine_sweep_stats* stats, int* d
   }
   *dev_status = st;
   return REFINE_OK;
+}
+
+extern "C" refine_status refine_rayleigh_ritz(refine_ctx* c, double* X, double* ritz) {
+  if (!c || !X) return REFINE_E_INVALID;
+  if (c->sticky != REFINE_OK) return c->sticky;
+  refine_status st = enqueue_rr(c, X);
+  if (st != REFINE_OK) return st;
+  if (ritz) RF_CK(c, cudaMemcpyAsync(ritz, ctx0(c)->ws.ritz, sizeof(double) * c->k, cudaMemcpyDeviceToHost, c->stream));
+  int dev = 0;
+  RF_CK(c, cudaMemcpyAsync(&dev, ctx0(c)->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaStreamSynchronize(c->stream));
+  return map_status(dev);
+}
+
+extern "C" refine_status refine_sweep_rr(refine_ctx* c, double* X, refine_sweep_stats* stats, double* ritz) {
+  if (!c || !X) return REFINE_E_INVALID;
+  if (c->sticky != REFINE_OK) return c->sticky;
+  refine_status st = enqueue_rr(c, X);
+  if (st != REFINE_OK) return st;
+  if (ritz) RF_CK(c, cudaMemcpyAsync(ritz, ctx0(c)->ws.ritz, sizeof(double) * c->k, cudaMemcpyDeviceToHost, c->stream));
+  int dev = 0;
+  RF_CK(c, cudaMemcpyAsync(&dev, ctx0(c)->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaStreamSynchronize(c->stream));
+  if (dev != ST_OK) return map_status(dev);
+  set_top_zero(c, 1);
+  st = enqueue_sweep(c, X);          // direct launches (the cached sweep graph has top_zero = 0)
+  set_top_zero(c, 0);
+  if (st != REFINE_OK) return st;
+  if ((st = read_stats(c, stats, &dev)) != REFINE_OK) return st;
+  return map_status(dev);
 }
 
 extern "C" refine_status refine_sweep(refine_ctx* c, double* X, refine_sweep_stats* stats) {
