@@ -68,6 +68,12 @@ def lib():
         L.oracle_jacobi_eig.argtypes = [i32, P, P, P]
         L.oracle_sweep_tz_dense.argtypes = [i64, i32, P, i64, d, P, d, C.POINTER(Stats)]
         L.oracle_sweep_tz_csr.argtypes = [i64, i32, P, P, P, d, P, d, C.POINTER(Stats)]
+        L.oracle_sweep_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, d, i32, i32, C.POINTER(Stats), P]
+        L.oracle_run_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, i32, d, d, i32, i32,
+                                    C.POINTER(i32), P]
+        L.oracle_apply_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, P]
+        L.oracle_norm_ex.argtypes = [C.c_int, i64, P, i64, P, P, P, d, i32]
+        L.oracle_norm_ex.restype = d
         L.oracle_num_threads.restype = C.c_int
         for f in ("oracle_apply_dense", "oracle_apply_csr", "oracle_modified_lu", "oracle_compact_wy_lu",
                   "oracle_compact_wy", "oracle_apply_h", "oracle_sweep_dense", "oracle_sweep_csr",
@@ -90,10 +96,12 @@ def _i32(a) -> np.ndarray:
 
 
 class Operator:
-    """A (dense n x n, or CSR with both triangles) and the Sec. 5.1 shift."""
+    """A (dense n x n, or CSR with both triangles) and the Sec. 5.1 shift (PAPER.md:1203);
+    square=True: the operator A^2 - shift I of Sec. 5.2, applied as A (A X)."""
 
-    def __init__(self, A=None, row_ptr=None, col_idx=None, val=None, shift: float = 0.0):
+    def __init__(self, A=None, row_ptr=None, col_idx=None, val=None, shift: float = 0.0, square: bool = False):
         self.shift = float(shift)
+        self.square = bool(square)
         if A is not None:
             self.is_csr = False
             self.A = _f64(A)
@@ -105,6 +113,9 @@ class Operator:
 
     def norm_inf(self) -> float:
         L = lib()
+        if self.square:
+            a = _ex_args(self)
+            return L.oracle_norm_ex(*a)
         if self.is_csr:
             return L.oracle_norm_inf_csr(self.n, _p(self.rp), _p(self.ci), _p(self.v), self.shift)
         return L.oracle_norm_inf_dense(self.n, _p(self.A), self.n, self.shift)
@@ -115,6 +126,10 @@ class Operator:
         k = X.shape[1]
         W = np.empty_like(X)
         L = lib()
+        if self.square:
+            a = _ex_args(self)
+            L.oracle_apply_ex(*a[:2], k, *a[2:], _p(X), _p(W))
+            return W
         if self.is_csr:
             L.oracle_apply_csr(self.n, k, _p(self.rp), _p(self.ci), _p(self.v), self.shift, _p(X), _p(W))
         else:
@@ -173,8 +188,23 @@ class SweepResult:
     debug: dict
 
 
-def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=False) -> SweepResult:
-    """One sweep of Alg. 4 on a copy of X."""
+def _ex_args(op):
+    if op.is_csr:
+        return (1, op.n, None, 0, _p(op.rp), _p(op.ci), _p(op.v), op.shift, int(op.square))
+    return (0, op.n, _p(op.A), op.n, None, None, None, op.shift, int(op.square))
+
+
+def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=False, kjudge=0) -> SweepResult:
+    """One sweep of Alg. 4 on a copy of X.  kjudge > 0: corr_norm over the leading
+    kjudge columns (K > k refinement)."""
+    if op.square or kjudge:
+        assert normalize and not debug
+        X = _f64(X).copy()
+        n, k = X.shape
+        st = Stats()
+        a = _ex_args(op)
+        s = lib().oracle_sweep_ex(*a[:2], k, *a[2:], _p(X), delta_c, int(beta_zero), int(kjudge), C.byref(st), None)
+        return SweepResult(X, s, st, {})
     X = _f64(X).copy()
     n, k = X.shape
     st = Stats()
@@ -197,7 +227,7 @@ def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=
 
 
 def run(op: Operator, X, iters: int, tol: float, delta_c=10.0, beta_zero=False, guard_window=3,
-        guard_factor=10.0):
+        guard_factor=10.0, kjudge=0):
     """Iterate sweeps until ||E_L||_F <= tol, iters, or divergence.
     Returns (X, status, iters_done, history[iters_done, 2] = (rel_resid, corr_norm))."""
     X = _f64(X).copy()
@@ -205,6 +235,11 @@ def run(op: Operator, X, iters: int, tol: float, delta_c=10.0, beta_zero=False, 
     hist = np.zeros((max(iters, 1), 2))
     done = C.c_int32(0)
     L = lib()
+    if op.square or kjudge:     # (no divergence guard on this entry point)
+        a = _ex_args(op)
+        s = L.oracle_run_ex(*a[:2], k, *a[2:], _p(X), iters, tol, delta_c, int(beta_zero), int(kjudge),
+                            C.byref(done), _p(hist))
+        return X, s, done.value, hist[:done.value]
     if op.is_csr:
         s = L.oracle_run_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(X), iters, tol, delta_c,
                              int(beta_zero), guard_window, guard_factor, C.byref(done), _p(hist))

@@ -22,6 +22,8 @@
  *   delta = c ||A|| u, c = 10
  *   shift B = A - alpha I       PAPER.md:1194-1209 (Sec. 5.1)
  *   Rayleigh-Ritz preprocessing PAPER.md:904-930 (Sec. 3.4), beta = 0 after it
+ *   shift-and-square B = A^2 - alpha I, applied as A (A X)   PAPER.md:1218-1243 (Sec. 5.2)
+ *   refine K > k columns, judge the leading k
  *
  * Readings where the paper is silent or misprinted are listed in DESIGN.md
  * ("Readings of the paper"); the ones that change arithmetic here:
@@ -86,11 +88,11 @@ typedef struct {
   /* csr */
   const int32_t* row_ptr; const int32_t* col_idx; const double* val;
   double shift;
+  int square;   /* 1: the operator is A^2 - shift I (Sec. 5.2), applied as A (A X) */
 } op_t;
 
-/* W = A X - shift X.  w_ij = fma chain over the row of A in ascending column
- * order starting from 0, then (shift != 0) w_ij = fma(-shift, x_ij, acc). */
-static void op_apply(const op_t* op, int32_t k, const double* X, double* W) {
+/* W = A X  (no shift): fma chain over the row of A in ascending column order from 0. */
+static void op_product(const op_t* op, int32_t k, const double* X, double* W) {
   const int64_t n = op->n;
   const int64_t RB = 8;   /* rows per block: cache reuse of X only, per-entry order unchanged */
   #pragma omp parallel for schedule(static)
@@ -117,14 +119,41 @@ static void op_apply(const op_t* op, int32_t k, const double* X, double* W) {
         }
       }
     }
-    if (op->shift != 0.0)
-      for (int64_t i = i0; i < i1; ++i)
-        for (int32_t j = 0; j < k; ++j) W[IDX(i, j, k)] = fma(-op->shift, X[IDX(i, j, k)], W[IDX(i, j, k)]);
   }
 }
 
-/* ||A - shift I||_inf = max_i sum_l |a_il - shift delta_il|   (reading R4) */
+/* W = A X - shift X  (or A (A X) - shift X when square; A^2 is never formed):
+ * each product an fma chain in ascending column order, then (shift != 0) w_ij = fma(-shift, x_ij, w_ij). */
+static void op_apply(const op_t* op, int32_t k, const double* X, double* W) {
+  const int64_t n = op->n;
+  if (op->square) {
+    double* T = (double*)malloc(sizeof(double) * (size_t)n * (size_t)k);
+    op_product(op, k, X, T);
+    op_product(op, k, T, W);
+    free(T);
+  } else {
+    op_product(op, k, X, W);
+  }
+  if (op->shift != 0.0) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+      for (int32_t j = 0; j < k; ++j) W[IDX(i, j, k)] = fma(-op->shift, X[IDX(i, j, k)], W[IDX(i, j, k)]);
+  }
+}
+
+/* ||A - shift I||_inf = max_i sum_l |a_il - shift delta_il|   (reading R4); for the squared
+ * operator the bound ||A||_inf^2 + |shift| >= ||A^2 - shift I||_2 (reading SQ1: A^2 is never formed) */
+static double op_norm_inf_plain(const op_t* op);
 static double op_norm_inf(const op_t* op) {
+  if (op->square) {
+    op_t a = *op;
+    a.square = 0; a.shift = 0.0;
+    const double na = op_norm_inf_plain(&a);
+    return na * na + fabs(op->shift);
+  }
+  return op_norm_inf_plain(op);
+}
+static double op_norm_inf_plain(const op_t* op) {
   double best = 0.0;
   for (int64_t i = 0; i < op->n; ++i) {
     nsum s = {0, 0};
@@ -348,6 +377,7 @@ typedef struct {
   int32_t beta_zero;   /* 0: beta_ij = -x_i^T x_j / 2; 1: beta = 0 (:460) */
   int32_t normalize;   /* 1: normalise columns after the update */
   int32_t top_zero;    /* 1: E_11 = 0 -- the sweep follows Rayleigh-Ritz (reading RR4) */
+  int32_t kjudge;      /* > 0: corr_norm over the leading kjudge columns only (K > k) */
 } oracle_opts;
 
 typedef struct {
@@ -492,8 +522,10 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   /* line 7: X~ = X + H E  with  H E = E - Y (T (Y^T E)) */
   double en;
   {
+    const int32_t kj = (o->kjudge > 0 && o->kjudge < k) ? o->kjudge : k;
     nsum s = {0, 0};
-    for (size_t t = 0; t < nk; ++t) nsum_add(&s, W[t] * W[t]);
+    for (size_t t = 0; t < nk; ++t)
+      if ((int32_t)(t % (size_t)k) < kj) nsum_add(&s, W[t] * W[t]);
     en = nsum_val(&s);
   }
   yt_b(n, k, Y, k, W, Z);                                   /* Qm = Y^T E */
@@ -548,7 +580,7 @@ done:
 }
 
 static void fill_opts(oracle_opts* o, double delta_c, int32_t beta_zero, int32_t normalize) {
-  o->delta_c = delta_c; o->beta_zero = beta_zero; o->normalize = normalize; o->top_zero = 0;
+  o->delta_c = delta_c; o->beta_zero = beta_zero; o->normalize = normalize; o->top_zero = 0; o->kjudge = 0;
 }
 
 int oracle_sweep_dense(int64_t n, int32_t k, const double* A, int64_t lda, double shift,
@@ -798,6 +830,48 @@ int oracle_rr_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci, co
 }
 /* k x k symmetric eigen-decomposition alone (tests): C (in, destroyed) -> Q, d (unsorted) */
 int oracle_jacobi_eig(int32_t k, double* C, double* Q, double* d) { return jacobi_eig(k, C, Q, d); }
+
+/* Extended entry points: square = 1 -> operator A^2 - shift I (Sec. 5.2);
+ * kjudge > 0 -> refine all k columns, judge (corr_norm, stopping) on the leading kjudge (K > k,
+ * PAPER.md:941-942, 958-967).  is_csr selects the dense (A, lda) or CSR (rp, ci, v) operand. */
+int oracle_sweep_ex(int is_csr, int64_t n, int32_t k, const double* A, int64_t lda, const int32_t* rp,
+                    const int32_t* ci, const double* v, double shift, int32_t square, double* X, double delta_c,
+                    int32_t beta_zero, int32_t kjudge, oracle_stats* st, double** dbg) {
+  op_t op = {is_csr, n, A, lda, rp, ci, v, shift, square};
+  oracle_opts o; fill_opts(&o, delta_c, beta_zero, 1); o.kjudge = kjudge;
+  return sweep(&op, k, X, op_norm_inf(&op), &o, st, dbg);
+}
+int oracle_run_ex(int is_csr, int64_t n, int32_t k, const double* A, int64_t lda, const int32_t* rp,
+                  const int32_t* ci, const double* v, double shift, int32_t square, double* X, int32_t iters,
+                  double tol, double delta_c, int32_t beta_zero, int32_t kjudge, int32_t* iters_done,
+                  double* history) {
+  op_t op = {is_csr, n, A, lda, rp, ci, v, shift, square};
+  oracle_opts o; fill_opts(&o, delta_c, beta_zero, 1); o.kjudge = kjudge;
+  const double normA = op_norm_inf(&op);
+  int status = OR_MAXITER;
+  int32_t t = 0;
+  for (; t < iters; ++t) {
+    oracle_stats s_;
+    const int s = sweep(&op, k, X, normA, &o, &s_, NULL);
+    if (s != OR_OK) { status = s; ++t; break; }
+    if (history) { history[2 * t] = s_.rel_resid; history[2 * t + 1] = s_.corr_norm; }
+    if (!isfinite(s_.corr_norm)) { status = OR_DIVERGED; ++t; break; }
+    if (s_.corr_norm <= tol) { status = OR_OK; ++t; break; }
+  }
+  if (iters_done) *iters_done = t;
+  return status;
+}
+int oracle_apply_ex(int is_csr, int64_t n, int32_t k, const double* A, int64_t lda, const int32_t* rp,
+                    const int32_t* ci, const double* v, double shift, int32_t square, const double* X, double* W) {
+  op_t op = {is_csr, n, A, lda, rp, ci, v, shift, square};
+  op_apply(&op, k, X, W);
+  return OR_OK;
+}
+double oracle_norm_ex(int is_csr, int64_t n, const double* A, int64_t lda, const int32_t* rp, const int32_t* ci,
+                      const double* v, double shift, int32_t square) {
+  op_t op = {is_csr, n, A, lda, rp, ci, v, shift, square};
+  return op_norm_inf(&op);
+}
 
 int oracle_num_threads(void) {
 #ifdef _OPENMP
