@@ -86,6 +86,11 @@ typedef struct {
   int32_t normalize;     /* 1: normalise columns after each update; default 1              */
   int32_t guard_window;  /* refine_run divergence guard window; default 3                                 */
   double guard_factor;   /* refine_run divergence guard growth factor; default 10                         */
+  int32_t square;        /* 1: the operator is A^2 - shift I applied as A (A X) (Sec. 5.2, PAPER.md:1218-1243;
+                            smallest-|lambda| targets); ||.|| in delta / rel_resid is ||A||_inf^2 + |shift|
+                            (reading SQ1).  world == 1 only (REFINE_E_UNSUPPORTED otherwise).  Default 0  */
+  int32_t kjudge;        /* > 0: refine all k columns but judge ||E_L||_F (stats, refine_run's stopping
+                            test) on the leading kjudge columns (K > k).  Default 0 = all */
 } refine_opts;
 
 /* Per-sweep diagnostics (host struct), for the sweep's input X^ (after the sign flip). */

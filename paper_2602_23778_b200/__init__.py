@@ -33,7 +33,8 @@ class refine_comm(C.Structure):
 
 class refine_opts(C.Structure):
     _fields_ = [("delta_c", C.c_double), ("beta_zero", C.c_int32), ("normalize", C.c_int32),
-                ("guard_window", C.c_int32), ("guard_factor", C.c_double)]
+                ("guard_window", C.c_int32), ("guard_factor", C.c_double), ("square", C.c_int32),
+                ("kjudge", C.c_int32)]
 
 
 class refine_sweep_stats(C.Structure):
@@ -116,9 +117,9 @@ def _check_dev(t, dtype, name):
         raise TypeError(f"{name} must be a contiguous CUDA tensor of dtype {dtype}")
 
 
-def _opts(delta_c=10.0, beta_zero=False, normalize=True, guard_window=3, guard_factor=10.0):
+def _opts(delta_c=10.0, beta_zero=False, normalize=True, guard_window=3, guard_factor=10.0, square=False, kjudge=0):
     return refine_opts(float(delta_c), int(bool(beta_zero)), int(bool(normalize)), int(guard_window),
-                       float(guard_factor))
+                       float(guard_factor), int(bool(square)), int(kjudge))
 
 
 @dataclass

@@ -116,6 +116,7 @@ struct Ws {
   // with D = 0 gives [X^T W | X^T X]), and the top-zero flag of the sweep that follows RR
   double *ritz, *zerod;
   int32_t top_zero;
+  int32_t kjudge;    // > 0: ||E_L||_F over the leading kjudge columns (K > k)
 };
 
 // X row of global index col: local rows first, else the halo (CSR row partition)

@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     ws.scal[j] = sig[j] / d[j];
     const double e2 = (ws.rr2[j] - 2.0 * pm + pgp) / (d[j] * d[j]);
     s_red[0][j] = r1 + ws.rr2[j];
-    s_red[1][j] = e1 + e2;
+    s_red[1][j] = (ws.kjudge > 0 && j >= ws.kjudge) ? 0.0 : e1 + e2;   // K > k: judge the leading kjudge
     double mg = INFINITY;
     for (int i = 0; i < k; ++i)
       if (i != j) mg = fmin(mg, fabs(d[j] - d[i]));

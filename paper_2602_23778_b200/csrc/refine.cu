@@ -206,14 +206,14 @@ template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}
 template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
 template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 2, 16};  static constexpr int C[4] = {64, 16, 1, 8}; };
 
+// Xg: the rows gathered (X, or A X for the second product of the squared operator), Xo: own rows
 template <bool HALO>
-static void launch_spmm(refine_ctx* c, bool vec, double* X) {
-  const Ws& ws = c->ws;
+static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double* Xo, const Ws& ws) {
   cudaStream_t s = c->stream;
   const int g = c->spmm_grid;
   if (vec && c->gather_R > 0) {   // vec: 16-byte aligned X / halo rows
     const int R = c->gather_R;
-    auto go = [&](auto kern) { kern<<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, X, R); };
+    auto go = [&](auto kern) { kern<<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, Xg, R, Xo); };
 #define RF_GATHER_K(KK)                                                          \
   case KK:                                                                       \
     if (c->gather_un == 5) go(spmm_gather_kernel<KK, HALO, 5>);                  \
@@ -234,20 +234,20 @@ static void launch_spmm(refine_ctx* c, bool vec, double* X) {
   }
   if (vec) {
     switch (c->k) {
-      case 2: spmm_csr_vec_kernel<1, 1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 4: spmm_csr_vec_kernel<1, 2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 8: spmm_csr_vec_kernel<1, 4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 16: spmm_csr_vec_kernel<1, 8, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 32: spmm_csr_vec_kernel<1, 16, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 64: spmm_csr_vec_kernel<1, 32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      default: spmm_csr_vec_kernel<2, 32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 2: spmm_csr_vec_kernel<1, 1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 4: spmm_csr_vec_kernel<1, 2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 8: spmm_csr_vec_kernel<1, 4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 16: spmm_csr_vec_kernel<1, 8, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 32: spmm_csr_vec_kernel<1, 16, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 64: spmm_csr_vec_kernel<1, 32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      default: spmm_csr_vec_kernel<2, 32, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
     }
   } else {
     switch ((c->k + 31) / 32) {
-      case 1: spmm_csr_kernel<1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 2: spmm_csr_kernel<2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      case 3: spmm_csr_kernel<3, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
-      default: spmm_csr_kernel<4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, X, X); break;
+      case 1: spmm_csr_kernel<1, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 2: spmm_csr_kernel<2, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      case 3: spmm_csr_kernel<3, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
+      default: spmm_csr_kernel<4, HALO><<<g, 256, 0, s>>>(ws, c->rp, c->ci, c->val, Xo, Xg); break;
     }
   }
 }
@@ -346,24 +346,33 @@ struct Kern {
           cudaEventRecord(c->ev_join, c->side);
           ++n;
         }
-        if (!c->csr) {
-          const double* Xb = c->multi ? c->Xfull : X;            // B operand: all n rows of X
-          const bool bv16 = xv16 && ((uintptr_t)Xb % 16 == 0);
-          const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
-          double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
-          c->mark();
-          gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
-              c->A, c->lda, Xb, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
-          c->mark();
-          w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(ws, X, c->nsplit, c->n_loc * c->k);
-          n += 2;
-        } else {
-          c->mark();
-          const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2 &&
-                           (ws.halo == nullptr || (uintptr_t)ws.halo % 16 == 0);
-          if (ws.halo) launch_spmm<true>(c, vec, X);
-          else launch_spmm<false>(c, vec, X);
-          n += 1;
+        // S1: W = A X - shift X, or (opts.square, Sec. 5.2) T = A X into X~'s buffer, then
+        // W = A T - shift X; the alpha / g partials are those of the last product.
+        for (int pass = 0; pass < (c->opts.square ? 2 : 1); ++pass) {
+          const bool last = pass + 1 == (c->opts.square ? 2 : 1);
+          Ws wp = ws;
+          if (!last) wp.shift = 0.0;
+          const double* Xg = pass ? ws.Xt : X;                   // operand of this product
+          if (pass) cudaMemcpyAsync(ws.Xt, ws.W, (size_t)c->n_loc * c->k * 8, cudaMemcpyDeviceToDevice, s);
+          if (!c->csr) {
+            const double* Xb = c->multi ? c->Xfull : Xg;           // B operand: all n rows
+            const bool bv16 = xv16 && ((uintptr_t)Xb % 16 == 0);
+            const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
+            double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
+            if (pass == 0) c->mark();
+            gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
+                c->A, c->lda, Xb, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
+            if (last) c->mark();
+            w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(wp, X, c->nsplit, c->n_loc * c->k);
+            n += 2;
+          } else {
+            if (pass == 0) c->mark();
+            const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2 &&
+                             (ws.halo == nullptr || (uintptr_t)ws.halo % 16 == 0);
+            if (ws.halo) launch_spmm<true>(c, vec, Xg, X, wp);
+            else launch_spmm<false>(c, vec, Xg, X, wp);
+            n += 1;
+          }
         }
         if (ph == 0 && c->multi) {
           ag_local_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
@@ -540,7 +549,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->n = n; c->k = k; c->kp = pad_kp(k);
   c->row_begin = row_begin; c->row_end = row_end; c->n_loc = row_end - row_begin;
   c->shift = shift;
-  c->opts = refine_opts{10.0, 0, 1, 3, 10.0};
+  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0};
   if (opts) c->opts = *opts;
   c->stream = (cudaStream_t)stream;
   RF_CK(c, cudaGetDevice(&c->device));
@@ -550,6 +559,8 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.top = (c->rank == 0) ? k : 0;
   ws.shift = shift;
   ws.beta_zero = c->opts.beta_zero;
+  ws.kjudge = c->opts.kjudge;
+  if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
   ws.world = world; ws.rank = rank;
   ws.multi = c->multi ? 1 : 0;
   ws.row0 = row_begin; ws.row1 = row_end;
@@ -603,10 +614,11 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   if (getenv("REFINE_KXK_TIMING")) RF_CK(c, cudaMalloc(&ws.tlog, 64 * sizeof(long long)));
   // local rows of ||A - shift I||_inf (one pass over A) -> delta = c ||A|| u
   double* rows = b + oRows;
+  const double nshift = c->opts.square ? 0.0 : shift;   // squared operator: ||A||_inf^2 + |shift| (SQ1)
   if (!c->csr)
-    absrow_max_dense_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->A, c->lda, c->n_loc, c->n, c->row_begin, shift, rows);
+    absrow_max_dense_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->A, c->lda, c->n_loc, c->n, c->row_begin, nshift, rows);
   else
-    absrow_max_csr_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, c->n_loc, c->row_begin, shift, rows);
+    absrow_max_csr_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, c->n_loc, c->row_begin, nshift, rows);
   max_kernel<<<1, 1024, 0, c->stream>>>(rows, c->n_loc, ws.stats + 7);
   unsigned long long* colr = reinterpret_cast<unsigned long long*>(b + oCol);
   if (c->csr && c->multi) {
@@ -668,6 +680,7 @@ static refine_status finalize_rank(refine_ctx* c, const std::vector<int64_t>& rb
   c->re_all = re;
   double normA = 0.0;
   for (double v : nrm) normA = std::max(normA, v);
+  if (c->opts.square) normA = normA * normA + std::fabs(c->shift);   // bound of ||A^2 - shift I|| (SQ1)
   c->ws.normA = normA;
   c->ws.delta = c->opts.delta_c * normA * std::ldexp(1.0, -53);
   if (c->multi && c->csr) {
@@ -697,7 +710,7 @@ static refine_status init_any(refine_ctx* c, int64_t n, int32_t k, int64_t row_b
     c->world = world;
     c->n = n; c->k = k; c->n_loc = n; c->row_begin = 0; c->row_end = n;
     c->stream = (cudaStream_t)stream;
-    c->opts = refine_opts{10.0, 0, 1, 3, 10.0};
+    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0};
     if (opts) c->opts = *opts;
     std::vector<int64_t> rb(world), re(world), lo(world), hi(world);
     std::vector<double> nrm(world);

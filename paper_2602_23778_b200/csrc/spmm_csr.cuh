@@ -17,8 +17,8 @@ template <int CPL, bool HALO>   // columns per lane = ceil(k / 32); HALO: row-pa
 __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx,
                                                        const double* __restrict__ val,
-                                                       const double* __restrict__ X,      // unused (see xrow)
-                                                       const double* __restrict__ Xloc) {  // local rows
+                                                       const double* __restrict__ X,      // own rows (x_i)
+                                                       const double* __restrict__ Xloc) {  // gathered rows
   __shared__ dd sa[8][KMAX], sg[8][KMAX];
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __r
         }
       }
     }
-    const double* xi = Xloc + i * k;
+    const double* xi = X + i * k;
     double* wi = ws.W + i * k;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
     }
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
-      const double2 x = reinterpret_cast<const double2*>(Xloc + i * K)[l + LPR * v];
+      const double2 x = reinterpret_cast<const double2*>(X + i * K)[l + LPR * v];   // own row
       double w0 = acc[2 * v], w1 = acc[2 * v + 1];
       if (ws.shift != 0.0) { w0 = __fma_rn(-ws.shift, x.x, w0); w1 = __fma_rn(-ws.shift, x.y, w1); }
       reinterpret_cast<double2*>(ws.W + i * K)[l + LPR * v] = make_double2(w0, w1);
@@ -212,7 +212,7 @@ RF_DEV double2 ldg2_at(const char* base, uint32_t idx2) {   // base + idx2 doubl
 template <int K, bool HALO, int UN_ = 8, int LPR_ = 0, int MINB_ = 0>
 __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spmm_gather_kernel(
     Ws ws, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ xoff, const double* __restrict__ val,
-    const double* __restrict__ Xloc, const int R) {
+    const double* __restrict__ Xloc, const int R, const double* __restrict__ Xown) {   // gathered rows / own rows
   using C = GatherCfg<K, UN_, LPR_, MINB_>;
   constexpr int LPR = C::LPR, VPL = C::VPL, RG = C::RG, RMAX = C::RMAX, NZCAP = C::NZCAP, UN = C::UN, K2 = K / 2;
   __shared__ int32_t s_rp[3][RMAX + 1];
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
   const int64_t nchunk = (n + R - 1) / R;
   const int T = (int)((nchunk - blockIdx.x + G - 1) / G);
   const char* Xb = reinterpret_cast<const char*>(Xloc);
+  const char* Xo = reinterpret_cast<const char*>(Xown);
   const char* Hb = reinterpret_cast<const char*>(ws.halo);
   char* Wb = reinterpret_cast<char*>(ws.W);
   auto r0_of = [=](int t) { return ((int64_t)t * G + blockIdx.x) * R; };
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
         const uint32_t i2 = rb2 + (uint32_t)rr * K2;
         double2 xi[VPL];
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) xi[v] = ldg2_at(Xb + 16 * LPR * v, i2);
+        for (int v = 0; v < VPL; ++v) xi[v] = ldg2_at(Xo + 16 * LPR * v, i2);
         double acc[2 * VPL];
 #pragma unroll
         for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;
