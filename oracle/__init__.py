@@ -38,7 +38,7 @@ def build(force: bool = False) -> str:
 
 class Stats(C.Structure):
     _fields_ = [("rel_resid", C.c_double), ("corr_norm", C.c_double), ("min_gap", C.c_double),
-                ("delta_hits", C.c_int32), ("flipped", C.c_int32)]
+                ("delta_hits", C.c_int32), ("flipped", C.c_int32), ("gram_dev", C.c_double)]
 
 
 _lib = None
@@ -74,6 +74,7 @@ def lib():
         L.oracle_apply_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, P]
         L.oracle_norm_ex.argtypes = [C.c_int, i64, P, i64, P, P, P, d, i32]
         L.oracle_norm_ex.restype = d
+        L.oracle_reorthogonalize.argtypes = [i64, i32, P, P]
         L.oracle_num_threads.restype = C.c_int
         for f in ("oracle_apply_dense", "oracle_apply_csr", "oracle_modified_lu", "oracle_compact_wy_lu",
                   "oracle_compact_wy", "oracle_apply_h", "oracle_sweep_dense", "oracle_sweep_csr",
@@ -277,6 +278,57 @@ def sweep_rr(op: Operator, X, delta_c=10.0):
     else:
         s = L.oracle_sweep_tz_dense(n, k, _p(op.A), n, op.shift, _p(Z), delta_c, C.byref(st))
     return SweepResult(Z, s, st, {}), ritz
+
+
+def reorthogonalize(X):
+    """Cholesky-QR reorthogonalisation X <- X L^{-T} (NEXT-4).  Returns (status, Z, gram_dev)."""
+    Z = np.array(X, dtype=np.float64, order="C", copy=True)
+    n, k = Z.shape
+    gd = C.c_double(0.0)
+    s = lib().oracle_reorthogonalize(n, k, _p(Z), C.byref(gd))
+    return s, Z, gd.value
+
+
+def run_policy(op: Operator, X, iters: int, tol: float, resid_tol: float = 0.0, reorth_tol: float = 0.0,
+               rr_fallback: bool = False, delta_c=10.0, beta_zero=False, guard_window=3, guard_factor=10.0):
+    """refine_run with the NEXT-4 policies (the loop is plain Python over the oracle's C sweeps):
+      * stop when ||E_L||_F <= tol or, resid_tol > 0, when the relative residual
+        ||A X - X D||_F / ||A|| <= resid_tol (PAPER.md:495-499);
+      * reorth_tol > 0: when a sweep's input has max|X^T X - I| > reorth_tol, reorthogonalise its
+        output (Cholesky QR; PAPER.md:508);
+      * the divergence guard (||E_L||_F grows >= guard_factor within guard_window sweeps,
+        PAPER.md:1155); rr_fallback: instead of stopping, continue with Rayleigh-Ritz iterations
+        (Sec. 3.4, the paper's "terminate and switch to preprocessing").
+    Returns (X, status, sweeps, history[(rel_resid, corr_norm, mode)]) with mode 0 = plain, 1 = RR."""
+    X = _f64(X).copy()
+    hist = []
+    mode = 0
+    cs = []
+    for t in range(iters):
+        if mode == 0:
+            res = sweep(op, X, delta_c=delta_c, beta_zero=beta_zero)
+        else:
+            res, _ = sweep_rr(op, X, delta_c=delta_c)
+        if res.status != OK:
+            return res.X, res.status, t + 1, np.array(hist)
+        st = res.stats
+        hist.append((st.rel_resid, st.corr_norm, mode))
+        if not np.isfinite(st.corr_norm):
+            return res.X, DIVERGED, t + 1, np.array(hist)
+        X = res.X
+        if st.corr_norm <= tol or (resid_tol > 0 and st.rel_resid <= resid_tol):
+            return X, OK, t + 1, np.array(hist)
+        cs.append(st.corr_norm)
+        if mode == 0 and guard_window > 0 and len(cs) > guard_window and cs[-1] >= guard_factor * cs[-1 - guard_window]:
+            if not rr_fallback:
+                return X, DIVERGED, t + 1, np.array(hist)
+            mode = 1
+            continue
+        if mode == 0 and reorth_tol > 0 and st.gram_dev > reorth_tol:
+            s, X, _ = reorthogonalize(X)
+            if s != OK:
+                return X, s, t + 1, np.array(hist)
+    return X, MAXITER, iters, np.array(hist)
 
 
 def jacobi_eig(Cm):

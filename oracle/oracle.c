@@ -386,6 +386,7 @@ typedef struct {
   double min_gap;      /* min_{i != j} |d_j - d_i| */
   int32_t delta_hits;  /* number of ordered pairs (i,j), i != j, that took the beta branch */
   int32_t flipped;     /* any sigma_j = -1 */
+  double gram_dev;     /* max_ij |(X^T X - I)_ij| of the sweep's input (NEXT-4 reorthogonalisation policy) */
 } oracle_stats;
 
 /* Optional dumps of the sweep's intermediates (each may be NULL):
@@ -412,7 +413,9 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   double* d = (double*)malloc(sizeof(double) * (size_t)k);
   double* nrm = (double*)malloc(sizeof(double) * (size_t)k);
   int status = OR_OK;
-  if (!W || !Y || !T || !U || !Z || !P || !sig || !alpha || !d || !nrm) { status = OR_E_NOMEM; goto done; }
+  double* X0 = st ? (double*)malloc(sizeof(double) * nk) : NULL;
+  if (!W || !Y || !T || !U || !Z || !P || !sig || !alpha || !d || !nrm || (st && !X0)) { status = OR_E_NOMEM; goto done; }
+  if (X0) memcpy(X0, X, sizeof(double) * nk);
 
   /* line 1: W = A X  (with the Sec. 5.1 shift) */
   op_apply(op, k, X, W);
@@ -558,6 +561,15 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   }
 
   if (st) {
+    double gd = 0.0;   /* Gram deviation of the (post-flip) input; |entries| are flip-invariant */
+    for (int32_t a = 0; a < k; ++a)
+      for (int32_t b = 0; b < k; ++b) {
+        nsum g = {0, 0};
+        for (int64_t i = 0; i < n; ++i) nsum_add(&g, X0[IDX(i, a, k)] * X0[IDX(i, b, k)]);
+        const double dv = fabs(nsum_val(&g) - (a == b ? 1.0 : 0.0));
+        if (dv > gd) gd = dv;
+      }
+    st->gram_dev = gd;
     st->rel_resid = sqrt(rr) / normA;
     st->corr_norm = sqrt(en);
     st->min_gap = (k > 1) ? min_gap : 0.0;
@@ -575,7 +587,7 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   for (size_t t = 0; t < nk; ++t)
     if (!isfinite(X[t])) { status = OR_DIVERGED; break; }
 done:
-  free(W); free(Y); free(T); free(U); free(Z); free(P); free(sig); free(alpha); free(d); free(nrm);
+  free(W); free(Y); free(T); free(U); free(Z); free(P); free(sig); free(alpha); free(d); free(nrm); free(X0);
   return status;
 }
 
@@ -871,6 +883,52 @@ double oracle_norm_ex(int is_csr, int64_t n, const double* A, int64_t lda, const
                       const double* v, double shift, int32_t square) {
   op_t op = {is_csr, n, A, lda, rp, ci, v, shift, square};
   return op_norm_inf(&op);
+}
+
+/* =========================================================================
+ * Reorthogonalisation ("optionally reorthogonalize"): Cholesky QR,
+ * X <- X L^{-T} with X^T X = L L^T (Neumaier Gram, plain k x k arithmetic), so the columns become
+ * orthonormal and span(X) is kept.  gram_dev (nullable): max |X^T X - I| before.  OR_E_INVALID if a
+ * pivot <= 4 k u G_jj (X rank deficient).
+ * ========================================================================= */
+int oracle_reorthogonalize(int64_t n, int32_t k, double* X, double* gram_dev) {
+  const size_t kk = (size_t)k * (size_t)k;
+  double* G = (double*)malloc(sizeof(double) * kk);
+  double* row = (double*)malloc(sizeof(double) * (size_t)k);
+  if (!G || !row) { free(G); free(row); return OR_E_NOMEM; }
+  double gd = 0.0;
+  for (int32_t a = 0; a < k; ++a)
+    for (int32_t b = 0; b < k; ++b) {
+      nsum g = {0, 0};
+      for (int64_t i = 0; i < n; ++i) nsum_add(&g, X[IDX(i, a, k)] * X[IDX(i, b, k)]);
+      G[IDX(a, b, k)] = nsum_val(&g);
+      const double dv = fabs(G[IDX(a, b, k)] - (a == b ? 1.0 : 0.0));
+      if (dv > gd) gd = dv;
+    }
+  if (gram_dev) *gram_dev = gd;
+  for (int32_t j = 0; j < k; ++j) {                 /* G = L L^T (lower) */
+    double sj = G[IDX(j, j, k)];
+    const double g0 = sj;
+    for (int32_t l = 0; l < j; ++l) sj -= G[IDX(j, l, k)] * G[IDX(j, l, k)];
+    if (!(sj > 4.0 * k * ldexp(1.0, -53) * g0)) { free(G); free(row); return OR_E_INVALID; }
+    const double ljj = sqrt(sj);
+    G[IDX(j, j, k)] = ljj;
+    for (int32_t i = j + 1; i < k; ++i) {
+      double t = G[IDX(i, j, k)];
+      for (int32_t l = 0; l < j; ++l) t -= G[IDX(i, l, k)] * G[IDX(j, l, k)];
+      G[IDX(i, j, k)] = t / ljj;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) {                 /* row x_i <- x_i L^{-T}: solve z L^T = x_i */
+    for (int32_t j = 0; j < k; ++j) {
+      double t = X[IDX(i, j, k)];
+      for (int32_t l = 0; l < j; ++l) t -= row[l] * G[IDX(j, l, k)];
+      row[j] = t / G[IDX(j, j, k)];
+    }
+    for (int32_t j = 0; j < k; ++j) X[IDX(i, j, k)] = row[j];
+  }
+  free(G); free(row);
+  return OR_OK;
 }
 
 int oracle_num_threads(void) {
