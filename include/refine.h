@@ -91,6 +91,13 @@ typedef struct {
                             (reading SQ1).  world == 1 only (REFINE_E_UNSUPPORTED otherwise).  Default 0  */
   int32_t kjudge;        /* > 0: refine all k columns but judge ||E_L||_F (stats, refine_run's stopping
                             test) on the leading kjudge columns (K > k).  Default 0 = all */
+  double resid_tol;      /* > 0: refine_run also stops (REFINE_OK) when rel_resid <= resid_tol
+                            (PAPER.md:495-499).  Default 0 = off                                            */
+  double reorth_tol;     /* > 0: sweeps report gram_dev, and refine_run reorthogonalises (Cholesky QR,
+                            refine_reorthogonalize) the output of every sweep whose input had
+                            gram_dev > reorth_tol.  world == 1.  Default 0 = off            */
+  int32_t rr_fallback;   /* 1: when refine_run's divergence guard trips, continue with refine_sweep_rr
+                            iterations instead of returning REFINE_DIVERGED        */
 } refine_opts;
 
 /* Per-sweep diagnostics (host struct), for the sweep's input X^ (after the sign flip). */
@@ -100,6 +107,7 @@ typedef struct {
   double min_gap;        /* min_{i != j} |d_j - d_i| over the k Rayleigh quotients                       */
   int32_t delta_hits;    /* ordered pairs (i, j), i != j, that took the beta branch        */
   int32_t flipped;       /* 1 if any sigma_j = -1 this sweep (X^ <- X^ Sigma)           */
+  double gram_dev;       /* max |X^T X - I| of the sweep's input when opts.reorth_tol > 0, else -1          */
 } refine_sweep_stats;
 
 /* Dense symmetric A (both triangles), FP64, row-major, device pointer.
@@ -138,7 +146,9 @@ refine_status refine_sweep_host(refine_ctx* c, const double* X_host_in, double* 
 
 /* Iterate sweeps on X (device) until ||E_L||_F <= tol (REFINE_OK), iters sweeps
  * (REFINE_MAXITER), divergence (REFINE_DIVERGED) or a device error.  Synchronises.
- * iters_done / last (nullable) report the sweeps executed and the last stats. */
+ * iters_done / last (nullable) report the sweeps executed and the last stats.
+ * opts.resid_tol / reorth_tol / rr_fallback add the NEXT-4 policies (see refine_opts);
+ * the plain loop runs without host synchronisation (device-side halting). */
 refine_status refine_run(refine_ctx* c, double* X, int32_t iters, double tol,
                          int32_t* iters_done, refine_sweep_stats* last);
 
@@ -152,6 +162,12 @@ refine_status refine_run(refine_ctx* c, double* X, int32_t iters, double tol,
  * D~.  Synchronises.  REFINE_E_INVALID if X^T X is not positive definite (X rank
  * deficient); X is then unchanged. */
 refine_status refine_rayleigh_ritz(refine_ctx* c, double* X, double* ritz);
+
+/* Reorthogonalisation ("optionally reorthogonalize"): Cholesky QR,
+ * X <- X L^{-T} with X^T X = L L^T (columns orthonormal, span kept).  gram_dev (host,
+ * nullable) receives max |X^T X - I| before.  Synchronises.  REFINE_E_INVALID if X is
+ * rank deficient (X unchanged). */
+refine_status refine_reorthogonalize(refine_ctx* c, double* X, double* gram_dev);
 
 /* One iteration of the preprocessed refinement: refine_rayleigh_ritz, then one sweep
  * whose E_L top block is set to its exact-arithmetic value 0 (beta = 0,

@@ -68,7 +68,7 @@ def lib():
         L.oracle_jacobi_eig.argtypes = [i32, P, P, P]
         L.oracle_sweep_tz_dense.argtypes = [i64, i32, P, i64, d, P, d, C.POINTER(Stats)]
         L.oracle_sweep_tz_csr.argtypes = [i64, i32, P, P, P, d, P, d, C.POINTER(Stats)]
-        L.oracle_sweep_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, d, i32, i32, C.POINTER(Stats), P]
+        L.oracle_sweep_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, d, i32, i32, i32, C.POINTER(Stats), P]
         L.oracle_run_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, i32, d, d, i32, i32,
                                     C.POINTER(i32), P]
         L.oracle_apply_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, P]
@@ -195,16 +195,18 @@ def _ex_args(op):
     return (0, op.n, _p(op.A), op.n, None, None, None, op.shift, int(op.square))
 
 
-def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=False, kjudge=0) -> SweepResult:
+def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=False, kjudge=0,
+          want_gram=False) -> SweepResult:
     """One sweep of Alg. 4 on a copy of X.  kjudge > 0: corr_norm over the leading
-    kjudge columns (K > k refinement)."""
-    if op.square or kjudge:
+    kjudge columns (K > k refinement); want_gram: stats.gram_dev (else -1)."""
+    if op.square or kjudge or want_gram:
         assert normalize and not debug
         X = _f64(X).copy()
         n, k = X.shape
         st = Stats()
         a = _ex_args(op)
-        s = lib().oracle_sweep_ex(*a[:2], k, *a[2:], _p(X), delta_c, int(beta_zero), int(kjudge), C.byref(st), None)
+        s = lib().oracle_sweep_ex(*a[:2], k, *a[2:], _p(X), delta_c, int(beta_zero), int(kjudge), int(want_gram),
+                                  C.byref(st), None)
         return SweepResult(X, s, st, {})
     X = _f64(X).copy()
     n, k = X.shape
@@ -306,7 +308,7 @@ def run_policy(op: Operator, X, iters: int, tol: float, resid_tol: float = 0.0, 
     cs = []
     for t in range(iters):
         if mode == 0:
-            res = sweep(op, X, delta_c=delta_c, beta_zero=beta_zero)
+            res = sweep(op, X, delta_c=delta_c, beta_zero=beta_zero, want_gram=reorth_tol > 0)
         else:
             res, _ = sweep_rr(op, X, delta_c=delta_c)
         if res.status != OK:

@@ -378,6 +378,7 @@ typedef struct {
   int32_t normalize;   /* 1: normalise columns after the update */
   int32_t top_zero;    /* 1: E_11 = 0 -- the sweep follows Rayleigh-Ritz (reading RR4) */
   int32_t kjudge;      /* > 0: corr_norm over the leading kjudge columns only (K > k) */
+  int32_t want_gram;   /* 1: stats.gram_dev = max |X^T X - I| of the input (else -1) */
 } oracle_opts;
 
 typedef struct {
@@ -413,8 +414,10 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   double* d = (double*)malloc(sizeof(double) * (size_t)k);
   double* nrm = (double*)malloc(sizeof(double) * (size_t)k);
   int status = OR_OK;
-  double* X0 = st ? (double*)malloc(sizeof(double) * nk) : NULL;
-  if (!W || !Y || !T || !U || !Z || !P || !sig || !alpha || !d || !nrm || (st && !X0)) { status = OR_E_NOMEM; goto done; }
+  double* X0 = (st && o->want_gram) ? (double*)malloc(sizeof(double) * nk) : NULL;
+  if (!W || !Y || !T || !U || !Z || !P || !sig || !alpha || !d || !nrm || (st && o->want_gram && !X0)) {
+    status = OR_E_NOMEM; goto done;
+  }
   if (X0) memcpy(X0, X, sizeof(double) * nk);
 
   /* line 1: W = A X  (with the Sec. 5.1 shift) */
@@ -561,14 +564,18 @@ static int sweep(const op_t* op, int32_t k, double* X, double normA, const oracl
   }
 
   if (st) {
-    double gd = 0.0;   /* Gram deviation of the (post-flip) input; |entries| are flip-invariant */
-    for (int32_t a = 0; a < k; ++a)
-      for (int32_t b = 0; b < k; ++b) {
-        nsum g = {0, 0};
-        for (int64_t i = 0; i < n; ++i) nsum_add(&g, X0[IDX(i, a, k)] * X0[IDX(i, b, k)]);
-        const double dv = fabs(nsum_val(&g) - (a == b ? 1.0 : 0.0));
-        if (dv > gd) gd = dv;
-      }
+    double gd = -1.0;  /* Gram deviation of the (post-flip) input; |entries| are flip-invariant */
+    if (X0) {
+      gd = 0.0;
+      #pragma omp parallel for schedule(static) reduction(max : gd)
+      for (int32_t a = 0; a < k; ++a)
+        for (int32_t b = 0; b < k; ++b) {
+          nsum g = {0, 0};
+          for (int64_t i = 0; i < n; ++i) nsum_add(&g, X0[IDX(i, a, k)] * X0[IDX(i, b, k)]);
+          const double dv = fabs(nsum_val(&g) - (a == b ? 1.0 : 0.0));
+          if (dv > gd) gd = dv;
+        }
+    }
     st->gram_dev = gd;
     st->rel_resid = sqrt(rr) / normA;
     st->corr_norm = sqrt(en);
@@ -592,7 +599,7 @@ done:
 }
 
 static void fill_opts(oracle_opts* o, double delta_c, int32_t beta_zero, int32_t normalize) {
-  o->delta_c = delta_c; o->beta_zero = beta_zero; o->normalize = normalize; o->top_zero = 0; o->kjudge = 0;
+  o->delta_c = delta_c; o->beta_zero = beta_zero; o->normalize = normalize; o->top_zero = 0; o->kjudge = 0; o->want_gram = 0;
 }
 
 int oracle_sweep_dense(int64_t n, int32_t k, const double* A, int64_t lda, double shift,
@@ -848,9 +855,9 @@ int oracle_jacobi_eig(int32_t k, double* C, double* Q, double* d) { return jacob
  * PAPER.md:941-942, 958-967).  is_csr selects the dense (A, lda) or CSR (rp, ci, v) operand. */
 int oracle_sweep_ex(int is_csr, int64_t n, int32_t k, const double* A, int64_t lda, const int32_t* rp,
                     const int32_t* ci, const double* v, double shift, int32_t square, double* X, double delta_c,
-                    int32_t beta_zero, int32_t kjudge, oracle_stats* st, double** dbg) {
+                    int32_t beta_zero, int32_t kjudge, int32_t want_gram, oracle_stats* st, double** dbg) {
   op_t op = {is_csr, n, A, lda, rp, ci, v, shift, square};
-  oracle_opts o; fill_opts(&o, delta_c, beta_zero, 1); o.kjudge = kjudge;
+  oracle_opts o; fill_opts(&o, delta_c, beta_zero, 1); o.kjudge = kjudge; o.want_gram = want_gram;
   return sweep(&op, k, X, op_norm_inf(&op), &o, st, dbg);
 }
 int oracle_run_ex(int is_csr, int64_t n, int32_t k, const double* A, int64_t lda, const int32_t* rp,

@@ -34,12 +34,13 @@ class refine_comm(C.Structure):
 class refine_opts(C.Structure):
     _fields_ = [("delta_c", C.c_double), ("beta_zero", C.c_int32), ("normalize", C.c_int32),
                 ("guard_window", C.c_int32), ("guard_factor", C.c_double), ("square", C.c_int32),
-                ("kjudge", C.c_int32)]
+                ("kjudge", C.c_int32), ("resid_tol", C.c_double), ("reorth_tol", C.c_double),
+                ("rr_fallback", C.c_int32)]
 
 
 class refine_sweep_stats(C.Structure):
     _fields_ = [("rel_resid", C.c_double), ("corr_norm", C.c_double), ("min_gap", C.c_double),
-                ("delta_hits", C.c_int32), ("flipped", C.c_int32)]
+                ("delta_hits", C.c_int32), ("flipped", C.c_int32), ("gram_dev", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -88,9 +89,11 @@ def lib() -> C.CDLL:
         L.refine_halo_plan.restype = i32
         L.refine_rayleigh_ritz.argtypes = [P, P, P]
         L.refine_sweep_rr.argtypes = [P, P, C.POINTER(refine_sweep_stats), P]
+        L.refine_reorthogonalize.argtypes = [P, P, P]
         for f in ("refine_init_dense", "refine_init_csr", "refine_sweep", "refine_sweep_host", "refine_run",
                   "refine_get_status", "refine_set_graph", "refine_nccl_id", "refine_debug_get",
-                  "refine_profile_begin", "refine_profile_end", "refine_rayleigh_ritz", "refine_sweep_rr"):
+                  "refine_profile_begin", "refine_profile_end", "refine_rayleigh_ritz", "refine_sweep_rr",
+                  "refine_reorthogonalize"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -117,9 +120,11 @@ def _check_dev(t, dtype, name):
         raise TypeError(f"{name} must be a contiguous CUDA tensor of dtype {dtype}")
 
 
-def _opts(delta_c=10.0, beta_zero=False, normalize=True, guard_window=3, guard_factor=10.0, square=False, kjudge=0):
+def _opts(delta_c=10.0, beta_zero=False, normalize=True, guard_window=3, guard_factor=10.0, square=False, kjudge=0,
+          resid_tol=0.0, reorth_tol=0.0, rr_fallback=False):
     return refine_opts(float(delta_c), int(bool(beta_zero)), int(bool(normalize)), int(guard_window),
-                       float(guard_factor), int(bool(square)), int(kjudge))
+                       float(guard_factor), int(bool(square)), int(kjudge), float(resid_tol), float(reorth_tol),
+                       int(bool(rr_fallback)))
 
 
 @dataclass
@@ -218,6 +223,14 @@ class Refiner:
         s = lib().refine_rayleigh_ritz(self._h, _ptr(X), C.c_void_p(ritz.ctypes.data))
         return s, ritz
 
+    def refine_reorthogonalize(self, X):
+        """Cholesky-QR reorthogonalisation of X in place.  Returns (status, gram_dev before)."""
+        import torch
+        _check_dev(X, torch.float64, "X")
+        gd = C.c_double(0.0)
+        s = lib().refine_reorthogonalize(self._h, _ptr(X), C.byref(gd))
+        return s, gd.value
+
     def refine_sweep_rr(self, X):
         """Rayleigh-Ritz, then one sweep with the E_L top block zero.
         Returns (status, refine_sweep_stats, ritz)."""
@@ -297,7 +310,7 @@ EXPORTED = ("refine_init_dense", "refine_init_csr", "refine_sweep", "refine_swee
             "refine_get_status", "refine_set_graph", "refine_kernels_per_sweep", "refine_destroy",
             "refine_status_string", "refine_nccl_id", "refine_debug_get", "refine_profile_begin",
             "refine_profile_end", "refine_kernel_name", "refine_halo_plan", "refine_rayleigh_ritz",
-            "refine_sweep_rr")
+            "refine_sweep_rr", "refine_reorthogonalize")
 
 
 def refine_halo_plan(world: int, rank: int, row_begin, row_end, col_lo, col_hi, cap: int = 64):

@@ -117,6 +117,8 @@ struct Ws {
   double *ritz, *zerod;
   int32_t top_zero;
   int32_t kjudge;    // > 0: ||E_L||_F over the leading kjudge columns (K > k)
+  int32_t want_gram; // 1: kxk_finish reports max |X^T X - I| of the sweep's input in stats[6] (else -1)
+  int* gate;         // refine_run reorthogonalisation gate: ST_OK when the gated pipeline must run
 };
 
 // X row of global index col: local rows first, else the halo (CSR row partition)

@@ -458,6 +458,23 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     ws.Csig[e] = sig[l] * (Pt[e] / d[j] + UB[e]);      // Csig = Sigma (P~ D^{-1} + U'^{-1} B)
   }
   __syncthreads();
+  // Gram deviation of the sweep's input (reorthogonalisation policy): G = X'_1^T X'_1 + G'
+  double gmax = -1.0;
+  if (ws.want_gram) {
+    cta_gemm(k, k, k, 1.0, Xp, k, true, Xp, k, false, 1.0, Gp, k, LB, k, sm);
+    double m = 0.0;
+    for (int e = tid; e < kk; e += nt) m = fmax(m, fabs(LB[e] - ((e / k == e % k) ? 1.0 : 0.0)));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) s_red[0][tid >> 5] = m;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < nt / 32; ++w) m = fmax(m, s_red[0][w]);
+      s_red[0][0] = m;
+    }
+    __syncthreads();
+    gmax = s_red[0][0];
+    __syncthreads();
+  }
   // per-column quantities and statistics
   if (tid < k) {
     const int j = tid;
@@ -491,6 +508,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     ws.stats[3] = (double)s_hits;
     ws.stats[4] = (fl > 0.0) ? 1.0 : 0.0;
     ws.stats[5] = rr;
+    ws.stats[6] = gmax;
   }
 }
 
@@ -545,8 +563,10 @@ __device__ void rr_rotate(int k, double* C, double* Q, int m, int round, double*
   __syncthreads();
 }
 
+// mode 1: reorthogonalisation by Cholesky QR: S = L^{-T} (no pencil, no Jacobi), and
+// max |X^T X - I| before it into ritz[0].
 __global__ void __launch_bounds__(KXK_THREADS) rr_kxk_kernel(Ws ws, const double* __restrict__ Xtop,
-                                                             const double* __restrict__ Wtop) {
+                                                             const double* __restrict__ Wtop, int mode) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double s_cs[KMAX / 2 + 1], s_sn[KMAX / 2 + 1], s_red[KXK_THREADS / 32];
   __shared__ int s_p[KMAX / 2 + 1], s_q[KMAX / 2 + 1], s_ord[KMAX], s_bad;
@@ -567,11 +587,24 @@ __global__ void __launch_bounds__(KXK_THREADS) rr_kxk_kernel(Ws ws, const double
   }
   for (int e = tid; e < kk; e += nt) X1[e] = Xtop[e];
   __syncthreads();
-  cta_gemm(k, k, k, 1.0, X1, k, true, Wtop, k, false, 1.0, ws.M2, k, M, k, sm);   // M = M2 + X_1^T W_1
+  if (mode == 0)
+    cta_gemm(k, k, k, 1.0, X1, k, true, Wtop, k, false, 1.0, ws.M2, k, M, k, sm);   // M = M2 + X_1^T W_1
   cta_gemm(k, k, k, 1.0, X1, k, true, X1, k, false, 1.0, ws.G2, k, G, k, sm);      // G = G2 + X_1^T X_1
-  for (int e = tid; e < kk; e += nt) {                                              // RR1
-    const int i = e / k, j = e % k;
-    if (i < j) { const double m = (M[e] + M[j * k + i]) / 2.0; M[e] = m; M[j * k + i] = m; }
+  if (mode == 0) {
+    for (int e = tid; e < kk; e += nt) {                                            // RR1
+      const int i = e / k, j = e % k;
+      if (i < j) { const double m = (M[e] + M[j * k + i]) / 2.0; M[e] = m; M[j * k + i] = m; }
+    }
+  } else {                                                                          // Gram deviation
+    double gm = 0.0;
+    for (int e = tid; e < kk; e += nt) gm = fmax(gm, fabs(G[e] - ((e / k == e % k) ? 1.0 : 0.0)));
+    for (int o = 16; o > 0; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if ((tid & 31) == 0) s_red[tid >> 5] = gm;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < nt / 32; ++w) gm = fmax(gm, s_red[w]);
+      ws.ritz[0] = gm;
+    }
   }
   __syncthreads();
   // Cholesky G = L L^T, right-looking, L in G's lower triangle
@@ -604,6 +637,17 @@ __global__ void __launch_bounds__(KXK_THREADS) rr_kxk_kernel(Ws ws, const double
   }
   __syncthreads();
   cta_trinv(k, Lt, true, Ui, tmp, sm);                                            // Ui = L^{-T}
+  if (mode == 1) {                                                                // Cholesky QR: S = L^{-T}
+    cta_gemm(k, k, k, 1.0, X1, k, false, Ui, k, false, 0.0, nullptr, 0, ws.Xt, k, sm);  // Z_1 = X_1 S
+    for (int e = tid; e < kk; e += nt) ws.Csig[e] = -Ui[e];
+    if (tid < k) {
+      ws.scal[tid] = 0.0;
+      double nt2 = 0.0;
+      for (int i = 0; i < k; ++i) nt2 = fma(ws.Xt[i * k + tid], ws.Xt[i * k + tid], nt2);
+      ws.ntop[tid] = nt2;
+    }
+    return;
+  }
   cta_gemm(k, k, k, 1.0, Ui, k, true, M, k, false, 0.0, nullptr, 0, T1, k, sm);   // Ui^T M
   cta_gemm(k, k, k, 1.0, T1, k, false, Ui, k, false, 0.0, nullptr, 0, Cm, k, sm); // C = Ui^T M Ui
   for (int e = tid; e < kk; e += nt) {

@@ -42,23 +42,29 @@ constexpr int ST_HALT_CONVERGED = 100;   // refine_run: device-side stop (conver
 
 struct RunState {   // device-resident refine_run bookkeeping
   int32_t done;     // sweeps completed
-  int32_t pad;
+  int32_t guard;    // 1: stopped by the divergence guard (refine_run's rr_fallback continues from there)
   double hist[4];   // last corr norms (ring) for the divergence guard
 };
 
+// After each sweep of refine_run: convergence (||E_L||_F <= tol; or rel_resid <=
+// resid_tol), divergence (non-finite; the growth guard), and the
+// reorthogonalisation gate (gram_dev of the sweep's input > reorth_tol).
 __global__ void run_check_kernel(int* status, RunState* rs, const double* stats, double tol, int window,
-                                 double factor) {
+                                 double factor, double resid_tol, double reorth_tol, int* gate) {
+  if (gate) *gate = 1;
   if (*status != ST_OK) return;
   const double c = stats[1];
   const int t = rs->done;
   rs->done = t + 1;
   if (!isfinite(c)) { *status = ST_DIVERGED; return; }
-  if (c <= tol) { *status = ST_HALT_CONVERGED; return; }
+  if (c <= tol || (resid_tol > 0.0 && stats[0] <= resid_tol)) { *status = ST_HALT_CONVERGED; return; }
   if (window > 0 && window <= 4 && t >= window && c >= factor * rs->hist[(t - window) & 3]) {
     *status = ST_DIVERGED;
+    rs->guard = 1;
     return;
   }
   rs->hist[t & 3] = c;
+  if (gate && reorth_tol > 0.0 && stats[6] > reorth_tol) *gate = ST_OK;
 }
 
 __global__ void absrow_max_dense_kernel(const double* A, int64_t lda, int64_t n_loc, int64_t n, int64_t row0,
@@ -138,6 +144,7 @@ struct refine_ctx {
   // CSR gather kernel (spmm_gather_kernel): rows per chunk (0 = not eligible -> vec / generic
   // kernel) and the precomputed gather offsets (owned; indexed by absolute CSR position)
   int gather_R = 0, gather_un = 8;
+  bool gated = false;   // phase(): launch with ws.status -> ws.gate (refine_run reorthogonalisation)
   int32_t* xoff_buf = nullptr;
   const int32_t* xoff = nullptr;
   double shift = 0.0;
@@ -331,7 +338,8 @@ struct Kern {
 
   // phase ph of one sweep on this rank (see the file header); returns kernels launched
   static int phase(refine_ctx* c, int ph, double* X) {
-    Ws& ws = c->ws;
+    Ws ws = c->ws;
+    if (c->gated) ws.status = ws.gate;     // refine_run's reorthogonalisation pipeline runs behind the gate
     cudaStream_t s = c->stream;
     int n = 0;
     const bool xv16 = (c->k % 2 == 0) && ((uintptr_t)X % 16 == 0);
@@ -391,8 +399,9 @@ struct Kern {
         break;
       }
       case 12:  // Rayleigh-Ritz k x k stage (rank 0)
+      case 13:  // reorthogonalisation (Cholesky QR) k x k stage (rank 0)
         if (c->rank == 0) {
-          rr_kxk_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
+          rr_kxk_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W, ph == 13 ? 1 : 0);
           n += 1;
         }
         break;
@@ -549,7 +558,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->n = n; c->k = k; c->kp = pad_kp(k);
   c->row_begin = row_begin; c->row_end = row_end; c->n_loc = row_end - row_begin;
   c->shift = shift;
-  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0};
+  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0};
   if (opts) c->opts = *opts;
   c->stream = (cudaStream_t)stream;
   RF_CK(c, cudaGetDevice(&c->device));
@@ -590,7 +599,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
                oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
-               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k);
+               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k), oGate = take(1);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
   c->pool_bytes = bytes;
@@ -609,6 +618,8 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.ag_send = b + oAgS; ws.ag_all = b + oAgA; ws.mg_all = c->multi ? b + oMgA : nullptr;
   ws.nrm_send = b + oNrS; ws.nrm_all = b + oNrA;
   ws.ritz = b + oRitz; ws.zerod = b + oZd; ws.top_zero = 0;   // (the pool is zeroed below)
+  ws.gate = reinterpret_cast<int*>(b + oGate);
+  ws.want_gram = c->opts.reorth_tol > 0.0 ? 1 : 0;
   c->run = reinterpret_cast<RunState*>(b + oRun);
   ws.tlog = nullptr;
   if (getenv("REFINE_KXK_TIMING")) RF_CK(c, cudaMalloc(&ws.tlog, 64 * sizeof(long long)));
@@ -710,7 +721,7 @@ static refine_status init_any(refine_ctx* c, int64_t n, int32_t k, int64_t row_b
     c->world = world;
     c->n = n; c->k = k; c->n_loc = n; c->row_begin = 0; c->row_end = n;
     c->stream = (cudaStream_t)stream;
-    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0};
+    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0};
     if (opts) c->opts = *opts;
     std::vector<int64_t> rb(world), re(world), lo(world), hi(world);
     std::vector<double> nrm(world);
@@ -950,22 +961,30 @@ static refine_status launch_sweep(refine_ctx* c, double* X) {
 
 // Rayleigh-Ritz preprocessing (Sec. 3.4): S1 -> pass B with D = 0 -> [gather]
 // -> rr_kxk (rank 0) -> [broadcast Csig = -S, scal = 0] -> pass C (Z_2 = X_2 S) -> norms -> X = Z.
-static refine_status enqueue_rr(refine_ctx* c, double* X) {
+static refine_status enqueue_rr(refine_ctx* c, double* X, int mode = 0, bool gated = false) {
+  // mode 0: Rayleigh-Ritz (S1, pass B with D = 0, rr_kxk, pass C, normalise);
+  // mode 1: reorthogonalisation by Cholesky QR (pass B for G only, rr_kxk mode 1, pass C, normalise).
+  // gated: refine_run's policy step -- every kernel runs behind ws.gate (no status reset).
   refine_ctx* one[1] = {c};
   refine_ctx** ranks = c->loopback ? c->kids.data() : one;
   const int nr = c->loopback ? (int)c->kids.size() : 1;
-  for (int i = 0; i < nr; ++i) RF_CK(c, cudaMemsetAsync(ranks[i]->ws.status, 0, sizeof(int), c->stream));
+  if (!gated)
+    for (int i = 0; i < nr; ++i) RF_CK(c, cudaMemsetAsync(ranks[i]->ws.status, 0, sizeof(int), c->stream));
   refine_status st;
-  if (c->multi && (st = collective(c, C_X, X)) != REFINE_OK) return st;
-  static const int phases[5] = {10, 11, 12, 4, 5};
-  static const int after[5] = {-1, C_MG, C_BC, C_NRM, -1};
-  for (int q = 0; q < 5; ++q) {
+  if (mode == 0 && c->multi && (st = collective(c, C_X, X)) != REFINE_OK) return st;
+  static const int ph_rr[5] = {10, 11, 12, 4, 5}, ph_ro[5] = {11, 13, 4, 5, -1};
+  static const int after[5] = {-1, C_MG, C_BC, C_NRM, -1}, after_ro[5] = {C_MG, C_BC, C_NRM, -1, -1};
+  const int* phases = mode == 0 ? ph_rr : ph_ro;
+  const int* aft = mode == 0 ? after : after_ro;
+  for (int q = 0; q < 5 && phases[q] >= 0; ++q) {
     for (int i = 0; i < nr; ++i) {
       refine_ctx* r = ranks[i];
       double* Xr = c->loopback ? X + r->row_begin * c->k : X;
+      r->gated = gated;
       dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, phases[q], Xr); });
+      r->gated = false;
     }
-    if (c->multi && after[q] >= 0 && (st = collective(c, after[q], X)) != REFINE_OK) return st;
+    if (c->multi && aft[q] >= 0 && (st = collective(c, aft[q], X)) != REFINE_OK) return st;
   }
   RF_CK(c, cudaGetLastError());
   return REFINE_OK;
@@ -998,6 +1017,7 @@ static refine_status read_stats(refine_ctx* c, refine_sweep_stats* stats, int* d
   if (stats) {
     stats->rel_resid = h[0]; stats->corr_norm = h[1]; stats->min_gap = h[2];
     stats->delta_hits = (int32_t)h[3]; stats->flipped = (int32_t)h[4];
+    stats->gram_dev = h[6];
   }
   *dev_status = st;
   return REFINE_OK;
@@ -1009,6 +1029,18 @@ extern "C" refine_status refine_rayleigh_ritz(refine_ctx* c, double* X, double* 
   refine_status st = enqueue_rr(c, X);
   if (st != REFINE_OK) return st;
   if (ritz) RF_CK(c, cudaMemcpyAsync(ritz, ctx0(c)->ws.ritz, sizeof(double) * c->k, cudaMemcpyDeviceToHost, c->stream));
+  int dev = 0;
+  RF_CK(c, cudaMemcpyAsync(&dev, ctx0(c)->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  RF_CK(c, cudaStreamSynchronize(c->stream));
+  return map_status(dev);
+}
+
+extern "C" refine_status refine_reorthogonalize(refine_ctx* c, double* X, double* gram_dev) {
+  if (!c || !X) return REFINE_E_INVALID;
+  if (c->sticky != REFINE_OK) return c->sticky;
+  refine_status st = enqueue_rr(c, X, 1);
+  if (st != REFINE_OK) return st;
+  if (gram_dev) RF_CK(c, cudaMemcpyAsync(gram_dev, ctx0(c)->ws.ritz, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   int dev = 0;
   RF_CK(c, cudaMemcpyAsync(&dev, ctx0(c)->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   RF_CK(c, cudaStreamSynchronize(c->stream));
@@ -1067,12 +1099,17 @@ extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, dou
     RF_CK(c, cudaMemsetAsync(r->run, 0, sizeof(RunState), c->stream));
     RF_CK(c, cudaMemsetAsync(r->ws.status, 0, sizeof(int), c->stream));
   }
+  // reorthogonalisation policy: single rank (the gated pipeline's collectives would
+  // run unconditionally at world > 1)
+  const bool reorth = c->opts.reorth_tol > 0.0 && !c->multi;
   for (int t = 0; t < iters; ++t) {
     refine_status st = enqueue_phases(c, X);
     if (st != REFINE_OK) return st;
     for (auto* r : ranks)      // every rank holds the same stats after the broadcast: same decision
       run_check_kernel<<<1, 1, 0, c->stream>>>(r->ws.status, r->run, r->ws.stats, tol, c->opts.guard_window,
-                                               c->opts.guard_factor);
+                                               c->opts.guard_factor, c->opts.resid_tol, c->opts.reorth_tol,
+                                               reorth ? r->ws.gate : nullptr);
+    if (reorth && (st = enqueue_rr(c, X, 1, true)) != REFINE_OK) return st;
     RF_CK(c, cudaGetLastError());
   }
   RunState rs;
@@ -1081,7 +1118,27 @@ extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, dou
   refine_sweep_stats st{};
   refine_status r = read_stats(c, &st, &ds);
   if (r != REFINE_OK) return r;
-  if (iters_done) *iters_done = rs.done;
+  int done = rs.done;
+  if (ds == ST_DIVERGED && rs.guard && c->opts.rr_fallback) {
+    // the correction grew rapidly -- switch to Rayleigh-Ritz preprocessing and
+    // continue with its iterations (RR + top-zero sweep) for the remaining budget
+    for (; done < iters; ) {
+      refine_status q = refine_sweep_rr(c, X, &st, nullptr);
+      ++done;
+      if (q != REFINE_OK) {
+        if (iters_done) *iters_done = done;
+        if (last) *last = st;
+        return q;
+      }
+      if (!std::isfinite(st.corr_norm)) { ds = ST_DIVERGED; break; }
+      if (st.corr_norm <= tol || (c->opts.resid_tol > 0.0 && st.rel_resid <= c->opts.resid_tol)) {
+        ds = ST_HALT_CONVERGED;
+        break;
+      }
+      ds = ST_OK;
+    }
+  }
+  if (iters_done) *iters_done = done;
   if (last) *last = st;
   if (ds == ST_HALT_CONVERGED) return REFINE_OK;
   if (ds == ST_OK) return REFINE_MAXITER;

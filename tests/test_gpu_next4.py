@@ -1,0 +1,104 @@
+"""GPU parity for SURVEY NEXT-4 (refine_run robustness policies) against the oracle through the
+C ABI: Cholesky-QR reorthogonalisation (refine_reorthogonalize), the Gram-deviation
+statistic, the residual stopping criterion, the reorthogonalisation policy and
+the divergence-triggered switch to Rayleigh-Ritz."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2602_23778_b200 as p
+    from paper_2602_23778_b200 import build
+    build.build()
+    p.lib()
+    assert torch.cuda.is_available()
+    return p
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_reorthogonalize_parity(pkg, kind):
+    if kind == "dense":
+        p = synth.small_dense(700, 12, m=8, noise=1e-3, seed=9)
+        R = pkg.Refiner.dense(p.A.cuda(), p.k)
+    else:
+        p = synth.small_laplacian((24, 22, 21), (1.0, 1.13, 1.29), 20, noise=1e-3)
+        R = pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k)
+    rng = np.random.default_rng(1)
+    X0 = p.X0.numpy() @ (np.eye(p.k) + 0.05 * rng.standard_normal((p.k, p.k)))
+    X = torch.from_numpy(X0).cuda()
+    s, gd = R.refine_reorthogonalize(X)
+    so, Zo, gdo = oracle.reorthogonalize(X0)
+    assert s == pkg.REFINE_OK and so == oracle.OK
+    assert abs(gd - gdo) <= 1e-12 * gdo
+    Z = X.cpu().numpy()
+    assert rel(Z, Zo) <= 1e-12
+    assert np.abs(Z.T @ Z - np.eye(p.k)).max() <= 1e-13
+
+
+def test_gram_dev_statistic(pkg):
+    p = synth.small_dense(400, 6, m=8, noise=1e-3, seed=4)
+    R = pkg.Refiner.dense(p.A.cuda(), p.k, reorth_tol=1.0)
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, st = R.refine_sweep(X, stats=True)
+    ref = oracle.sweep(oracle.Operator(A=p.A.numpy()), xin, want_gram=True)
+    assert abs(st.gram_dev - ref.stats.gram_dev) <= 1e-12 + 1e-10 * ref.stats.gram_dev
+    s, st = pkg.Refiner.dense(p.A.cuda(), p.k).refine_sweep(p.X0.cuda().clone(), stats=True)
+    assert st.gram_dev == -1.0
+
+
+def test_residual_stopping(pkg):
+    p = synth.small_dense(256, 4, m=8, noise=1e-5, seed=3)
+    op = oracle.Operator(A=p.A.numpy())
+    R = pkg.Refiner.dense(p.A.cuda(), p.k, resid_tol=1e-9)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 50, 0.0)
+    Xo, so, ito, ho = oracle.run_policy(op, p.X0.numpy(), 50, 0.0, resid_tol=1e-9)
+    assert s == pkg.REFINE_OK and so == oracle.OK and it == ito
+    assert st.rel_resid <= 1e-9
+    assert rel(X.cpu().numpy(), Xo) <= 1e-9
+
+
+def test_reorth_policy(pkg):
+    n, k = 300, 5
+    p = synth.small_dense(n, k, m=8, noise=1e-7, seed=7, fp32=False)
+    X0 = p.X0.numpy() @ (np.eye(k) + 3e-3 * np.random.default_rng(2).standard_normal((k, k)))
+    op = oracle.Operator(A=p.A.numpy())
+    R = pkg.Refiner.dense(p.A.cuda(), k, reorth_tol=1e-6)
+    X = torch.from_numpy(X0).cuda()
+    s, it, st = R.refine_run(X, 200, 1e-13)
+    Xo, so, ito, ho = oracle.run_policy(op, X0, 200, 1e-13, reorth_tol=1e-6)
+    assert s == pkg.REFINE_OK and so == oracle.OK and abs(it - ito) <= 1
+    Xg, Xt = X.cpu().numpy(), p.X.numpy()
+    sg = np.sign(np.sum(Xg * Xt, 0))
+    assert np.abs(Xg * sg - Xt).max() <= 100 * n * U
+    assert np.abs(Xg.T @ Xg - np.eye(k)).max() <= 1e-12
+
+
+def test_divergence_falls_back_to_rayleigh_ritz(pkg):
+    n, k = 256, 4
+    p = synth.small_dense(n, k, m=8, lam_target=np.array([10.0, 9.0, 9.0 + 9e-12, 8.0]), rest=1.0,
+                          noise=1e-4, seed=5)
+    R = pkg.Refiner.dense(p.A.cuda(), k)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 80, 1e-13)
+    assert s == pkg.REFINE_DIVERGED
+    R = pkg.Refiner.dense(p.A.cuda(), k, rr_fallback=True)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 80, 1e-13)
+    assert s == pkg.REFINE_OK and st.corr_norm <= 1e-13
+    Q, _ = np.linalg.qr(X.cpu().numpy())
+    Xt = p.X.numpy()
+    assert np.linalg.norm(Xt - Q @ (Q.T @ Xt)) <= 100 * n * U

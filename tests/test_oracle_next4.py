@@ -36,7 +36,7 @@ def test_reorthogonalize_rank_deficient():
 def test_sweep_reports_gram_deviation():
     p = synth.small_dense(256, 4, m=8, noise=1e-3, seed=12)
     X = p.X0.numpy()
-    res = oracle.sweep(oracle.Operator(A=p.A.numpy()), X)
+    res = oracle.sweep(oracle.Operator(A=p.A.numpy()), X, want_gram=True)
     assert abs(res.stats.gram_dev - np.abs(X.T @ X - np.eye(4)).max()) <= 1e-14
 
 
@@ -80,7 +80,7 @@ def test_reorthogonalisation_policy():
     op = oracle.Operator(A=p.A.numpy())
     X, s, it, hist = oracle.run_policy(op, X0, 200, 1e-13, reorth_tol=1e-6)
     assert s == oracle.OK
-    res = oracle.sweep(op, X)
+    res = oracle.sweep(op, X, want_gram=True)
     assert res.stats.gram_dev <= 1e-10
     Xt = p.X.numpy()
     sg = np.sign(np.sum(X * Xt, 0))
