@@ -1,0 +1,307 @@
+// tc_passes.cuh -- NEXT-2: the tall-skinny products of the sweep on the 5th-generation
+// tensor cores (tcgen05 / TMEM), in mixed precision ("some matrix-matrix
+// multiplications in the applications of H and H^T may be computed in lower precision while keeping
+// the accumulation and the small k x k computations in double").
+//
+// Precision scheme: every FP64 operand value v is rounded to f = fp32(v) and
+// split f = v_hi + v_lo with v_hi = bf16(f), v_lo = bf16(f - v_hi) (the remainder is exact in
+// FP32); a product a b is taken as
+// a_hi b_hi + a_hi b_lo + a_lo b_hi on tcgen05.mma kind::f16 (bf16 x bf16 products are exact in the
+// FP32 accumulator), which drops a_lo b_lo and the bf16 rounding of v_lo: relative error ~2^-16
+// per product.  The FP32 TMEM accumulator sums at most KC = 512 rows before it is drained into FP64
+// partials, and the partials are summed in FP64 (fixed order) -- so the k x k results carry a
+// relative error ~1e-5 of sum |a||b|, i.e. the correction E_L is computed to ~1e-5 relative while
+// the residual R = W - X D and every k x k step stay FP64: the refinement contracts at
+// max(gamma, ~1e-5) per sweep and still reaches FP64 accuracy (tests/test_gpu_mixed.py).
+//
+// UMMA operand layout: canonical K-major, no swizzle: element (row r, k) of a tile at byte
+// (r / 8) * SBO + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2, LBO = 128 B (core matrices along K),
+// SBO = (TK / 8) * 128 B (along M / N); descriptor version 1 (verified by tools/umma_test.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include "common.cuh"
+
+namespace rf {
+
+// ---------------------------------------------------------------- tcgen05 helpers
+RF_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;              // descriptor version 1 (sm_100); base offset 0; SWIZZLE_NONE
+  return d;
+}
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int m, int n) {   // BF16 x BF16 -> F32, K-major
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+RF_DEV void umma_bf16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+RF_DEV void umma_commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+RF_DEV void mbar_init(uint64_t* mbar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count));
+}
+RF_DEV void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(mbar)), "r"(parity)
+        : "memory");
+}
+RF_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+RF_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+RF_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// 16 consecutive FP32 accumulator columns of this warp's 32 TMEM lanes
+RF_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+RF_DEV void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+// Two values v0, v1 (consecutive K) -> packed bf16x2 hi and lo words: v ~ f = fp32(v) (relative
+// 2^-24), hi = bf16(f), lo = bf16(f - hi) (f - hi exact in FP32); lower half = v0.  One F2F per
+// value; the bf16 rounding is the paired cvt.rn.bf16x2.f32.
+RF_DEV void split2_bf16(double v0, double v1, uint32_t& hi, uint32_t& lo) {
+  const float f0 = (float)v0, f1 = (float)v1;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(f1), "f"(f0));
+  const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xFFFF0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(f1 - h1), "f"(f0 - h0));
+}
+RF_DEV constexpr uint32_t kmaj_off(int r, int k, uint32_t sbo) {
+  return (uint32_t)(r / 8) * sbo + (uint32_t)(k / 8) * 128u + (uint32_t)(r % 8) * 16u + (uint32_t)(k % 8) * 2u;
+}
+
+// ---------------------------------------------------------------- pass B on tcgen05 (k = 128)
+// [M2 | G2] = X_2^T [R_2 | X_2] over rows >= top (R = W - X D formed in FP64, rr_j = sum r_ij^2 in
+// FP64), per CTA a contiguous row chunk; the CTA's FP64 partial goes to the passB2 slot layout
+// (bpart[(c * 4 + tile) * 128 * 64 + a * 64 + b % 64], brr[c * 128 + j]) so passB2_reduce_kernel<128>
+// sums the CTAs in fixed order.  One CTA per SM, warp-specialised:
+//   warp 8 (producer): bulk-copies the X and W rows of each 16-row stage (contiguous 16 KB each,
+//     cp.async.bulk completing on the slot's "full" mbarrier) into an NS-slot FP64 ring as soon as
+//     the converters release a slot ("empty" mbarrier): up to (NS - 1) x 32 KB in flight per SM;
+//   warps 0-7 (converters): form R = W - X D and the bf16 hi/lo splits of X and R into the UMMA
+//     operand buffer of the stage; thread 0 issues tcgen05.mma (M = 128, N = 256, K = 16) for
+//     hi*hi, hi*lo, lo*hi into the TMEM accumulator and commits to the buffer's mbarrier;
+//   warps 9-12 (drain): every KC rows the tensor-core accumulator (TMEM columns 0-255) is added
+//     into a second FP32 sum (TMEM columns 256-511) with round-to-nearest CUDA-core adds (error
+//     control, header) and released for the next block; at the end the second sum is written to
+//     the CTA's FP64 partial.
+constexpr int TCB_K = 128, TCB_N = 256, TCB_TK = 16, TCB_NS = 5, TCB_NO = 2, TCB_CONV = 256;
+constexpr int TCB_THREADS = TCB_CONV + 32 + 128;
+#ifndef TCB_KC_OVERRIDE
+constexpr int TCB_KC = 512;
+#else
+constexpr int TCB_KC = TCB_KC_OVERRIDE;
+#endif
+constexpr int TCB_SPB = TCB_KC / TCB_TK;                           // stages per accumulator block
+constexpr uint32_t TCB_SBO = (TCB_TK / 8) * 128;                   // 256 B
+constexpr uint32_t TCB_A_BYTES = TCB_K * TCB_TK * 2, TCB_B_BYTES = TCB_N * TCB_TK * 2;
+constexpr uint32_t TCB_OPS = 2 * TCB_A_BYTES + 2 * TCB_B_BYTES;    // A_hi, A_lo, B_hi, B_lo: 24 KB
+constexpr uint32_t TCB_ROWB = TCB_TK * TCB_K * 8;                  // 16 KB of X (or W) rows per stage
+constexpr int TCB_SMEM = TCB_NS * 2 * TCB_ROWB + TCB_NO * TCB_OPS;  // 208 KB
+
+RF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+RF_DEV void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+RF_DEV void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
+RF_DEV void conv_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(TCB_CONV) : "memory"); }
+
+__global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const double* __restrict__ X) {
+  extern __shared__ __align__(16) unsigned char tcb_smem[];
+  __shared__ __align__(8) uint64_t full[TCB_NS], empty[TCB_NS], mmad[TCB_NO], accf[2], acce[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ double sd[TCB_K];
+  if (*ws.status != ST_OK) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + TCB_TK - 1) / TCB_TK * TCB_TK;
+  const int64_t rb = ws.top + (int64_t)blockIdx.x * per;
+  const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
+  const int nst = (re > rb) ? (int)((re - rb + TCB_TK - 1) / TCB_TK) : 0;
+  const int nblk = (nst + TCB_SPB - 1) / TCB_SPB;
+  unsigned char* F = tcb_smem;                              // [NS][X rows | W rows] FP64
+  unsigned char* OP = tcb_smem + TCB_NS * 2 * TCB_ROWB;     // [NO][A_hi | A_lo | B_hi | B_lo] bf16
+  double* part = ws.bpart + (int64_t)blockIdx.x * 4 * TCB_K * 64;
+  for (int j = tid; j < TCB_K; j += TCB_THREADS) sd[j] = ws.d[j];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(2 * TCB_N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < TCB_NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], TCB_CONV / 32);
+    }
+    for (int i = 0; i < TCB_NO; ++i) mbar_init(&mmad[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 4);
+    }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  double rr = 0.0;
+  if (warp == TCB_CONV / 32) {                     // ---- producer
+    if (lane == 0) {
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % TCB_NS;
+        if (t >= TCB_NS) mbar_wait(&empty[s], ((t / TCB_NS) - 1) & 1);
+        const int64_t r0 = rb + (int64_t)t * TCB_TK;
+        const uint32_t bytes = (uint32_t)min((int64_t)TCB_TK, re - r0) * TCB_K * 8;
+        unsigned char* f = F + s * 2 * TCB_ROWB;
+        mbar_expect_tx(&full[s], 2 * bytes);
+        bulk_g2s(f, X + r0 * TCB_K, bytes, &full[s]);
+        bulk_g2s(f + TCB_ROWB, ws.W + r0 * TCB_K, bytes, &full[s]);
+      }
+    }
+  } else if (warp > TCB_CONV / 32) {               // ---- drain: TMEM lanes 32 (warp % 4) ..
+    const int m = 32 * (warp & 3) + lane;
+    const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&accf[0], j & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < TCB_N; c0 += 16) {
+        float v[16], u[16];
+        tmem_ld16(tl + c0, v);
+        if (j > 0) {
+          tmem_ld16(tl + TCB_N + c0, u);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] += u[e];
+        }
+        tmem_st16(tl + TCB_N + c0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[0]);
+    }
+    if (nst == 0) {   // empty chunk: zero partial
+      for (int e = tid - (TCB_CONV + 32); e < 4 * TCB_K * 64; e += 128) part[e] = 0.0;
+    } else {
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < TCB_N; c0 += 16) {
+        float v[16];
+        tmem_ld16(tl + TCB_N + c0, v);
+        double* p = part + ((c0 >> 6) * TCB_K + m) * 64 + (c0 & 63);
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(v[e], v[e + 1]);
+      }
+    }
+  } else {                                          // ---- converters + MMA issue
+    const uint32_t idesc = umma_idesc_bf16(TCB_K, TCB_N);
+    // thread -> column col and row quads q0, q0 + 2, ...: per warp instruction the FP64 reads are
+    // two 128 B row segments and the 8 B operand stores two 128 B core-matrix rows (no conflicts)
+    const int col = 16 * warp + (lane & 15), q0 = lane >> 4;
+    const double dcol = sd[col];
+    for (int t = 0; t < nst; ++t) {
+      const int s = t % TCB_NS, o = t % TCB_NO;
+      mbar_wait(&full[s], (t / TCB_NS) & 1);                             // rows landed
+      if (t >= TCB_NO) mbar_wait(&mmad[o], ((t / TCB_NO) - 1) & 1);     // OP[o] free
+      const int nr = (int)min((int64_t)TCB_TK, re - (rb + (int64_t)t * TCB_TK));
+      const double* fx = reinterpret_cast<const double*>(F + s * 2 * TCB_ROWB);
+      const double* fw = fx + TCB_TK * TCB_K;
+      unsigned char* st = OP + o * TCB_OPS;
+      unsigned char *Ahi = st, *Alo = st + TCB_A_BYTES, *Bhi = st + 2 * TCB_A_BYTES,
+                    *Blo = st + 2 * TCB_A_BYTES + TCB_B_BYTES;
+#pragma unroll
+      for (int q = q0; q < TCB_TK / 4; q += 2) {
+        const int r = 4 * q;
+        double x[4], qv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool v = r + j < nr;
+          x[j] = v ? fx[(r + j) * TCB_K + col] : 0.0;
+          const double w = v ? fw[(r + j) * TCB_K + col] : 0.0;
+          qv[j] = __fma_rn(-x[j], dcol, w);             // R = W - X D (FP64)
+          rr = __fma_rn(qv[j], qv[j], rr);
+        }
+        uint2 xh, xl, rh, rl;
+        split2_bf16(x[0], x[1], xh.x, xl.x);
+        split2_bf16(x[2], x[3], xh.y, xl.y);
+        split2_bf16(qv[0], qv[1], rh.x, rl.x);
+        split2_bf16(qv[2], qv[3], rh.y, rl.y);
+        const uint32_t oa = kmaj_off(col, r, TCB_SBO);             // A = X^T: (m = col, k = row); B rows 0.. = R
+        const uint32_t ob = kmaj_off(TCB_K + col, r, TCB_SBO);     // B rows 128.. = X
+        *reinterpret_cast<uint2*>(Ahi + oa) = xh;
+        *reinterpret_cast<uint2*>(Alo + oa) = xl;
+        *reinterpret_cast<uint2*>(Bhi + oa) = rh;
+        *reinterpret_cast<uint2*>(Blo + oa) = rl;
+        *reinterpret_cast<uint2*>(Bhi + ob) = xh;
+        *reinterpret_cast<uint2*>(Blo + ob) = xl;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);        // this warp is done reading F[s]
+      fence_async_smem();
+      tc_fence_before();
+      conv_sync();
+      if (tid == 0) {
+        const int j = t / TCB_SPB, ts = t % TCB_SPB;   // accumulator block j, stage ts within it
+        if (ts == 0 && j >= 1) mbar_wait(&acce[0], (j - 1) & 1);   // block j - 1 drained
+        tc_fence_after();
+        const uint32_t td = tmem;
+        const uint32_t acc = ts > 0;
+        const uint64_t a_hi = umma_desc(smem_u32(Ahi), 128, TCB_SBO), a_lo = umma_desc(smem_u32(Alo), 128, TCB_SBO);
+        const uint64_t b_hi = umma_desc(smem_u32(Bhi), 128, TCB_SBO), b_lo = umma_desc(smem_u32(Blo), 128, TCB_SBO);
+#ifndef TCB_EXP_NOMMA
+        umma_bf16(td, a_hi, b_hi, idesc, acc);
+        umma_bf16(td, a_hi, b_lo, idesc, 1);
+        umma_bf16(td, a_lo, b_hi, idesc, 1);
+#endif
+        umma_commit(&mmad[o]);
+        if (ts == TCB_SPB - 1 || t == nst - 1) umma_commit(&accf[0]);
+      }
+    }
+  }
+  __syncthreads();
+  double* srr = reinterpret_cast<double*>(tcb_smem);     // the FP64 ring is free now
+  if (tid < TCB_CONV) srr[tid] = rr;                     // column 16 w + (l & 15) from lanes l, l + 16
+  __syncthreads();
+  if (tid < TCB_K) {
+    const int t0 = 32 * (tid >> 4) + (tid & 15);
+    ws.brr[(int64_t)blockIdx.x * TCB_K + tid] = srr[t0] + srr[t0 + 16];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * TCB_N));
+}
+
+}  // namespace rf
