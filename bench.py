@@ -146,7 +146,7 @@ def partition(n, world, rank):
     return rb, n - blk * (world - rank - 1)
 
 
-def make_refiner(p, world, rank):
+def make_refiner(p, world, rank, **opts):
     """Refiner for this rank: world == 1 -> whole problem; world > 1 -> row partition over NCCL
     (ncclUniqueId from rank 0, broadcast over torch.distributed).  Returns (Refiner, X_local)."""
     import torch
@@ -154,13 +154,14 @@ def make_refiner(p, world, rank):
     stream = torch.cuda.current_stream()
     if world == 1:
         if p.kind == "dense":
-            return pkg.Refiner.dense(p.A, p.k, shift=p.shift, stream=stream), p.X0.clone()
-        return pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, shift=p.shift, stream=stream), p.X0.clone()
+            return pkg.Refiner.dense(p.A, p.k, shift=p.shift, stream=stream, **opts), p.X0.clone()
+        return (pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, shift=p.shift, stream=stream, **opts),
+                p.X0.clone())
     import torch.distributed as dist
     obj = [pkg.refine_nccl_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     rb, re = partition(p.n, world, rank)
-    kw = dict(shift=p.shift, stream=stream, row_begin=rb, row_end=re, rank=rank, world=world, nccl_id=obj[0])
+    kw = dict(shift=p.shift, stream=stream, row_begin=rb, row_end=re, rank=rank, world=world, nccl_id=obj[0], **opts)
     if p.kind == "dense":
         R = pkg.Refiner.dense(p.A[rb:re], p.k, n=p.n, **kw)
     else:
@@ -168,7 +169,7 @@ def make_refiner(p, world, rank):
     return R, p.X0[rb:re].clone()
 
 
-def time_ours(p, steps, warmup, world, local, profile=True, rank=0):
+def time_ours(p, steps, warmup, world, local, profile=True, rank=0, opts=None):
     """Device-timed sweeps: CUDA events on the library's stream, barrier + sync on both sides.
 
     The timed value replays the sweep as a CUDA graph (refine_set_graph) with no instrumentation;
@@ -176,7 +177,7 @@ def time_ours(p, steps, warmup, world, local, profile=True, rank=0):
     (refine_profile_begin/end) for the kernel breakdown and the roofline of the dominant kernel."""
     import torch
     stream = torch.cuda.current_stream()
-    R, X = make_refiner(p, world, rank)
+    R, X = make_refiner(p, world, rank, **(opts or {}))
 
     def timed(n):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -222,6 +223,21 @@ def time_rr(R, X, reps=3):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps, s
+
+
+def time_mixed(q, local, steps=5):
+    """NEXT-2 (opts.mixed, k = 128 only): the same sweep with passes B and C on tcgen05 in the
+    bf16x3 scheme; device-timed like the FP64 sweep (graph replay)."""
+    import torch
+    if q.k != 128:
+        return None
+    ms, kern, R, X, st, s, prof = time_ours(q, steps, 3, 1, local, opts={"mixed": True})
+    out = {"sweeps_s": 1000.0 / ms, "ms_per_sweep": ms, "ms_per_sweep_instrumented": prof, "kernels_ms": kern,
+           "status": s, "what": "refine_opts.mixed: X_2^T [R_2|X_2] and X_2 Csig on tcgen05 (bf16x3 split, FP32 "
+           "TMEM accumulators drained to FP64 every 512 rows); R, w scaling, k x k and reductions FP64"}
+    del R, X
+    torch.cuda.empty_cache()
+    return out
 
 
 def time_e2e(R, p, steps, warmup, world=1, rank=0):
@@ -382,6 +398,9 @@ def main():
             "roofline": roofline_for(p, kern, ms_prof or ms_max, fp64, hbm, n_loc=partition(p.n, world, rank)[1] - partition(p.n, world, rank)[0]),
             "gpu_launches": R.kernels_per_sweep() * args.steps}
     if world == 1:
+        mx = time_mixed(p, local, max(3, args.steps // 2)) if p.k == 128 else None
+        if mx:
+            line["mixed_next2"] = mx
         rr_ms, rr_s = time_rr(R, X)
         line["rayleigh_ritz"] = {"ms": rr_ms, "status": rr_s, "what": "refine_rayleigh_ritz (NEXT-1, Sec. 3.4): "
                                  "S1 + pass B (D = 0) + k x k Cholesky/Jacobi + pass C + normalise"}
@@ -406,7 +425,11 @@ def main():
                          "rayleigh_ritz_ms": qrr,
                          "kernels_ms": qk, "roofline": roofline_for(q, qk, qprof or qms, fp64, hbm),
                          "frac_of_sweep_roofline": max(qf / (fp64 * 1e12), qb / (hbm * 1e9)) / (qms * 1e-3)}
-            del QR, QX, q
+            del QR, QX
+            torch.cuda.empty_cache()
+            if q.k == 128:
+                per[name]["mixed_next2"] = time_mixed(q, local)
+            del q
             torch.cuda.empty_cache()
         line["per_config"] = per
     if rank == 0 and world == 1 and not args.no_extra and not args.no_cpu:

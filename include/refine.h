@@ -98,6 +98,17 @@ typedef struct {
                             gram_dev > reorth_tol.  world == 1.  Default 0 = off            */
   int32_t rr_fallback;   /* 1: when refine_run's divergence guard trips, continue with refine_sweep_rr
                             iterations instead of returning REFINE_DIVERGED        */
+  int32_t mixed;         /* NEXT-2 ("matrix-matrix multiplications in the applications
+                            of H and H^T may be computed in lower precision while keeping the
+                            accumulation and the small k x k computations in double"): 1 = the sweep's
+                            tall-skinny products X_2^T [R_2 | X_2] (pass B) and X_2 Csig (pass C) on the
+                            bf16 tensor cores (tcgen05) with every FP64 operand split into two bf16
+                            terms (three products, relative error ~1e-5 of an O(residual) quantity);
+                            R = W - X D, the w scaling, every k x k step and all reductions stay FP64.
+                            The sweep still converges to FP64 accuracy, at a per-sweep rate
+                            max(gamma, ~1e-5 kappa).  Requires k == 128 (else REFINE_E_UNSUPPORTED)
+                            and a 16-byte aligned X (else the FP64 passes run).  Rayleigh-Ritz and
+                            reorthogonalisation steps always run in FP64 (their products are O(1)). */
 } refine_opts;
 
 /* Per-sweep diagnostics (host struct), for the sweep's input X^ (after the sign flip). */

@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(256) normalize_kernel(Ws ws, double* __restric
   }
   const double* invn = ws.multi ? sinv : ws.invn;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
-  if ((k & 1) == 0 && (256 % (k / 2)) == 0) {
+  if ((k & 1) == 0 && (256 % (k / 2)) == 0 && ((uintptr_t)X & 15) == 0) {   // (X may be only 8-byte aligned)
     const int64_t total2 = ws.n_loc * (k / 2);
     const int j = (int)(tid % (k / 2)) * 2;
     const double s0 = invn[j], s1 = invn[j + 1];

@@ -32,6 +32,7 @@
 #include "kxk.cuh"
 #include "passes.cuh"
 #include "spmm_csr.cuh"
+#include "tc_passes.cuh"
 #include "nccl_dl.h"
 
 using namespace rf;
@@ -145,6 +146,7 @@ struct refine_ctx {
   // kernel) and the precomputed gather offsets (owned; indexed by absolute CSR position)
   int gather_R = 0, gather_un = 8;
   bool gated = false;   // phase(): launch with ws.status -> ws.gate (refine_run reorthogonalisation)
+  bool in_rr = false;   // phase(): a Rayleigh-Ritz / Cholesky-QR step (O(1) products: always FP64)
   int32_t* xoff_buf = nullptr;
   const int32_t* xoff = nullptr;
   double shift = 0.0;
@@ -288,6 +290,10 @@ struct Kern {
     if ((e = cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passC, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
+    if (KP == 128 && c->opts.mixed) {   // NEXT-2 tcgen05 passes (tc_passes.cuh)
+      if ((e = cudaFuncSetAttribute(passB_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCB_SMEM))) return e;
+      if ((e = cudaFuncSetAttribute(passC_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCC_SMEM))) return e;
+    }
     int occ = 1;
     // dense GEMM: split-K so the grid fills whole waves of resident CTAs
     if (!c->csr) {
@@ -331,9 +337,17 @@ struct Kern {
   }
 
   static void sizes(refine_ctx* c, size_t& bpart, size_t& brr, size_t& nslot) {
-    bpart = (size_t)c->passb_grid_y * B_NT * B_TILE;
-    brr = (size_t)c->passb_grid_y * KP;
-    nslot = (size_t)c->passc_grid * KP;
+    // the tcgen05 passes (opts.mixed) write one partial per SM in the same slot layouts
+    const size_t cb = (KP == 128 && c->opts.mixed) ? std::max(c->passb_grid_y, c->sms) : c->passb_grid_y;
+    const size_t cc = (KP == 128 && c->opts.mixed) ? std::max(c->passc_grid, c->sms) : c->passc_grid;
+    bpart = cb * B_NT * B_TILE;
+    brr = cb * KP;
+    nslot = cc * KP;
+  }
+  // NEXT-2: this sweep's passes B and C on tcgen05 (k == 128, not a Rayleigh-Ritz / QR step,
+  // 16-byte aligned X for the bulk copies)
+  static bool use_tc(const refine_ctx* c, const double* X) {
+    return KP == 128 && c->opts.mixed && c->k == 128 && !c->in_rr && ((uintptr_t)X % 16 == 0);
   }
 
   // phase ph of one sweep on this rank (see the file header); returns kernels launched
@@ -412,6 +426,13 @@ struct Kern {
         break;
       case 2:  // S4 reductions
         c->mark();
+        if (use_tc(c, X)) {   // NEXT-2: X_2^T [R_2 | X_2] on tcgen05, one FP64 partial per SM
+          passB_tc_kernel<<<c->sms, TCB_THREADS, TCB_SMEM, s>>>(ws, X);
+          c->mark();
+          passB2_reduce_kernel<128><<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(ws, c->sms);
+          n += 2;
+          break;
+        }
         if (B2 && B2C::PAIRED)
           passB<<<dim3(7 * (c->passb_grid_y / 2)), B_THREADS, B_SMEM, s>>>(ws, X, xv16);
         else
@@ -430,6 +451,15 @@ struct Kern {
         break;
       case 4:  // S6
         c->mark();
+        if (use_tc(c, X)) {   // NEXT-2: X_2 Csig on tcgen05, norm partials one per SM
+          Ws wm = ws;
+          wm.n_nslot = c->sms;
+          passC_tc_kernel<<<c->sms, TCC_THREADS, TCC_SMEM, s>>>(wm, X);
+          c->mark();
+          norm_reduce_kernel<<<1, KXK_THREADS, 0, s>>>(wm);
+          n += 2;
+          break;
+        }
         passC<<<dim3(c->passc_grid, KP / CNC), CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
         c->mark();
         norm_reduce_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
@@ -558,7 +588,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->n = n; c->k = k; c->kp = pad_kp(k);
   c->row_begin = row_begin; c->row_end = row_end; c->n_loc = row_end - row_begin;
   c->shift = shift;
-  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0};
+  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0, 0};
   if (opts) c->opts = *opts;
   c->stream = (cudaStream_t)stream;
   RF_CK(c, cudaGetDevice(&c->device));
@@ -570,6 +600,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.beta_zero = c->opts.beta_zero;
   ws.kjudge = c->opts.kjudge;
   if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
+  if (c->opts.mixed && k != 128) return REFINE_E_UNSUPPORTED;                    // tcgen05 passes: k = 128
   ws.world = world; ws.rank = rank;
   ws.multi = c->multi ? 1 : 0;
   ws.row0 = row_begin; ws.row1 = row_end;
@@ -721,7 +752,7 @@ static refine_status init_any(refine_ctx* c, int64_t n, int32_t k, int64_t row_b
     c->world = world;
     c->n = n; c->k = k; c->n_loc = n; c->row_begin = 0; c->row_end = n;
     c->stream = (cudaStream_t)stream;
-    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0};
+    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0, 0};
     if (opts) c->opts = *opts;
     std::vector<int64_t> rb(world), re(world), lo(world), hi(world);
     std::vector<double> nrm(world);
@@ -981,8 +1012,10 @@ static refine_status enqueue_rr(refine_ctx* c, double* X, int mode = 0, bool gat
       refine_ctx* r = ranks[i];
       double* Xr = c->loopback ? X + r->row_begin * c->k : X;
       r->gated = gated;
+      r->in_rr = true;
       dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, phases[q], Xr); });
       r->gated = false;
+      r->in_rr = false;
     }
     if (c->multi && aft[q] >= 0 && (st = collective(c, aft[q], X)) != REFINE_OK) return st;
   }

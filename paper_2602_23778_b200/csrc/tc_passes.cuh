@@ -72,6 +72,15 @@ RF_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
+RF_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+}
 RF_DEV void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
@@ -113,11 +122,7 @@ RF_DEV constexpr uint32_t kmaj_off(int r, int k, uint32_t sbo) {
 //     the CTA's FP64 partial.
 constexpr int TCB_K = 128, TCB_N = 256, TCB_TK = 16, TCB_NS = 5, TCB_NO = 2, TCB_CONV = 256;
 constexpr int TCB_THREADS = TCB_CONV + 32 + 128;
-#ifndef TCB_KC_OVERRIDE
-constexpr int TCB_KC = 512;
-#else
-constexpr int TCB_KC = TCB_KC_OVERRIDE;
-#endif
+constexpr int TCB_KC = 512;   // rows per TMEM block (tools/tcb_test.cu: 2048 -> 512 cuts the G error 2.6x, +1.6% time)
 constexpr int TCB_SPB = TCB_KC / TCB_TK;                           // stages per accumulator block
 constexpr uint32_t TCB_SBO = (TCB_TK / 8) * 128;                   // 256 B
 constexpr uint32_t TCB_A_BYTES = TCB_K * TCB_TK * 2, TCB_B_BYTES = TCB_N * TCB_TK * 2;
@@ -280,11 +285,9 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
         const uint32_t acc = ts > 0;
         const uint64_t a_hi = umma_desc(smem_u32(Ahi), 128, TCB_SBO), a_lo = umma_desc(smem_u32(Alo), 128, TCB_SBO);
         const uint64_t b_hi = umma_desc(smem_u32(Bhi), 128, TCB_SBO), b_lo = umma_desc(smem_u32(Blo), 128, TCB_SBO);
-#ifndef TCB_EXP_NOMMA
         umma_bf16(td, a_hi, b_hi, idesc, acc);
         umma_bf16(td, a_hi, b_lo, idesc, 1);
         umma_bf16(td, a_lo, b_hi, idesc, 1);
-#endif
         umma_commit(&mmad[o]);
         if (ts == TCB_SPB - 1 || t == nst - 1) umma_commit(&accf[0]);
       }
@@ -302,6 +305,204 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * TCB_N));
+}
+
+// ---------------------------------------------------------------- pass C on tcgen05 (k = 128)
+// x~_i = w_i (Sigma D^-1) - x_i Csig for rows i >= top (eq. update-X through the implicit H, see
+// passC_kernel), with the product x_i Csig -- an O(residual) term, PAPER.md:504-507 -- on tcgen05
+// in the bf16x3 scheme and the w_i scaling, the subtraction and the column sums of squares in FP64.
+// Transposed product per 64-row slot: D (128 x 64, TMEM lanes = output columns j, TMEM columns =
+// the slot's rows) = Csig^T (A, 128 x 128, split once per CTA, resident) . X_slot^T (B, N = 64).
+// The M = 128 MMAs are bound by the SMEM read of A (tools/umma_sw_test.cu: ~48 cycles per MMA at
+// N <= 64), so N = 64 rows per MMA.  Operands use the 128-byte-swizzled K-major layout, which
+// also makes the converters' row-contiguous 4-byte stores conflict-free.
+// One CTA per SM, a contiguous row chunk per CTA, warp-specialised:
+//   warp 12 (producer): one bulk copy per 64-row X slot (contiguous) into a 2-slot FP64 ring;
+//   warps 0-3 (converters): bf16 hi/lo splits of the X slot into the UMMA B buffer; thread 0
+//     issues 3 x 8 tcgen05.mma (M = 128, N = 64, K = 16) into the slot's TMEM columns;
+//   warps 4-11 (epilogue, TMEM lane quarter = warp % 4, 32 rows each): the W entries are loaded
+//     (coalesced) before waiting for the MMA; tcgen05.ld of the rows of column j,
+//     x~ = fma(w, s_j, -D), coalesced stores of X~, FP64 column sums of squares.
+constexpr int TCC_K = 128, TCC_TN = 64, TCC_NS = 2, TCC_NT = 4;
+constexpr int TCC_CONV = 128, TCC_EPI = 256, TCC_THREADS = TCC_CONV + TCC_EPI + 32;
+constexpr int TCC_RPW = TCC_TN / (TCC_EPI / 128);            // slot rows per epilogue warp
+constexpr uint32_t TCC_SLOT = TCC_TN * TCC_K * 8;              // 64 KB of X rows
+constexpr uint32_t TCC_A_BYTES = TCC_K * TCC_K * 2, TCC_B_BYTES = TCC_TN * TCC_K * 2;
+constexpr int TCC_SMEM = 1024 + 2 * TCC_A_BYTES + 2 * TCC_B_BYTES + TCC_NS * TCC_SLOT;   // 225 KB
+
+// 128-byte swizzle, K-major: element (r, k) of an R-row bf16 operand (64-wide K atoms, 8-row groups
+// 1024 B apart, the 16-byte chunk index XOR row % 8); atoms 1024-byte aligned
+RF_DEV constexpr uint32_t sw128_off(int r, int k, int R) {
+  return (uint32_t)(k / 64) * (R * 128) + (uint32_t)(r / 8) * 1024 + (uint32_t)(r % 8) * 128 +
+         (uint32_t)((((k % 64) / 8) ^ (r % 8)) * 16) + (uint32_t)(k % 8) * 2;
+}
+RF_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8-row groups 1024 B apart
+  d |= (uint64_t)1 << 46;                  // descriptor version 1
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+// K step kk (16 elements) of an R-row swizzled operand at base: the start moves 32 B inside the atom
+RF_DEV uint64_t sw128_kdesc(uint32_t base, int kk, int R) {
+  return umma_desc_sw128(base + (uint32_t)(kk / 4) * (R * 128) + (uint32_t)(kk % 4) * 32);
+}
+RF_DEV void conv_sync_c() { asm volatile("bar.sync 1, %0;\n" ::"n"(TCC_CONV) : "memory"); }
+
+__global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const double* __restrict__ X) {
+  extern __shared__ __align__(16) unsigned char tcc_raw[];
+  __shared__ __align__(8) uint64_t full[TCC_NS], empty[TCC_NS], opfree, accf[TCC_NT], acce[TCC_NT];
+  __shared__ uint32_t tmem_base;
+  __shared__ double ssc[TCC_K];
+  if (*ws.status != ST_OK) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + TCC_TN - 1) / TCC_TN * TCC_TN;
+  const int64_t rb = ws.top + (int64_t)blockIdx.x * per;
+  const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
+  const int nst = (re > rb) ? (int)((re - rb + TCC_TN - 1) / TCC_TN) : 0;
+  unsigned char* base = tcc_raw + ((1024 - (smem_u32(tcc_raw) & 1023)) & 1023);   // 1024-B aligned
+  unsigned char* Ahi = base;
+  unsigned char* Alo = base + TCC_A_BYTES;
+  unsigned char* Bhi = base + 2 * TCC_A_BYTES;
+  unsigned char* Blo = Bhi + TCC_B_BYTES;
+  unsigned char* F = Blo + TCC_B_BYTES;                              // [NS][64 X rows] FP64
+  // A = Csig^T: element (m = j, k = l) = Csig[l][j], split once
+  for (int e = tid; e < TCC_K * TCC_K / 2; e += TCC_THREADS) {
+    const int j = e % TCC_K, l = 2 * (e / TCC_K);
+    uint32_t hi, lo;
+    split2_bf16(ws.Csig[l * TCC_K + j], ws.Csig[(l + 1) * TCC_K + j], hi, lo);
+    const uint32_t off = sw128_off(j, l, TCC_K);
+    *reinterpret_cast<uint32_t*>(Ahi + off) = hi;
+    *reinterpret_cast<uint32_t*>(Alo + off) = lo;
+  }
+  for (int j = tid; j < TCC_K; j += TCC_THREADS) ssc[j] = ws.scal[j];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(TCC_NT * TCC_TN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < TCC_NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], TCC_CONV / 32);
+    }
+    mbar_init(&opfree, 1);
+    for (int i = 0; i < TCC_NT; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], TCC_EPI / 32);
+    }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  double nacc = 0.0;
+  if (warp == (TCC_CONV + TCC_EPI) / 32) {          // ---- producer
+    if (lane == 0) {
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % TCC_NS;
+        if (t >= TCC_NS) mbar_wait(&empty[s], ((t / TCC_NS) - 1) & 1);
+        const int64_t r0 = rb + (int64_t)t * TCC_TN;
+        const uint32_t bytes = (uint32_t)min((int64_t)TCC_TN, re - r0) * TCC_K * 8;
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s(F + s * TCC_SLOT, X + r0 * TCC_K, bytes, &full[s]);
+      }
+    }
+  } else if (warp < TCC_CONV / 32) {                // ---- converters + MMA issue
+    const uint32_t idesc = umma_idesc_bf16(TCC_K, TCC_TN);
+    for (int t = 0; t < nst; ++t) {
+      const int s = t % TCC_NS;
+      mbar_wait(&full[s], (t / TCC_NS) & 1);
+      if (t >= 1) mbar_wait(&opfree, (t - 1) & 1);   // the previous slot's MMAs have read B
+      const int nr = (int)min((int64_t)TCC_TN, re - (rb + (int64_t)t * TCC_TN));
+      const double* fx = reinterpret_cast<const double*>(F + s * TCC_SLOT);
+      // warp w: rows w, w + 4, ...; lane: columns 2 lane, 2 lane + 1 and 64 + 2 lane, 65 + 2 lane
+#pragma unroll 4
+      for (int r = warp; r < TCC_TN; r += TCC_CONV / 32) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int l = 64 * h + 2 * lane;
+          double2 v = make_double2(0.0, 0.0);
+          if (r < nr) v = *reinterpret_cast<const double2*>(fx + r * TCC_K + l);
+          uint32_t hi, lo;
+          split2_bf16(v.x, v.y, hi, lo);
+          const uint32_t off = sw128_off(r, l, TCC_TN);
+          *reinterpret_cast<uint32_t*>(Bhi + off) = hi;
+          *reinterpret_cast<uint32_t*>(Blo + off) = lo;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);        // X rows of the slot consumed
+      fence_async_smem();
+      tc_fence_before();
+      conv_sync_c();
+      if (tid == 0) {
+        const int a = t % TCC_NT;
+        if (t >= TCC_NT) mbar_wait(&acce[a], ((t / TCC_NT) - 1) & 1);   // TMEM columns read out
+        tc_fence_after();
+        const uint32_t td = tmem + (uint32_t)(a * TCC_TN);
+        const uint32_t ah = smem_u32(Ahi), al = smem_u32(Alo), bh = smem_u32(Bhi), bl = smem_u32(Blo);
+#pragma unroll
+        for (int kk = 0; kk < TCC_K / 16; ++kk) {
+          const uint64_t dah = sw128_kdesc(ah, kk, TCC_K), dal = sw128_kdesc(al, kk, TCC_K);
+          const uint64_t dbh = sw128_kdesc(bh, kk, TCC_TN), dbl = sw128_kdesc(bl, kk, TCC_TN);
+          umma_bf16(td, dah, dbh, idesc, kk > 0);
+          umma_bf16(td, dah, dbl, idesc, 1);
+          umma_bf16(td, dal, dbh, idesc, 1);
+        }
+        umma_commit(&opfree);
+        umma_commit(&accf[a]);
+      }
+    }
+  } else {                                          // ---- epilogue: column j, TMEM lane quarter warp % 4
+    const int j = 32 * (warp & 3) + lane, rh = (warp - TCC_CONV / 32) / 4 * TCC_RPW;
+    const double sj = ssc[j];
+    const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)rh;
+    for (int t = 0; t < nst; ++t) {
+      const int a = t % TCC_NT;
+      const int64_t r0 = rb + (int64_t)t * TCC_TN + rh;
+      const int nr = (int)min((int64_t)TCC_RPW, re - r0);
+      double w[TCC_RPW];
+#pragma unroll
+      for (int r = 0; r < TCC_RPW; ++r) w[r] = (r < nr) ? __ldcs(ws.W + (r0 + r) * TCC_K + j) : 0.0;
+      mbar_wait(&accf[a], (t / TCC_NT) & 1);
+      tc_fence_after();
+      float v[TCC_RPW];
+#pragma unroll
+      for (int c = 0; c < TCC_RPW; c += 16) tmem_ld16(tl + (uint32_t)(a * TCC_TN + c), *reinterpret_cast<float(*)[16]>(v + c));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[a]);
+#pragma unroll
+      for (int r = 0; r < TCC_RPW; ++r) {
+        if (r < nr) {
+          const double x = __fma_rn(w[r], sj, -(double)v[r]);
+          __stcs(ws.Xt + (r0 + r) * TCC_K + j, x);
+          nacc = __fma_rn(x, x, nacc);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* snorm = reinterpret_cast<double*>(F);      // the ring is free now
+  if (warp >= TCC_CONV / 32 && warp < (TCC_CONV + TCC_EPI) / 32) snorm[tid - TCC_CONV] = nacc;
+  __syncthreads();
+  if (tid < TCC_K) {                                 // column j: epilogue warps (j / 32) + 4 h, lane j % 32
+    double v = 0.0;
+#pragma unroll
+    for (int h = 0; h < TCC_EPI / 128; ++h) v += snorm[128 * h + tid];
+    ws.nslot[(int64_t)blockIdx.x * TCC_K + tid] = v;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TCC_NT * TCC_TN));
 }
 
 }  // namespace rf
