@@ -510,6 +510,40 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     ws.stats[5] = rr;
     ws.stats[6] = gmax;
   }
+  // S7 folded into this kernel: the column norms of X~ over the
+  // rows >= top follow from the pass-B sums, with x~_i = w'_i D^-1 - x'_i C' and w' = r' + x' D:
+  //   ||x~_2j||^2 = (rr_j + 2 d_j M'_jj + d_j^2 G'_jj) / d_j^2 - (2 / d_j) sum_l C'_lj (M'_lj + d_j G'_lj)
+  //                 + (C'^T G' C')_jj
+  // (the first term ~ 1, the others O(residual): no cancellation).  1 / ||x~_j|| is then folded
+  // into the top rows written here and into pass C's Csig and scal, so pass C writes the final X.
+  double* Cp = S + 15 * kk;                            // C' = P~ D^-1 + U'^-1 B
+  double* GC = Z;                                      // G' C' (Z is dead)
+  for (int e = tid; e < kk; e += nt) Cp[e] = Pt[e] / d[e % k] + UB[e];
+  __syncthreads();
+  cta_gemm(k, k, k, 1.0, Gp, k, false, Cp, k, false, 0.0, nullptr, 0, GC, k, sm);
+  if (tid < k) {
+    const int j = tid;
+    const double dj = d[j];
+    double t2 = 0.0, t3 = 0.0;
+    for (int l = 0; l < k; ++l) {
+      const double c = Cp[l * k + j];
+      t2 = fma(c, fma(dj, Gp[l * k + j], Mp[l * k + j]), t2);
+      t3 = fma(c, GC[l * k + j], t3);
+    }
+    const double t1 = fma(dj, fma(dj, Gp[j * k + j], 2.0 * Mp[j * k + j]), ws.rr2[j]) / (dj * dj);
+    const double tail = t1 - 2.0 * t2 / dj + t3;
+    const double nrm = sqrt(ws.ntop[j] + tail);
+    const double inv = ws.normalize ? 1.0 / nrm : 1.0;
+    if (!isfinite(inv) || !(nrm > 0.0)) atomicCAS(ws.status, ST_OK, ST_DIVERGED);
+    ws.invn[j] = inv;
+    ws.scal[j] *= inv;
+  }
+  __syncthreads();
+  for (int e = tid; e < kk; e += nt) {
+    const double inv = ws.invn[e % k];
+    Xtop[e] = ws.Xt[e] * inv;                          // final top rows of X
+    ws.Csig[e] *= inv;
+  }
 }
 
 // ---------------------------------------------------------------- rr_kxk (Rayleigh-Ritz, Sec. 3.4)

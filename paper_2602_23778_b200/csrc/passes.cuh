@@ -446,17 +446,21 @@ __global__ void __launch_bounds__(PB_RED_THREADS) passB2_reduce_kernel(Ws ws, in
       s = sum_strided(ws.brr + (int64_t)c0 * KP + j, KP, c1 - c0);
     } else {
       int a = e / (2 * k), bb = e % (2 * k);
-      int col;                                           // column in the padded [R | X] space
-      if (bb < k) {
-        col = bb;
-      } else {                                           // G[a][g] = G[min][max] (upper triangle)
-        const int g = bb - k, lo = a < g ? a : g, hi = a < g ? g : a;
-        a = lo;
-        col = KP + hi;
+      if (ws.bdiag && (bb == a || bb == k + a)) {        // tcgen05 pass B: the FP64 diagonals
+        s = sum_strided(ws.bdiag + (int64_t)c0 * 2 * KP + (bb == a ? 0 : KP) + a, 2 * KP, c1 - c0);
+      } else {
+        int col;                                         // column in the padded [R | X] space
+        if (bb < k) {
+          col = bb;
+        } else {                                         // G[a][g] = G[min][max] (upper triangle)
+          const int g = bb - k, lo = a < g ? a : g, hi = a < g ? g : a;
+          a = lo;
+          col = KP + hi;
+        }
+        const int tile = col / C::TB, off = a * C::TB + (col % C::TB);
+        s = sum_strided(ws.bpart + ((int64_t)c0 * C::NT + tile) * (C::TA * C::TB) + off,
+                        (int64_t)C::NT * C::TA * C::TB, c1 - c0);
       }
-      const int tile = col / C::TB, off = a * C::TB + (col % C::TB);
-      s = sum_strided(ws.bpart + ((int64_t)c0 * C::NT + tile) * (C::TA * C::TB) + off,
-                      (int64_t)C::NT * C::TA * C::TB, c1 - c0);
     }
   }
   part[rg][el] = s;
@@ -488,7 +492,7 @@ struct PassCCfg {
 
 template <int KP, int NC, int BM, int WARPS_M, int WARPS_N>
 __global__ void __launch_bounds__(PassCCfg<KP, NC, BM, WARPS_M, WARPS_N>::THREADS)
-passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
+passC_kernel(Ws ws, const double* X, double* out, int vec16) {
   using C = PassCCfg<KP, NC, BM, WARPS_M, WARPS_N>;
   extern __shared__ __align__(16) double smem[];
   __shared__ double ssc[NC];
@@ -585,12 +589,12 @@ passC_kernel(Ws ws, double* __restrict__ X, int vec16) {
         const double x0 = __fma_rn(w[i][j][0], ssc[cl], -acc[i][j][0]);
         const double x1 = __fma_rn(w[i][j][1], ssc[cl + 1], -acc[i][j][1]);
         if (vec16 && c < k) {
-          *reinterpret_cast<double2*>(ws.Xt + g * k + c) = make_double2(x0, x1);
+          *reinterpret_cast<double2*>(out + g * k + c) = make_double2(x0, x1);
           nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]);
           nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]);
         } else {
-          if (c < k) { ws.Xt[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
-          if (c + 1 < k) { ws.Xt[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
+          if (c < k) { out[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
+          if (c + 1 < k) { out[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
         }
       }
     }

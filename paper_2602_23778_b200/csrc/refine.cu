@@ -147,6 +147,7 @@ struct refine_ctx {
   int gather_R = 0, gather_un = 8;
   bool gated = false;   // phase(): launch with ws.status -> ws.gate (refine_run reorthogonalisation)
   bool in_rr = false;   // phase(): a Rayleigh-Ritz / Cholesky-QR step (O(1) products: always FP64)
+  double* bdiag = nullptr;   // NEXT-2 pass B: FP64 diagonal partials (sms x 2 kp), in the pool
   int32_t* xoff_buf = nullptr;
   const int32_t* xoff = nullptr;
   double shift = 0.0;
@@ -213,7 +214,7 @@ template <> struct Tiles<8>   { static constexpr int G[5] = {64, 16, 8, 32, 4}; 
 template <> struct Tiles<16>  { static constexpr int G[5] = {64, 16, 16, 32, 4};  static constexpr int B[5] = {16, 32, 2, 4, 32};  static constexpr int C[4] = {16, 64, 8, 1}; };
 template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}; static constexpr int B[5] = {32, 64, 2, 4, 32};  static constexpr int C[4] = {32, 64, 4, 2}; };
 template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
-template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 2, 16};  static constexpr int C[4] = {64, 16, 1, 8}; };
+template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 2, 16};  static constexpr int C[4] = {128, 32, 2, 8}; };
 
 // Xg: the rows gathered (X, or A X for the second product of the squared operator), Xo: own rows
 template <bool HALO>
@@ -284,6 +285,7 @@ struct Kern {
   static constexpr int B_NT = B2 ? B2C::NT : BC::NTILES;
   static constexpr size_t B_TILE = B2 ? (size_t)B2C::TA * B2C::TB : (size_t)BTA * BTB;
   static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN>;
+  static_assert(CNC == KP, "pass C writes X in place: one CTA must own whole rows (all k columns)");
 
   static cudaError_t setup(refine_ctx* c) {
     cudaError_t e;
@@ -427,9 +429,11 @@ struct Kern {
       case 2:  // S4 reductions
         c->mark();
         if (use_tc(c, X)) {   // NEXT-2: X_2^T [R_2 | X_2] on tcgen05, one FP64 partial per SM
-          passB_tc_kernel<<<c->sms, TCB_THREADS, TCB_SMEM, s>>>(ws, X);
+          Ws wb = ws;
+          wb.bdiag = c->bdiag;   // + the FP64 diagonals of M2, G2
+          passB_tc_kernel<<<c->sms, TCB_THREADS, TCB_SMEM, s>>>(wb, X);
           c->mark();
-          passB2_reduce_kernel<128><<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(ws, c->sms);
+          passB2_reduce_kernel<128><<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(wb, c->sms);
           n += 2;
           break;
         }
@@ -449,23 +453,27 @@ struct Kern {
           n += 1;
         }
         break;
-      case 4:  // S6
+      case 4:  // S6 (+ S7: a sweep's Csig / scal already carry 1 / ||x~_j||, so pass C writes the
+               // final X in place; Rayleigh-Ritz / QR steps write X~ and normalise in phase 5)
         c->mark();
-        if (use_tc(c, X)) {   // NEXT-2: X_2 Csig on tcgen05, norm partials one per SM
-          Ws wm = ws;
-          wm.n_nslot = c->sms;
-          passC_tc_kernel<<<c->sms, TCC_THREADS, TCC_SMEM, s>>>(wm, X);
-          c->mark();
-          norm_reduce_kernel<<<1, KXK_THREADS, 0, s>>>(wm);
-          n += 2;
+        if (!c->in_rr) {
+          if (use_tc(c, X))   // NEXT-2: X_2 Csig on tcgen05
+            passC_tc_kernel<<<c->sms, TCC_THREADS, TCC_SMEM, s>>>(ws, X, X);
+          else
+            passC<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, X, xv16);
+          n += 1;
           break;
         }
-        passC<<<dim3(c->passc_grid, KP / CNC), CC::THREADS, CC::SMEM, s>>>(ws, X, xv16);
+        passC<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, ws.Xt, xv16);
         c->mark();
         norm_reduce_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
         n += 2;
         break;
-      case 5:  // S7
+      case 5:  // S7 (Rayleigh-Ritz / QR steps; a sweep normalised in kxk_finish / pass C)
+        if (!c->in_rr) {
+          c->mark();
+          break;
+        }
         if (c->opts.normalize) {
           c->mark();
           normalize_kernel<<<c->sms * 8, 256, 0, s>>>(ws, X);
@@ -630,7 +638,8 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
                oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
-               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k), oGate = take(1);
+               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k), oGate = take(1),
+               oBd = take(c->opts.mixed ? (size_t)c->sms * 2 * c->kp : 0);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
   c->pool_bytes = bytes;
@@ -651,6 +660,9 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.ritz = b + oRitz; ws.zerod = b + oZd; ws.top_zero = 0;   // (the pool is zeroed below)
   ws.gate = reinterpret_cast<int*>(b + oGate);
   ws.want_gram = c->opts.reorth_tol > 0.0 ? 1 : 0;
+  ws.normalize = c->opts.normalize ? 1 : 0;
+  ws.bdiag = nullptr;
+  c->bdiag = c->opts.mixed ? b + oBd : nullptr;
   c->run = reinterpret_cast<RunState*>(b + oRun);
   ws.tlog = nullptr;
   if (getenv("REFINE_KXK_TIMING")) RF_CK(c, cudaMalloc(&ws.tlog, 64 * sizeof(long long)));
@@ -943,7 +955,7 @@ static refine_status enqueue_phases(refine_ctx* c, double* X) {
   refine_ctx* one[1] = {c};
   refine_ctx** ranks = c->loopback ? c->kids.data() : one;
   const int nr = c->loopback ? (int)c->kids.size() : 1;
-  static const int after[6] = {C_AG, -1, C_MG, C_BC, C_NRM, -1};
+  static const int after[6] = {C_AG, -1, C_MG, C_BC, -1, -1};
   refine_status st;
   if (multi && (st = collective(c, C_X, X)) != REFINE_OK) return st;
   int launches = 0;
@@ -1202,18 +1214,17 @@ extern "C" int32_t refine_kernels_per_sweep(const refine_ctx* c) {
     for (auto* kid : c->kids) n += refine_kernels_per_sweep(kid);
     return n;
   }
-  const int per = (c->csr ? 8 : 9) + (c->opts.normalize ? 1 : 0);   // incl. kxk_lu (side stream)
+  const int per = c->csr ? 7 : 8;   // incl. kxk_lu (side stream)
   if (!c->multi) return per;
   return per + 1 - (c->rank == 0 ? 0 : 2);   // + ag_local; kxk_lu / kxk_finish on rank 0 only
 }
 
 static const char* kernel_names_dense[] = {"gemm_ax", "w_finish", "kxk_rq", "passB", "passB_reduce",
-                                           "kxk_finish", "passC", "norm_reduce", "normalize"};
-static const char* kernel_names_csr[] = {"spmm_csr", "kxk_rq", "passB", "passB_reduce",
-                                         "kxk_finish", "passC", "norm_reduce", "normalize"};
+                                           "kxk_finish", "passC"};
+static const char* kernel_names_csr[] = {"spmm_csr", "kxk_rq", "passB", "passB_reduce", "kxk_finish", "passC"};
 
 extern "C" const char* refine_kernel_name(const refine_ctx* c, int32_t i) {
-  if (!c || i < 0 || i >= (c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0)) return "";
+  if (!c || i < 0 || i >= (c->csr ? 6 : 7)) return "";
   return c->csr ? kernel_names_csr[i] : kernel_names_dense[i];
 }
 
@@ -1222,7 +1233,7 @@ extern "C" refine_status refine_profile_begin(refine_ctx* c, int32_t max_sweeps)
   if (c->loopback) return REFINE_E_UNSUPPORTED;
   if (c->use_graph) return REFINE_E_UNSUPPORTED;      // events are recorded at enqueue time
   if (c->prof_ev) return REFINE_E_INVALID;
-  c->prof_per_sweep = ((c->csr ? 7 : 8) + (c->opts.normalize ? 1 : 0)) + 1;   // kernel slots (mark() positions)
+  c->prof_per_sweep = (c->csr ? 6 : 7) + 1;   // kernel slots (mark() positions)
   c->prof_cap = c->prof_per_sweep * max_sweeps;
   c->prof_ev = new (std::nothrow) cudaEvent_t[c->prof_cap];
   if (!c->prof_ev) return REFINE_E_NOMEM;

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
-  double rr = 0.0;
+  double rr = 0.0, xr = 0.0, xx = 0.0;
   if (warp == TCB_CONV / 32) {                     // ---- producer
     if (lane == 0) {
       for (int t = 0; t < nst; ++t) {
@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
           const double w = v ? fw[(r + j) * TCB_K + col] : 0.0;
           qv[j] = __fma_rn(-x[j], dcol, w);             // R = W - X D (FP64)
           rr = __fma_rn(qv[j], qv[j], rr);
+          xr = __fma_rn(x[j], qv[j], xr);               // diagonals of M2, G2 in FP64
+          xx = __fma_rn(x[j], x[j], xx);
         }
         uint2 xh, xl, rh, rl;
         split2_bf16(x[0], x[1], xh.x, xl.x);
@@ -295,11 +297,18 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   }
   __syncthreads();
   double* srr = reinterpret_cast<double*>(tcb_smem);     // the FP64 ring is free now
-  if (tid < TCB_CONV) srr[tid] = rr;                     // column 16 w + (l & 15) from lanes l, l + 16
+  if (tid < TCB_CONV) {                                  // column 16 w + (l & 15) from lanes l, l + 16
+    srr[tid] = rr;
+    srr[TCB_CONV + tid] = xr;
+    srr[2 * TCB_CONV + tid] = xx;
+  }
   __syncthreads();
   if (tid < TCB_K) {
     const int t0 = 32 * (tid >> 4) + (tid & 15);
     ws.brr[(int64_t)blockIdx.x * TCB_K + tid] = srr[t0] + srr[t0 + 16];
+    double* bd = ws.bdiag + (int64_t)blockIdx.x * 2 * TCB_K;
+    bd[tid] = srr[TCB_CONV + t0] + srr[TCB_CONV + t0 + 16];
+    bd[TCB_K + tid] = srr[2 * TCB_CONV + t0] + srr[2 * TCB_CONV + t0 + 16];
   }
   tc_fence_before();
   __syncthreads();
@@ -351,7 +360,7 @@ RF_DEV uint64_t sw128_kdesc(uint32_t base, int kk, int R) {
 }
 RF_DEV void conv_sync_c() { asm volatile("bar.sync 1, %0;\n" ::"n"(TCC_CONV) : "memory"); }
 
-__global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const double* __restrict__ X) {
+__global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const double* X, double* out) {
   extern __shared__ __align__(16) unsigned char tcc_raw[];
   __shared__ __align__(8) uint64_t full[TCC_NS], empty[TCC_NS], opfree, accf[TCC_NT], acce[TCC_NT];
   __shared__ uint32_t tmem_base;
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
       for (int r = 0; r < TCC_RPW; ++r) {
         if (r < nr) {
           const double x = __fma_rn(w[r], sj, -(double)v[r]);
-          __stcs(ws.Xt + (r0 + r) * TCC_K + j, x);
+          __stcs(out + (r0 + r) * TCC_K + j, x);
           nacc = __fma_rn(x, x, nacc);
         }
       }

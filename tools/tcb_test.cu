@@ -23,6 +23,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&X, n * k * 8); cudaMalloc(&W, n * k * 8); cudaMalloc(&d, k * 8); cudaMalloc(&st, 4);
   const int chunks = 256;
   cudaMalloc(&bp, (size_t)chunks * 4 * 128 * 64 * 8); cudaMalloc(&brr, (size_t)chunks * 128 * 8);
+  double* bd; cudaMalloc(&bd, (size_t)chunks * 2 * 128 * 8);
   cudaMalloc(&out1, (2 * k * k + k) * 8); cudaMalloc(&out2, (2 * k * k + k) * 8);
   fill<<<1184, 256>>>(X, n * k, 1, 1.0 / sqrt((double)n));
   fill<<<1184, 256>>>(W, n * k, 2, 1.0 / sqrt((double)n));
@@ -46,6 +47,7 @@ int main(int argc, char** argv) {
   // tcgen05
   cudaFuncSetAttribute(passB_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCB_SMEM);
   ws.M2 = out2; ws.G2 = out2 + k * k; ws.rr2 = out2 + 2 * k * k;
+  ws.bdiag = bd;   // FP64 diagonals of M2, G2
   passB_tc_kernel<<<sms, TCB_THREADS, TCB_SMEM>>>(ws, X);
   cudaError_t e = cudaDeviceSynchronize();
   printf("first tc launch: %s\n", cudaGetErrorString(e));

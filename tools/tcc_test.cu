@@ -33,27 +33,27 @@ int main(int argc, char** argv) {
   cudaMemset(Xt1, 0, n * k * 8); cudaMemset(Xt2, 0, n * k * 8);
   Ws ws{};
   ws.n_loc = n; ws.k = k; ws.kp = 128; ws.top = top; ws.W = W; ws.Csig = Cs; ws.scal = sc; ws.status = st;
-  using CC = PassCCfg<128, 64, 16, 1, 8>;
-  auto pc = passC_kernel<128, 64, 16, 1, 8>;
+  using CC = PassCCfg<128, 128, 32, 2, 8>;
+  auto pc = passC_kernel<128, 128, 32, 2, 8>;
   cudaFuncSetAttribute(pc, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pc, CC::THREADS, CC::SMEM);
-  const int g1 = sms * occ / 2;
+  const int g1 = sms * occ;
   ws.Xt = Xt1; ws.nslot = ns1;
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  pc<<<dim3(g1, 2), CC::THREADS, CC::SMEM>>>(ws, X, 1);
+  pc<<<dim3(g1, 1), CC::THREADS, CC::SMEM>>>(ws, X, Xt1, 1);
   cudaEventRecord(a);
-  pc<<<dim3(g1, 2), CC::THREADS, CC::SMEM>>>(ws, X, 1);
+  pc<<<dim3(g1, 1), CC::THREADS, CC::SMEM>>>(ws, X, Xt1, 1);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms1; cudaEventElapsedTime(&ms1, a, b);
   cudaFuncSetAttribute(passC_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCC_SMEM);
   ws.Xt = Xt2; ws.nslot = ns2;
-  passC_tc_kernel<<<sms, TCC_THREADS, TCC_SMEM>>>(ws, X);
+  passC_tc_kernel<<<sms, TCC_THREADS, TCC_SMEM>>>(ws, X, Xt2);
   cudaError_t e = cudaDeviceSynchronize();
   printf("first tc launch: %s\n", cudaGetErrorString(e));
   cudaEventRecord(a);
-  passC_tc_kernel<<<sms, TCC_THREADS, TCC_SMEM>>>(ws, X);
+  passC_tc_kernel<<<sms, TCC_THREADS, TCC_SMEM>>>(ws, X, Xt2);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   e = cudaDeviceSynchronize();
