@@ -53,6 +53,9 @@ __device__ __noinline__ void cta_gemm_t(int M, int N, int K, double alpha, const
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) acc[t][0] = acc[t][1] = 0.0;
   const int Mp = tm * 8, Np = tn * 8;
+  const bool glob = __isGlobal(A) && __isGlobal(B);
+  const bool blk = (MAXT == 8) && tm == 16 && tn == 16;
+  const int bi0 = (warp >> 2) * 16, bj0 = (warp & 3) * 32;
   long long* tl = g_gemm_tlog;
   int ts = 0;
   if (tl && tid == 0) tl[ts] = clock64();
@@ -62,30 +65,62 @@ __device__ __noinline__ void cta_gemm_t(int M, int N, int K, double alpha, const
     __syncthreads();
     if (tl && tid == 0 && ts < 14) tl[ts] = clock64();
     ++ts;
-    // stage op(A)(0:Mp, kk:kk+32) and op(B)(kk:kk+32, 0:Np), zero-padded
-    for (int e = tid; e < PANEL * Mp; e += KXK_THREADS) {
-      int i, p;
-      if (ta) { i = e % Mp; p = e / Mp; } else { p = e & (PANEL - 1); i = e >> 5; }
-      As[i * LDA_P + p] = (p < pk && i < M) ? (ta ? A[(kk + p) * lda + i] : A[i * lda + kk + p]) : 0.0;
-    }
-    for (int e = tid; e < PANEL * Np; e += KXK_THREADS) {
-      int j, p;
-      if (tb) { p = e & (PANEL - 1); j = e >> 5; } else { j = e % Np; p = e / Np; }
-      Bs[p * LDB_P + j] = (p < pk && j < N) ? (tb ? B[j * ldb + kk + p] : B[(kk + p) * ldb + j]) : 0.0;
+    // stage op(A)(0:Mp, kk:kk+32) and op(B)(kk:kk+32, 0:Np), zero-padded.  Global operands go
+    // through cp.async (every copy of the panel in flight at once: one L2 round trip per panel,
+    // not one per element); shared-memory operands (kxk_lu's small-k factors) are copied directly.
+    if (glob) {
+      for (int e = tid; e < PANEL * Mp; e += KXK_THREADS) {
+        int i, p;
+        if (ta) { i = e % Mp; p = e / Mp; } else { p = e & (PANEL - 1); i = e >> 5; }
+        const bool ok = p < pk && i < M;
+        cp_async8(As + i * LDA_P + p, ok ? (ta ? A + (kk + p) * lda + i : A + i * lda + kk + p) : A, ok);
+      }
+      for (int e = tid; e < PANEL * Np; e += KXK_THREADS) {
+        int j, p;
+        if (tb) { p = e & (PANEL - 1); j = e >> 5; } else { j = e % Np; p = e / Np; }
+        const bool ok = p < pk && j < N;
+        cp_async8(Bs + p * LDB_P + j, ok ? (tb ? B + j * ldb + kk + p : B + (kk + p) * ldb + j) : B, ok);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+    } else {
+      for (int e = tid; e < PANEL * Mp; e += KXK_THREADS) {
+        int i, p;
+        if (ta) { i = e % Mp; p = e / Mp; } else { p = e & (PANEL - 1); i = e >> 5; }
+        As[i * LDA_P + p] = (p < pk && i < M) ? (ta ? A[(kk + p) * lda + i] : A[i * lda + kk + p]) : 0.0;
+      }
+      for (int e = tid; e < PANEL * Np; e += KXK_THREADS) {
+        int j, p;
+        if (tb) { p = e & (PANEL - 1); j = e >> 5; } else { j = e % Np; p = e / Np; }
+        Bs[p * LDB_P + j] = (p < pk && j < N) ? (tb ? B[j * ldb + kk + p] : B[(kk + p) * ldb + j]) : 0.0;
+      }
     }
     __syncthreads();
     if (tl && tid == 0 && ts < 14) tl[ts] = clock64();
     ++ts;
+    if (blk) {   // 16 x 16 tiles: warp w owns a 2 x 4 block (A / B fragments reused 4 / 2 times)
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      const int tile = warp + 32 * t;
-      if (tile < ntile) {
-        const int i0 = (tile / tn) * 8, j0 = (tile % tn) * 8;
+      for (int p = 0; p < PANEL; p += 4) {
+        double a[2], b[4];
 #pragma unroll
-        for (int p = 0; p < PANEL; p += 4) {
-          const double a = As[(i0 + (lane >> 2)) * LDA_P + p + (lane & 3)];
-          const double b = Bs[(p + (lane & 3)) * LDB_P + j0 + (lane >> 2)];
-          dmma(acc[t][0], acc[t][1], a, b);
+        for (int r = 0; r < 2; ++r) a[r] = As[(bi0 + 8 * r + (lane >> 2)) * LDA_P + p + (lane & 3)];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) b[c] = Bs[(p + (lane & 3)) * LDB_P + bj0 + 8 * c + (lane >> 2)];
+#pragma unroll
+        for (int t = 0; t < (MAXT == 8 ? 8 : 0); ++t) dmma(acc[t][0], acc[t][1], a[t >> 2], b[t & 3]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        const int tile = warp + 32 * t;
+        if (tile < ntile) {
+          const int i0 = (tile / tn) * 8, j0 = (tile % tn) * 8;
+#pragma unroll
+          for (int p = 0; p < PANEL; p += 4) {
+            const double a = As[(i0 + (lane >> 2)) * LDA_P + p + (lane & 3)];
+            const double b = Bs[(p + (lane & 3)) * LDB_P + j0 + (lane >> 2)];
+            dmma(acc[t][0], acc[t][1], a, b);
+          }
         }
       }
     }
@@ -93,8 +128,9 @@ __device__ __noinline__ void cta_gemm_t(int M, int N, int K, double alpha, const
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
     const int tile = warp + 32 * t;
-    if (tile < ntile) {
-      const int i = (tile / tn) * 8 + (lane >> 2), j = (tile % tn) * 8 + 2 * (lane & 3);
+    if (blk || tile < ntile) {
+      const int i = blk ? bi0 + 8 * (t >> 2) + (lane >> 2) : (tile / tn) * 8 + (lane >> 2);
+      const int j = blk ? bj0 + 8 * (t & 3) + 2 * (lane & 3) : (tile % tn) * 8 + 2 * (lane & 3);
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         if (i < M && j + h < N) {
@@ -119,6 +155,67 @@ __device__ __forceinline__ void cta_gemm(int M, int N, int K, double alpha, cons
   if (nt <= 32) cta_gemm_t<1>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C0, ldc0, C, ldc, sm);
   else if (nt <= 64) cta_gemm_t<2>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C0, ldc0, C, ldc, sm);
   else cta_gemm_t<8>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C0, ldc0, C, ldc, sm);
+}
+
+// Row block of a k x k product for kxk_finish's cluster CTAs: C (M x N) = alpha op(A) B + beta C0
+// with M <= 32, N, K <= 128, op(A) and B staged WHOLE (all K) in shared memory by one burst of
+// cp.async copies (one L2 round trip per product instead of one per 32-deep panel).  Warp w owns
+// output tiles w and w + 32.  Starts and ends with a barrier.
+constexpr int FK_SMEM = 32 * (KMAX + 4) + KMAX * (KMAX + 8);   // doubles
+__device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, const double* A, int lda, bool ta,
+                                            const double* B, int ldb, double beta, const double* C0, int ldc0,
+                                            double* C, int ldc, double* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, ntile = tm * tn;
+  const int Mp = tm * 8, Np = tn * 8, Kp = (K + 3) & ~3;
+  const int lda_s = Kp + 4, ldb_s = Np + 8;
+  double* As = sm;                      // [Mp][lda_s]  As[i][p] = op(A)(i, p)
+  double* Bs = sm + Mp * lda_s;         // [Kp][ldb_s]  Bs[p][j] = B(p, j)
+  __syncthreads();
+  if (__isGlobal(A) && __isGlobal(B)) {
+    for (int e = tid; e < Mp * Kp; e += KXK_THREADS) {
+      int i, p;
+      if (ta) { i = e % Mp; p = e / Mp; } else { p = e % Kp; i = e / Kp; }
+      const bool ok = p < K && i < M;
+      cp_async8(As + i * lda_s + p, ok ? (ta ? A + p * lda + i : A + i * lda + p) : A, ok);
+    }
+    for (int e = tid; e < Kp * Np; e += KXK_THREADS) {
+      const int j = e % Np, p = e / Np;
+      const bool ok = p < K && j < N;
+      cp_async8(Bs + p * ldb_s + j, ok ? B + p * ldb + j : B, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else {
+    for (int e = tid; e < Mp * Kp; e += KXK_THREADS) {
+      int i, p;
+      if (ta) { i = e % Mp; p = e / Mp; } else { p = e % Kp; i = e / Kp; }
+      As[i * lda_s + p] = (p < K && i < M) ? (ta ? A[p * lda + i] : A[i * lda + p]) : 0.0;
+    }
+    for (int e = tid; e < Kp * Np; e += KXK_THREADS) {
+      const int j = e % Np, p = e / Np;
+      Bs[p * ldb_s + j] = (p < K && j < N) ? B[p * ldb + j] : 0.0;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int tile = warp + 32 * t;
+    if (tile < ntile) {
+      const int i0 = (tile / tn) * 8, j0 = (tile % tn) * 8;
+      double c0 = 0.0, c1 = 0.0;
+      const double* ap = As + (i0 + (lane >> 2)) * lda_s + (lane & 3);
+      const double* bp = Bs + (lane & 3) * ldb_s + j0 + (lane >> 2);
+#pragma unroll 8
+      for (int p = 0; p < Kp; p += 4) dmma(c0, c1, ap[p], bp[p * ldb_s]);
+      const int i = i0 + (lane >> 2), j = j0 + 2 * (lane & 3);
+      if (i < M) {
+        if (j < N) C[i * ldc + j] = (beta != 0.0) ? fma(beta, C0[i * ldc0 + j], alpha * c0) : alpha * c0;
+        if (j + 1 < N) C[i * ldc + j + 1] = (beta != 0.0) ? fma(beta, C0[i * ldc0 + j + 1], alpha * c1) : alpha * c1;
+      }
+    }
+  }
+  __syncthreads();
 }
 
 // Inverse of a k x k triangular matrix S (ld k) into R (ld k).  upper: S upper triangular;
@@ -379,6 +476,31 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_lu_kernel(Ws ws, const double
 }
 
 // ---------------------------------------------------------------- kxk_finish
+// One thread-block cluster of kxk_cluster(k) CTAs (1024 threads each): CTA r owns rows
+// [r0, r1) of every k x k result (a multiple of 8 rows), so each cta_gemm call computes its row
+// block (M = r1 - r0) and the elementwise steps run on its rows; barrier.cluster (release /
+// acquire: global-memory results of the other CTAs become visible) separates dependent phases.
+// The per-column statistics and norms run on CTA 0.  k <= 32 runs as a single CTA.
+RF_DEV unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+RF_DEV unsigned cluster_nctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+  return r;
+}
+RF_DEV void cluster_sync() {
+  if (cluster_nctarank() == 1) {   // single CTA: a block barrier orders its global accesses too
+    __syncthreads();
+    return;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__host__ __device__ constexpr int kxk_cluster(int k) { return k >= 128 ? 8 : (k >= 64 ? 4 : (k > 32 ? 2 : 1)); }
+constexpr int KXK_SCRATCH_EXTRA = 64;   // doubles after the 16 k x k scratch matrices (cluster partials)
+
 // Xtop/Wtop: the top k rows of X^ (in/out) and W (un-flipped), ld k.
 __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* __restrict__ Xtop,
                                                                  const double* __restrict__ Wtop) {
@@ -387,24 +509,36 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   __shared__ double s_red[4][KMAX];
   if (*ws.status != ST_OK) return;
   const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
+  const int crank = (int)cluster_ctarank(), ncl = (int)cluster_nctarank();
+  const int per = (((k + ncl - 1) / ncl) + 7) & ~7;
+  const int r0 = min(k, crank * per), r1 = min(k, r0 + per), nr = r1 - r0;
   double* S = ws.scratch;
   double *Xp = S, *R1 = S + kk, *Mp = S + 2 * kk, *Gp = S + 3 * kk, *Ui = S + 4 * kk, *Z = S + 5 * kk,
          *P = S + 6 * kk, *V1 = S + 7 * kk, *Pt = S + 8 * kk, *GPt = S + 9 * kk, *S2 = S + 10 * kk,
          *Qm = S + 11 * kk, *B = S + 12 * kk, *LB = S + 13 * kk, *UB = S + 14 * kk;
+  double* part = S + 16 * kk;                          // [0, 8): delta hits, [8, 16): gram max per CTA
   const double* sig = ws.sigma;
   const double* d = ws.d;
+  // this CTA's rows of C = alpha op(A) B + beta C0 (k x k operands, B not transposed)
+  auto rgemm = [&](double alpha, const double* A, bool ta, const double* Bm, double beta, const double* C0, double* C) {
+    if (nr > 0)
+      cta_gemm_fullk(nr, k, k, alpha, ta ? A + r0 : A + r0 * k, k, ta, Bm, k, beta, C0 ? C0 + r0 * k : nullptr, k,
+                     C + r0 * k, k, sm);
+  };
   if (tid == 0) s_hits = 0;
-  if (ws.tlog && tid == 0) g_gemm_tlog = ws.tlog + 40;
+  if (crank == 0) RF_TSTAMP(ws, 20);
+  if (ws.tlog && tid == 0 && crank == 0) g_gemm_tlog = ws.tlog + 40;
   if (ws.multi) {   // [M2 | G2 | rr2] of every rank, summed in rank order (M2, G2, rr2 are contiguous)
     const int64_t cnt = 2 * kk + k;
-    for (int64_t e = tid; e < cnt; e += nt) {
+    for (int64_t e = crank * nt + tid; e < cnt; e += (int64_t)ncl * nt) {
       double sum = ws.mg_all[e];
       for (int r = 1; r < ws.world; ++r) sum += ws.mg_all[(int64_t)r * cnt + e];
       ws.M2[e] = sum;
     }
-    __syncthreads();
+    cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 21);
   }
-  for (int i = tid >> 5; i < k; i += 32)
+  for (int i = r0 + (tid >> 5); i < r1; i += 32)
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     const double xp = Xtop[e] * sig[j];
@@ -414,14 +548,19 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     Gp[e] = sig[i] * ws.G2[e] * sig[j];
     Ui[e] = sig[i] * ws.Uinv[e];                      // U'^{-1} = Sigma U^{-1}
   }
-  __syncthreads();
-  cta_gemm(k, k, k, 1.0, ws.L, k, true, R1, k, false, 0.0, nullptr, 0, Z, k, sm);   // Z = L^T R_1
-  cta_gemm(k, k, k, 1.0, Ui, k, true, Mp, k, false, 1.0, Z, k, Z, k, sm);           //   + U'^{-T} M'
-  cta_gemm(k, k, k, 1.0, ws.T, k, true, Z, k, false, 0.0, nullptr, 0, P, k, sm);    // P = T^T Z
-  cta_gemm(k, k, k, -1.0, ws.L, k, false, P, k, false, 1.0, R1, k, V1, k, sm);      // V_1 = R_1 - L P
-  cta_gemm(k, k, k, 1.0, Ui, k, false, P, k, false, 0.0, nullptr, 0, Pt, k, sm);   // P~ = U'^{-1} P
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 22);
+  rgemm(1.0, ws.L, true, R1, 0.0, nullptr, Z);        // Z = L^T R_1
+  rgemm(1.0, Ui, true, Mp, 1.0, Z, Z);                //   + U'^{-T} M'
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 23);
+  rgemm(1.0, ws.T, true, Z, 0.0, nullptr, P);         // P = T^T Z
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 24);
+  rgemm(-1.0, ws.L, false, P, 1.0, R1, V1);           // V_1 = R_1 - L P
+  rgemm(1.0, Ui, false, P, 0.0, nullptr, Pt);         // P~ = U'^{-1} P
   // E_11 (line 6): beta needs the Gram G = X'^T X' = X'_1^T X'_1 + G'
-  for (int i = tid >> 5; i < k; i += 32)
+  for (int i = r0 + (tid >> 5); i < r1; i += 32)
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     double v;
@@ -442,74 +581,22 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     }
     ws.E11[e] = v;
   }
-  cta_gemm(k, k, k, 1.0, Gp, k, false, Pt, k, false, 0.0, nullptr, 0, GPt, k, sm);  // G' P~ (barrier inside)
-  for (int i = tid >> 5; i < k; i += 32)
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 25);
+  rgemm(1.0, Gp, false, Pt, 0.0, nullptr, GPt);       // G' P~
+  for (int i = r0 + (tid >> 5); i < r1; i += 32)
     for (int j = tid & 31; j < k; j += 32) S2[i * k + j] = (Mp[i * k + j] - GPt[i * k + j]) / d[j];
-  __syncthreads();
-  cta_gemm(k, k, k, 1.0, ws.L, k, true, ws.E11, k, false, 0.0, nullptr, 0, Qm, k, sm);  // Qm = L^T E_11
-  cta_gemm(k, k, k, 1.0, Ui, k, true, S2, k, false, 1.0, Qm, k, Qm, k, sm);             //   + U'^{-T} S2
-  cta_gemm(k, k, k, 1.0, ws.T, k, false, Qm, k, false, 0.0, nullptr, 0, B, k, sm);      // B = T Qm
-  cta_gemm(k, k, k, 1.0, ws.L, k, false, B, k, false, 0.0, nullptr, 0, LB, k, sm);      // L B
-  cta_gemm(k, k, k, 1.0, Ui, k, false, B, k, false, 0.0, nullptr, 0, UB, k, sm);        // U'^{-1} B
-  for (int l = tid >> 5; l < k; l += 32)
-    for (int j = tid & 31; j < k; j += 32) {
-    const int e = l * k + j;
-    ws.Xt[e] = Xp[e] + (ws.E11[e] - LB[e]);            // X~_1 = X'_1 + (E_11 - L B)  (top rows of X~)
-    ws.Csig[e] = sig[l] * (Pt[e] / d[j] + UB[e]);      // Csig = Sigma (P~ D^{-1} + U'^{-1} B)
-  }
-  __syncthreads();
-  // Gram deviation of the sweep's input (reorthogonalisation policy): G = X'_1^T X'_1 + G'
-  double gmax = -1.0;
-  if (ws.want_gram) {
-    cta_gemm(k, k, k, 1.0, Xp, k, true, Xp, k, false, 1.0, Gp, k, LB, k, sm);
-    double m = 0.0;
-    for (int e = tid; e < kk; e += nt) m = fmax(m, fabs(LB[e] - ((e / k == e % k) ? 1.0 : 0.0)));
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((tid & 31) == 0) s_red[0][tid >> 5] = m;
-    __syncthreads();
-    if (tid == 0) {
-      for (int w = 1; w < nt / 32; ++w) m = fmax(m, s_red[0][w]);
-      s_red[0][0] = m;
-    }
-    __syncthreads();
-    gmax = s_red[0][0];
-    __syncthreads();
-  }
-  // per-column quantities and statistics
-  if (tid < k) {
-    const int j = tid;
-    double nt2 = 0.0, r1 = 0.0, e1 = 0.0, pm = 0.0, pgp = 0.0;
-    for (int i = 0; i < k; ++i) {
-      const double x = ws.Xt[i * k + j];
-      nt2 = fma(x, x, nt2);
-      r1 = fma(R1[i * k + j], R1[i * k + j], r1);
-      e1 = fma(ws.E11[i * k + j], ws.E11[i * k + j], e1);
-      pm = fma(Pt[i * k + j], Mp[i * k + j], pm);
-      pgp = fma(Pt[i * k + j], GPt[i * k + j], pgp);
-    }
-    ws.ntop[j] = nt2;
-    ws.scal[j] = sig[j] / d[j];
-    const double e2 = (ws.rr2[j] - 2.0 * pm + pgp) / (d[j] * d[j]);
-    s_red[0][j] = r1 + ws.rr2[j];
-    s_red[1][j] = (ws.kjudge > 0 && j >= ws.kjudge) ? 0.0 : e1 + e2;   // K > k: judge the leading kjudge
-    double mg = INFINITY;
-    for (int i = 0; i < k; ++i)
-      if (i != j) mg = fmin(mg, fabs(d[j] - d[i]));
-    s_red[2][j] = mg;
-    s_red[3][j] = (sig[j] < 0.0) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double rr = 0.0, en = 0.0, mg = INFINITY, fl = 0.0;
-    for (int j = 0; j < k; ++j) { rr += s_red[0][j]; en += s_red[1][j]; mg = fmin(mg, s_red[2][j]); fl += s_red[3][j]; }
-    ws.stats[0] = sqrt(rr) / ws.normA;
-    ws.stats[1] = sqrt(fmax(en, 0.0));
-    ws.stats[2] = (k > 1) ? mg : 0.0;
-    ws.stats[3] = (double)s_hits;
-    ws.stats[4] = (fl > 0.0) ? 1.0 : 0.0;
-    ws.stats[5] = rr;
-    ws.stats[6] = gmax;
-  }
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 26);
+  rgemm(1.0, ws.L, true, ws.E11, 0.0, nullptr, Qm);   // Qm = L^T E_11
+  rgemm(1.0, Ui, true, S2, 1.0, Qm, Qm);              //   + U'^{-T} S2
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 27);
+  rgemm(1.0, ws.T, false, Qm, 0.0, nullptr, B);       // B = T Qm
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 28);
+  rgemm(1.0, ws.L, false, B, 0.0, nullptr, LB);       // L B
+  rgemm(1.0, Ui, false, B, 0.0, nullptr, UB);         // U'^{-1} B
   // S7 folded into this kernel: the column norms of X~ over the
   // rows >= top follow from the pass-B sums, with x~_i = w'_i D^-1 - x'_i C' and w' = r' + x' D:
   //   ||x~_2j||^2 = (rr_j + 2 d_j M'_jj + d_j^2 G'_jj) / d_j^2 - (2 / d_j) sum_l C'_lj (M'_lj + d_j G'_lj)
@@ -518,32 +605,114 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   // into the top rows written here and into pass C's Csig and scal, so pass C writes the final X.
   double* Cp = S + 15 * kk;                            // C' = P~ D^-1 + U'^-1 B
   double* GC = Z;                                      // G' C' (Z is dead)
-  for (int e = tid; e < kk; e += nt) Cp[e] = Pt[e] / d[e % k] + UB[e];
-  __syncthreads();
-  cta_gemm(k, k, k, 1.0, Gp, k, false, Cp, k, false, 0.0, nullptr, 0, GC, k, sm);
-  if (tid < k) {
-    const int j = tid;
-    const double dj = d[j];
-    double t2 = 0.0, t3 = 0.0;
-    for (int l = 0; l < k; ++l) {
-      const double c = Cp[l * k + j];
-      t2 = fma(c, fma(dj, Gp[l * k + j], Mp[l * k + j]), t2);
-      t3 = fma(c, GC[l * k + j], t3);
-    }
-    const double t1 = fma(dj, fma(dj, Gp[j * k + j], 2.0 * Mp[j * k + j]), ws.rr2[j]) / (dj * dj);
-    const double tail = t1 - 2.0 * t2 / dj + t3;
-    const double nrm = sqrt(ws.ntop[j] + tail);
-    const double inv = ws.normalize ? 1.0 / nrm : 1.0;
-    if (!isfinite(inv) || !(nrm > 0.0)) atomicCAS(ws.status, ST_OK, ST_DIVERGED);
-    ws.invn[j] = inv;
-    ws.scal[j] *= inv;
+  for (int l = r0 + (tid >> 5); l < r1; l += 32)
+    for (int j = tid & 31; j < k; j += 32) {
+    const int e = l * k + j;
+    ws.Xt[e] = Xp[e] + (ws.E11[e] - LB[e]);            // X~_1 = X'_1 + (E_11 - L B)  (top rows of X~)
+    Cp[e] = Pt[e] / d[j] + UB[e];
+    ws.Csig[e] = sig[l] * Cp[e];                       // Csig = Sigma (P~ D^{-1} + U'^{-1} B)
   }
-  __syncthreads();
-  for (int e = tid; e < kk; e += nt) {
-    const double inv = ws.invn[e % k];
+  if (tid == 0) part[crank] = (double)s_hits;
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 29);
+  rgemm(1.0, Gp, false, Cp, 0.0, nullptr, GC);
+  // Gram deviation of the sweep's input (reorthogonalisation policy): G = X'_1^T X'_1 + G'
+  if (ws.want_gram) {
+    rgemm(1.0, Xp, true, Xp, 1.0, Gp, LB);
+    double m = 0.0;
+    for (int e = r0 * k + tid; e < r1 * k; e += nt) m = fmax(m, fabs(LB[e] - ((e / k == e % k) ? 1.0 : 0.0)));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) s_red[0][tid >> 5] = m;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < nt / 32; ++w) m = fmax(m, s_red[0][w]);
+      part[8 + crank] = m;
+    }
+  }
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 30);
+  if (crank == 0) {
+    // per-column sums over the k rows, by all 1024 threads: thread (g, j) takes rows l = g, g + NG, ..
+    // (fixed partition, groups combined in order -- deterministic)
+    constexpr int NQ = 7;
+    const int NG = min(nt / k, k);                     // row groups (k <= 128: >= 8 unless k < 8)
+    double* cs = sm;                                   // [NG][NQ][k] partials (cta_gemm's panel space)
+    double* sd = sm + (size_t)NG * NQ * k;             // d
+    for (int j = tid; j < k; j += nt) sd[j] = d[j];
+    if (tid < NG * k) {
+      const int g = tid / k, j = tid % k;
+      const double dj = d[j];
+      double q[NQ] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int l = g; l < k; l += NG) {
+        const int e = l * k + j;
+        const double x = ws.Xt[e], r = R1[e], ee = ws.E11[e], pt = Pt[e], c = Cp[e];
+        q[0] = fma(x, x, q[0]);                        // ||x~_1j||^2 (top rows)
+        q[1] = fma(r, r, q[1]);                        // ||R_1j||^2
+        q[2] = fma(ee, ee, q[2]);                      // ||E_11 j||^2
+        q[3] = fma(pt, Mp[e], q[3]);                   // (P~^T M')_jj
+        q[4] = fma(pt, GPt[e], q[4]);                  // (P~^T G' P~)_jj
+        q[5] = fma(c, fma(dj, Gp[e], Mp[e]), q[5]);    // sum_l C'_lj (M'_lj + d_j G'_lj)
+        q[6] = fma(c, GC[e], q[6]);                    // (C'^T G' C')_jj
+      }
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) cs[((size_t)g * NQ + u) * k + j] = q[u];
+    }
+    __syncthreads();
+    if (tid < k) {
+      const int j = tid;
+      double q[NQ];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        q[u] = cs[(size_t)u * k + j];
+        for (int g = 1; g < NG; ++g) q[u] += cs[((size_t)g * NQ + u) * k + j];
+      }
+      const double nt2 = q[0];
+      ws.ntop[j] = nt2;
+      const double e2 = (ws.rr2[j] - 2.0 * q[3] + q[4]) / (d[j] * d[j]);
+      s_red[0][j] = q[1] + ws.rr2[j];
+      s_red[1][j] = (ws.kjudge > 0 && j >= ws.kjudge) ? 0.0 : q[2] + e2;   // K > k: judge the leading kjudge
+      double mg = INFINITY;
+      for (int i = 0; i < k; ++i)
+        if (i != j) mg = fmin(mg, fabs(sd[j] - sd[i]));
+      s_red[2][j] = mg;
+      s_red[3][j] = (sig[j] < 0.0) ? 1.0 : 0.0;
+      // column norm of X~: top rows + the identity above -> 1 / ||x~_j||
+      const double dj = sd[j];
+      const double t1 = fma(dj, fma(dj, Gp[j * k + j], 2.0 * Mp[j * k + j]), ws.rr2[j]) / (dj * dj);
+      const double tail = t1 - 2.0 * q[5] / dj + q[6];
+      const double nrm = sqrt(nt2 + tail);
+      const double inv = ws.normalize ? 1.0 / nrm : 1.0;
+      if (!isfinite(inv) || !(nrm > 0.0)) atomicCAS(ws.status, ST_OK, ST_DIVERGED);
+      ws.invn[j] = inv;
+      ws.scal[j] = sig[j] / d[j] * inv;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double rr = 0.0, en = 0.0, mg = INFINITY, fl = 0.0, hits = 0.0, gmax = -1.0;
+      for (int j = 0; j < k; ++j) { rr += s_red[0][j]; en += s_red[1][j]; mg = fmin(mg, s_red[2][j]); fl += s_red[3][j]; }
+      for (int c = 0; c < ncl; ++c) {
+        hits += part[c];
+        if (ws.want_gram) gmax = fmax(gmax, part[8 + c]);
+      }
+      ws.stats[0] = sqrt(rr) / ws.normA;
+      ws.stats[1] = sqrt(fmax(en, 0.0));
+      ws.stats[2] = (k > 1) ? mg : 0.0;
+      ws.stats[3] = hits;
+      ws.stats[4] = (fl > 0.0) ? 1.0 : 0.0;
+      ws.stats[5] = rr;
+      ws.stats[6] = ws.want_gram ? gmax : -1.0;
+    }
+  }
+  cluster_sync();
+  if (crank == 0) RF_TSTAMP(ws, 31);
+  for (int i = r0 + (tid >> 5); i < r1; i += 32)
+    for (int j = tid & 31; j < k; j += 32) {
+    const int e = i * k + j;
+    const double inv = ws.invn[j];
     Xtop[e] = ws.Xt[e] * inv;                          // final top rows of X
     ws.Csig[e] *= inv;
   }
+  if (crank == 0) RF_TSTAMP(ws, 32);
 }
 
 // ---------------------------------------------------------------- rr_kxk (Rayleigh-Ritz, Sec. 3.4)

@@ -262,6 +262,27 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
   }
 }
 
+// kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs
+static void launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
+  if (kxk_cluster(ws.k) == 1) {   // (a plain launch is an implicit 1-CTA cluster)
+    kxk_finish_kernel<<<1, KXK_THREADS, FK_SMEM * 8, s>>>(ws, X, ws.W);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kxk_cluster(ws.k), 1, 1);
+  cfg.blockDim = dim3(KXK_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = FK_SMEM * 8;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kxk_cluster(ws.k);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kxk_finish_kernel, ws, X, (const double*)ws.W);
+}
+
 template <int KP>
 struct Kern {
   using TT = Tiles<KP>;
@@ -449,7 +470,7 @@ struct Kern {
         c->mark();
         if (c->rank == 0) {
           cudaStreamWaitEvent(s, c->ev_join, 0);
-          kxk_finish_kernel<<<1, KXK_THREADS, PANEL_SMEM * 8, s>>>(ws, X, ws.W);
+          launch_kxk_finish(ws, X, s);
           n += 1;
         }
         break;
@@ -525,7 +546,10 @@ static cudaError_t gather_geometry_un(refine_ctx* c, const std::vector<int32_t>&
   c->gather_un = UN;
   if (R > 0) {
     const int64_t chunks = (n + R - 1) / R;
-    c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sms * occ, chunks));
+    // rank 0 leaves one SM to kxk_lu (one 1024-thread CTA forked onto the side stream): a
+    // persistent grid sized to every SM would otherwise park one SM's CTAs behind it
+    const int sms = (c->rank == 0 && c->sms > 1) ? c->sms - 1 : c->sms;
+    c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, chunks));
   }
   return cudaSuccess;
 }
@@ -618,7 +642,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   RF_CK(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   RF_CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RF_CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-  RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
+  RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_SMEM * 8));
   RF_CK(c, cudaFuncSetAttribute(rr_kxk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
   // workspace sizes (doubles)
   size_t bpart = 0, brr = 0, nslot = 0;
@@ -636,7 +660,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oBrr = take(brr), oMg = take(2 * kk + k), oNs = take(nslot),
                oAl = take(k), oD = take(k), oRd = take(k), oSg = take(k), oU = take(kk), oL = take(kk),
                oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
-               oScr = take(16 * kk), oRows = take((size_t)c->n_loc), oRun = take(8),
+               oScr = take(16 * kk + KXK_SCRATCH_EXTRA), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
                oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k), oGate = take(1),
                oBd = take(c->opts.mixed ? (size_t)c->sms * 2 * c->kp : 0);

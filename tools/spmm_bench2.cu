@@ -85,7 +85,7 @@ static void gather_case(const char* name, const Prob& p, int sms, const double* 
   ws.ag = p.ag; ws.status = p.st;
   const int gx = sms * occ;
   cudaMemset(p.W, 0, p.n * p.k * 8);
-  float ms = timeit([&] { kern<<<gx, 256>>>(ws, p.rp, p.xoff, p.v, p.X, R); });
+  float ms = timeit([&] { kern<<<gx, 256>>>(ws, p.rp, p.xoff, p.v, p.X, R, p.X); });
   std::vector<double> a(p.n * p.k), b(p.n * p.k);
   cudaMemcpy(a.data(), p.W, a.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(b.data(), Wref, b.size() * 8, cudaMemcpyDeviceToHost);
