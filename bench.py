@@ -226,10 +226,10 @@ def time_rr(R, X, reps=3):
 
 
 def time_mixed(q, local, steps=5):
-    """NEXT-2 (opts.mixed, k = 128 only): the same sweep with passes B and C on tcgen05 in the
+    """NEXT-2 (opts.mixed, k a multiple of 16, >= 32): the same sweep with passes B and C on tcgen05 in the
     bf16x3 scheme; device-timed like the FP64 sweep (graph replay)."""
     import torch
-    if q.k != 128:
+    if q.k % 16 or q.k < 32:
         return None
     ms, kern, R, X, st, s, prof = time_ours(q, steps, 3, 1, local, opts={"mixed": True})
     out = {"sweeps_s": 1000.0 / ms, "ms_per_sweep": ms, "ms_per_sweep_instrumented": prof, "kernels_ms": kern,
@@ -398,7 +398,7 @@ def main():
             "roofline": roofline_for(p, kern, ms_prof or ms_max, fp64, hbm, n_loc=partition(p.n, world, rank)[1] - partition(p.n, world, rank)[0]),
             "gpu_launches": R.kernels_per_sweep() * args.steps}
     if world == 1:
-        mx = time_mixed(p, local, max(3, args.steps // 2)) if p.k == 128 else None
+        mx = time_mixed(p, local, max(3, args.steps // 2))
         if mx:
             line["mixed_next2"] = mx
         rr_ms, rr_s = time_rr(R, X)
@@ -427,8 +427,9 @@ def main():
                          "frac_of_sweep_roofline": max(qf / (fp64 * 1e12), qb / (hbm * 1e9)) / (qms * 1e-3)}
             del QR, QX
             torch.cuda.empty_cache()
-            if q.k == 128:
-                per[name]["mixed_next2"] = time_mixed(q, local)
+            mx = time_mixed(q, local)
+            if mx:
+                per[name]["mixed_next2"] = mx
             del q
             torch.cuda.empty_cache()
         line["per_config"] = per

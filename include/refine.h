@@ -106,7 +106,8 @@ typedef struct {
                             terms (three products, relative error ~1e-5 of an O(residual) quantity);
                             R = W - X D, the w scaling, every k x k step and all reductions stay FP64.
                             The sweep still converges to FP64 accuracy, at a per-sweep rate
-                            max(gamma, ~1e-5 kappa).  Requires k == 128 (else REFINE_E_UNSUPPORTED)
+                            max(gamma, ~1e-5 kappa).  Requires k a multiple of 16, k >= 32 (else
+                            REFINE_E_UNSUPPORTED)
                             and a 16-byte aligned X (else the FP64 passes run).  Rayleigh-Ritz and
                             reorthogonalisation steps always run in FP64 (their products are O(1)). */
 } refine_opts;

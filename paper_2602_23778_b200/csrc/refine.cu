@@ -313,7 +313,7 @@ struct Kern {
     if ((e = cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passC, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
-    if (KP == 128 && c->opts.mixed) {   // NEXT-2 tcgen05 passes (tc_passes.cuh)
+    if (KP >= 32 && c->opts.mixed) {   // NEXT-2 tcgen05 passes (tc_passes.cuh)
       if ((e = cudaFuncSetAttribute(passB_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCB_SMEM))) return e;
       if ((e = cudaFuncSetAttribute(passC_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCC_SMEM))) return e;
     }
@@ -361,16 +361,17 @@ struct Kern {
 
   static void sizes(refine_ctx* c, size_t& bpart, size_t& brr, size_t& nslot) {
     // the tcgen05 passes (opts.mixed) write one partial per SM in the same slot layouts
-    const size_t cb = (KP == 128 && c->opts.mixed) ? std::max(c->passb_grid_y, c->sms) : c->passb_grid_y;
-    const size_t cc = (KP == 128 && c->opts.mixed) ? std::max(c->passc_grid, c->sms) : c->passc_grid;
-    bpart = cb * B_NT * B_TILE;
+    const bool tc = KP >= 32 && c->opts.mixed;
+    const size_t cb = tc ? std::max(c->passb_grid_y, c->sms) : c->passb_grid_y;
+    const size_t cc = tc ? std::max(c->passc_grid, c->sms) : c->passc_grid;
+    bpart = std::max(cb * B_NT * B_TILE, tc ? (size_t)c->sms * 2 * KP * KP : 0);   // (tc: passB2 slot layout)
     brr = cb * KP;
     nslot = cc * KP;
   }
-  // NEXT-2: this sweep's passes B and C on tcgen05 (k == 128, not a Rayleigh-Ritz / QR step,
-  // 16-byte aligned X for the bulk copies)
+  // NEXT-2: this sweep's passes B and C on tcgen05 (k a multiple of 16 in [32, 128], not a
+  // Rayleigh-Ritz / QR step, 16-byte aligned X for the bulk copies)
   static bool use_tc(const refine_ctx* c, const double* X) {
-    return KP == 128 && c->opts.mixed && c->k == 128 && !c->in_rr && ((uintptr_t)X % 16 == 0);
+    return KP >= 32 && c->opts.mixed && c->k % 16 == 0 && !c->in_rr && ((uintptr_t)X % 16 == 0);
   }
 
   // phase ph of one sweep on this rank (see the file header); returns kernels launched
@@ -454,7 +455,8 @@ struct Kern {
           wb.bdiag = c->bdiag;   // + the FP64 diagonals of M2, G2
           passB_tc_kernel<<<c->sms, TCB_THREADS, TCB_SMEM, s>>>(wb, X);
           c->mark();
-          passB2_reduce_kernel<128><<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(wb, c->sms);
+          passB2_reduce_kernel<(KP >= 32 ? KP : 32)><<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(
+              wb, c->sms);
           n += 2;
           break;
         }
@@ -632,7 +634,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.beta_zero = c->opts.beta_zero;
   ws.kjudge = c->opts.kjudge;
   if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
-  if (c->opts.mixed && k != 128) return REFINE_E_UNSUPPORTED;                    // tcgen05 passes: k = 128
+  if (c->opts.mixed && (k % 16 != 0 || k < 32)) return REFINE_E_UNSUPPORTED;    // tcgen05 passes: 16 | k >= 32
   ws.world = world; ws.rank = rank;
   ws.multi = c->multi ? 1 : 0;
   ws.row0 = row_begin; ws.row1 = row_end;

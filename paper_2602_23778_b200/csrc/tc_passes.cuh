@@ -105,11 +105,12 @@ RF_DEV constexpr uint32_t kmaj_off(int r, int k, uint32_t sbo) {
   return (uint32_t)(r / 8) * sbo + (uint32_t)(k / 8) * 128u + (uint32_t)(r % 8) * 16u + (uint32_t)(k % 8) * 2u;
 }
 
-// ---------------------------------------------------------------- pass B on tcgen05 (k = 128)
+// ---------------------------------------------------------------- pass B on tcgen05 (k = 32 .. 128)
 // [M2 | G2] = X_2^T [R_2 | X_2] over rows >= top (R = W - X D formed in FP64, rr_j = sum r_ij^2 in
 // FP64), per CTA a contiguous row chunk; the CTA's FP64 partial goes to the passB2 slot layout
-// (bpart[(c * 4 + tile) * 128 * 64 + a * 64 + b % 64], brr[c * 128 + j]) so passB2_reduce_kernel<128>
-// sums the CTAs in fixed order.  One CTA per SM, warp-specialised:
+// (bpart[(c * NT + tile) * KP * 64 + a * 64 + b % 64] with [R | X] column b, X at KP, NT = 2 KP / 64;
+// brr[c * KP + j]) so passB2_reduce_kernel<KP> sums the CTAs in fixed order.  k % 16 == 0, k >= 32:
+// M = 128 (A = X^T, rows >= k zero), N = 2k.  One CTA per SM, warp-specialised:
 //   warp 8 (producer): bulk-copies the X and W rows of each 16-row stage (contiguous 16 KB each,
 //     cp.async.bulk completing on the slot's "full" mbarrier) into an NS-slot FP64 ring as soon as
 //     the converters release a slot ("empty" mbarrier): up to (NS - 1) x 32 KB in flight per SM;
@@ -157,10 +158,14 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
   const int nst = (re > rb) ? (int)((re - rb + TCB_TK - 1) / TCB_TK) : 0;
   const int nblk = (nst + TCB_SPB - 1) / TCB_SPB;
-  unsigned char* F = tcb_smem;                              // [NS][X rows | W rows] FP64
+  const int k = ws.k, KP = ws.kp, N = 2 * k;                 // k % 16 == 0, 32 <= k <= 128
+  unsigned char* F = tcb_smem;                              // [NS][X rows | W rows] FP64 (row stride k)
   unsigned char* OP = tcb_smem + TCB_NS * 2 * TCB_ROWB;     // [NO][A_hi | A_lo | B_hi | B_lo] bf16
-  double* part = ws.bpart + (int64_t)blockIdx.x * 4 * TCB_K * 64;
-  for (int j = tid; j < TCB_K; j += TCB_THREADS) sd[j] = ws.d[j];
+  double* part = ws.bpart + (int64_t)blockIdx.x * 2 * KP * KP;   // passB2 slot layout (TA = KP, TB = 64)
+  for (int j = tid; j < TCB_K; j += TCB_THREADS) sd[j] = j < k ? ws.d[j] : 0.0;
+  // A rows >= k (padding of M = 128) stay zero; the converters write rows < k only
+  for (int e = tid; e < TCB_NO * TCB_OPS / 16; e += TCB_THREADS) reinterpret_cast<uint4*>(OP)[e] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
                  "r"(2 * TCB_N));
@@ -189,11 +194,11 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
         const int s = t % TCB_NS;
         if (t >= TCB_NS) mbar_wait(&empty[s], ((t / TCB_NS) - 1) & 1);
         const int64_t r0 = rb + (int64_t)t * TCB_TK;
-        const uint32_t bytes = (uint32_t)min((int64_t)TCB_TK, re - r0) * TCB_K * 8;
+        const uint32_t bytes = (uint32_t)min((int64_t)TCB_TK, re - r0) * k * 8;
         unsigned char* f = F + s * 2 * TCB_ROWB;
         mbar_expect_tx(&full[s], 2 * bytes);
-        bulk_g2s(f, X + r0 * TCB_K, bytes, &full[s]);
-        bulk_g2s(f + TCB_ROWB, ws.W + r0 * TCB_K, bytes, &full[s]);
+        bulk_g2s(f, X + r0 * k, bytes, &full[s]);
+        bulk_g2s(f + TCB_ROWB, ws.W + r0 * k, bytes, &full[s]);
       }
     }
   } else if (warp > TCB_CONV / 32) {               // ---- drain: TMEM lanes 32 (warp % 4) ..
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
       mbar_wait(&accf[0], j & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < TCB_N; c0 += 16) {
+      for (int c0 = 0; c0 < N; c0 += 16) {
         float v[16], u[16];
         tmem_ld16(tl + c0, v);
         if (j > 0) {
@@ -218,23 +223,27 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
       if (lane == 0) mbar_arrive(&acce[0]);
     }
     if (nst == 0) {   // empty chunk: zero partial
-      for (int e = tid - (TCB_CONV + 32); e < 4 * TCB_K * 64; e += 128) part[e] = 0.0;
+      for (int e = tid - (TCB_CONV + 32); e < 2 * KP * KP; e += 128) part[e] = 0.0;
     } else {
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < TCB_N; c0 += 16) {
+      for (int c0 = 0; c0 < N; c0 += 16) {   // accumulator column c -> [R | X] column (X at KP)
         float v[16];
         tmem_ld16(tl + TCB_N + c0, v);
-        double* p = part + ((c0 >> 6) * TCB_K + m) * 64 + (c0 & 63);
+        const int pc = c0 < k ? c0 : KP + (c0 - k);
+        double* p = part + ((pc >> 6) * KP + m) * 64 + (pc & 63);
+        if (m < k) {
 #pragma unroll
-        for (int e = 0; e < 16; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(v[e], v[e + 1]);
+          for (int e = 0; e < 16; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(v[e], v[e + 1]);
+        }
       }
     }
   } else {                                          // ---- converters + MMA issue
-    const uint32_t idesc = umma_idesc_bf16(TCB_K, TCB_N);
+    const uint32_t idesc = umma_idesc_bf16(TCB_K, N);
     // thread -> column col and row quads q0, q0 + 2, ...: per warp instruction the FP64 reads are
     // two 128 B row segments and the 8 B operand stores two 128 B core-matrix rows (no conflicts)
     const int col = 16 * warp + (lane & 15), q0 = lane >> 4;
+    const bool act = col < k;
     const double dcol = sd[col];
     for (int t = 0; t < nst; ++t) {
       const int s = t % TCB_NS, o = t % TCB_NO;
@@ -242,19 +251,19 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
       if (t >= TCB_NO) mbar_wait(&mmad[o], ((t / TCB_NO) - 1) & 1);     // OP[o] free
       const int nr = (int)min((int64_t)TCB_TK, re - (rb + (int64_t)t * TCB_TK));
       const double* fx = reinterpret_cast<const double*>(F + s * 2 * TCB_ROWB);
-      const double* fw = fx + TCB_TK * TCB_K;
+      const double* fw = reinterpret_cast<const double*>(F + s * 2 * TCB_ROWB + TCB_ROWB);
       unsigned char* st = OP + o * TCB_OPS;
       unsigned char *Ahi = st, *Alo = st + TCB_A_BYTES, *Bhi = st + 2 * TCB_A_BYTES,
                     *Blo = st + 2 * TCB_A_BYTES + TCB_B_BYTES;
 #pragma unroll
-      for (int q = q0; q < TCB_TK / 4; q += 2) {
+      for (int q = q0; q < (act ? TCB_TK / 4 : 0); q += 2) {
         const int r = 4 * q;
         double x[4], qv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const bool v = r + j < nr;
-          x[j] = v ? fx[(r + j) * TCB_K + col] : 0.0;
-          const double w = v ? fw[(r + j) * TCB_K + col] : 0.0;
+          x[j] = v ? fx[(r + j) * k + col] : 0.0;
+          const double w = v ? fw[(r + j) * k + col] : 0.0;
           qv[j] = __fma_rn(-x[j], dcol, w);             // R = W - X D (FP64)
           rr = __fma_rn(qv[j], qv[j], rr);
           xr = __fma_rn(x[j], qv[j], xr);               // diagonals of M2, G2 in FP64
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
         split2_bf16(qv[0], qv[1], rh.x, rl.x);
         split2_bf16(qv[2], qv[3], rh.y, rl.y);
         const uint32_t oa = kmaj_off(col, r, TCB_SBO);             // A = X^T: (m = col, k = row); B rows 0.. = R
-        const uint32_t ob = kmaj_off(TCB_K + col, r, TCB_SBO);     // B rows 128.. = X
+        const uint32_t ob = kmaj_off(k + col, r, TCB_SBO);         // B rows k.. = X
         *reinterpret_cast<uint2*>(Ahi + oa) = xh;
         *reinterpret_cast<uint2*>(Alo + oa) = xl;
         *reinterpret_cast<uint2*>(Bhi + oa) = rh;
@@ -303,12 +312,12 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
     srr[2 * TCB_CONV + tid] = xx;
   }
   __syncthreads();
-  if (tid < TCB_K) {
+  if (tid < k) {
     const int t0 = 32 * (tid >> 4) + (tid & 15);
-    ws.brr[(int64_t)blockIdx.x * TCB_K + tid] = srr[t0] + srr[t0 + 16];
-    double* bd = ws.bdiag + (int64_t)blockIdx.x * 2 * TCB_K;
+    ws.brr[(int64_t)blockIdx.x * KP + tid] = srr[t0] + srr[t0 + 16];
+    double* bd = ws.bdiag + (int64_t)blockIdx.x * 2 * KP;
     bd[tid] = srr[TCB_CONV + t0] + srr[TCB_CONV + t0 + 16];
-    bd[TCB_K + tid] = srr[2 * TCB_CONV + t0] + srr[2 * TCB_CONV + t0 + 16];
+    bd[KP + tid] = srr[2 * TCB_CONV + t0] + srr[2 * TCB_CONV + t0 + 16];
   }
   tc_fence_before();
   __syncthreads();
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * TCB_N));
 }
 
-// ---------------------------------------------------------------- pass C on tcgen05 (k = 128)
+// ---------------------------------------------------------------- pass C on tcgen05 (k = 32 .. 128)
 // x~_i = w_i (Sigma D^-1) - x_i Csig for rows i >= top (eq. update-X through the implicit H, see
 // passC_kernel), with the product x_i Csig -- an O(residual) term, PAPER.md:504-507 -- on tcgen05
 // in the bf16x3 scheme and the w_i scaling, the subtraction and the column sums of squares in FP64.
@@ -378,16 +387,19 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
   unsigned char* Bhi = base + 2 * TCC_A_BYTES;
   unsigned char* Blo = Bhi + TCC_B_BYTES;
   unsigned char* F = Blo + TCC_B_BYTES;                              // [NS][64 X rows] FP64
-  // A = Csig^T: element (m = j, k = l) = Csig[l][j], split once
-  for (int e = tid; e < TCC_K * TCC_K / 2; e += TCC_THREADS) {
+  const int k = ws.k, KP = ws.kp;                    // k % 16 == 0, 32 <= k <= 128
+  const int KPAD = k <= 64 ? 64 : 128;               // K padded to whole 64-wide swizzle atoms
+  // A = Csig^T: element (m = j, k = l) = Csig[l][j] (ld k), split once; zero for j, l >= k
+  for (int e = tid; e < TCC_K * KPAD / 2; e += TCC_THREADS) {
     const int j = e % TCC_K, l = 2 * (e / TCC_K);
     uint32_t hi, lo;
-    split2_bf16(ws.Csig[l * TCC_K + j], ws.Csig[(l + 1) * TCC_K + j], hi, lo);
+    const bool ok = j < k && l < k;
+    split2_bf16(ok ? ws.Csig[l * k + j] : 0.0, ok ? ws.Csig[(l + 1) * k + j] : 0.0, hi, lo);
     const uint32_t off = sw128_off(j, l, TCC_K);
     *reinterpret_cast<uint32_t*>(Ahi + off) = hi;
     *reinterpret_cast<uint32_t*>(Alo + off) = lo;
   }
-  for (int j = tid; j < TCC_K; j += TCC_THREADS) ssc[j] = ws.scal[j];
+  for (int j = tid; j < TCC_K; j += TCC_THREADS) ssc[j] = j < k ? ws.scal[j] : 0.0;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
                  "r"(TCC_NT * TCC_TN));
@@ -417,9 +429,9 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
         const int s = t % TCC_NS;
         if (t >= TCC_NS) mbar_wait(&empty[s], ((t / TCC_NS) - 1) & 1);
         const int64_t r0 = rb + (int64_t)t * TCC_TN;
-        const uint32_t bytes = (uint32_t)min((int64_t)TCC_TN, re - r0) * TCC_K * 8;
+        const uint32_t bytes = (uint32_t)min((int64_t)TCC_TN, re - r0) * k * 8;
         mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(F + s * TCC_SLOT, X + r0 * TCC_K, bytes, &full[s]);
+        bulk_g2s(F + s * TCC_SLOT, X + r0 * k, bytes, &full[s]);
       }
     }
   } else if (warp < TCC_CONV / 32) {                // ---- converters + MMA issue
@@ -433,11 +445,10 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
       // warp w: rows w, w + 4, ...; lane: columns 2 lane, 2 lane + 1 and 64 + 2 lane, 65 + 2 lane
 #pragma unroll 4
       for (int r = warp; r < TCC_TN; r += TCC_CONV / 32) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < KPAD / 64; ++h) {
           const int l = 64 * h + 2 * lane;
           double2 v = make_double2(0.0, 0.0);
-          if (r < nr) v = *reinterpret_cast<const double2*>(fx + r * TCC_K + l);
+          if (r < nr && l < k) v = *reinterpret_cast<const double2*>(fx + r * k + l);
           uint32_t hi, lo;
           split2_bf16(v.x, v.y, hi, lo);
           const uint32_t off = sw128_off(r, l, TCC_TN);
@@ -457,7 +468,7 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
         const uint32_t td = tmem + (uint32_t)(a * TCC_TN);
         const uint32_t ah = smem_u32(Ahi), al = smem_u32(Alo), bh = smem_u32(Bhi), bl = smem_u32(Blo);
 #pragma unroll
-        for (int kk = 0; kk < TCC_K / 16; ++kk) {
+        for (int kk = 0; kk < KPAD / 16; ++kk) {
           const uint64_t dah = sw128_kdesc(ah, kk, TCC_K), dal = sw128_kdesc(al, kk, TCC_K);
           const uint64_t dbh = sw128_kdesc(bh, kk, TCC_TN), dbl = sw128_kdesc(bl, kk, TCC_TN);
           umma_bf16(td, dah, dbh, idesc, kk > 0);
@@ -470,6 +481,7 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
     }
   } else {                                          // ---- epilogue: column j, TMEM lane quarter warp % 4
     const int j = 32 * (warp & 3) + lane, rh = (warp - TCC_CONV / 32) / 4 * TCC_RPW;
+    const bool act = j < k;
     const double sj = ssc[j];
     const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)rh;
     for (int t = 0; t < nst; ++t) {
@@ -478,7 +490,7 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
       const int nr = (int)min((int64_t)TCC_RPW, re - r0);
       double w[TCC_RPW];
 #pragma unroll
-      for (int r = 0; r < TCC_RPW; ++r) w[r] = (r < nr) ? __ldcs(ws.W + (r0 + r) * TCC_K + j) : 0.0;
+      for (int r = 0; r < TCC_RPW; ++r) w[r] = (act && r < nr) ? __ldcs(ws.W + (r0 + r) * k + j) : 0.0;
       mbar_wait(&accf[a], (t / TCC_NT) & 1);
       tc_fence_after();
       float v[TCC_RPW];
@@ -489,9 +501,9 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
       if (lane == 0) mbar_arrive(&acce[a]);
 #pragma unroll
       for (int r = 0; r < TCC_RPW; ++r) {
-        if (r < nr) {
+        if (act && r < nr) {
           const double x = __fma_rn(w[r], sj, -(double)v[r]);
-          __stcs(out + (r0 + r) * TCC_K + j, x);
+          __stcs(out + (r0 + r) * k + j, x);
           nacc = __fma_rn(x, x, nacc);
         }
       }
@@ -501,11 +513,11 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
   double* snorm = reinterpret_cast<double*>(F);      // the ring is free now
   if (warp >= TCC_CONV / 32 && warp < (TCC_CONV + TCC_EPI) / 32) snorm[tid - TCC_CONV] = nacc;
   __syncthreads();
-  if (tid < TCC_K) {                                 // column j: epilogue warps (j / 32) + 4 h, lane j % 32
+  if (tid < k) {                                     // column j: epilogue warps (j / 32) + 4 h, lane j % 32
     double v = 0.0;
 #pragma unroll
     for (int h = 0; h < TCC_EPI / 128; ++h) v += snorm[128 * h + tid];
-    ws.nslot[(int64_t)blockIdx.x * TCC_K + tid] = v;
+    ws.nslot[(int64_t)blockIdx.x * KP + tid] = v;
   }
   tc_fence_before();
   __syncthreads();
