@@ -108,7 +108,9 @@ typedef struct {
                             The sweep still converges to FP64 accuracy, at a per-sweep rate
                             max(gamma, ~1e-5 kappa).  Requires k a multiple of 16, k >= 32 (else
                             REFINE_E_UNSUPPORTED)
-                            and a 16-byte aligned X (else the FP64 passes run).  Rayleigh-Ritz and
+                            and a 16-byte aligned X (else the FP64 passes run).  1: pass C (2k^2
+                            flop vs 24k bytes per row) uses the tensor cores only for k > 64 where the
+                            FP64 pass is compute bound; 2: both passes on tcgen05 at every k.  Rayleigh-Ritz and
                             reorthogonalisation steps always run in FP64 (their products are O(1)). */
 } refine_opts;
 

@@ -124,7 +124,7 @@ def _opts(delta_c=10.0, beta_zero=False, normalize=True, guard_window=3, guard_f
           resid_tol=0.0, reorth_tol=0.0, rr_fallback=False, mixed=False):
     return refine_opts(float(delta_c), int(bool(beta_zero)), int(bool(normalize)), int(guard_window),
                        float(guard_factor), int(bool(square)), int(kjudge), float(resid_tol), float(reorth_tol),
-                       int(bool(rr_fallback)), int(bool(mixed)))
+                       int(bool(rr_fallback)), int(mixed))
 
 
 @dataclass

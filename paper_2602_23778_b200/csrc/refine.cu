@@ -306,6 +306,7 @@ struct Kern {
   static constexpr int B_NT = B2 ? B2C::NT : BC::NTILES;
   static constexpr size_t B_TILE = B2 ? (size_t)B2C::TA * B2C::TB : (size_t)BTA * BTB;
   static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN>;
+  static constexpr int TKP = KP >= 32 ? KP : 32;   // tcgen05 passes (NEXT-2) exist for KP >= 32
   static_assert(CNC == KP, "pass C writes X in place: one CTA must own whole rows (all k columns)");
 
   static cudaError_t setup(refine_ctx* c) {
@@ -314,8 +315,10 @@ struct Kern {
     if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passC, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
     if (KP >= 32 && c->opts.mixed) {   // NEXT-2 tcgen05 passes (tc_passes.cuh)
-      if ((e = cudaFuncSetAttribute(passB_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCB_SMEM))) return e;
-      if ((e = cudaFuncSetAttribute(passC_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCC_SMEM))) return e;
+      if ((e = cudaFuncSetAttribute(passB_tc_kernel<TKP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    TcbCfg<TKP>::SMEM))) return e;
+      if ((e = cudaFuncSetAttribute(passC_tc_kernel<TKP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    TccCfg<TKP>::SMEM))) return e;
     }
     int occ = 1;
     // dense GEMM: split-K so the grid fills whole waves of resident CTAs
@@ -372,6 +375,12 @@ struct Kern {
   // Rayleigh-Ritz / QR step, 16-byte aligned X for the bulk copies)
   static bool use_tc(const refine_ctx* c, const double* X) {
     return KP >= 32 && c->opts.mixed && c->k % 16 == 0 && !c->in_rr && ((uintptr_t)X % 16 == 0);
+  }
+  // pass C on tcgen05 only where the FP64 pass is compute bound: 2k^2 flop vs 24k bytes per row
+  // crosses over at k ~ 68 on this part (DMMA 37 TFLOP/s, HBM 6.5 TB/s), so k <= 64 keeps the
+  // FP64 pass C (already at the HBM roofline); opts.mixed = 2 forces it (tests, measurements)
+  static bool use_tc_c(const refine_ctx* c, const double* X) {
+    return use_tc(c, X) && (c->k > 64 || c->opts.mixed >= 2);
   }
 
   // phase ph of one sweep on this rank (see the file header); returns kernels launched
@@ -453,7 +462,7 @@ struct Kern {
         if (use_tc(c, X)) {   // NEXT-2: X_2^T [R_2 | X_2] on tcgen05, one FP64 partial per SM
           Ws wb = ws;
           wb.bdiag = c->bdiag;   // + the FP64 diagonals of M2, G2
-          passB_tc_kernel<<<c->sms, TCB_THREADS, TCB_SMEM, s>>>(wb, X);
+          passB_tc_kernel<TKP><<<c->sms, TCB_THREADS, TcbCfg<TKP>::SMEM, s>>>(wb, X);
           c->mark();
           passB2_reduce_kernel<(KP >= 32 ? KP : 32)><<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(
               wb, c->sms);
@@ -480,8 +489,8 @@ struct Kern {
                // final X in place; Rayleigh-Ritz / QR steps write X~ and normalise in phase 5)
         c->mark();
         if (!c->in_rr) {
-          if (use_tc(c, X))   // NEXT-2: X_2 Csig on tcgen05
-            passC_tc_kernel<<<c->sms, TCC_THREADS, TCC_SMEM, s>>>(ws, X, X);
+          if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
+            passC_tc_kernel<TKP><<<c->sms, TCC_THREADS, TccCfg<TKP>::SMEM, s>>>(ws, X, X);
           else
             passC<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, X, xv16);
           n += 1;

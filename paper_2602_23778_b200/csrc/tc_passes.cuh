@@ -121,15 +121,23 @@ RF_DEV constexpr uint32_t kmaj_off(int r, int k, uint32_t sbo) {
 //     into a second FP32 sum (TMEM columns 256-511) with round-to-nearest CUDA-core adds (error
 //     control, header) and released for the next block; at the end the second sum is written to
 //     the CTA's FP64 partial.
-constexpr int TCB_K = 128, TCB_N = 256, TCB_TK = 16, TCB_NS = 5, TCB_NO = 2, TCB_CONV = 256;
+constexpr int TCB_K = 128, TCB_N = 256, TCB_NO = 2, TCB_CONV = 256;
 constexpr int TCB_THREADS = TCB_CONV + 32 + 128;
 constexpr int TCB_KC = 512;   // rows per TMEM block (tools/tcb_test.cu: 2048 -> 512 cuts the G error 2.6x, +1.6% time)
-constexpr int TCB_SPB = TCB_KC / TCB_TK;                           // stages per accumulator block
-constexpr uint32_t TCB_SBO = (TCB_TK / 8) * 128;                   // 256 B
-constexpr uint32_t TCB_A_BYTES = TCB_K * TCB_TK * 2, TCB_B_BYTES = TCB_N * TCB_TK * 2;
-constexpr uint32_t TCB_OPS = 2 * TCB_A_BYTES + 2 * TCB_B_BYTES;    // A_hi, A_lo, B_hi, B_lo: 24 KB
-constexpr uint32_t TCB_ROWB = TCB_TK * TCB_K * 8;                  // 16 KB of X (or W) rows per stage
-constexpr int TCB_SMEM = TCB_NS * 2 * TCB_ROWB + TCB_NO * TCB_OPS;  // 208 KB
+// Per padded width KP: TK rows per stage (a 16 KB FP64 slab of X, and one of W, at every KP), NS
+// ring slots, the UMMA operand buffer (A = X^T padded to M = 128 rows, B = [R | X] with N = 2k rows).
+template <int KP>
+struct TcbCfg {
+  static constexpr int TK = 16 * 128 / KP;                         // 16 / 32 / 64 rows
+  static constexpr int NS = KP == 32 ? 4 : 5;
+  static constexpr int SPB = TCB_KC / TK;                          // stages per accumulator block
+  static constexpr uint32_t SBO = (TK / 8) * 128;
+  static constexpr uint32_t A_BYTES = TCB_K * TK * 2, B_BYTES = 2 * KP * TK * 2;
+  static constexpr uint32_t OPS = 2 * A_BYTES + 2 * B_BYTES;       // A_hi, A_lo, B_hi, B_lo
+  static constexpr uint32_t ROWB = TK * KP * 8;                    // 16 KB
+  static constexpr int SMEM = NS * 2 * ROWB + TCB_NO * OPS;        // 208 / 224 / 224 KB
+  static constexpr int CB = KP / 16, QG = 8 / CB;                  // converter column blocks, quad groups
+};
 
 RF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -145,26 +153,29 @@ RF_DEV void mbar_arrive(uint64_t* mbar) {
 }
 RF_DEV void conv_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(TCB_CONV) : "memory"); }
 
+template <int KP>
 __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const double* __restrict__ X) {
+  using C = TcbCfg<KP>;
+  constexpr int TK = C::TK, NS = C::NS;
   extern __shared__ __align__(16) unsigned char tcb_smem[];
-  __shared__ __align__(8) uint64_t full[TCB_NS], empty[TCB_NS], mmad[TCB_NO], accf[2], acce[2];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS], mmad[TCB_NO], accf[2], acce[2];
   __shared__ uint32_t tmem_base;
-  __shared__ double sd[TCB_K];
+  __shared__ double sd[KP];
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t rows = ws.n_loc - ws.top;
-  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + TCB_TK - 1) / TCB_TK * TCB_TK;
+  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + TK - 1) / TK * TK;
   const int64_t rb = ws.top + (int64_t)blockIdx.x * per;
   const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
-  const int nst = (re > rb) ? (int)((re - rb + TCB_TK - 1) / TCB_TK) : 0;
-  const int nblk = (nst + TCB_SPB - 1) / TCB_SPB;
-  const int k = ws.k, KP = ws.kp, N = 2 * k;                 // k % 16 == 0, 32 <= k <= 128
+  const int nst = (re > rb) ? (int)((re - rb + TK - 1) / TK) : 0;
+  const int nblk = (nst + C::SPB - 1) / C::SPB;
+  const int k = ws.k, N = 2 * k;                            // k % 16 == 0, KP / 2 < k <= KP
   unsigned char* F = tcb_smem;                              // [NS][X rows | W rows] FP64 (row stride k)
-  unsigned char* OP = tcb_smem + TCB_NS * 2 * TCB_ROWB;     // [NO][A_hi | A_lo | B_hi | B_lo] bf16
+  unsigned char* OP = tcb_smem + NS * 2 * C::ROWB;          // [NO][A_hi | A_lo | B_hi | B_lo] bf16
   double* part = ws.bpart + (int64_t)blockIdx.x * 2 * KP * KP;   // passB2 slot layout (TA = KP, TB = 64)
-  for (int j = tid; j < TCB_K; j += TCB_THREADS) sd[j] = j < k ? ws.d[j] : 0.0;
+  for (int j = tid; j < KP; j += TCB_THREADS) sd[j] = j < k ? ws.d[j] : 0.0;
   // A rows >= k (padding of M = 128) stay zero; the converters write rows < k only
-  for (int e = tid; e < TCB_NO * TCB_OPS / 16; e += TCB_THREADS) reinterpret_cast<uint4*>(OP)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = tid; e < TCB_NO * (int)C::OPS / 16; e += TCB_THREADS) reinterpret_cast<uint4*>(OP)[e] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
@@ -172,7 +183,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int i = 0; i < TCB_NS; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], TCB_CONV / 32);
     }
@@ -191,14 +202,14 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   if (warp == TCB_CONV / 32) {                     // ---- producer
     if (lane == 0) {
       for (int t = 0; t < nst; ++t) {
-        const int s = t % TCB_NS;
-        if (t >= TCB_NS) mbar_wait(&empty[s], ((t / TCB_NS) - 1) & 1);
-        const int64_t r0 = rb + (int64_t)t * TCB_TK;
-        const uint32_t bytes = (uint32_t)min((int64_t)TCB_TK, re - r0) * k * 8;
-        unsigned char* f = F + s * 2 * TCB_ROWB;
+        const int s = t % NS;
+        if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+        const int64_t r0 = rb + (int64_t)t * TK;
+        const uint32_t bytes = (uint32_t)min((int64_t)TK, re - r0) * k * 8;
+        unsigned char* f = F + s * 2 * C::ROWB;
         mbar_expect_tx(&full[s], 2 * bytes);
         bulk_g2s(f, X + r0 * k, bytes, &full[s]);
-        bulk_g2s(f + TCB_ROWB, ws.W + r0 * k, bytes, &full[s]);
+        bulk_g2s(f + C::ROWB, ws.W + r0 * k, bytes, &full[s]);
       }
     }
   } else if (warp > TCB_CONV / 32) {               // ---- drain: TMEM lanes 32 (warp % 4) ..
@@ -240,23 +251,24 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
     }
   } else {                                          // ---- converters + MMA issue
     const uint32_t idesc = umma_idesc_bf16(TCB_K, N);
-    // thread -> column col and row quads q0, q0 + 2, ...: per warp instruction the FP64 reads are
-    // two 128 B row segments and the 8 B operand stores two 128 B core-matrix rows (no conflicts)
-    const int col = 16 * warp + (lane & 15), q0 = lane >> 4;
+    // thread -> column col = 16 (w % CB) + (l & 15) and row quads q0, q0 + 2 QG, ... (q0 = (l >> 4) +
+    // 2 (w / CB)): per warp instruction the FP64 reads are two 128 B row segments and the 8 B
+    // operand stores two 128 B core-matrix rows (no bank conflicts)
+    const int col = 16 * (warp % C::CB) + (lane & 15), q0 = (lane >> 4) + 2 * (warp / C::CB);
     const bool act = col < k;
     const double dcol = sd[col];
     for (int t = 0; t < nst; ++t) {
-      const int s = t % TCB_NS, o = t % TCB_NO;
-      mbar_wait(&full[s], (t / TCB_NS) & 1);                             // rows landed
+      const int s = t % NS, o = t % TCB_NO;
+      mbar_wait(&full[s], (t / NS) & 1);                                 // rows landed
       if (t >= TCB_NO) mbar_wait(&mmad[o], ((t / TCB_NO) - 1) & 1);     // OP[o] free
-      const int nr = (int)min((int64_t)TCB_TK, re - (rb + (int64_t)t * TCB_TK));
-      const double* fx = reinterpret_cast<const double*>(F + s * 2 * TCB_ROWB);
-      const double* fw = reinterpret_cast<const double*>(F + s * 2 * TCB_ROWB + TCB_ROWB);
-      unsigned char* st = OP + o * TCB_OPS;
-      unsigned char *Ahi = st, *Alo = st + TCB_A_BYTES, *Bhi = st + 2 * TCB_A_BYTES,
-                    *Blo = st + 2 * TCB_A_BYTES + TCB_B_BYTES;
+      const int nr = (int)min((int64_t)TK, re - (rb + (int64_t)t * TK));
+      const double* fx = reinterpret_cast<const double*>(F + s * 2 * C::ROWB);
+      const double* fw = reinterpret_cast<const double*>(F + s * 2 * C::ROWB + C::ROWB);
+      unsigned char* st = OP + o * C::OPS;
+      unsigned char *Ahi = st, *Alo = st + C::A_BYTES, *Bhi = st + 2 * C::A_BYTES,
+                    *Blo = st + 2 * C::A_BYTES + C::B_BYTES;
 #pragma unroll
-      for (int q = q0; q < (act ? TCB_TK / 4 : 0); q += 2) {
+      for (int q = q0; q < (act ? TK / 4 : 0); q += 2 * C::QG) {
         const int r = 4 * q;
         double x[4], qv[4];
 #pragma unroll
@@ -274,8 +286,8 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
         split2_bf16(x[2], x[3], xh.y, xl.y);
         split2_bf16(qv[0], qv[1], rh.x, rl.x);
         split2_bf16(qv[2], qv[3], rh.y, rl.y);
-        const uint32_t oa = kmaj_off(col, r, TCB_SBO);             // A = X^T: (m = col, k = row); B rows 0.. = R
-        const uint32_t ob = kmaj_off(k + col, r, TCB_SBO);         // B rows k.. = X
+        const uint32_t oa = kmaj_off(col, r, C::SBO);              // A = X^T: (m = col, k = row); B rows 0.. = R
+        const uint32_t ob = kmaj_off(k + col, r, C::SBO);          // B rows k.. = X
         *reinterpret_cast<uint2*>(Ahi + oa) = xh;
         *reinterpret_cast<uint2*>(Alo + oa) = xl;
         *reinterpret_cast<uint2*>(Bhi + oa) = rh;
@@ -289,35 +301,44 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
       tc_fence_before();
       conv_sync();
       if (tid == 0) {
-        const int j = t / TCB_SPB, ts = t % TCB_SPB;   // accumulator block j, stage ts within it
+        const int j = t / C::SPB, ts = t % C::SPB;     // accumulator block j, stage ts within it
         if (ts == 0 && j >= 1) mbar_wait(&acce[0], (j - 1) & 1);   // block j - 1 drained
         tc_fence_after();
-        const uint32_t td = tmem;
-        const uint32_t acc = ts > 0;
-        const uint64_t a_hi = umma_desc(smem_u32(Ahi), 128, TCB_SBO), a_lo = umma_desc(smem_u32(Alo), 128, TCB_SBO);
-        const uint64_t b_hi = umma_desc(smem_u32(Bhi), 128, TCB_SBO), b_lo = umma_desc(smem_u32(Blo), 128, TCB_SBO);
-        umma_bf16(td, a_hi, b_hi, idesc, acc);
-        umma_bf16(td, a_hi, b_lo, idesc, 1);
-        umma_bf16(td, a_lo, b_hi, idesc, 1);
+        const uint32_t a_hi = smem_u32(Ahi), a_lo = smem_u32(Alo), b_hi = smem_u32(Bhi), b_lo = smem_u32(Blo);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk) {
+          const uint32_t ko = kk * 256;                // 16 rows = 2 core matrices along K
+          const uint64_t dah = umma_desc(a_hi + ko, 128, C::SBO), dal = umma_desc(a_lo + ko, 128, C::SBO);
+          const uint64_t dbh = umma_desc(b_hi + ko, 128, C::SBO), dbl = umma_desc(b_lo + ko, 128, C::SBO);
+          umma_bf16(tmem, dah, dbh, idesc, (ts > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16(tmem, dah, dbl, idesc, 1);
+          umma_bf16(tmem, dal, dbh, idesc, 1);
+        }
         umma_commit(&mmad[o]);
-        if (ts == TCB_SPB - 1 || t == nst - 1) umma_commit(&accf[0]);
+        if (ts == C::SPB - 1 || t == nst - 1) umma_commit(&accf[0]);
       }
     }
   }
   __syncthreads();
   double* srr = reinterpret_cast<double*>(tcb_smem);     // the FP64 ring is free now
-  if (tid < TCB_CONV) {                                  // column 16 w + (l & 15) from lanes l, l + 16
+  if (tid < TCB_CONV) {
     srr[tid] = rr;
     srr[TCB_CONV + tid] = xr;
     srr[2 * TCB_CONV + tid] = xx;
   }
   __syncthreads();
-  if (tid < k) {
-    const int t0 = 32 * (tid >> 4) + (tid & 15);
-    ws.brr[(int64_t)blockIdx.x * KP + tid] = srr[t0] + srr[t0 + 16];
+  if (tid < k) {   // column j: warps (j / 16) + CB g (g < QG), lanes (j % 16) and (j % 16) + 16, fixed order
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int g = 0; g < C::QG; ++g) {
+      const int t0 = 32 * ((tid >> 4) + C::CB * g) + (tid & 15);
+      a0 += srr[t0] + srr[t0 + 16];
+      a1 += srr[TCB_CONV + t0] + srr[TCB_CONV + t0 + 16];
+      a2 += srr[2 * TCB_CONV + t0] + srr[2 * TCB_CONV + t0 + 16];
+    }
+    ws.brr[(int64_t)blockIdx.x * KP + tid] = a0;
     double* bd = ws.bdiag + (int64_t)blockIdx.x * 2 * KP;
-    bd[tid] = srr[TCB_CONV + t0] + srr[TCB_CONV + t0 + 16];
-    bd[KP + tid] = srr[2 * TCB_CONV + t0] + srr[2 * TCB_CONV + t0 + 16];
+    bd[tid] = a1;
+    bd[KP + tid] = a2;
   }
   tc_fence_before();
   __syncthreads();
@@ -329,24 +350,30 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
 // x~_i = w_i (Sigma D^-1) - x_i Csig for rows i >= top (eq. update-X through the implicit H, see
 // passC_kernel), with the product x_i Csig -- an O(residual) term, PAPER.md:504-507 -- on tcgen05
 // in the bf16x3 scheme and the w_i scaling, the subtraction and the column sums of squares in FP64.
-// Transposed product per 64-row slot: D (128 x 64, TMEM lanes = output columns j, TMEM columns =
-// the slot's rows) = Csig^T (A, 128 x 128, split once per CTA, resident) . X_slot^T (B, N = 64).
-// The M = 128 MMAs are bound by the SMEM read of A (tools/umma_sw_test.cu: ~48 cycles per MMA at
-// N <= 64), so N = 64 rows per MMA.  Operands use the 128-byte-swizzled K-major layout, which
-// also makes the converters' row-contiguous 4-byte stores conflict-free.
+// Transposed product per 64-column MMA: D (128 x 64, TMEM lanes = output columns, TMEM columns =
+// slab rows) = A . B^T with K = 128.  k <= 64 packs G = 128 / KP row groups into one MMA: B row n =
+// [x_{n} | x_{64 + n} | ...] (each KP wide, zero padded) and A = blockdiag(Csig^T, ..., Csig^T),
+// so TMEM lane quarter g * KP / 32 .. holds the products of rows g * 64 + n (all 4 lane quarters
+// and all epilogue warps stay busy at every k).  The M = 128 MMAs are bound by the SMEM read of A
+// (tools/umma_sw_test.cu: ~48 cycles per MMA at N <= 64), so a slab is 64 G rows (64 KB of X).
+// Operands use the 128-byte-swizzled K-major layout (row-contiguous 4-byte stores conflict-free).
 // One CTA per SM, a contiguous row chunk per CTA, warp-specialised:
-//   warp 12 (producer): one bulk copy per 64-row X slot (contiguous) into a 2-slot FP64 ring;
-//   warps 0-3 (converters): bf16 hi/lo splits of the X slot into the UMMA B buffer; thread 0
-//     issues 3 x 8 tcgen05.mma (M = 128, N = 64, K = 16) into the slot's TMEM columns;
-//   warps 4-11 (epilogue, TMEM lane quarter = warp % 4, 32 rows each): the W entries are loaded
-//     (coalesced) before waiting for the MMA; tcgen05.ld of the rows of column j,
-//     x~ = fma(w, s_j, -D), coalesced stores of X~, FP64 column sums of squares.
-constexpr int TCC_K = 128, TCC_TN = 64, TCC_NS = 2, TCC_NT = 4;
+//   warp 12 (producer): one bulk copy per slab (contiguous X rows) into a 2-slot FP64 ring;
+//   warps 0-3 (converters): bf16 hi/lo splits of the slab into the UMMA B buffer; thread 0
+//     issues 3 x 8 tcgen05.mma (M = 128, N = 64, K = 16) into the slab's TMEM columns;
+//   warps 4-11 (epilogue, TMEM lane quarter = warp % 4, 32 columns each): the W entries are loaded
+//     (coalesced) before waiting for the MMA; tcgen05.ld, x~ = fma(w, s_j, -D), coalesced
+//     stores of X~, FP64 column sums of squares.
+constexpr int TCC_K = 128, TCC_NS = 2, TCC_TN = 64, TCC_NT = 4, TCC_RPW = 32;
 constexpr int TCC_CONV = 128, TCC_EPI = 256, TCC_THREADS = TCC_CONV + TCC_EPI + 32;
-constexpr int TCC_RPW = TCC_TN / (TCC_EPI / 128);            // slot rows per epilogue warp
-constexpr uint32_t TCC_SLOT = TCC_TN * TCC_K * 8;              // 64 KB of X rows
 constexpr uint32_t TCC_A_BYTES = TCC_K * TCC_K * 2, TCC_B_BYTES = TCC_TN * TCC_K * 2;
-constexpr int TCC_SMEM = 1024 + 2 * TCC_A_BYTES + 2 * TCC_B_BYTES + TCC_NS * TCC_SLOT;   // 225 KB
+template <int KP>
+struct TccCfg {
+  static constexpr int G = 128 / KP;                               // row groups packed along K
+  static constexpr int SROWS = TCC_TN * G;                         // slab rows: 64 / 128 / 256
+  static constexpr uint32_t SLOT = SROWS * KP * 8;                 // 64 KB of X rows
+  static constexpr int SMEM = 1024 + 2 * TCC_A_BYTES + 2 * TCC_B_BYTES + TCC_NS * SLOT;   // 225 KB
+};
 
 // 128-byte swizzle, K-major: element (r, k) of an R-row bf16 operand (64-wide K atoms, 8-row groups
 // 1024 B apart, the 16-byte chunk index XOR row % 8); atoms 1024-byte aligned
@@ -369,37 +396,40 @@ RF_DEV uint64_t sw128_kdesc(uint32_t base, int kk, int R) {
 }
 RF_DEV void conv_sync_c() { asm volatile("bar.sync 1, %0;\n" ::"n"(TCC_CONV) : "memory"); }
 
+template <int KP>
 __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const double* X, double* out) {
+  using C = TccCfg<KP>;
+  constexpr int G = C::G, SROWS = C::SROWS;
   extern __shared__ __align__(16) unsigned char tcc_raw[];
   __shared__ __align__(8) uint64_t full[TCC_NS], empty[TCC_NS], opfree, accf[TCC_NT], acce[TCC_NT];
   __shared__ uint32_t tmem_base;
-  __shared__ double ssc[TCC_K];
+  __shared__ double ssc[KP];
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = ws.k;                                // k % 16 == 0, KP / 2 < k <= KP
   const int64_t rows = ws.n_loc - ws.top;
-  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + TCC_TN - 1) / TCC_TN * TCC_TN;
+  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + SROWS - 1) / SROWS * SROWS;
   const int64_t rb = ws.top + (int64_t)blockIdx.x * per;
   const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
-  const int nst = (re > rb) ? (int)((re - rb + TCC_TN - 1) / TCC_TN) : 0;
+  const int nst = (re > rb) ? (int)((re - rb + SROWS - 1) / SROWS) : 0;
   unsigned char* base = tcc_raw + ((1024 - (smem_u32(tcc_raw) & 1023)) & 1023);   // 1024-B aligned
   unsigned char* Ahi = base;
   unsigned char* Alo = base + TCC_A_BYTES;
   unsigned char* Bhi = base + 2 * TCC_A_BYTES;
   unsigned char* Blo = Bhi + TCC_B_BYTES;
-  unsigned char* F = Blo + TCC_B_BYTES;                              // [NS][64 X rows] FP64
-  const int k = ws.k, KP = ws.kp;                    // k % 16 == 0, 32 <= k <= 128
-  const int KPAD = k <= 64 ? 64 : 128;               // K padded to whole 64-wide swizzle atoms
-  // A = Csig^T: element (m = j, k = l) = Csig[l][j] (ld k), split once; zero for j, l >= k
-  for (int e = tid; e < TCC_K * KPAD / 2; e += TCC_THREADS) {
-    const int j = e % TCC_K, l = 2 * (e / TCC_K);
+  unsigned char* F = Blo + TCC_B_BYTES;                              // [NS][slab rows] FP64 (row stride k)
+  // A = blockdiag(Csig^T): element (m = g KP + j, l = g KP + l') = Csig[l'][j] (ld k), split once
+  for (int e = tid; e < TCC_K * TCC_K / 2; e += TCC_THREADS) {
+    const int m = e % TCC_K, l = 2 * (e / TCC_K);
+    const int j = m % KP, lp = l % KP;
+    const bool ok = (m / KP == l / KP) && j < k && lp < k;
     uint32_t hi, lo;
-    const bool ok = j < k && l < k;
-    split2_bf16(ok ? ws.Csig[l * k + j] : 0.0, ok ? ws.Csig[(l + 1) * k + j] : 0.0, hi, lo);
-    const uint32_t off = sw128_off(j, l, TCC_K);
+    split2_bf16(ok ? ws.Csig[lp * k + j] : 0.0, ok ? ws.Csig[(lp + 1) * k + j] : 0.0, hi, lo);
+    const uint32_t off = sw128_off(m, l, TCC_K);
     *reinterpret_cast<uint32_t*>(Ahi + off) = hi;
     *reinterpret_cast<uint32_t*>(Alo + off) = lo;
   }
-  for (int j = tid; j < TCC_K; j += TCC_THREADS) ssc[j] = j < k ? ws.scal[j] : 0.0;
+  for (int j = tid; j < KP; j += TCC_THREADS) ssc[j] = j < k ? ws.scal[j] : 0.0;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
                  "r"(TCC_NT * TCC_TN));
@@ -428,10 +458,10 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
       for (int t = 0; t < nst; ++t) {
         const int s = t % TCC_NS;
         if (t >= TCC_NS) mbar_wait(&empty[s], ((t / TCC_NS) - 1) & 1);
-        const int64_t r0 = rb + (int64_t)t * TCC_TN;
-        const uint32_t bytes = (uint32_t)min((int64_t)TCC_TN, re - r0) * k * 8;
+        const int64_t r0 = rb + (int64_t)t * SROWS;
+        const uint32_t bytes = (uint32_t)min((int64_t)SROWS, re - r0) * k * 8;
         mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(F + s * TCC_SLOT, X + r0 * k, bytes, &full[s]);
+        bulk_g2s(F + s * C::SLOT, X + r0 * k, bytes, &full[s]);
       }
     }
   } else if (warp < TCC_CONV / 32) {                // ---- converters + MMA issue
@@ -439,25 +469,30 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
     for (int t = 0; t < nst; ++t) {
       const int s = t % TCC_NS;
       mbar_wait(&full[s], (t / TCC_NS) & 1);
-      if (t >= 1) mbar_wait(&opfree, (t - 1) & 1);   // the previous slot's MMAs have read B
-      const int nr = (int)min((int64_t)TCC_TN, re - (rb + (int64_t)t * TCC_TN));
-      const double* fx = reinterpret_cast<const double*>(F + s * TCC_SLOT);
-      // warp w: rows w, w + 4, ...; lane: columns 2 lane, 2 lane + 1 and 64 + 2 lane, 65 + 2 lane
+      if (t >= 1) mbar_wait(&opfree, (t - 1) & 1);   // the previous slab's MMAs have read B
+      const int nr = (int)min((int64_t)SROWS, re - (rb + (int64_t)t * SROWS));
+      const double* fx = reinterpret_cast<const double*>(F + s * C::SLOT);
+      // warp w: slab rows w, w + 4, ... (row r -> B row r % 64, K columns (r / 64) KP + l');
+      // lane: l' = 2 lane (+ 64 for KP = 128)
 #pragma unroll 4
-      for (int r = warp; r < TCC_TN; r += TCC_CONV / 32) {
-        for (int h = 0; h < KPAD / 64; ++h) {
-          const int l = 64 * h + 2 * lane;
-          double2 v = make_double2(0.0, 0.0);
-          if (r < nr && l < k) v = *reinterpret_cast<const double2*>(fx + r * k + l);
-          uint32_t hi, lo;
-          split2_bf16(v.x, v.y, hi, lo);
-          const uint32_t off = sw128_off(r, l, TCC_TN);
-          *reinterpret_cast<uint32_t*>(Bhi + off) = hi;
-          *reinterpret_cast<uint32_t*>(Blo + off) = lo;
+      for (int r = warp; r < SROWS; r += TCC_CONV / 32) {
+        const int n = r % TCC_TN, g = r / TCC_TN;
+#pragma unroll
+        for (int h = 0; h < (KP + 63) / 64; ++h) {
+          const int lp = 64 * h + 2 * lane;
+          if (lp < KP) {
+            double2 v = make_double2(0.0, 0.0);
+            if (r < nr && lp < k) v = *reinterpret_cast<const double2*>(fx + r * k + lp);
+            uint32_t hi, lo;
+            split2_bf16(v.x, v.y, hi, lo);
+            const uint32_t off = sw128_off(n, g * KP + lp, TCC_TN);
+            *reinterpret_cast<uint32_t*>(Bhi + off) = hi;
+            *reinterpret_cast<uint32_t*>(Blo + off) = lo;
+          }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);        // X rows of the slot consumed
+      if (lane == 0) mbar_arrive(&empty[s]);        // X rows of the slab consumed
       fence_async_smem();
       tc_fence_before();
       conv_sync_c();
@@ -468,7 +503,7 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
         const uint32_t td = tmem + (uint32_t)(a * TCC_TN);
         const uint32_t ah = smem_u32(Ahi), al = smem_u32(Alo), bh = smem_u32(Bhi), bl = smem_u32(Blo);
 #pragma unroll
-        for (int kk = 0; kk < KPAD / 16; ++kk) {
+        for (int kk = 0; kk < TCC_K / 16; ++kk) {
           const uint64_t dah = sw128_kdesc(ah, kk, TCC_K), dal = sw128_kdesc(al, kk, TCC_K);
           const uint64_t dbh = sw128_kdesc(bh, kk, TCC_TN), dbl = sw128_kdesc(bl, kk, TCC_TN);
           umma_bf16(td, dah, dbh, idesc, kk > 0);
@@ -479,14 +514,15 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
         umma_commit(&accf[a]);
       }
     }
-  } else {                                          // ---- epilogue: column j, TMEM lane quarter warp % 4
-    const int j = 32 * (warp & 3) + lane, rh = (warp - TCC_CONV / 32) / 4 * TCC_RPW;
+  } else {                                          // ---- epilogue: TMEM lane m = 32 (warp % 4) + lane
+    const int m = 32 * (warp & 3) + lane, g = m / KP, j = m % KP;
+    const int rh = (warp - TCC_CONV / 32) / 4 * TCC_RPW;
     const bool act = j < k;
     const double sj = ssc[j];
     const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)rh;
     for (int t = 0; t < nst; ++t) {
       const int a = t % TCC_NT;
-      const int64_t r0 = rb + (int64_t)t * TCC_TN + rh;
+      const int64_t r0 = rb + (int64_t)t * SROWS + g * TCC_TN + rh;   // slab rows of TMEM columns rh ..
       const int nr = (int)min((int64_t)TCC_RPW, re - r0);
       double w[TCC_RPW];
 #pragma unroll
@@ -513,10 +549,11 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
   double* snorm = reinterpret_cast<double*>(F);      // the ring is free now
   if (warp >= TCC_CONV / 32 && warp < (TCC_CONV + TCC_EPI) / 32) snorm[tid - TCC_CONV] = nacc;
   __syncthreads();
-  if (tid < k) {                                     // column j: epilogue warps (j / 32) + 4 h, lane j % 32
+  if (tid < k) {   // column j: lanes m = g KP + j of both row halves, groups and halves in fixed order
     double v = 0.0;
+    for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int h = 0; h < TCC_EPI / 128; ++h) v += snorm[128 * h + tid];
+      for (int h = 0; h < TCC_EPI / 128; ++h) v += snorm[128 * h + g * KP + tid];
     ws.nslot[(int64_t)blockIdx.x * KP + tid] = v;
   }
   tc_fence_before();

@@ -63,7 +63,7 @@ def test_mixed_one_step_vs_oracle(pkg, kind, n, k):
     of 1e-5 of the correction (the sweep's sign flips X^ = X Sigma removed first) plus the FP64
     parity floor; the FP64-decided quantities (flips, delta hits, the residual) are equal."""
     p = make(kind, n, k)
-    R = refiner(pkg, p, mixed=True)
+    R = refiner(pkg, p, mixed=2)              # both passes on tcgen05 at every k
     op = op_of(p)
     X = p.X0.cuda().clone()
     worst = 0.0
@@ -96,7 +96,7 @@ def test_mixed_converges_to_fp64_accuracy(pkg):
     p = synth.small_dense(n, k, m=8, lam_target=lt, rest=1.0, noise=1e-6, seed=19)
     res = {}
     for mixed in (False, True):
-        R = refiner(pkg, p, mixed=mixed)
+        R = refiner(pkg, p, mixed=2 if mixed else 0)
         X = p.X0.cuda().clone()
         s, it, st = R.refine_run(X, 60, 1e-13)
         assert s == pkg.REFINE_OK, (mixed, s)
@@ -152,7 +152,7 @@ def test_mixed_converges_k32(pkg):
     p = synth.small_dense(2000, k, m=8, lam_target=lt, rest=1.0, noise=1e-6, seed=23)
     res = {}
     for mixed in (False, True):
-        R = refiner(pkg, p, mixed=mixed)
+        R = refiner(pkg, p, mixed=2 if mixed else 0)
         X = p.X0.cuda().clone()
         s, it, st = R.refine_run(X, 60, 1e-13)
         assert s == pkg.REFINE_OK, (mixed, s)

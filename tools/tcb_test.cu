@@ -45,14 +45,14 @@ int main(int argc, char** argv) {
   cudaEventSynchronize(b);
   float ms1; cudaEventElapsedTime(&ms1, a, b);
   // tcgen05
-  cudaFuncSetAttribute(passB_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCB_SMEM);
+  cudaFuncSetAttribute(passB_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcbCfg<128>::SMEM);
   ws.M2 = out2; ws.G2 = out2 + k * k; ws.rr2 = out2 + 2 * k * k;
   ws.bdiag = bd;   // FP64 diagonals of M2, G2
-  passB_tc_kernel<<<sms, TCB_THREADS, TCB_SMEM>>>(ws, X);
+  passB_tc_kernel<128><<<sms, TCB_THREADS, TcbCfg<128>::SMEM>>>(ws, X);
   cudaError_t e = cudaDeviceSynchronize();
   printf("first tc launch: %s\n", cudaGetErrorString(e));
   cudaEventRecord(a);
-  passB_tc_kernel<<<sms, TCB_THREADS, TCB_SMEM>>>(ws, X);
+  passB_tc_kernel<128><<<sms, TCB_THREADS, TcbCfg<128>::SMEM>>>(ws, X);
   cudaEventRecord(b);
   passB2_reduce_kernel<128><<<(2 * k * k + k + 31) / 32, PB_RED_THREADS>>>(ws, sms);
   cudaEventSynchronize(b);

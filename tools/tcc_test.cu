@@ -47,13 +47,13 @@ int main(int argc, char** argv) {
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms1; cudaEventElapsedTime(&ms1, a, b);
-  cudaFuncSetAttribute(passC_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TCC_SMEM);
+  cudaFuncSetAttribute(passC_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TccCfg<128>::SMEM);
   ws.Xt = Xt2; ws.nslot = ns2;
-  passC_tc_kernel<<<sms, TCC_THREADS, TCC_SMEM>>>(ws, X, Xt2);
+  passC_tc_kernel<128><<<sms, TCC_THREADS, TccCfg<128>::SMEM>>>(ws, X, Xt2);
   cudaError_t e = cudaDeviceSynchronize();
   printf("first tc launch: %s\n", cudaGetErrorString(e));
   cudaEventRecord(a);
-  passC_tc_kernel<<<sms, TCC_THREADS, TCC_SMEM>>>(ws, X, Xt2);
+  passC_tc_kernel<128><<<sms, TCC_THREADS, TccCfg<128>::SMEM>>>(ws, X, Xt2);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   e = cudaDeviceSynchronize();
