@@ -178,3 +178,34 @@ def test_mixed_unaligned_x_runs_fp64(pkg):
     assert s == pkg.REFINE_OK
     ref = oracle.sweep(op_of(p), xin)
     assert fro(X.cpu().numpy() - ref.X) <= 1e-10 * fro(ref.X)
+
+
+@pytest.mark.parametrize("kind,world", [("dense", 3), ("csr3d", 4)])
+def test_mixed_loopback_ranks(pkg, kind, world):
+    """The mixed sweep on emulated ranks (row partition, gathered k x k partials) agrees with the
+    single-rank mixed sweep to the mixed tolerance (per-rank chunking changes the bf16x3 sums)."""
+    p = make(kind, 1100 if kind == "dense" else None, 128)
+    X1, Xp = p.X0.cuda().clone(), p.X0.cuda().clone()
+    xin = p.X0.numpy()
+    s1, _ = refiner(pkg, p, mixed=1).refine_sweep(X1, stats=True)
+    s2, _ = refiner(pkg, p, mixed=1, world=world).refine_sweep(Xp, stats=True)
+    assert s1 == s2 == pkg.REFINE_OK
+    a, b = X1.cpu().numpy(), Xp.cpu().numpy()
+    sig = np.where(np.sum(a * xin, axis=0) < 0, -1.0, 1.0)
+    corr = fro(a - xin * sig)
+    assert fro(a - b) <= 1e-2 * corr + 1e-10 * fro(a)
+
+
+def test_mixed_sweep_rr(pkg):
+    """Rayleigh-Ritz (FP64) followed by the top-zero sweep in mixed precision vs the oracle."""
+    p = make("dense", 1100, 128)
+    R = refiner(pkg, p, mixed=1)
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, st, ritz = R.refine_sweep_rr(X)
+    ref, ro = oracle.sweep_rr(op_of(p), xin)
+    assert s == pkg.REFINE_OK and ref.status == oracle.OK
+    assert np.abs(ritz - ro).max() <= 1e-12 * np.abs(ro).max()
+    Xo = ref.X
+    sig = np.where(np.sum(Xo * X.cpu().numpy(), axis=0) < 0, -1.0, 1.0)
+    assert fro(X.cpu().numpy() * sig - Xo) <= 1e-6 * fro(Xo)
