@@ -240,6 +240,22 @@ def time_mixed(q, local, steps=5):
     return out
 
 
+def time_emul(q, local, steps=5):
+    """Dense S1 with FP64 accuracy on the INT8 tensor cores (refine_opts.emul, ozaki.cuh; k a
+    multiple of 16, <= 64): the same sweep, device-timed (graph replay)."""
+    import torch
+    if q.kind != "dense" or q.k % 16 or q.k > 64:
+        return None
+    ms, kern, R, X, st, s, prof = time_ours(q, steps, 3, 1, local, opts={"emul": True})
+    out = {"sweeps_s": 1000.0 / ms, "ms_per_sweep": ms, "ms_per_sweep_instrumented": prof, "kernels_ms": kern,
+           "status": s, "what": "refine_opts.emul: W = A X^ from 8 x 7-bit int8 slices of A (rows, once) and X^ "
+           "(columns, per sweep) on tcgen05.mma kind::i8 with exact int32 level sums combined in FP64 "
+           "(diagonal in FP64); the gemm_ax slot includes the per-sweep X slicing"}
+    del R, X
+    torch.cuda.empty_cache()
+    return out
+
+
 def time_e2e(R, p, steps, warmup, world=1, rank=0):
     """Host buffers through the C ABI: H2D of X^, sweep, D2H of the result, each step."""
     import torch
@@ -401,6 +417,9 @@ def main():
         mx = time_mixed(p, local, max(3, args.steps // 2))
         if mx:
             line["mixed_next2"] = mx
+        em = time_emul(p, local, max(3, args.steps // 2))
+        if em:
+            line["emul_ozaki"] = em
         rr_ms, rr_s = time_rr(R, X)
         line["rayleigh_ritz"] = {"ms": rr_ms, "status": rr_s, "what": "refine_rayleigh_ritz (NEXT-1, Sec. 3.4): "
                                  "S1 + pass B (D = 0) + k x k Cholesky/Jacobi + pass C + normalise"}
@@ -430,6 +449,9 @@ def main():
             mx = time_mixed(q, local)
             if mx:
                 per[name]["mixed_next2"] = mx
+            em = time_emul(q, local)
+            if em:
+                per[name]["emul_ozaki"] = em
             del q
             torch.cuda.empty_cache()
         line["per_config"] = per

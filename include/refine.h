@@ -112,6 +112,15 @@ typedef struct {
                             flop vs 24k bytes per row) uses the tensor cores only for k > 64 where the
                             FP64 pass is compute bound; 2: both passes on tcgen05 at every k.  Rayleigh-Ritz and
                             reorthogonalisation steps always run in FP64 (their products are O(1)). */
+  int32_t emul;          /* dense A only: 1 = S1 (W = A X^) with FP64 accuracy on the INT8 tensor cores
+                            (Ozaki splitting, ozaki.cuh): A's rows are scaled to their max and cut into
+                            8 int8 slices of 7 bits ONCE at init (n_loc x n x 8 bytes extra device
+                            memory), X^'s columns likewise every sweep; the slice products are exact
+                            int32 sums on tcgen05.mma kind::i8, combined in FP64.  Truncation error
+                            <= 2^-56 max|A_i.| max|X_.j| per product term: relative to the row and
+                            column MAXIMA (rows with a very wide dynamic range should use DMMA).
+                            0 (default) = DMMA FP64.
+                            Requires k a multiple of 16, k <= 64 (else REFINE_E_UNSUPPORTED). */
 } refine_opts;
 
 /* Per-sweep diagnostics (host struct), for the sweep's input X^ (after the sign flip). */

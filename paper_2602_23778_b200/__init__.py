@@ -35,7 +35,7 @@ class refine_opts(C.Structure):
     _fields_ = [("delta_c", C.c_double), ("beta_zero", C.c_int32), ("normalize", C.c_int32),
                 ("guard_window", C.c_int32), ("guard_factor", C.c_double), ("square", C.c_int32),
                 ("kjudge", C.c_int32), ("resid_tol", C.c_double), ("reorth_tol", C.c_double),
-                ("rr_fallback", C.c_int32), ("mixed", C.c_int32)]
+                ("rr_fallback", C.c_int32), ("mixed", C.c_int32), ("emul", C.c_int32)]
 
 
 class refine_sweep_stats(C.Structure):
@@ -121,10 +121,10 @@ def _check_dev(t, dtype, name):
 
 
 def _opts(delta_c=10.0, beta_zero=False, normalize=True, guard_window=3, guard_factor=10.0, square=False, kjudge=0,
-          resid_tol=0.0, reorth_tol=0.0, rr_fallback=False, mixed=False):
+          resid_tol=0.0, reorth_tol=0.0, rr_fallback=False, mixed=False, emul=False):
     return refine_opts(float(delta_c), int(bool(beta_zero)), int(bool(normalize)), int(guard_window),
                        float(guard_factor), int(bool(square)), int(kjudge), float(resid_tol), float(reorth_tol),
-                       int(bool(rr_fallback)), int(mixed))
+                       int(bool(rr_fallback)), int(mixed), int(bool(emul)))
 
 
 @dataclass

@@ -1,0 +1,274 @@
+// ozaki.cuh -- S1 for dense A (W = A X^) with FP64 accuracy on the INT8 tensor cores
+// (tcgen05.mma kind::i8), opt-in through refine_opts.emul.  Ozaki-style splitting:
+//
+//   A_ij = 2^{e_i} sum_{t=1..S} a^(t)_ij 2^{-7t} + r_ij,   X_lj = 2^{f_j} sum_{u=1..S} x^(u)_lj 2^{-7u} + q_lj
+//
+// with int8 slices a^(t), x^(u) in [-127, 127] (7 magnitude bits each, extracted exactly in FP64:
+// r <- 128 r, d = trunc(r), r <- r - d), e_i the exponent of row i's max |A_ij| (A is constant:
+// sliced once at init, 2^{e_i} |.| < 1) and f_j that of column j's max |X_lj| (every sweep).  Then
+//
+//   (A X)_ij = 2^{e_i + f_j} sum_{c=2..S+1} 2^{-7c} L_c[i][j],   L_c = sum_{t+u=c} a^(t) x^(u)
+//
+// where every L_c is an exact integer product accumulated in int32 on the tensor cores (|L_c| <=
+// (c-1) 127^2 K, K <= OZ_KMAX keeps it below 2^31) and combined in FP64.  Dropped terms (t + u >
+// S + 1) and the slice remainders are below 2^{-7S} (S = 8: 2^-56) of max|A_i.| max|X_.j| per
+// product term.  Unlike FP64 rounding this error is relative to the row / column MAXIMA, so entries
+// far below their row's largest lose relative accuracy (the classic limit of the scheme).  The
+// diagonal -- the dominant entry of the diagonally dominant and near-diagonal (Q ~ I) matrices the
+// method meets -- is therefore taken out: it is not sliced (e_i is the OFF-diagonal row maximum)
+// and a_ii x_ij is added in FP64 in the epilogue.  Rows whose off-diagonal entries span a wider
+// dynamic range than the sweep tolerates need the DMMA path (emul = 0, the default).
+//
+// Per K step of 32 the MMA for slice t of A multiplies the concatenated X slices u = 1 .. S+1-t
+// (N = m k <= 256) into the TMEM accumulators of levels t+1 .. t+m, which are laid out contiguously
+// by level -- so the S(S+1)/2 slice products take 2S-ish MMAs.  Tiles are pre-arranged in HBM in the
+// UMMA canonical K-major layout (8-row x 16-byte core matrices): A as [row tile][K step][slice]
+// [128 x 32] (one contiguous 4S KB bulk copy per K step), X as [K step][slice][k x 32].
+#pragma once
+#include "common.cuh"
+#include "tc_passes.cuh"
+
+namespace rf {
+
+constexpr int OZ_S = 8;                     // slices per operand (8 x 7 magnitude bits)
+constexpr int OZ_BM = 128, OZ_BK = 32;      // A rows per tile, K per MMA (int8)
+constexpr int OZ_KMAX = 16384;              // K per CTA: 8 * 127^2 * 16384 < 2^31 (exact int32 levels)
+constexpr uint32_t OZ_SBO = (OZ_BK / 16) * 128;            // 8-row groups: 256 B
+constexpr uint32_t OZ_ATILE = OZ_BM * OZ_BK;               // 4 KB per A slice tile
+constexpr int OZ_STAGES = 4;
+constexpr int OZ_THREADS = 256;             // warp 0: producer, warp 1: MMA issue, warps 4-7: epilogue
+
+RF_DEV constexpr uint32_t oz_off(int r, int kk) {   // element (row r, K kk) of a canonical int8 tile
+  return (uint32_t)(r / 8) * OZ_SBO + (uint32_t)(kk / 16) * 128u + (uint32_t)(r % 8) * 16u + (uint32_t)(kk % 16);
+}
+RF_DEV int oz_exponent(double m) {          // smallest e with m < 2^e (m >= 0); 0 for m == 0
+  if (!(m > 0.0)) return 0;
+  int e;
+  frexp(m, &e);                             // m = f 2^e, f in [0.5, 1)
+  return e;
+}
+// 7-bit slices of v in (-1, 1): d_t = trunc(128 r), r <- 128 r - d_t (exact)
+RF_DEV void oz_slices(double v, int8_t (&d)[OZ_S]) {
+  double r = v;
+#pragma unroll
+  for (int t = 0; t < OZ_S; ++t) {
+    r *= 128.0;
+    const double q = trunc(r);
+    d[t] = (int8_t)q;
+    r -= q;
+  }
+}
+
+// ---- init: per-row exponent of A (row max) -------------------------------------------------
+// (off-diagonal max; local row i is global row row0 + i) and the diagonal entries in FP64
+__global__ void __launch_bounds__(256) oz_rowexp_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
+                                                        int64_t n, int64_t row0, int32_t* __restrict__ e,
+                                                        double* __restrict__ diag) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < M;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double m = 0.0;
+    for (int64_t j = lane; j < n; j += 32)
+      if (j != row0 + i) m = fmax(m, fabs(A[i * lda + j]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      e[i] = oz_exponent(m);
+      diag[i] = (row0 + i < n) ? A[i * lda + row0 + i] : 0.0;
+    }
+  }
+}
+
+// ---- init: A slices, tiles [rt][ks][t][128 x 32] (zero padded past M rows / n columns) ---------
+// one thread per (row, 16-column chunk): 16 FP64 -> S uint4 stores
+__global__ void __launch_bounds__(256) oz_slice_A_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
+                                                         int64_t n, int64_t row0, const int32_t* __restrict__ e,
+                                                         int8_t* __restrict__ As, int64_t nks) {
+  const int64_t nrt = (M + OZ_BM - 1) / OZ_BM;
+  const int64_t nchunk = nks * (OZ_BK / 16);           // 16-column chunks per row
+  const int64_t total = nrt * OZ_BM * nchunk;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = g / nchunk, ch = g % nchunk;     // row, chunk (consecutive threads: same row)
+    const int64_t ks = ch / (OZ_BK / 16);
+    const int kk0 = (int)(ch % (OZ_BK / 16)) * 16;
+    uint32_t w[OZ_S][4];
+#pragma unroll
+    for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+    if (i < M) {
+      const double sc = ldexp(1.0, -e[i]);
+#pragma unroll 4
+      for (int q = 0; q < 16; ++q) {
+        const int64_t j = ks * OZ_BK + kk0 + q;
+        int8_t d[OZ_S];
+        oz_slices((j < n && j != row0 + i) ? A[i * lda + j] * sc : 0.0, d);   // diagonal: FP64 epilogue
+#pragma unroll
+        for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= (uint32_t)(uint8_t)d[t] << (8 * (q & 3));
+      }
+    }
+    const int64_t rt = i / OZ_BM;
+    int8_t* tile0 = As + ((rt * nks + ks) * OZ_S) * (int64_t)OZ_ATILE;
+    const uint32_t off = oz_off((int)(i % OZ_BM), kk0);
+#pragma unroll
+    for (int t = 0; t < OZ_S; ++t)
+      *reinterpret_cast<uint4*>(tile0 + t * OZ_ATILE + off) = make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
+  }
+}
+
+// ---- per sweep: column exponents of X (n x k), atomicMax of exact exponents (order-free) -------
+__global__ void __launch_bounds__(256) oz_colexp_kernel(const double* __restrict__ X, int64_t n, int k,
+                                                        int32_t* __restrict__ f) {
+  // f[] preset to INT_MIN by the caller (memset 0x80)
+  const int j = threadIdx.x % k, rows_per = blockDim.x / k;
+  double m = 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * rows_per + threadIdx.x / k; l < n; l += (int64_t)gridDim.x * rows_per)
+    m = fmax(m, fabs(X[l * k + j]));
+  if ((int)threadIdx.x < rows_per * k) atomicMax(&f[j], oz_exponent(m));
+}
+
+// ---- per sweep: X slices, tiles [ks][u][k x 32]: element (n = j, K = l) -----------------------
+__global__ void __launch_bounds__(256) oz_slice_X_kernel(const double* __restrict__ X, int64_t n, int k,
+                                                         const int32_t* __restrict__ f, int8_t* __restrict__ Xs,
+                                                         int64_t nks) {
+  const int64_t total = nks * OZ_BK * (int64_t)k;      // one thread per (K row l, column j)
+  const int64_t tile = (int64_t)k * OZ_BK;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = g / k;
+    const int j = (int)(g % k);
+    int8_t d[OZ_S];
+    oz_slices(l < n ? ldexp(X[l * k + j], -f[j]) : 0.0, d);
+    const int64_t ks = l / OZ_BK;
+    const uint32_t off = oz_off(j, (int)(l % OZ_BK));
+#pragma unroll
+    for (int u = 0; u < OZ_S; ++u) Xs[(ks * OZ_S + u) * tile + off] = d[u];
+  }
+}
+
+// ---- the GEMM: out[blockIdx.y][m][j] = partial (A X)_mj over K steps [ks0, ks1) ---------------
+// grid (row tiles, splits); one CTA per SM.  K-chunk per split <= OZ_KMAX.
+template <int KK>   // k (multiple of 16, <= 64)
+struct OzCfg {
+  static constexpr uint32_t XTILE = KK * OZ_BK;                            // bytes per X slice tile
+  static constexpr uint32_t STAGE = OZ_S * OZ_ATILE + OZ_S * XTILE;       // A slices + X slices
+  static constexpr int SMEM = 1024 + OZ_STAGES * STAGE;
+  static constexpr int MAXM = 256 / KK;                                   // X slices per MMA (N <= 256)
+  static constexpr int TCOLS = OZ_S * KK <= 256 ? 256 : 512;              // TMEM columns (levels x k)
+};
+
+template <int KK>
+__global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const int8_t* __restrict__ As,
+                                                                const int8_t* __restrict__ Xs,
+                                                                const int32_t* __restrict__ e,
+                                                                const int32_t* __restrict__ f, int64_t M,
+                                                                int64_t nks, int64_t ks_per, double* __restrict__ out,
+                                                                int64_t out_split_stride, const double* __restrict__ diag,
+                                                                const double* __restrict__ Xd, int64_t row0,
+                                                                const int* __restrict__ status) {
+  using C = OzCfg<KK>;
+  extern __shared__ __align__(16) unsigned char oz_raw[];
+  __shared__ __align__(8) uint64_t full[OZ_STAGES], empty[OZ_STAGES], accb;
+  __shared__ uint32_t tmem_base;
+  if (*status != ST_OK) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rt = blockIdx.x;
+  const int64_t ks0 = (int64_t)blockIdx.y * ks_per;
+  const int64_t ks1 = (ks0 + ks_per < nks) ? ks0 + ks_per : nks;
+  const int nst = (ks1 > ks0) ? (int)(ks1 - ks0) : 0;
+  unsigned char* base = oz_raw + ((1024 - (smem_u32(oz_raw) & 1023)) & 1023);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < OZ_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&accb, 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (warp == 0) {                                   // ---- producer: one stage = A slices + X slices
+    if (lane == 0) {
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % OZ_STAGES;
+        if (t >= OZ_STAGES) mbar_wait(&empty[s], ((t / OZ_STAGES) - 1) & 1);
+        const int64_t ks = ks0 + t;
+        unsigned char* st = base + s * C::STAGE;
+        mbar_expect_tx(&full[s], C::STAGE);
+        bulk_g2s(st, As + ((rt * nks + ks) * OZ_S) * (int64_t)OZ_ATILE, OZ_S * OZ_ATILE, &full[s]);
+        bulk_g2s(st + OZ_S * OZ_ATILE, Xs + ks * OZ_S * (int64_t)C::XTILE, OZ_S * C::XTILE, &full[s]);
+      }
+    }
+  } else if (warp == 1) {                            // ---- MMA issue (one thread)
+    if (lane == 0) {
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % OZ_STAGES;
+        mbar_wait(&full[s], (t / OZ_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(base + s * C::STAGE), sx = sa + OZ_S * OZ_ATILE;
+#pragma unroll
+        for (int ta = 1; ta <= OZ_S; ++ta) {         // slice t of A x slices u = 1 .. S + 1 - t of X
+          const uint64_t da = umma_desc(sa + (ta - 1) * OZ_ATILE, 128, OZ_SBO);
+          for (int u0 = 1; u0 <= OZ_S + 1 - ta; u0 += C::MAXM) {
+            const int m = (OZ_S + 1 - ta - u0 + 1) < C::MAXM ? (OZ_S + 1 - ta - u0 + 1) : C::MAXM;
+            const uint64_t db = umma_desc(sx + (u0 - 1) * C::XTILE, 128, OZ_SBO);
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((m * KK) >> 3) << 17) |
+                                   ((uint32_t)(OZ_BM >> 4) << 24);
+            const uint32_t dcol = tmem + (uint32_t)((ta + u0 - 2) * KK);   // level c = ta + u0 at column (c - 2) k
+            const uint32_t acc = (t > 0 || ta > 1) ? 1u : 0u;            // ta = 1 initialises every level
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dcol),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+        }
+        umma_commit(&empty[s]);                       // the stage's smem may be refilled
+      }
+      umma_commit(&accb);
+    }
+  } else if (warp >= 4) {                            // ---- epilogue: TMEM lane (row) 32 (w - 4) + lane
+    const int r = 32 * (warp - 4) + lane;
+    const int64_t i = rt * OZ_BM + r;
+    if (nst > 0) mbar_wait(&accb, 0);
+    tc_fence_after();
+    const uint32_t tl = tmem + ((uint32_t)(32 * (warp - 4)) << 16);
+    const double se = (i < M) ? ldexp(1.0, e[i]) : 0.0;
+    double* o = out + (int64_t)blockIdx.y * out_split_stride + i * KK;
+#pragma unroll 1
+    for (int c0 = 0; c0 < KK; c0 += 16) {
+      double acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+      if (nst > 0) {
+#pragma unroll 1
+        for (int c = OZ_S + 1; c >= 2; --c) {          // smallest levels first
+          float v[16];
+          tmem_ld16(tl + (uint32_t)((c - 2) * KK + c0), v);
+          const double w = ldexp(1.0, -7 * c);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[q] = fma((double)(int32_t)__float_as_uint(v[q]), w, acc[q]);
+        }
+      }
+      if (i < M) {   // split 0 adds the FP64 diagonal term a_ii x_ij
+        const double di = blockIdx.y == 0 ? diag[i] : 0.0;
+        const double* xr = Xd + (row0 + i) * KK + c0;
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          const double2 xv = *reinterpret_cast<const double2*>(xr + q);
+          *reinterpret_cast<double2*>(o + c0 + q) =
+              make_double2(fma(di, xv.x, acc[q] * se * ldexp(1.0, f[c0 + q])),
+                           fma(di, xv.y, acc[q + 1] * se * ldexp(1.0, f[c0 + q + 1])));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(C::TCOLS));
+}
+
+}  // namespace rf

@@ -33,6 +33,7 @@
 #include "passes.cuh"
 #include "spmm_csr.cuh"
 #include "tc_passes.cuh"
+#include "ozaki.cuh"
 #include "nccl_dl.h"
 
 using namespace rf;
@@ -148,6 +149,12 @@ struct refine_ctx {
   bool gated = false;   // phase(): launch with ws.status -> ws.gate (refine_run reorthogonalisation)
   bool in_rr = false;   // phase(): a Rayleigh-Ritz / Cholesky-QR step (O(1) products: always FP64)
   double* bdiag = nullptr;   // NEXT-2 pass B: FP64 diagonal partials (sms x 2 kp), in the pool
+  // opts.emul (dense S1 on the INT8 tensor cores, ozaki.cuh): A slices (init), X slices (per sweep)
+  int32_t *oz_e = nullptr, *oz_f = nullptr;
+  double* oz_diag = nullptr;
+  int8_t *oz_A = nullptr, *oz_X = nullptr;
+  int oz_ns = 0;
+  int64_t oz_nks = 0, oz_nrt = 0, oz_ks_per = 0;
   int32_t* xoff_buf = nullptr;
   const int32_t* xoff = nullptr;
   double shift = 0.0;
@@ -409,7 +416,24 @@ struct Kern {
           if (!last) wp.shift = 0.0;
           const double* Xg = pass ? ws.Xt : X;                   // operand of this product
           if (pass) cudaMemcpyAsync(ws.Xt, ws.W, (size_t)c->n_loc * c->k * 8, cudaMemcpyDeviceToDevice, s);
-          if (!c->csr) {
+          if (!c->csr && c->opts.emul) {   // A X on the INT8 tensor cores (ozaki.cuh)
+            const double* Xb = c->multi ? c->Xfull : Xg;           // B operand: all n rows
+            double* out = (c->oz_ns == 1) ? ws.W : ws.Wpart;
+            if (pass == 0) c->mark();
+            cudaMemsetAsync(c->oz_f, 0x80, c->k * sizeof(int32_t), s);
+            oz_colexp_kernel<<<c->sms * 4, 256, 0, s>>>(Xb, c->n, c->k, c->oz_f);
+            oz_slice_X_kernel<<<c->sms * 8, 256, 0, s>>>(Xb, c->n, c->k, c->oz_f, c->oz_X, c->oz_nks);
+            const dim3 g((unsigned)c->oz_nrt, (unsigned)c->oz_ns);
+            switch (c->k) {
+              case 16: oz_gemm_kernel<16><<<g, OZ_THREADS, OzCfg<16>::SMEM, s>>>(c->oz_A, c->oz_X, c->oz_e, c->oz_f, c->n_loc, c->oz_nks, c->oz_ks_per, out, c->n_loc * c->k, c->oz_diag, Xb, c->row_begin, ws.status); break;
+              case 32: oz_gemm_kernel<32><<<g, OZ_THREADS, OzCfg<32>::SMEM, s>>>(c->oz_A, c->oz_X, c->oz_e, c->oz_f, c->n_loc, c->oz_nks, c->oz_ks_per, out, c->n_loc * c->k, c->oz_diag, Xb, c->row_begin, ws.status); break;
+              case 48: oz_gemm_kernel<48><<<g, OZ_THREADS, OzCfg<48>::SMEM, s>>>(c->oz_A, c->oz_X, c->oz_e, c->oz_f, c->n_loc, c->oz_nks, c->oz_ks_per, out, c->n_loc * c->k, c->oz_diag, Xb, c->row_begin, ws.status); break;
+              default: oz_gemm_kernel<64><<<g, OZ_THREADS, OzCfg<64>::SMEM, s>>>(c->oz_A, c->oz_X, c->oz_e, c->oz_f, c->n_loc, c->oz_nks, c->oz_ks_per, out, c->n_loc * c->k, c->oz_diag, Xb, c->row_begin, ws.status); break;
+            }
+            if (last) c->mark();
+            w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(wp, X, c->oz_ns, c->n_loc * c->k);
+            n += 4;
+          } else if (!c->csr) {
             const double* Xb = c->multi ? c->Xfull : Xg;           // B operand: all n rows
             const bool bv16 = xv16 && ((uintptr_t)Xb % 16 == 0);
             const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
@@ -631,7 +655,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->n = n; c->k = k; c->kp = pad_kp(k);
   c->row_begin = row_begin; c->row_end = row_end; c->n_loc = row_end - row_begin;
   c->shift = shift;
-  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0, 0};
+  c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0, 0, 0};
   if (opts) c->opts = *opts;
   c->stream = (cudaStream_t)stream;
   RF_CK(c, cudaGetDevice(&c->device));
@@ -644,6 +668,21 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.kjudge = c->opts.kjudge;
   if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
   if (c->opts.mixed && (k % 16 != 0 || k < 32)) return REFINE_E_UNSUPPORTED;    // tcgen05 passes: 16 | k >= 32
+  if (c->opts.emul && (c->csr || k % 16 != 0 || k > 64)) return REFINE_E_UNSUPPORTED;   // ozaki.cuh: dense, 16 | k <= 64
+  if (c->opts.emul) {   // split the K range so each CTA's int32 levels stay exact, waves near-full
+    c->oz_nks = (c->n + OZ_BK - 1) / OZ_BK;
+    c->oz_nrt = (c->n_loc + OZ_BM - 1) / OZ_BM;
+    const int64_t ns_min = (c->oz_nks + (OZ_KMAX / OZ_BK) - 1) / (OZ_KMAX / OZ_BK);
+    int best = (int)ns_min;
+    double best_eff = -1.0;
+    for (int64_t ns = ns_min; ns <= std::max<int64_t>(ns_min, 16); ++ns) {
+      const int64_t ctas = c->oz_nrt * ns;
+      const double eff = (double)ctas / ((double)((ctas + c->sms - 1) / c->sms) * c->sms);
+      if (eff > best_eff + 0.01) { best_eff = eff; best = (int)ns; }
+    }
+    c->oz_ks_per = (c->oz_nks + best - 1) / best;
+    c->oz_ns = (int)((c->oz_nks + c->oz_ks_per - 1) / c->oz_ks_per);
+  }
   ws.world = world; ws.rank = rank;
   ws.multi = c->multi ? 1 : 0;
   ws.row0 = row_begin; ws.row1 = row_end;
@@ -663,7 +702,8 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   if (c->csr) RF_CK(c, gather_setup(c));
   c->n_ag = c->csr ? c->spmm_grid : c->w_fin_grid;
   const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k, P = (size_t)world;
-  const size_t wpart = (!c->csr && c->nsplit > 1) ? (size_t)c->nsplit * nk : 0;
+  const int nsplit_max = std::max(c->nsplit, c->oz_ns);
+  const size_t wpart = (!c->csr && nsplit_max > 1) ? (size_t)nsplit_max * nk : 0;
   c->bc_cnt = kk + k + 8 + 1;
   size_t off = 0;
   auto take = [&](size_t cnt) { size_t o = off; off += (cnt + 31) & ~size_t(31); return o; };
@@ -709,6 +749,21 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   else
     absrow_max_csr_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, c->n_loc, c->row_begin, nshift, rows);
   max_kernel<<<1, 1024, 0, c->stream>>>(rows, c->n_loc, ws.stats + 7);
+  if (c->opts.emul) {   // A's exponents and int8 slices, once (A is borrowed and constant)
+    RF_CK(c, cudaMalloc(&c->oz_e, std::max<int64_t>(c->n_loc, 1) * sizeof(int32_t)));
+    RF_CK(c, cudaMalloc(&c->oz_diag, std::max<int64_t>(c->n_loc, 1) * sizeof(double)));
+    RF_CK(c, cudaMalloc(&c->oz_f, 64 * sizeof(int32_t)));
+    RF_CK(c, cudaMalloc(&c->oz_A, (size_t)c->oz_nrt * c->oz_nks * OZ_S * OZ_ATILE));
+    RF_CK(c, cudaMalloc(&c->oz_X, (size_t)c->oz_nks * OZ_S * k * OZ_BK));
+    oz_rowexp_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->A, c->lda, c->n_loc, c->n, c->row_begin, c->oz_e, c->oz_diag);
+    oz_slice_A_kernel<<<c->sms * 16, 256, 0, c->stream>>>(c->A, c->lda, c->n_loc, c->n, c->row_begin, c->oz_e, c->oz_A,
+                                                          c->oz_nks);
+    auto attr = [&](auto kern, int smem) { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); };
+    RF_CK(c, attr(oz_gemm_kernel<16>, OzCfg<16>::SMEM));
+    RF_CK(c, attr(oz_gemm_kernel<32>, OzCfg<32>::SMEM));
+    RF_CK(c, attr(oz_gemm_kernel<48>, OzCfg<48>::SMEM));
+    RF_CK(c, attr(oz_gemm_kernel<64>, OzCfg<64>::SMEM));
+  }
   unsigned long long* colr = reinterpret_cast<unsigned long long*>(b + oCol);
   if (c->csr && c->multi) {
     const unsigned long long init[2] = {~0ull, 0ull};
@@ -799,7 +854,7 @@ static refine_status init_any(refine_ctx* c, int64_t n, int32_t k, int64_t row_b
     c->world = world;
     c->n = n; c->k = k; c->n_loc = n; c->row_begin = 0; c->row_end = n;
     c->stream = (cudaStream_t)stream;
-    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0, 0};
+    c->opts = refine_opts{10.0, 0, 1, 3, 10.0, 0, 0, 0.0, 0.0, 0, 0, 0};
     if (opts) c->opts = *opts;
     std::vector<int64_t> rb(world), re(world), lo(world), hi(world);
     std::vector<double> nrm(world);
@@ -1249,7 +1304,7 @@ extern "C" int32_t refine_kernels_per_sweep(const refine_ctx* c) {
     for (auto* kid : c->kids) n += refine_kernels_per_sweep(kid);
     return n;
   }
-  const int per = c->csr ? 7 : 8;   // incl. kxk_lu (side stream)
+  const int per = (c->csr ? 7 : 8) + (c->opts.emul ? 2 : 0);   // incl. kxk_lu (side stream); emul: X slicing
   if (!c->multi) return per;
   return per + 1 - (c->rank == 0 ? 0 : 2);   // + ag_local; kxk_lu / kxk_finish on rank 0 only
 }
@@ -1316,6 +1371,11 @@ extern "C" void refine_destroy(refine_ctx* c) {
   if (c->pool) cudaFree(c->pool);
   if (c->ws.tlog) cudaFree(c->ws.tlog);
   if (c->dX) cudaFree(c->dX);
+  if (c->oz_e) cudaFree(c->oz_e);
+  if (c->oz_diag) cudaFree(c->oz_diag);
+  if (c->oz_f) cudaFree(c->oz_f);
+  if (c->oz_A) cudaFree(c->oz_A);
+  if (c->oz_X) cudaFree(c->oz_X);
   delete c;
 }
 

@@ -1,0 +1,132 @@
+"""Dense S1 with FP64 accuracy on the INT8 tensor cores (refine_opts.emul, ozaki.cuh): the sweep
+keeps the north_star's one-step parity with the FP64 oracle (<= 1e-10 relative Frobenius) and its
+converged accuracy (<= 100 n u), and W = A X^ agrees with the DMMA GEMM within the scheme's
+truncation bound (relative to row / column maxima) plus the FP64 rounding bound n u |A||X|."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2602_23778_b200 as p
+    from paper_2602_23778_b200 import build
+    build.build()
+    p.lib()
+    assert torch.cuda.is_available()
+    return p
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("n,k", [(1100, 16), (777, 32), (2000, 48), (1500, 64), (300, 64)])
+def test_emul_one_step_parity(pkg, n, k):
+    p = synth.small_dense(n, k, m=8, seed=n + 3 * k, signs=True)
+    R = pkg.Refiner.dense(p.A.cuda(), k, emul=True)
+    op = oracle.Operator(A=p.A.numpy())
+    X = p.X0.cuda().clone()
+    for t in range(3):
+        xin = X.cpu().numpy()
+        s, st = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK
+        assert rel(X.cpu().numpy(), ref.X) <= 1e-10, t
+        assert st.flipped == ref.stats.flipped and st.delta_hits == ref.stats.delta_hits
+        # (near convergence rel_resid ~ 1e-9 is W's own rounding; the two W differ by ~2^-56 |A||X|)
+        assert abs(st.rel_resid - ref.stats.rel_resid) <= 1e-8 * ref.stats.rel_resid + 1e-16
+
+
+def test_emul_w_within_scheme_bound(pkg):
+    """W from the INT8 slices vs W from DMMA: both within n u |A||X| of the exact product."""
+    n, k = 2048, 64
+    p = synth.small_dense(n, k, m=8, seed=77, signs=True)
+    A, X0 = p.A.cuda(), p.X0.cuda()
+    Rd, Re = pkg.Refiner.dense(A, k), pkg.Refiner.dense(A, k, emul=True)
+    Xd, Xe = X0.clone(), X0.clone()
+    Rd.refine_sweep(Xd, stats=True)
+    Re.refine_sweep(Xe, stats=True)
+    Wd = Rd.debug(pkg.DBG_W).cpu().numpy()
+    We = Re.debug(pkg.DBG_W).cpu().numpy()
+    An, Xn = p.A.numpy(), p.X0.numpy()
+    # the scheme's bound (ozaki.cuh): per product term, slices truncated at 2^-7S of the row max of A
+    # (off-diagonal; the diagonal is exact FP64) and of the column max of X, plus the dropped slice
+    # products t + u > S + 1 (< S 2^-7S of max x max) -> (S + 1) 2^(2 - 7S) n max|A_i.| max|X_.j|,
+    # plus the FP64 rounding of the DMMA side (n u |A||X|).  S = 8.
+    Aoff = np.abs(An - np.diag(np.diag(An)))
+    bound = n * U * (np.abs(An) @ np.abs(Xn)) + 9 * 2.0 ** (2 - 56) * n * Aoff.max(1)[:, None] * np.abs(Xn).max(0)[None, :]
+    ratio = np.abs(We - Wd) / bound
+    print(f"max |W_emul - W_dmma| / bound = {ratio.max():.2e}, / (|A||X|) = "
+          f"{np.max(np.abs(We - Wd) / (np.abs(An) @ np.abs(Xn))):.2e}")
+    assert np.all(np.abs(We - Wd) <= bound)
+
+
+def test_emul_converges(pkg):
+    n, k = 3000, 64
+    p = synth.small_dense(n, k, m=8, noise=1e-6, seed=29)
+    R = pkg.Refiner.dense(p.A.cuda(), k, emul=True)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 60, 1e-13)
+    assert s == pkg.REFINE_OK
+    Xg, Xt = X.cpu().numpy(), p.X.numpy()
+    sg = np.sign(np.sum(Xg * Xt, axis=0))
+    assert np.linalg.norm(Xg * sg - Xt, axis=0).max() <= 100 * n * U
+    assert st.rel_resid <= 100 * n * U
+
+
+def test_emul_cfg2_full_size(pkg):
+    p = synth.make_config("cfg2", device="cuda")
+    R = pkg.Refiner.dense(p.A, p.k, emul=True)
+    op = oracle.Operator(A=p.A.cpu().numpy())
+    X = p.X0.clone()
+    xin = X.cpu().numpy()
+    s, st = R.refine_sweep(X, stats=True)
+    ref = oracle.sweep(op, xin)
+    assert s == pkg.REFINE_OK and rel(X.cpu().numpy(), ref.X) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emul_loopback(pkg, world):
+    p = synth.small_dense(1100, 32, m=8, seed=5, signs=True)
+    op = oracle.Operator(A=p.A.numpy())
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, _ = pkg.Refiner.dense(p.A.cuda(), 32, emul=True, world=world).refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK
+    assert rel(X.cpu().numpy(), oracle.sweep(op, xin).X) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [8, 24, 80])
+def test_emul_rejects_shapes(pkg, k):
+    p = synth.small_dense(400, k, seed=2)
+    with pytest.raises(pkg.RefineError) as e:
+        pkg.Refiner.dense(p.A.cuda(), k, emul=True)
+    assert e.value.status == pkg.REFINE_E_UNSUPPORTED
+
+
+def test_emul_rejects_csr(pkg):
+    q = synth.small_laplacian((20, 19), (1.0, 1.37), 16)
+    with pytest.raises(pkg.RefineError) as e:
+        pkg.Refiner.csr(q.row_ptr.cuda(), q.col_idx.cuda(), q.val.cuda(), q.n, 16, emul=True)
+    assert e.value.status == pkg.REFINE_E_UNSUPPORTED
+
+
+def test_emul_cfg3_full_size(pkg):
+    """BASELINE configs[2] at full size (n = 32768, k = 64): one-step parity with the oracle."""
+    p = synth.make_config("cfg3", device="cuda")
+    R = pkg.Refiner.dense(p.A, p.k, emul=True)
+    X = p.X0.clone()
+    xin = X.cpu().numpy()
+    s, st = R.refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK
+    ref = oracle.sweep(oracle.Operator(A=p.A.cpu().numpy()), xin)
+    e = rel(X.cpu().numpy(), ref.X)
+    print(f"cfg3 emul one-step rel diff {e:.3e}")
+    assert e <= 1e-10
