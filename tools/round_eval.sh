@@ -3,7 +3,7 @@
 set -x
 O=gpurun_out/r01
 mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q --timeout 400 2>&1 | tail -3 > $O/pytest_gpu.txt
+[ -n "$SKIP_TESTS" ] || timeout 1500 python -m pytest tests -m gpu -q --timeout 400 2>&1 | tail -3 > $O/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/reference.json 2> $O/reference.err
@@ -22,3 +22,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pas
   -o $O/full_cfg5_mixed python bench.py --config cfg5 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
 ls -la $O
 cat $O/pytest_gpu.txt $O/smoke.txt
+# summaries on the box (the .ncu-rep files can exceed gpurun's 64 MiB copy-back limit)
+for c in cfg3 cfg5; do python tools/ncu_summary.py launches $O/launches_$c.csv $O/launches_$c.json > /dev/null; done
+python tools/ncu_summary.py report $O/full_cfg3_gemm.ncu-rep $O/ncu_gemm_cfg3.json > /dev/null
+python tools/ncu_summary.py report $O/full_cfg4.ncu-rep $O/ncu_cfg4.json > /dev/null
+python tools/ncu_summary.py report $O/full_cfg5.ncu-rep $O/ncu_cfg5.json > /dev/null
+python tools/ncu_summary.py report $O/full_cfg5_mixed.ncu-rep $O/ncu_cfg5_mixed.json > /dev/null
+[ -n "$KEEP_REPS" ] || rm -f $O/*.ncu-rep
