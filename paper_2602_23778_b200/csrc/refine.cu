@@ -219,7 +219,7 @@ template <int KP> struct Tiles;
 //                 GEMM: BM  WM  WN  BK  ST | passB: TA  TB  WA WB  BR | passC: NC BM WM WN
 template <> struct Tiles<8>   { static constexpr int G[5] = {64, 16, 8, 32, 4};   static constexpr int B[5] = {8, 16, 1, 2, 32};   static constexpr int C[4] = {8, 64, 8, 1}; };
 template <> struct Tiles<16>  { static constexpr int G[5] = {64, 16, 16, 32, 4};  static constexpr int B[5] = {16, 32, 2, 4, 32};  static constexpr int C[4] = {16, 64, 8, 1}; };
-template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}; static constexpr int B[5] = {32, 64, 2, 4, 32};  static constexpr int C[4] = {32, 64, 4, 2}; };
+template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}; static constexpr int B[5] = {32, 64, 1, 4, 32};  static constexpr int C[4] = {32, 64, 4, 2}; };
 template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
 template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 2, 16};  static constexpr int C[4] = {128, 32, 2, 8}; };
 
