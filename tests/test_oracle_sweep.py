@@ -323,7 +323,7 @@ def test_invalid_k():
 
 def test_delta_branch_beta():
     """lam_1 = lam_2 inside the targets: |d_2 - d_1| <= delta takes beta_ij = -x_i^T x_j/2
-     or 0 (:460).  Parity unpinned beyond this construction."""
+    (PAPER.md:443, 457) or 0 (:460)."""
     n = 20
     A = np.diag(np.concatenate([[3.0, 3.0], np.linspace(-1, 1, n - 2)]))
     X = np.eye(n, 2)
@@ -357,6 +357,30 @@ def test_delta_branch_exact_tie():
     assert r.debug["E"][0, 1] == -(Xf[:, 0] @ Xf[:, 1]) / 2
     r0 = oracle.sweep(oracle.Operator(A=A), X, debug=True, beta_zero=True)
     assert r0.debug["E"][0, 1] == 0.0 and r0.debug["E"][1, 0] == 0.0
+
+
+def test_delta_branch_near_tie_both_sides():
+    """Rayleigh quotients a NONZERO distance apart (reading R5): a gap below
+    delta = c ||A||_inf u takes the beta branch (E_01 = -x^_0^T x^_1 / 2), a gap above it the
+    regular V_01 / (d_1 - d_0) -- the threshold is the paper's, the rest is a dot product."""
+    n = 12
+    for dl, hit in ((2.0 ** -50, True), (2.0 ** -40, False)):
+        lam = np.concatenate([[4.0, 4.0 + dl], np.linspace(-1, 1, n - 2)])
+        A = np.diag(lam)
+        X = np.zeros((n, 2)); X[0, 0] = X[1, 1] = 1.0
+        X[4, 0] = X[4, 1] = 1e-3
+        r = oracle.sweep(oracle.Operator(A=A), X, debug=True)
+        d = r.debug["dtilde"]
+        gap = abs(d[1] - d[0])
+        delta = 10.0 * np.abs(A).sum(1).max() * U
+        assert gap > 0.0
+        assert (gap <= delta) == hit
+        assert r.stats.delta_hits == (2 if hit else 0)
+        Xf = X * r.debug["sigma"]
+        if hit:
+            assert r.debug["E"][0, 1] == -(Xf[:, 0] @ Xf[:, 1]) / 2
+        else:
+            assert r.debug["E"][0, 1] != -(Xf[:, 0] @ Xf[:, 1]) / 2
 
 
 def test_thread_count_invariance():
