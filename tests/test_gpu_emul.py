@@ -130,3 +130,24 @@ def test_emul_cfg3_full_size(pkg):
     e = rel(X.cpu().numpy(), ref.X)
     print(f"cfg3 emul one-step rel diff {e:.3e}")
     assert e <= 1e-10
+
+
+def test_emul_with_square(pkg):
+    """emul under the shift-and-square operator (Sec. 5.2): both products A (A X) on the INT8 path."""
+    q = synth.small_laplacian((17, 13), (1.0, 1.37), 16, noise=1e-5, seed=11)
+    rp, ci, v = q.row_ptr.numpy(), q.col_idx.numpy(), q.val.numpy()
+    L = np.zeros((q.n, q.n))
+    for i in range(q.n):
+        L[i, ci[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+    L = q.meta["sigma"] * np.eye(q.n) - L                 # the Dirichlet Laplacian
+    mu = np.sort(np.linalg.eigvalsh(L))
+    alpha = (np.abs(L).sum(1).max() ** 2 + mu[16] ** 2) / 2
+    R = pkg.Refiner.dense(torch.from_numpy(L).cuda(), 16, shift=alpha, square=True, emul=True)
+    op = oracle.Operator(A=L, shift=alpha, square=True)
+    X = q.X0.cuda().clone()
+    for t in range(3):
+        xin = X.cpu().numpy()
+        s, _ = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK
+        assert rel(X.cpu().numpy(), ref.X) <= 1e-10, t

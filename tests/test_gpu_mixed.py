@@ -209,3 +209,19 @@ def test_mixed_sweep_rr(pkg):
     Xo = ref.X
     sig = np.where(np.sum(Xo * X.cpu().numpy(), axis=0) < 0, -1.0, 1.0)
     assert fro(X.cpu().numpy() * sig - Xo) <= 1e-6 * fro(Xo)
+
+
+def test_mixed_with_kjudge(pkg):
+    """K = 64 refined columns judged on the leading 32 in mixed precision: the
+    judged ||E_L|| follows the oracle's to the mixed tolerance."""
+    n, K, k = 1500, 64, 32
+    p = synth.small_dense(n, K, m=8, noise=1e-5, seed=41, signs=True)
+    R = refiner(pkg, p, mixed=2, kjudge=k)
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, st = R.refine_sweep(X, stats=True)
+    ref = oracle.sweep(op_of(p), xin, kjudge=k)
+    assert s == pkg.REFINE_OK and ref.status == oracle.OK
+    assert abs(st.corr_norm - ref.stats.corr_norm) <= 1e-2 * ref.stats.corr_norm
+    sig = np.where(np.sum(ref.X * xin, axis=0) < 0, -1.0, 1.0)
+    assert fro(X.cpu().numpy() - ref.X) <= 1e-2 * fro(ref.X - xin * sig) + 1e-10 * fro(ref.X)
