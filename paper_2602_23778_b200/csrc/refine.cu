@@ -149,6 +149,7 @@ struct refine_ctx {
   bool gated = false;   // phase(): launch with ws.status -> ws.gate (refine_run reorthogonalisation)
   bool in_rr = false;   // phase(): a Rayleigh-Ritz / Cholesky-QR step (O(1) products: always FP64)
   double* bdiag = nullptr;   // NEXT-2 pass B: FP64 diagonal partials (sms x 2 kp), in the pool
+  int4 spmm_ord = {0, 0, 0, 0};   // spmm_gather chunk order (spmm_csr.cuh chunk_of; x = 0: identity)
   // opts.emul (dense S1 on the INT8 tensor cores, ozaki.cuh): A slices (init), X slices (per sweep)
   int32_t *oz_e = nullptr, *oz_f = nullptr;
   double* oz_diag = nullptr;
@@ -230,7 +231,8 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
   const int g = c->spmm_grid;
   if (vec && c->gather_R > 0) {   // vec: 16-byte aligned X / halo rows
     const int R = c->gather_R;
-    auto go = [&](auto kern) { kern<<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, Xg, R, Xo); };
+    const int4 ord = HALO ? make_int4(0, 0, 0, 0) : c->spmm_ord;
+    auto go = [&](auto kern) { kern<<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, Xg, R, Xo, ord); };
 #define RF_GATHER_K(KK)                                                          \
   case KK:                                                                       \
     if (c->gather_un == 5) go(spmm_gather_kernel<KK, HALO, 5>);                  \
@@ -589,6 +591,8 @@ static cudaError_t gather_geometry_un(refine_ctx* c, const std::vector<int32_t>&
   return cudaSuccess;
 }
 
+static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, int RG);
+
 // batch size UN: the smallest of {5, 7, 8} covering 95% of the rows (the stencils' 5 / 7)
 template <int K>
 static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp) {
@@ -601,9 +605,54 @@ static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp
     acc += cnt[v];
     if (acc * 100 >= n * 95) { p95 = v; break; }
   }
-  if (p95 <= 5) return gather_geometry_un<K, 5>(c, rp);
-  if (p95 <= 7) return gather_geometry_un<K, 7>(c, rp);
-  return gather_geometry_un<K, 8>(c, rp);
+  cudaError_t e;
+  if (p95 <= 5) e = gather_geometry_un<K, 5>(c, rp);
+  else if (p95 <= 7) e = gather_geometry_un<K, 7>(c, rp);
+  else e = gather_geometry_un<K, 8>(c, rp);
+  if (e != cudaSuccess) return e;
+  return gather_order(c, rp, GatherCfg<K>::RG);
+}
+
+// Stencil-aware chunk order for the gather kernel (spmm_csr.cuh chunk_of): the row offsets present
+// in (nearly) every sampled row; three levels {1, d2, d3} with d2 | d3 (a 3-D stencil in
+// lexicographic order) and a +-d3 reuse window larger than about a fifth of L2 select the tiled
+// order; the chunk size becomes the largest divisor of d2 not above R and not below the row groups.
+// REFINE_SPMM_ORDER=1 forces it whenever the structure is found (tests), =0 disables it.
+static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, int RG) {
+  c->spmm_ord = make_int4(0, 0, 0, 0);
+  const char* env = getenv("REFINE_SPMM_ORDER");
+  if ((env && env[0] == '0') || c->multi || c->gather_R <= 0) return cudaSuccess;
+  const int64_t S = std::min<int64_t>(c->n_loc, 65536);
+  const int64_t nz = (int64_t)rp[S] - rp[0];
+  if (S < 64 || nz <= 0) return cudaSuccess;
+  std::vector<int32_t> ci(nz);
+  cudaError_t e = cudaMemcpy(ci.data(), c->ci + rp[0], nz * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  std::vector<std::pair<int64_t, int64_t>> cnt;          // (offset, count), few distinct offsets
+  for (int64_t i = 0; i < S; ++i)
+    for (int32_t q = rp[i]; q < rp[i + 1]; ++q) {
+      const int64_t o = std::llabs((int64_t)ci[q - rp[0]] - (c->row_begin + i));
+      if (o == 0) continue;
+      auto it = std::find_if(cnt.begin(), cnt.end(), [&](const std::pair<int64_t, int64_t>& p) { return p.first == o; });
+      if (it != cnt.end()) ++it->second;
+      else if (cnt.size() < 16) cnt.push_back({o, 1});
+      else return cudaSuccess;                              // not a stencil
+    }
+  std::vector<int64_t> lv;
+  for (auto& p : cnt)
+    if (p.second >= S / 4) lv.push_back(p.first);
+  std::sort(lv.begin(), lv.end());
+  if (lv.size() != 3 || lv[0] != 1 || lv[2] % lv[1] != 0) return cudaSuccess;
+  const int64_t d2 = lv[1], d3 = lv[2];
+  const bool force = env && env[0] == '1';
+  if (!force && 2 * d3 * c->k * 8 < (int64_t)24 << 20) return cudaSuccess;   // window fits L2 already
+  int R = 0;
+  for (int r = std::min<int>(c->gather_R, (int)d2); r >= RG; --r)
+    if (d2 % r == 0) { R = r; break; }                  // (r >= RG: every row group busy)
+  if (R == 0) return cudaSuccess;
+  c->gather_R = R;
+  c->spmm_ord = make_int4((int)(d2 / R), (int)(d3 / d2), 16, (int)((c->n_loc + d3 - 1) / d3));   // 16 lines per tile
+  return cudaSuccess;
 }
 
 static cudaError_t gather_setup(refine_ctx* c) {

@@ -207,12 +207,34 @@ RF_DEV double2 ldg2_at(const char* base, uint32_t idx2) {   // base + idx2 doubl
   return __ldg(reinterpret_cast<const double2*>(base + (uint64_t)idx2 * 16u));
 }
 
+// Chunk order (ord.x > 0, single rank): a matrix whose nonzeros sit at row offsets {1, d2, d3}
+// (a 3-D stencil in lexicographic order: d2 = one grid line, d3 = one plane) is swept in tiles of
+// ord.z lines across all planes -- position q -> (tile, plane, line in tile, chunk in line) --
+// so a row's +-d3 neighbours are gathered a few chunks apart instead of 2 d3 rows apart (which
+// exceeds L2 at cfg5: X was read 1.7x).  ord = (chunks per line, lines per plane, lines per tile,
+// planes); chunk positions past the matrix are skipped.  W and every fma chain are unchanged.
+RF_DEV int64_t chunk_of(int64_t q, int4 ord) {   // (positions < 2^31: 32-bit index arithmetic)
+  if (ord.x == 0) return q;
+  const uint32_t qq = (uint32_t)q;
+  const uint32_t cx = qq % (uint32_t)ord.x;
+  uint32_t r = qq / (uint32_t)ord.x;
+  const uint32_t yy = r % (uint32_t)ord.z;
+  r /= (uint32_t)ord.z;
+  const uint32_t z = r % (uint32_t)ord.w, tb = r / (uint32_t)ord.w;
+  const uint32_t y = tb * (uint32_t)ord.z + yy;
+  return y < (uint32_t)ord.y ? ((int64_t)z * ord.y + y) * ord.x + cx : -1;
+}
+RF_DEV int64_t chunk_positions(int64_t nchunk, int4 ord) {
+  return ord.x == 0 ? nchunk : (int64_t)((ord.y + ord.z - 1) / ord.z) * ord.z * ord.w * ord.x;
+}
+
 // requires n_loc * K / 2 < 2^31 and halo rows * K / 2 < 2^31 (checked at init).  (Measured and
 // dropped: L1 prefetch of the next row's gathers, two rows per group in flight -- both slower.)
 template <int K, bool HALO, int UN_ = 8, int LPR_ = 0, int MINB_ = 0>
 __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spmm_gather_kernel(
     Ws ws, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ xoff, const double* __restrict__ val,
-    const double* __restrict__ Xloc, const int R, const double* __restrict__ Xown) {   // gathered rows / own rows
+    const double* __restrict__ Xloc, const int R, const double* __restrict__ Xown,   // gathered rows / own rows
+    const int4 ord) {
   using C = GatherCfg<K, UN_, LPR_, MINB_>;
   constexpr int LPR = C::LPR, VPL = C::VPL, RG = C::RG, RMAX = C::RMAX, NZCAP = C::NZCAP, UN = C::UN, K2 = K / 2;
   __shared__ int32_t s_rp[3][RMAX + 1];
@@ -223,25 +245,33 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
   const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
   const int64_t n = ws.n_loc, G = gridDim.x;
   const int64_t nchunk = (n + R - 1) / R;
-  const int T = (int)((nchunk - blockIdx.x + G - 1) / G);
+  const int64_t npos = chunk_positions(nchunk, ord);
+  const int T = (int)((npos - blockIdx.x + G - 1) / G);
   const char* Xb = reinterpret_cast<const char*>(Xloc);
   const char* Xo = reinterpret_cast<const char*>(Xown);
   const char* Hb = reinterpret_cast<const char*>(ws.halo);
   char* Wb = reinterpret_cast<char*>(ws.W);
-  auto r0_of = [=](int t) { return ((int64_t)t * G + blockIdx.x) * R; };
-  auto nr_of = [=](int t) { return (int)min((int64_t)R, n - r0_of(t)); };
-  auto stage_rp = [&](int t) {
+  // chunk at position t G + blockIdx.x, or -1 (padding / past the matrix); computed once per
+  // position (rolling ids of positions t, t + 1, t + 2 in registers)
+  auto pos_id = [=](int t) -> int64_t {
+    if (t >= T) return -1;
+    const int64_t id = chunk_of((int64_t)t * G + blockIdx.x, ord);
+    return id < nchunk ? id : (int64_t)-1;
+  };
+  auto r0_of = [=](int64_t id) { return id < 0 ? (int64_t)0 : id * R; };
+  auto nr_of = [=](int64_t id) { return id < 0 ? 0 : (int)min((int64_t)R, n - id * R); };
+  auto stage_rp = [&](int t, int64_t id) {
     if (t >= T) return;
-    const int nr = nr_of(t);
-    const int32_t* g = row_ptr + r0_of(t);
+    const int nr = nr_of(id);
+    const int32_t* g = row_ptr + r0_of(id);
     int32_t* d = s_rp[t % 3];
     for (int i = tid; i <= nr; i += 256)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(d + i)), "l"(g + i));
   };
-  auto stage_nz = [&](int t) {   // needs s_rp[t % 3]
+  auto stage_nz = [&](int t, int64_t id) {   // needs s_rp[t % 3]
     if (t >= T) return;
     const int32_t* r = s_rp[t % 3];
-    const int32_t p0 = r[0], cnt = r[nr_of(t)] - p0;
+    const int32_t p0 = r[0], cnt = r[nr_of(id)] - p0;
     for (int i = tid; i < cnt; i += 256) {
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&s_off[t & 1][i])), "l"(xoff + p0 + i));
       cp_async8(&s_v[t & 1][i], val + p0 + i, true);
@@ -249,12 +279,13 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
   };
 #pragma unroll
   for (int q = 0; q < 4 * VPL; ++q) s_acc[q][tid] = dd{0.0, 0.0};
-  stage_rp(0);
+  int64_t id_c = pos_id(0), id_n = pos_id(1);
+  stage_rp(0, id_c);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  stage_nz(0);
-  stage_rp(1);
+  stage_nz(0, id_c);
+  stage_rp(1, id_n);
   cp_async_commit();
   double ba[2 * VPL], bg[2 * VPL];
 #pragma unroll
@@ -264,13 +295,16 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
   for (int t = 0; t < T; ++t) {
     cp_async_wait<0>();
     __syncthreads();
-    stage_nz(t + 1);   // row_ptr of chunk t+1 arrived with the previous group
-    stage_rp(t + 2);
+    const int64_t id_nn = pos_id(t + 2);
+    stage_nz(t + 1, id_n);   // row_ptr of chunk t+1 arrived with the previous group
+    stage_rp(t + 2, id_nn);
     cp_async_commit();
     const int32_t* r = s_rp[t % 3];
-    const int nr = nr_of(t);
+    const int nr = nr_of(id_c);
     const int32_t p0 = r[0];
-    const uint32_t rb2 = (uint32_t)r0_of(t) * K2 + l;   // double2 index of (chunk row 0, this lane)
+    const uint32_t rb2 = (uint32_t)r0_of(id_c) * K2 + l;   // double2 index of (chunk row 0, this lane)
+    id_c = id_n;
+    id_n = id_nn;
     const int32_t* so = s_off[t & 1];
     const double* sv = s_v[t & 1];
     auto gather = [&](int32_t off, int v) -> double2 {

@@ -367,3 +367,20 @@ def test_csr_gather_matches_vec_kernel(pkg, monkeypatch):
     Rb.refine_sweep(Xb)
     assert torch.equal(Ra.debug(pkg.DBG_W), Rb.debug(pkg.DBG_W))
     assert rel(Xa.cpu().numpy(), Xb.cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,k", [((24, 22, 21), 128), ((24, 22, 21), 32), ((16, 15, 13), 8)])
+def test_csr_stencil_chunk_order(pkg, dims, k, monkeypatch):
+    """The tiled chunk order of the gather kernel (3-D stencils, spmm_csr.cuh chunk_of), forced on
+    small grids: W bit-identical to the oracle's fma chains and one-step parity."""
+    monkeypatch.setenv("REFINE_SPMM_ORDER", "1")
+    p = synth.small_laplacian(dims, (1.0, 1.13, 1.29), k)
+    R = refiner(pkg, p)
+    op = op_of(p)
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, _ = R.refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK
+    ref = oracle.sweep(op, xin, debug=True)
+    assert rel(X.cpu().numpy(), ref.X) <= TOL
+    assert np.array_equal(R.debug(pkg.DBG_W).cpu().numpy() * ref.debug["sigma"], ref.debug["W"])

@@ -75,7 +75,8 @@ struct Prob {
 
 
 template <int K, int PF = 0, int LPR = 0, int MINB = 0, int UN = 8>
-static void gather_case(const char* name, const Prob& p, int sms, const double* Wref, int R, int occ_override = 0) {
+static void gather_case(const char* name, const Prob& p, int sms, const double* Wref, int R, int4 ord = {0, 0, 0, 0}) {
+  const int occ_override = 0;
   auto kern = spmm_gather_kernel<K, false, UN, LPR, MINB>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
@@ -85,13 +86,13 @@ static void gather_case(const char* name, const Prob& p, int sms, const double* 
   ws.ag = p.ag; ws.status = p.st;
   const int gx = sms * occ;
   cudaMemset(p.W, 0, p.n * p.k * 8);
-  float ms = timeit([&] { kern<<<gx, 256>>>(ws, p.rp, p.xoff, p.v, p.X, R, p.X); });
+  float ms = timeit([&] { kern<<<gx, 256>>>(ws, p.rp, p.xoff, p.v, p.X, R, p.X, ord); });
   std::vector<double> a(p.n * p.k), b(p.n * p.k);
   cudaMemcpy(a.data(), p.W, a.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(b.data(), Wref, b.size() * 8, cudaMemcpyDeviceToHost);
   int64_t bad = 0;
   for (size_t i = 0; i < a.size(); ++i) bad += (a[i] != b[i]);
-  printf("%s gather PF=%d LPR=%d MINB=%d UN=%d K=%d R=%d occ=%d grid=%d: %.3f ms %6.0f GB/s  mismatches %lld\n", name, PF, LPR, MINB, UN, K, R, occ, gx, ms,
+  printf("%s gather ord=(%d,%d,%d,%d) MINB=%d UN=%d K=%d R=%d occ=%d grid=%d: %.3f ms %6.0f GB/s  mismatches %lld\n", name, ord.x, ord.y, ord.z, ord.w, MINB, UN, K, R, occ, gx, ms,
          p.bytes / ms / 1e6, (long long)bad);
 }
 
@@ -158,6 +159,7 @@ int main(int argc, char** argv) {
     Prob p = make(160, 160, 160, 128);
     double* Wref = prod_case<2, 32>("cfg5", p, sms);
     gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32);
+    for (int ty : {4, 8, 16, 32}) gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32, make_int4(5, 160, ty, 160));
   }
   return 0;
 }
