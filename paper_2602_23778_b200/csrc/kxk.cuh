@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     // per-column sums over the k rows, by all 1024 threads: thread (g, j) takes rows l = g, g + NG, ..
     // (fixed partition, groups combined in order -- deterministic)
     constexpr int NQ = 7;
-    const int NG = min(nt / k, k);                     // row groups (k <= 128: >= 8 unless k < 8)
+    const int NG = min(8, k);                          // row groups (a short combine chain)
     double* cs = sm;                                   // [NG][NQ][k] partials (cta_gemm's panel space)
     double* sd = sm + (size_t)NG * NQ * k;             // d
     for (int j = tid; j < k; j += nt) sd[j] = d[j];
