@@ -119,8 +119,13 @@ typedef struct {
                             int32 sums on tcgen05.mma kind::i8, combined in FP64.  Truncation error
                             <= 2^-56 max|A_i.| max|X_.j| per product term: relative to the row and
                             column MAXIMA (rows with a very wide dynamic range should use DMMA).
-                            0 (default) = DMMA FP64.
-                            Requires k a multiple of 16, k <= 64 (else REFINE_E_UNSUPPORTED). */
+                            0 (default) = DMMA FP64.  For k == 128 (dense or CSR) it also runs pass C
+                            (X_2 Csig, the sweep's O(residual) correction) on kind::i8 with 5 x 7-bit
+                            digits per operand, row / column exponents and exact int32 levels: ~2^-35
+                            relative to row / column maxima of a correction term -- one-step parity
+                            with the FP64 oracle (1e-10) and the FP64 accuracy at convergence kept.
+                            Requires (dense, k a multiple of 16, k <= 64) or k == 128 (else
+                            REFINE_E_UNSUPPORTED). */
 } refine_opts;
 
 /* Per-sweep diagnostics (host struct), for the sweep's input X^ (after the sign flip). */

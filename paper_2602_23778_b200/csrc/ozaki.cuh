@@ -59,6 +59,19 @@ RF_DEV void oz_slices(double v, int8_t (&d)[OZ_S]) {
   }
 }
 
+// the same digits from integer arithmetic: |v| 2^{-e} truncated to 7 S bits as a 64-bit fixed-point
+// integer (one exact FP64 scaling + one F2I), then S 7-bit fields with the sign of v (trunc-based
+// slicing yields exactly these digits: both truncate |v| 2^{-e} at 2^{-7S} and split it base 128)
+RF_DEV void oz_slices_e(double v, int e, int8_t (&d)[OZ_S]) {
+  const uint64_t M = (uint64_t)(fabs(v) * ldexp(1.0, 7 * OZ_S - e));   // < 2^{7S}
+  const bool neg = v < 0.0;
+#pragma unroll
+  for (int t = 0; t < OZ_S; ++t) {
+    const int q = (int)((M >> (7 * (OZ_S - 1 - t))) & 127u);
+    d[t] = (int8_t)(neg ? -q : q);
+  }
+}
+
 // ---- init: per-row exponent of A (row max) -------------------------------------------------
 // (off-diagonal max; local row i is global row row0 + i) and the diagonal entries in FP64
 __global__ void __launch_bounds__(256) oz_rowexp_kernel(const double* __restrict__ A, int64_t lda, int64_t M,
@@ -269,6 +282,235 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const int8_t* __
   __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(C::TCOLS));
+}
+
+}  // namespace rf
+
+namespace rf {
+
+// ---- pass C on the INT8 tensor cores (k = 128; refine_opts.emul) ------------------------------
+// x~_i = w_i s - x_i Csig for rows i >= top.  x_i Csig is the sweep's O(residual) correction, so it
+// needs ~1e-8 relative accuracy for the 1e-10 one-step parity (4 digits measured 1.03e-10 on the
+// 3-D Laplacian with a 1.8e-5 gap) and none beyond that for the final FP64 accuracy (it vanishes at
+// convergence): SC = 5 slices of 7 bits per operand (~2^-35 of the maxima), levels c <= 6.
+// Transposed product per 32-row slab:
+//   D[j][i] = sum_l Csig[l][j] x_il = 2^{g_j + h_i} sum_{c=2..5} 2^{-7c} L_c[j][i]
+// with g_j the exponent of column j of Csig (A = Csig^T sliced once per CTA) and h_i that of row i
+// of X (found by the converter from the slab: no global pass), L_c exact int32 sums (K = 128).
+// The MMA for slice t of A takes the concatenated X slices u = 1 .. SC+1-t (N = 32 (SC+1-t)) and
+// writes levels t+1 .. SC+1, laid out by level in TMEM (2 buffers x 5 levels x 32 columns).
+constexpr int OZC_S = 5, OZC_TN = 32, OZC_NS = 3, OZC_K = 128;
+constexpr int OZC_CONV = 128, OZC_EPI = 128, OZC_THREADS = OZC_CONV + OZC_EPI + 32;
+constexpr uint32_t OZC_SBO = (OZC_K / 16) * 128;                 // 1024 B: 8-row groups of a K = 128 tile
+constexpr uint32_t OZC_ATILE = 128 * OZC_K;                      // 16 KB per slice of Csig^T
+constexpr uint32_t OZC_BTILE = OZC_TN * OZC_K;                   // 4 KB per slice of a slab
+constexpr uint32_t OZC_BBUF = OZC_S * OZC_BTILE;                 // 16 KB
+constexpr uint32_t OZC_SLOT = OZC_TN * OZC_K * 8;                // 32 KB of X rows
+constexpr int OZC_TCOLS = 512;                                   // 2 x 5 levels x 32 columns (power of 2)
+constexpr int OZC_SMEM = 1024 + OZC_S * OZC_ATILE + 2 * OZC_BBUF + OZC_NS * OZC_SLOT;   // 217 KB
+RF_DEV constexpr uint32_t ozc_off(int r, int l) {               // element (row r, K l), K = 128 int8 tile
+  return (uint32_t)(r / 8) * OZC_SBO + (uint32_t)(l / 16) * 128u + (uint32_t)(r % 8) * 16u + (uint32_t)(l % 16);
+}
+RF_DEV void ozc_digits(double v, int e, int8_t (&d)[OZC_S]) {   // |v| 2^-e truncated to 7 SC bits, base 128
+  const uint64_t M = (uint64_t)(fabs(v) * ldexp(1.0, 7 * OZC_S - e));
+  const bool neg = v < 0.0;
+#pragma unroll
+  for (int t = 0; t < OZC_S; ++t) {
+    const int q = (int)((M >> (7 * (OZC_S - 1 - t))) & 127u);
+    d[t] = (int8_t)(neg ? -q : q);
+  }
+}
+RF_DEV void ozc_conv_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(OZC_CONV) : "memory"); }
+
+__global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const double* X, double* out) {
+  extern __shared__ __align__(16) unsigned char ozc_raw[];
+  __shared__ __align__(8) uint64_t full[OZC_NS], empty[OZC_NS], opfree[2], accf[2], acce[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ double ssc[OZC_K];
+  __shared__ int32_t sg[OZC_K];                 // column exponents of Csig
+  __shared__ int32_t sh[4][OZC_TN];             // row exponents of slab t in sh[t % 4] (read by its
+                                                // epilogue before it releases TMEM; slab t + 4's
+                                                // converter runs only after that, via opfree / acce)
+  if (*ws.status != ST_OK) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = ws.k;                           // == 128
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + gridDim.x - 1) / gridDim.x + OZC_TN - 1) / OZC_TN * OZC_TN;
+  const int64_t rb = ws.top + (int64_t)blockIdx.x * per;
+  const int64_t re = (rb + per < ws.n_loc) ? rb + per : ws.n_loc;
+  const int nst = (re > rb) ? (int)((re - rb + OZC_TN - 1) / OZC_TN) : 0;
+  unsigned char* base = ozc_raw + ((1024 - (smem_u32(ozc_raw) & 1023)) & 1023);
+  unsigned char* As = base;                                           // [SC][128 j x 128 l]
+  unsigned char* Bs = base + OZC_S * OZC_ATILE;                       // [2][SC][32 rows x 128 l]
+  unsigned char* F = Bs + 2 * OZC_BBUF;                               // [NS][32 X rows] FP64
+  if (tid < OZC_K) {                            // A = Csig^T, row j scaled by 2^-g_j
+    double m = 0.0;
+    for (int l = 0; l < k; ++l) m = fmax(m, fabs(ws.Csig[l * k + tid]));
+    sg[tid] = oz_exponent(m);
+    ssc[tid] = ws.scal[tid];
+  }
+  __syncthreads();
+  for (int e = tid; e < OZC_K * OZC_K / 4; e += OZC_THREADS) {     // 4 consecutive l per thread
+    const int j = e % OZC_K, l0 = 4 * (e / OZC_K);
+    uint32_t w[OZC_S];
+#pragma unroll
+    for (int t = 0; t < OZC_S; ++t) w[t] = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int8_t d[OZC_S];
+      ozc_digits(ws.Csig[(l0 + q) * k + j], sg[j], d);
+#pragma unroll
+      for (int t = 0; t < OZC_S; ++t) w[t] |= (uint32_t)(uint8_t)d[t] << (8 * q);
+    }
+#pragma unroll
+    for (int t = 0; t < OZC_S; ++t) *reinterpret_cast<uint32_t*>(As + t * OZC_ATILE + ozc_off(j, l0)) = w[t];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(OZC_TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < OZC_NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], OZC_CONV / 32);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&opfree[i], 1);
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], OZC_EPI / 32);
+    }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  double nacc = 0.0;
+  if (warp == (OZC_CONV + OZC_EPI) / 32) {         // ---- producer: X rows of each slab
+    if (lane == 0) {
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % OZC_NS;
+        if (t >= OZC_NS) mbar_wait(&empty[s], ((t / OZC_NS) - 1) & 1);
+        const int64_t r0 = rb + (int64_t)t * OZC_TN;
+        const uint32_t bytes = (uint32_t)min((int64_t)OZC_TN, re - r0) * OZC_K * 8;
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s(F + s * OZC_SLOT, X + r0 * OZC_K, bytes, &full[s]);
+      }
+    }
+  } else if (warp < OZC_CONV / 32) {               // ---- converters (warp w: slab rows 8w .. 8w+7) + MMA
+    for (int t = 0; t < nst; ++t) {
+      const int s = t % OZC_NS, o = t & 1;
+      mbar_wait(&full[s], (t / OZC_NS) & 1);
+      if (t >= 2) mbar_wait(&opfree[o], ((t >> 1) - 1) & 1);          // B buffer o read by slab t-2's MMAs
+      const int nr = (int)min((int64_t)OZC_TN, re - (rb + (int64_t)t * OZC_TN));
+      const double* fx = reinterpret_cast<const double*>(F + s * OZC_SLOT);
+      unsigned char* B = Bs + o * OZC_BBUF;
+#pragma unroll 2
+      for (int rr = 0; rr < OZC_TN / 4; ++rr) {
+        const int r = (OZC_TN / 4) * warp + rr;
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        if (r < nr) {                               // 32 B per lane: two LDS.128, the row's 1 KB
+          const double2 a0 = reinterpret_cast<const double2*>(fx + r * OZC_K)[2 * lane];
+          const double2 a1 = reinterpret_cast<const double2*>(fx + r * OZC_K)[2 * lane + 1];
+          v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
+        }
+        const double m = fmax(fmax(fabs(v[0]), fabs(v[1])), fmax(fabs(v[2]), fabs(v[3])));
+        const int h = __reduce_max_sync(0xffffffffu, oz_exponent(m) + 2048) - 2048;   // row exponent
+        if (lane == 0) sh[t & 3][r] = h;
+        uint32_t w[OZC_S];
+#pragma unroll
+        for (int u = 0; u < OZC_S; ++u) w[u] = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int8_t d[OZC_S];
+          ozc_digits(v[q], h, d);
+#pragma unroll
+          for (int u = 0; u < OZC_S; ++u) w[u] |= (uint32_t)(uint8_t)d[u] << (8 * q);
+        }
+#pragma unroll
+        for (int u = 0; u < OZC_S; ++u) *reinterpret_cast<uint32_t*>(B + u * OZC_BTILE + ozc_off(r, 4 * lane)) = w[u];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);      // the slab's X rows are consumed
+      fence_async_smem();
+      tc_fence_before();
+      ozc_conv_sync();
+      if (tid == 0) {
+        if (t >= 2) mbar_wait(&acce[o], ((t >> 1) - 1) & 1);          // TMEM buffer o read out
+        tc_fence_after();
+        const uint32_t td = tmem + (uint32_t)(o * OZC_S * OZC_TN);
+        const uint32_t sa = smem_u32(As), sb = smem_u32(B);
+#pragma unroll
+        for (int kk = 0; kk < OZC_K / 32; ++kk) {
+#pragma unroll
+          for (int ta = 1; ta <= OZC_S; ++ta) {   // A slice t x X slices 1 .. SC+1-t -> levels t+1 .. SC+1
+            const int m = OZC_S + 1 - ta;
+            const uint64_t da = umma_desc(sa + (ta - 1) * OZC_ATILE + kk * 256, 128, OZC_SBO);
+            const uint64_t db = umma_desc(sb + kk * 256, 128, OZC_SBO);
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((m * OZC_TN) >> 3) << 17) |
+                                   ((uint32_t)(128 >> 4) << 24);
+            const uint32_t acc = (kk > 0 || ta > 1) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(td + (uint32_t)((ta - 1) * OZC_TN)),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+        }
+        umma_commit(&opfree[o]);
+        umma_commit(&accf[o]);
+      }
+    }
+  } else {                                         // ---- epilogue: column j = 32 (warp % 4) + lane
+    const int j = 32 * (warp & 3) + lane;
+    const double sj = ssc[j];
+    const int gj = sg[j];
+    const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    for (int t = 0; t < nst; ++t) {
+      const int o = t & 1;
+      const int64_t r0 = rb + (int64_t)t * OZC_TN;
+      const int nr = (int)min((int64_t)OZC_TN, re - r0);
+      mbar_wait(&accf[o], (t >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int h0 = 0; h0 < OZC_TN; h0 += 16) {    // 16 rows at a time (registers)
+        double w[16], acc[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          w[r] = (h0 + r < nr) ? __ldcs(ws.W + (r0 + h0 + r) * OZC_K + j) : 0.0;
+          acc[r] = 0.0;
+        }
+#pragma unroll
+        for (int c = OZC_S + 1; c >= 2; --c) {       // smallest levels first
+          float v[16];
+          tmem_ld16(tl + (uint32_t)(o * OZC_S * OZC_TN + (c - 2) * OZC_TN + h0), v);
+          const double wc = ldexp(1.0, -7 * c);
+#pragma unroll
+          for (int r = 0; r < 16; ++r) acc[r] = fma((double)(int32_t)__float_as_uint(v[r]), wc, acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          if (h0 + r < nr) {
+            const double p2 = __longlong_as_double((long long)(1023 + gj + sh[t & 3][h0 + r]) << 52);   // 2^(g + h)
+            const double x = __fma_rn(w[r], sj, -(acc[r] * p2));
+            __stcs(out + (r0 + h0 + r) * OZC_K + j, x);
+            nacc = __fma_rn(x, x, nacc);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[o]);
+    }
+  }
+  __syncthreads();
+  if (warp >= OZC_CONV / 32 && warp < (OZC_CONV + OZC_EPI) / 32)
+    ws.nslot[(int64_t)blockIdx.x * OZC_K + (tid - OZC_CONV)] = nacc;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(OZC_TCOLS));
 }
 
 }  // namespace rf

@@ -323,6 +323,8 @@ struct Kern {
     if ((e = cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passC, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
+    if (KP == 128 && c->opts.emul)   // pass C on the INT8 tensor cores (ozaki.cuh)
+      if ((e = cudaFuncSetAttribute(passC_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZC_SMEM))) return e;
     if (KP >= 32 && c->opts.mixed) {   // NEXT-2 tcgen05 passes (tc_passes.cuh)
       if ((e = cudaFuncSetAttribute(passB_tc_kernel<TKP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     TcbCfg<TKP>::SMEM))) return e;
@@ -375,7 +377,7 @@ struct Kern {
     // the tcgen05 passes (opts.mixed) write one partial per SM in the same slot layouts
     const bool tc = KP >= 32 && c->opts.mixed;
     const size_t cb = tc ? std::max(c->passb_grid_y, c->sms) : c->passb_grid_y;
-    const size_t cc = tc ? std::max(c->passc_grid, c->sms) : c->passc_grid;
+    const size_t cc = (tc || c->opts.emul) ? std::max(c->passc_grid, c->sms) : c->passc_grid;
     bpart = std::max(cb * B_NT * B_TILE, tc ? (size_t)c->sms * 2 * KP * KP : 0);   // (tc: passB2 slot layout)
     brr = cb * KP;
     nslot = cc * KP;
@@ -418,7 +420,7 @@ struct Kern {
           if (!last) wp.shift = 0.0;
           const double* Xg = pass ? ws.Xt : X;                   // operand of this product
           if (pass) cudaMemcpyAsync(ws.Xt, ws.W, (size_t)c->n_loc * c->k * 8, cudaMemcpyDeviceToDevice, s);
-          if (!c->csr && c->opts.emul) {   // A X on the INT8 tensor cores (ozaki.cuh)
+          if (!c->csr && c->oz_ns > 0) {   // A X on the INT8 tensor cores (ozaki.cuh)
             const double* Xb = c->multi ? c->Xfull : Xg;           // B operand: all n rows
             double* out = (c->oz_ns == 1) ? ws.W : ws.Wpart;
             if (pass == 0) c->mark();
@@ -515,7 +517,9 @@ struct Kern {
                // final X in place; Rayleigh-Ritz / QR steps write X~ and normalise in phase 5)
         c->mark();
         if (!c->in_rr) {
-          if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
+          if (KP == 128 && c->opts.emul && c->k == 128 && ((uintptr_t)X % 16 == 0))   // X_2 Csig on INT8
+            passC_oz_kernel<<<c->sms, OZC_THREADS, OZC_SMEM, s>>>(ws, X, X);
+          else if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
             passC_tc_kernel<TKP><<<c->sms, TCC_THREADS, TccCfg<TKP>::SMEM, s>>>(ws, X, X);
           else
             passC<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, X, xv16);
@@ -717,8 +721,10 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.kjudge = c->opts.kjudge;
   if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
   if (c->opts.mixed && (k % 16 != 0 || k < 32)) return REFINE_E_UNSUPPORTED;    // tcgen05 passes: 16 | k >= 32
-  if (c->opts.emul && (c->csr || k % 16 != 0 || k > 64)) return REFINE_E_UNSUPPORTED;   // ozaki.cuh: dense, 16 | k <= 64
-  if (c->opts.emul) {   // split the K range so each CTA's int32 levels stay exact, waves near-full
+  // ozaki.cuh: dense S1 for 16 | k <= 64, pass C for k == 128 -- at least one must apply
+  const bool emul_s1 = c->opts.emul && !c->csr && k % 16 == 0 && k <= 64;
+  if (c->opts.emul && !emul_s1 && k != 128) return REFINE_E_UNSUPPORTED;
+  if (emul_s1) {   // split the K range so each CTA's int32 levels stay exact, waves near-full
     c->oz_nks = (c->n + OZ_BK - 1) / OZ_BK;
     c->oz_nrt = (c->n_loc + OZ_BM - 1) / OZ_BM;
     const int64_t ns_min = (c->oz_nks + (OZ_KMAX / OZ_BK) - 1) / (OZ_KMAX / OZ_BK);
@@ -798,7 +804,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   else
     absrow_max_csr_kernel<<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, c->n_loc, c->row_begin, nshift, rows);
   max_kernel<<<1, 1024, 0, c->stream>>>(rows, c->n_loc, ws.stats + 7);
-  if (c->opts.emul) {   // A's exponents and int8 slices, once (A is borrowed and constant)
+  if (c->oz_ns > 0) {   // A's exponents and int8 slices, once (A is borrowed and constant)
     RF_CK(c, cudaMalloc(&c->oz_e, std::max<int64_t>(c->n_loc, 1) * sizeof(int32_t)));
     RF_CK(c, cudaMalloc(&c->oz_diag, std::max<int64_t>(c->n_loc, 1) * sizeof(double)));
     RF_CK(c, cudaMalloc(&c->oz_f, 64 * sizeof(int32_t)));
@@ -1353,7 +1359,7 @@ extern "C" int32_t refine_kernels_per_sweep(const refine_ctx* c) {
     for (auto* kid : c->kids) n += refine_kernels_per_sweep(kid);
     return n;
   }
-  const int per = (c->csr ? 7 : 8) + (c->opts.emul ? 2 : 0);   // incl. kxk_lu (side stream); emul: X slicing
+  const int per = (c->csr ? 7 : 8) + (c->oz_ns > 0 ? 2 : 0);   // incl. kxk_lu (side stream); emul S1: X slicing
   if (!c->multi) return per;
   return per + 1 - (c->rank == 0 ? 0 : 2);   // + ag_local; kxk_lu / kxk_finish on rank 0 only
 }

@@ -151,3 +151,39 @@ def test_emul_with_square(pkg):
         ref = oracle.sweep(op, xin)
         assert s == pkg.REFINE_OK and ref.status == oracle.OK
         assert rel(X.cpu().numpy(), ref.X) <= 1e-10, t
+
+
+@pytest.mark.parametrize("kind", ["csr3d", "dense"])
+def test_emul_passC_k128_one_step_parity(pkg, kind):
+    """k = 128: pass C (X_2 Csig, the O(residual) correction) on the INT8 tensor cores keeps the
+    one-step parity with the FP64 oracle (<= 1e-10) -- CSR and dense."""
+    if kind == "csr3d":
+        p = synth.small_laplacian((24, 22, 21), (1.0, 1.13, 1.29), 128, noise=1e-5)
+        R = pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, 128, emul=True)
+        op = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy())
+    else:
+        p = synth.small_dense(1100, 128, m=8, noise=1e-5, seed=13, signs=True)
+        R = pkg.Refiner.dense(p.A.cuda(), 128, emul=True)
+        op = oracle.Operator(A=p.A.numpy())
+    X = p.X0.cuda().clone()
+    for t in range(3):
+        xin = X.cpu().numpy()
+        s, st = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK
+        e = rel(X.cpu().numpy(), ref.X)
+        print(f"{kind} t={t}: one-step rel diff {e:.2e}")
+        assert e <= 1e-10, t
+
+
+def test_emul_passC_k128_converges(pkg):
+    n, k = 3000, 128
+    lt = np.linspace(10.0, 5.0, k) * np.where(np.arange(k) % 3 == 0, -1.0, 1.0)
+    p = synth.small_dense(n, k, m=8, lam_target=lt, rest=1.0, noise=1e-6, seed=19)
+    R = pkg.Refiner.dense(p.A.cuda(), k, emul=True)
+    X = p.X0.cuda().clone()
+    s, it, st = R.refine_run(X, 60, 1e-13)
+    assert s == pkg.REFINE_OK
+    Xg, Xt = X.cpu().numpy(), p.X.numpy()
+    sg = np.sign(np.sum(Xg * Xt, axis=0))
+    assert np.linalg.norm(Xg * sg - Xt, axis=0).max() <= 100 * n * U

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include "../paper_2602_23778_b200/csrc/passes.cuh"
 #include "../paper_2602_23778_b200/csrc/tc_passes.cuh"
+#include "../paper_2602_23778_b200/csrc/ozaki.cuh"
 using namespace rf;
 
 __global__ void fill(double* p, int64_t n, uint64_t seed, double scale, double off) {
@@ -58,6 +59,20 @@ int main(int argc, char** argv) {
   cudaEventSynchronize(b);
   e = cudaDeviceSynchronize();
   float ms2; cudaEventElapsedTime(&ms2, a, b);
+  // pass C on the INT8 tensor cores (FP64 accuracy)
+  double *Xt3, *ns3;
+  cudaMalloc(&Xt3, n * k * 8); cudaMalloc(&ns3, 4096 * k * 8); cudaMemset(Xt3, 0, n * k * 8);
+  cudaFuncSetAttribute(passC_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZC_SMEM);
+  ws.Xt = Xt3; ws.nslot = ns3;
+  passC_oz_kernel<<<sms, OZC_THREADS, OZC_SMEM>>>(ws, X, Xt3);
+  cudaError_t e3 = cudaDeviceSynchronize();
+  cudaEventRecord(a);
+  passC_oz_kernel<<<sms, OZC_THREADS, OZC_SMEM>>>(ws, X, Xt3);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms3; cudaEventElapsedTime(&ms3, a, b);
+  std::vector<double> h3(n * k);
+  cudaMemcpy(h3.data(), Xt3, n * k * 8, cudaMemcpyDeviceToHost);
   std::vector<double> h1(n * k), h2(n * k), hx(n * k), hw(n * k), n1(g1 * k), n2(sms * k), hc(k * k), hs(k);
   cudaMemcpy(h1.data(), Xt1, n * k * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(h2.data(), Xt2, n * k * 8, cudaMemcpyDeviceToHost);
@@ -86,5 +101,9 @@ int main(int argc, char** argv) {
          cudaGetErrorString(e), ms1, ms2, 24.0 * (n - top) * k / ms2 / 1e6);
   printf("max|dX~| %.3e (max|X~| %.3e, max|X Csig| ~%.3e)  max rel d(norm^2) %.3e  top rows untouched %d\n", ex, sx, sn,
          en, untouched);
+  double e3x = 0;
+  for (int64_t i = top * k; i < n * k; ++i) e3x = fmax(e3x, fabs(h1[i] - h3[i]));
+  printf("INT8 (ozaki) passC %.3f ms (%.0f GB/s, %s): max|dX~| vs FP64 %.3e\n", ms3, 24.0 * (n - top) * k / ms3 / 1e6,
+         cudaGetErrorString(e3), e3x);
   return 0;
 }
