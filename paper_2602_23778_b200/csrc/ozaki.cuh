@@ -407,30 +407,50 @@ __global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const d
       const int nr = (int)min((int64_t)OZC_TN, re - (rb + (int64_t)t * OZC_TN));
       const double* fx = reinterpret_cast<const double*>(F + s * OZC_SLOT);
       unsigned char* B = Bs + o * OZC_BBUF;
+      // warp w owns slab rows 8w .. 8w+7.  (1) row exponents: lanes read 4 values of a row each,
+      // redux.max of the exponents; (2) digits: lane (r8 = lane / 4, c = lane % 4) converts values
+      // 16 g + 4 c .. +3 of row 8w + r8, so one store instruction fills a whole 8-row x 16-byte core
+      // matrix (32 distinct banks)
+      constexpr int RPW = OZC_TN / 4;               // rows per converter warp (8)
 #pragma unroll 2
-      for (int rr = 0; rr < OZC_TN / 4; ++rr) {
-        const int r = (OZC_TN / 4) * warp + rr;
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        if (r < nr) {                               // 32 B per lane: two LDS.128, the row's 1 KB
+      for (int rr = 0; rr < RPW; ++rr) {
+        const int r = RPW * warp + rr;
+        double m = 0.0;
+        if (r < nr) {
           const double2 a0 = reinterpret_cast<const double2*>(fx + r * OZC_K)[2 * lane];
           const double2 a1 = reinterpret_cast<const double2*>(fx + r * OZC_K)[2 * lane + 1];
-          v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
+          m = fmax(fmax(fabs(a0.x), fabs(a0.y)), fmax(fabs(a1.x), fabs(a1.y)));
         }
-        const double m = fmax(fmax(fabs(v[0]), fabs(v[1])), fmax(fabs(v[2]), fabs(v[3])));
         const int h = __reduce_max_sync(0xffffffffu, oz_exponent(m) + 2048) - 2048;   // row exponent
         if (lane == 0) sh[t & 3][r] = h;
-        uint32_t w[OZC_S];
+      }
+      __syncwarp();
+      {
+        const int r = RPW * warp + (lane >> 2), c = lane & 3;
+        const int h = sh[t & 3][r];
+        const bool ok = r < nr;
+#pragma unroll 2
+        for (int g = 0; g < OZC_K / 16; ++g) {
+          const int l0 = 16 * g + 4 * c;
+          double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+          if (ok) {
+            a0 = *reinterpret_cast<const double2*>(fx + r * OZC_K + l0);
+            a1 = *reinterpret_cast<const double2*>(fx + r * OZC_K + l0 + 2);
+          }
+          const double v[4] = {a0.x, a0.y, a1.x, a1.y};
+          uint32_t w[OZC_S];
 #pragma unroll
-        for (int u = 0; u < OZC_S; ++u) w[u] = 0u;
+          for (int u = 0; u < OZC_S; ++u) w[u] = 0u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          int8_t d[OZC_S];
-          ozc_digits(v[q], h, d);
+          for (int q = 0; q < 4; ++q) {
+            int8_t d[OZC_S];
+            ozc_digits(v[q], h, d);
 #pragma unroll
-          for (int u = 0; u < OZC_S; ++u) w[u] |= (uint32_t)(uint8_t)d[u] << (8 * q);
+            for (int u = 0; u < OZC_S; ++u) w[u] |= (uint32_t)(uint8_t)d[u] << (8 * q);
+          }
+#pragma unroll
+          for (int u = 0; u < OZC_S; ++u) *reinterpret_cast<uint32_t*>(B + u * OZC_BTILE + ozc_off(r, l0)) = w[u];
         }
-#pragma unroll
-        for (int u = 0; u < OZC_S; ++u) *reinterpret_cast<uint32_t*>(B + u * OZC_BTILE + ozc_off(r, 4 * lane)) = w[u];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);      // the slab's X rows are consumed
