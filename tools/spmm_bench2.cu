@@ -159,7 +159,13 @@ int main(int argc, char** argv) {
     Prob p = make(160, 160, 160, 128);
     double* Wref = prod_case<2, 32>("cfg5", p, sms);
     gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32);
-    for (int ty : {4, 8, 16, 32}) gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32, make_int4(5, 160, ty, 160));
+    const int4 o = make_int4(5, 160, 16, 160);
+    gather_case<128, 0, 0, 2, 7>("cfg5", p, sms, Wref, 32, o);
+    gather_case<128, 0, 0, 3, 7>("cfg5", p, sms, Wref, 32, o);
+    gather_case<128, 0, 0, 3, 4>("cfg5", p, sms, Wref, 32, o);
+    gather_case<128, 0, 0, 4, 4>("cfg5", p, sms, Wref, 32, o);
+    gather_case<128, 0, 0, 3, 3>("cfg5", p, sms, Wref, 32, o);
+    gather_case<128, 0, 0, 2, 4>("cfg5", p, sms, Wref, 32, o);
   }
   return 0;
 }
