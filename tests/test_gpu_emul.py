@@ -187,3 +187,21 @@ def test_emul_passC_k128_converges(pkg):
     Xg, Xt = X.cpu().numpy(), p.X.numpy()
     sg = np.sign(np.sum(Xg * Xt, axis=0))
     assert np.linalg.norm(Xg * sg - Xt, axis=0).max() <= 100 * n * U
+
+
+def test_emul_passC_loopback_and_with_mixed(pkg):
+    """k = 128 pass C on INT8 on emulated ranks (row partition) and together with the tcgen05
+    pass B of NEXT-2 (mixed + emul): one-step results against the oracle."""
+    p = synth.small_dense(1100, 128, m=8, noise=1e-5, seed=13, signs=True)
+    op = oracle.Operator(A=p.A.numpy())
+    xin = p.X0.numpy()
+    ref = oracle.sweep(op, xin)
+    X = p.X0.cuda().clone()
+    s, _ = pkg.Refiner.dense(p.A.cuda(), 128, emul=True, world=3).refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK and rel(X.cpu().numpy(), ref.X) <= 1e-10
+    X = p.X0.cuda().clone()
+    s, _ = pkg.Refiner.dense(p.A.cuda(), 128, emul=True, mixed=1).refine_sweep(X, stats=True)
+    assert s == pkg.REFINE_OK
+    sig = np.where(np.sum(ref.X * xin, axis=0) < 0, -1.0, 1.0)
+    corr = np.linalg.norm(ref.X - xin * sig)
+    assert np.linalg.norm(X.cpu().numpy() - ref.X) <= 1e-2 * corr + 1e-10 * np.linalg.norm(ref.X)
