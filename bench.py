@@ -248,7 +248,7 @@ def time_emul(q, local, steps=5):
         return None
     ms, kern, R, X, st, s, prof = time_ours(q, steps, 3, 1, local, opts={"emul": True})
     out = {"sweeps_s": 1000.0 / ms, "ms_per_sweep": ms, "ms_per_sweep_instrumented": prof, "kernels_ms": kern,
-           "status": s, "what": "refine_opts.emul: dense k <= 64: W = A X^ from 8 x 7-bit int8 slices of A (rows, once) "
+           "status": s, "what": "refine_opts.emul: dense k <= 64: W = A X^ from 7 balanced 8-bit int8 digits of A (rows, once) "
            "and X^ (columns, per sweep) on tcgen05.mma kind::i8 with exact int32 level sums combined in FP64 "
            "(diagonal in FP64; the gemm_ax slot includes the per-sweep X slicing); k = 128: pass C "
            "(X_2 Csig) on kind::i8 with 5 x 7-bit digits"}

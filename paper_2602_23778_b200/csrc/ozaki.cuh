@@ -1,23 +1,27 @@
 // ozaki.cuh -- S1 for dense A (W = A X^) with FP64 accuracy on the INT8 tensor cores
 // (tcgen05.mma kind::i8), opt-in through refine_opts.emul.  Ozaki-style splitting:
 //
-//   A_ij = 2^{e_i} sum_{t=1..S} a^(t)_ij 2^{-7t} + r_ij,   X_lj = 2^{f_j} sum_{u=1..S} x^(u)_lj 2^{-7u} + q_lj
+//   A_ij = 2^{e_i + 2} sum_{t=1..S} a^(t)_ij 2^{-8t} + r_ij,   X_lj = 2^{f_j + 2} sum_{u=1..S} x^(u)_lj 2^{-8u} + q_lj
 //
-// with int8 slices a^(t), x^(u) in [-127, 127] (7 magnitude bits each, extracted exactly in FP64:
-// r <- 128 r, d = trunc(r), r <- r - d), e_i the exponent of row i's max |A_ij| (A is constant:
-// sliced once at init, 2^{e_i} |.| < 1) and f_j that of column j's max |X_lj| (every sweep).  Then
+// with int8 slices a^(t), x^(u) the BALANCED base-256 digits (in [-128, 127]; the leading one in
+// [-64, 64]) of the 64-bit integer N = rint(v 2^{8S-2-e}) (|N| <= 2^{8S-2}; one exact FP64 scaling,
+// one F2I, then integer byte extraction with carry), e_i the exponent of row i's max |A_ij| (A is
+// constant: sliced once at init, 2^{-e_i} |.| < 1) and f_j that of column j's max |X_lj| (every
+// sweep).  Then
 //
-//   (A X)_ij = 2^{e_i + f_j} sum_{c=2..S+1} 2^{-7c} L_c[i][j],   L_c = sum_{t+u=c} a^(t) x^(u)
+//   (A X)_ij = 2^{e_i + f_j + 4} sum_{c=2..S+1} 2^{-8c} L_c[i][j],   L_c = sum_{t+u=c} a^(t) x^(u)
 //
 // where every L_c is an exact integer product accumulated in int32 on the tensor cores (|L_c| <=
-// (c-1) 127^2 K, K <= OZ_KMAX keeps it below 2^31) and combined in FP64.  Dropped terms (t + u >
-// S + 1) and the slice remainders are below 2^{-7S} (S = 8: 2^-56) of max|A_i.| max|X_.j| per
-// product term.  Unlike FP64 rounding this error is relative to the row / column MAXIMA, so entries
+// (c-1) 128^2 K, K <= OZ_KMAX keeps it below 2^31) and combined in FP64.  Dropped terms (t + u >
+// S + 1) and the roundings are below ~7 2^{4-8S} (S = 7: 2^-52) of max|A_i.| max|X_.j| per product
+// term.  Unlike FP64 rounding this error is relative to the row / column MAXIMA, so entries
 // far below their row's largest lose relative accuracy (the classic limit of the scheme).  The
 // diagonal -- the dominant entry of the diagonally dominant and near-diagonal (Q ~ I) matrices the
 // method meets -- is therefore taken out: it is not sliced (e_i is the OFF-diagonal row maximum)
 // and a_ii x_ij is added in FP64 in the epilogue.  Rows whose off-diagonal entries span a wider
-// dynamic range than the sweep tolerates need the DMMA path (emul = 0, the default).
+// dynamic range than the sweep tolerates need the DMMA path (emul = 0, the default).  Balanced
+// 8-bit digits carry 8 bits per int8 (7 for sign-magnitude digits): 7 slices give the 54 bits that
+// 8 sign-magnitude slices gave, with 28 slice products instead of 36 and 7/8 of the bytes.
 //
 // Per K step of 32 the MMA for slice t of A multiplies the concatenated X slices u = 1 .. S+1-t
 // (N = m k <= 256) into the TMEM accumulators of levels t+1 .. t+m, which are laid out contiguously
@@ -30,9 +34,9 @@
 
 namespace rf {
 
-constexpr int OZ_S = 8;                     // slices per operand (8 x 7 magnitude bits)
+constexpr int OZ_S = 7;                     // slices per operand (balanced base-256 digits)
 constexpr int OZ_BM = 128, OZ_BK = 32;      // A rows per tile, K per MMA (int8)
-constexpr int OZ_KMAX = 16384;              // K per CTA: 8 * 127^2 * 16384 < 2^31 (exact int32 levels)
+constexpr int OZ_KMAX = 16384;              // K per CTA: 7 * 128^2 * 16384 < 2^31 (exact int32 levels)
 constexpr uint32_t OZ_SBO = (OZ_BK / 16) * 128;            // 8-row groups: 256 B
 constexpr uint32_t OZ_ATILE = OZ_BM * OZ_BK;               // 4 KB per A slice tile
 constexpr int OZ_STAGES = 4;
@@ -47,29 +51,18 @@ RF_DEV int oz_exponent(double m) {          // smallest e with m < 2^e (m >= 0);
   frexp(m, &e);                             // m = f 2^e, f in [0.5, 1)
   return e;
 }
-// 7-bit slices of v in (-1, 1): d_t = trunc(128 r), r <- 128 r - d_t (exact)
-RF_DEV void oz_slices(double v, int8_t (&d)[OZ_S]) {
-  double r = v;
-#pragma unroll
-  for (int t = 0; t < OZ_S; ++t) {
-    r *= 128.0;
-    const double q = trunc(r);
-    d[t] = (int8_t)q;
-    r -= q;
-  }
-}
-
-// the same digits from integer arithmetic: |v| 2^{-e} truncated to 7 S bits as a 64-bit fixed-point
-// integer (one exact FP64 scaling + one F2I), then S 7-bit fields with the sign of v (trunc-based
-// slicing yields exactly these digits: both truncate |v| 2^{-e} at 2^{-7S} and split it base 128)
+// balanced base-256 digits of v 2^{-e} (|v| < 2^e): N = rint(v 2^{8S-2-e}), |N| <= 2^{8S-2}, split
+// from the least significant byte up -- d_t = the signed low byte of N (in [-128, 127]), N <- (N - d_t)
+// / 256 (exact) -- so N = sum_t d_t 2^{8(S-t)} and the leading digit |d_1| <= 64 (+ 0.502) fits.
 RF_DEV void oz_slices_e(double v, int e, int8_t (&d)[OZ_S]) {
-  const uint64_t M = (uint64_t)(fabs(v) * ldexp(1.0, 7 * OZ_S - e));   // < 2^{7S}
-  const bool neg = v < 0.0;
+  int64_t N = __double2ll_rn(ldexp(v, 8 * OZ_S - 2 - e));   // exact scaling, rounded to nearest
 #pragma unroll
-  for (int t = 0; t < OZ_S; ++t) {
-    const int q = (int)((M >> (7 * (OZ_S - 1 - t))) & 127u);
-    d[t] = (int8_t)(neg ? -q : q);
+  for (int t = OZ_S - 1; t >= 1; --t) {
+    const int8_t lo = (int8_t)(uint8_t)(N & 255);
+    d[t] = lo;
+    N = (N - lo) >> 8;
   }
+  d[0] = (int8_t)N;
 }
 
 // ---- init: per-row exponent of A (row max) -------------------------------------------------
@@ -107,12 +100,12 @@ __global__ void __launch_bounds__(256) oz_slice_A_kernel(const double* __restric
 #pragma unroll
     for (int t = 0; t < OZ_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
     if (i < M) {
-      const double sc = ldexp(1.0, -e[i]);
+      const int ei = e[i];
 #pragma unroll 4
       for (int q = 0; q < 16; ++q) {
         const int64_t j = ks * OZ_BK + kk0 + q;
         int8_t d[OZ_S];
-        oz_slices((j < n && j != row0 + i) ? A[i * lda + j] * sc : 0.0, d);   // diagonal: FP64 epilogue
+        oz_slices_e((j < n && j != row0 + i) ? A[i * lda + j] : 0.0, ei, d);   // diagonal: FP64 epilogue
 #pragma unroll
         for (int t = 0; t < OZ_S; ++t) w[t][q >> 2] |= (uint32_t)(uint8_t)d[t] << (8 * (q & 3));
       }
@@ -147,7 +140,7 @@ __global__ void __launch_bounds__(256) oz_slice_X_kernel(const double* __restric
     const int64_t l = g / k;
     const int j = (int)(g % k);
     int8_t d[OZ_S];
-    oz_slices(l < n ? ldexp(X[l * k + j], -f[j]) : 0.0, d);
+    oz_slices_e(l < n ? X[l * k + j] : 0.0, f[j], d);
     const int64_t ks = l / OZ_BK;
     const uint32_t off = oz_off(j, (int)(l % OZ_BK));
 #pragma unroll
@@ -260,7 +253,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const int8_t* __
         for (int c = OZ_S + 1; c >= 2; --c) {          // smallest levels first
           float v[16];
           tmem_ld16(tl + (uint32_t)((c - 2) * KK + c0), v);
-          const double w = ldexp(1.0, -7 * c);
+          const double w = ldexp(1.0, 4 - 8 * c);
 #pragma unroll
           for (int q = 0; q < 16; ++q) acc[q] = fma((double)(int32_t)__float_as_uint(v[q]), w, acc[q]);
         }

@@ -40,7 +40,7 @@ def test_emul_one_step_parity(pkg, n, k):
         assert s == pkg.REFINE_OK and ref.status == oracle.OK
         assert rel(X.cpu().numpy(), ref.X) <= 1e-10, t
         assert st.flipped == ref.stats.flipped and st.delta_hits == ref.stats.delta_hits
-        # (near convergence rel_resid ~ 1e-9 is W's own rounding; the two W differ by ~2^-56 |A||X|)
+        # (near convergence rel_resid ~ 1e-9 is W's own rounding; the two W differ by ~2^-54 |A||X|)
         assert abs(st.rel_resid - ref.stats.rel_resid) <= 1e-8 * ref.stats.rel_resid + 1e-16
 
 
@@ -56,12 +56,13 @@ def test_emul_w_within_scheme_bound(pkg):
     Wd = Rd.debug(pkg.DBG_W).cpu().numpy()
     We = Re.debug(pkg.DBG_W).cpu().numpy()
     An, Xn = p.A.numpy(), p.X0.numpy()
-    # the scheme's bound (ozaki.cuh): per product term, slices truncated at 2^-7S of the row max of A
-    # (off-diagonal; the diagonal is exact FP64) and of the column max of X, plus the dropped slice
-    # products t + u > S + 1 (< S 2^-7S of max x max) -> (S + 1) 2^(2 - 7S) n max|A_i.| max|X_.j|,
-    # plus the FP64 rounding of the DMMA side (n u |A||X|).  S = 8.
+    # the scheme's bound (ozaki.cuh): per product term, both operands rounded at 2^-55 of 2^e (e the
+    # exponent of the off-diagonal row max of A -- the diagonal is exact FP64 -- or of the column max
+    # of X; 2^e < 2 max), plus the dropped slice products t + u > S + 1 (16 (S - 1) 128^2 2^-8(S+2)
+    # (1 + 2^-8 + ...) < 6.1 2^-54 for S = 7) -> 8.2 2^-54 2^(e + f) < 8.2 2^(2 - 54) n max|A_i.| max|X_.j|,
+    # plus the FP64 rounding of the DMMA side (n u |A||X|).
     Aoff = np.abs(An - np.diag(np.diag(An)))
-    bound = n * U * (np.abs(An) @ np.abs(Xn)) + 9 * 2.0 ** (2 - 56) * n * Aoff.max(1)[:, None] * np.abs(Xn).max(0)[None, :]
+    bound = n * U * (np.abs(An) @ np.abs(Xn)) + 8.2 * 2.0 ** (2 - 54) * n * Aoff.max(1)[:, None] * np.abs(Xn).max(0)[None, :]
     ratio = np.abs(We - Wd) / bound
     print(f"max |W_emul - W_dmma| / bound = {ratio.max():.2e}, / (|A||X|) = "
           f"{np.max(np.abs(We - Wd) / (np.abs(An) @ np.abs(Xn))):.2e}")
@@ -73,7 +74,10 @@ def test_emul_converges(pkg):
     p = synth.small_dense(n, k, m=8, noise=1e-6, seed=29)
     R = pkg.Refiner.dense(p.A.cuda(), k, emul=True)
     X = p.X0.cuda().clone()
-    s, it, st = R.refine_run(X, 60, 1e-13)
+    # corr_norm's floor is W's error, here the scheme's (relative to row / column maxima, ozaki.cuh):
+    # 2e-13 .. 5e-13 measured at this size (DMMA: 7e-14 .. 1.7e-13), so the stopping tolerance is 1e-12;
+    # the accuracy bar below is the same as on DMMA
+    s, it, st = R.refine_run(X, 60, 1e-12)
     assert s == pkg.REFINE_OK
     Xg, Xt = X.cpu().numpy(), p.X.numpy()
     sg = np.sign(np.sum(Xg * Xt, axis=0))
@@ -182,7 +186,10 @@ def test_emul_passC_k128_converges(pkg):
     p = synth.small_dense(n, k, m=8, lam_target=lt, rest=1.0, noise=1e-6, seed=19)
     R = pkg.Refiner.dense(p.A.cuda(), k, emul=True)
     X = p.X0.cuda().clone()
-    s, it, st = R.refine_run(X, 60, 1e-13)
+    # corr_norm's floor is W's error, here the scheme's (relative to row / column maxima, ozaki.cuh):
+    # 2e-13 .. 5e-13 measured at this size (DMMA: 7e-14 .. 1.7e-13), so the stopping tolerance is 1e-12;
+    # the accuracy bar below is the same as on DMMA
+    s, it, st = R.refine_run(X, 60, 1e-12)
     assert s == pkg.REFINE_OK
     Xg, Xt = X.cpu().numpy(), p.X.numpy()
     sg = np.sign(np.sum(Xg * Xt, axis=0))
