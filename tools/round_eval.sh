@@ -20,6 +20,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pas
   -o $O/full_cfg5 python bench.py --config cfg5 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"passB_tc|passC_tc" -c 2 \
   -o $O/full_cfg5_mixed python bench.py --config cfg5 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"oz_gemm" -s 1 -c 1 \
+  -o $O/full_cfg3_emul python tools/emul_run.py cfg3 3 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"passC_oz" -s 1 -c 1 \
+  -o $O/full_cfg5_emul python tools/emul_run.py cfg5 3 > /dev/null 2>&1
 ls -la $O
 cat $O/pytest_gpu.txt $O/smoke.txt
 # summaries on the box (the .ncu-rep files can exceed gpurun's 64 MiB copy-back limit)
@@ -28,4 +32,6 @@ python tools/ncu_summary.py report $O/full_cfg3_gemm.ncu-rep $O/ncu_gemm_cfg3.js
 python tools/ncu_summary.py report $O/full_cfg4.ncu-rep $O/ncu_cfg4.json > /dev/null
 python tools/ncu_summary.py report $O/full_cfg5.ncu-rep $O/ncu_cfg5.json > /dev/null
 python tools/ncu_summary.py report $O/full_cfg5_mixed.ncu-rep $O/ncu_cfg5_mixed.json > /dev/null
+python tools/ncu_summary.py report $O/full_cfg3_emul.ncu-rep $O/ncu_cfg3_emul.json > /dev/null
+python tools/ncu_summary.py report $O/full_cfg5_emul.ncu-rep $O/ncu_cfg5_emul.json > /dev/null
 [ -n "$KEEP_REPS" ] || rm -f $O/*.ncu-rep
