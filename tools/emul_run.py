@@ -1,0 +1,15 @@
+"""A few sweeps of one config with refine_opts.emul (for ncu captures of oz_gemm / passC_oz).
+  python tools/emul_run.py cfg3 [sweeps]"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, synth, paper_2602_23778_b200 as pkg
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+p = synth.make_config(name, device="cuda")
+R = (pkg.Refiner.dense(p.A, p.k, emul=True) if p.kind == "dense" else
+     pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, emul=True))
+X = p.X0.clone()
+for _ in range(sweeps):
+    s, st = R.refine_sweep(X, stats=True)
+torch.cuda.synchronize()
+print(name, "status", s, "rel_resid", st.rel_resid)
