@@ -113,12 +113,13 @@ typedef struct {
                             FP64 pass is compute bound; 2: both passes on tcgen05 at every k.  Rayleigh-Ritz and
                             reorthogonalisation steps always run in FP64 (their products are O(1)). */
   int32_t emul;          /* dense A only: 1 = S1 (W = A X^) with FP64 accuracy on the INT8 tensor cores
-                            (Ozaki splitting, ozaki.cuh): A's rows are scaled to their max and cut into
-                            8 int8 slices of 7 bits ONCE at init (n_loc x n x 8 bytes extra device
-                            memory), X^'s columns likewise every sweep; the slice products are exact
-                            int32 sums on tcgen05.mma kind::i8, combined in FP64.  Truncation error
-                            <= 2^-56 max|A_i.| max|X_.j| per product term: relative to the row and
-                            column MAXIMA (rows with a very wide dynamic range should use DMMA).
+                            (Ozaki splitting, ozaki.cuh): A's rows are scaled to their off-diagonal
+                            max and cut into 7 balanced base-256 int8 digits (54 bits) ONCE at init
+                            (n_loc x n x 7 bytes extra device memory; the diagonal stays FP64), X^'s
+                            columns likewise every sweep; the slice products are exact int32 sums on
+                            tcgen05.mma kind::i8, combined in FP64.  Error <= ~2^-50 max|A_i.| max|X_.j|
+                            per product term: relative to the row and column MAXIMA (rows with a very
+                            wide dynamic range should use DMMA).
                             0 (default) = DMMA FP64.  For k == 128 (dense or CSR) it also runs pass C
                             (X_2 Csig, the sweep's O(residual) correction) on kind::i8 with 5 x 7-bit
                             digits per operand, row / column exponents and exact int32 levels: ~2^-35
