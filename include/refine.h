@@ -117,7 +117,7 @@ typedef struct {
                             max and cut into 7 balanced base-256 int8 digits (54 bits) ONCE at init
                             (n_loc x n x 7 bytes extra device memory; the diagonal stays FP64), X^'s
                             columns likewise every sweep; the slice products are exact int32 sums on
-                            tcgen05.mma kind::i8, combined in FP64.  Error <= ~2^-50 max|A_i.| max|X_.j|
+                            tcgen05.mma kind::i8, combined in FP64.  Error <= 8.2 2^-52 max|A_i.| max|X_.j|
                             per product term: relative to the row and column MAXIMA (rows with a very
                             wide dynamic range should use DMMA).
                             0 (default) = DMMA FP64.  For k == 128 (dense or CSR) it also runs pass C
