@@ -293,7 +293,7 @@ namespace rf {
 // The MMA for slice t of A takes the concatenated X slices u = 1 .. SC+1-t (N = 32 (SC+1-t)) and
 // writes levels t+1 .. SC+1, laid out by level in TMEM (2 buffers x 5 levels x 32 columns).
 constexpr int OZC_S = 5, OZC_TN = 32, OZC_NS = 3, OZC_K = 128;
-constexpr int OZC_CONV = 128, OZC_EPI = 128, OZC_THREADS = OZC_CONV + OZC_EPI + 32;
+constexpr int OZC_CONV = 128, OZC_EPI = 128, OZC_THREADS = OZC_CONV + OZC_EPI + 32 + 32;   // + producer, MMA
 constexpr uint32_t OZC_SBO = (OZC_K / 16) * 128;                 // 1024 B: 8-row groups of a K = 128 tile
 constexpr uint32_t OZC_ATILE = 128 * OZC_K;                      // 16 KB per slice of Csig^T
 constexpr uint32_t OZC_BTILE = OZC_TN * OZC_K;                   // 4 KB per slice of a slab
@@ -313,11 +313,10 @@ RF_DEV void ozc_digits(double v, int e, int8_t (&d)[OZC_S]) {   // |v| 2^-e trun
     d[t] = (int8_t)(neg ? -q : q);
   }
 }
-RF_DEV void ozc_conv_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(OZC_CONV) : "memory"); }
 
 __global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const double* X, double* out) {
   extern __shared__ __align__(16) unsigned char ozc_raw[];
-  __shared__ __align__(8) uint64_t full[OZC_NS], empty[OZC_NS], opfree[2], accf[2], acce[2];
+  __shared__ __align__(8) uint64_t full[OZC_NS], empty[OZC_NS], opfree[2], cvd[2], accf[2], acce[2];
   __shared__ uint32_t tmem_base;
   __shared__ double ssc[OZC_K];
   __shared__ int32_t sg[OZC_K];                 // column exponents of Csig
@@ -370,6 +369,7 @@ __global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const d
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&opfree[i], 1);
+      mbar_init(&cvd[i], OZC_CONV);
       mbar_init(&accf[i], 1);
       mbar_init(&acce[i], OZC_EPI / 32);
     }
@@ -447,14 +447,19 @@ __global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const d
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);      // the slab's X rows are consumed
-      fence_async_smem();
-      tc_fence_before();
-      ozc_conv_sync();
-      if (tid == 0) {
+      fence_async_smem();                         // digit stores -> the tensor core's async proxy
+      mbar_arrive(&cvd[o]);
+    }
+  } else if (warp == (OZC_CONV + OZC_EPI) / 32 + 1) {   // ---- MMA issue (one thread), decoupled from the converters
+    if (lane == 0) {
+      const uint32_t sa = smem_u32(As);
+      for (int t = 0; t < nst; ++t) {
+        const int o = t & 1;
+        mbar_wait(&cvd[o], (t >> 1) & 1);                              // B buffer o converted
         if (t >= 2) mbar_wait(&acce[o], ((t >> 1) - 1) & 1);          // TMEM buffer o read out
         tc_fence_after();
+        const uint32_t sb = smem_u32(Bs + o * OZC_BBUF);
         const uint32_t td = tmem + (uint32_t)(o * OZC_S * OZC_TN);
-        const uint32_t sa = smem_u32(As), sb = smem_u32(B);
 #pragma unroll
         for (int kk = 0; kk < OZC_K / 32; ++kk) {
 #pragma unroll

@@ -122,7 +122,7 @@ RF_DEV constexpr uint32_t kmaj_off(int r, int k, uint32_t sbo) {
 //     control, header) and released for the next block; at the end the second sum is written to
 //     the CTA's FP64 partial.
 constexpr int TCB_K = 128, TCB_N = 256, TCB_NO = 2, TCB_CONV = 256;
-constexpr int TCB_THREADS = TCB_CONV + 32 + 128;
+constexpr int TCB_THREADS = TCB_CONV + 32 + 128 + 32;   // converters, producer, drain, MMA issue
 constexpr int TCB_KC = 512;   // rows per TMEM block (tools/tcb_test.cu: 2048 -> 512 cuts the G error 2.6x, +1.6% time)
 // Per padded width KP: TK rows per stage (a 16 KB FP64 slab of X, and one of W, at every KP), NS
 // ring slots, the UMMA operand buffer (A = X^T padded to M = 128 rows, B = [R | X] with N = 2k rows).
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   using C = TcbCfg<KP>;
   constexpr int TK = C::TK, NS = C::NS;
   extern __shared__ __align__(16) unsigned char tcb_smem[];
-  __shared__ __align__(8) uint64_t full[NS], empty[NS], mmad[TCB_NO], accf[2], acce[2];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS], mmad[TCB_NO], conv[TCB_NO], accf[2], acce[2];
   __shared__ uint32_t tmem_base;
   __shared__ double sd[KP];
   if (*ws.status != ST_OK) return;
@@ -187,7 +187,10 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], TCB_CONV / 32);
     }
-    for (int i = 0; i < TCB_NO; ++i) mbar_init(&mmad[i], 1);
+    for (int i = 0; i < TCB_NO; ++i) {
+      mbar_init(&mmad[i], 1);
+      mbar_init(&conv[i], TCB_CONV);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&accf[i], 1);
       mbar_init(&acce[i], 4);
@@ -210,6 +213,31 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
         mbar_expect_tx(&full[s], 2 * bytes);
         bulk_g2s(f, X + r0 * k, bytes, &full[s]);
         bulk_g2s(f + C::ROWB, ws.W + r0 * k, bytes, &full[s]);
+      }
+    }
+  } else if (warp == TCB_CONV / 32 + 5) {          // ---- MMA issue (one thread), decoupled from the converters
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(TCB_K, 2 * ws.k);
+      for (int t = 0; t < nst; ++t) {
+        const int o = t % TCB_NO;
+        mbar_wait(&conv[o], (t / TCB_NO) & 1);              // OP[o] written (and fenced) by every converter
+        const int j = t / C::SPB, ts = t % C::SPB;          // accumulator block j, stage ts within it
+        if (ts == 0 && j >= 1) mbar_wait(&acce[0], (j - 1) & 1);   // block j - 1 drained
+        tc_fence_after();
+        unsigned char* st = OP + o * C::OPS;
+        const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + C::A_BYTES), b_hi = smem_u32(st + 2 * C::A_BYTES),
+                       b_lo = smem_u32(st + 2 * C::A_BYTES + C::B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk) {
+          const uint32_t ko = kk * 256;                // 16 rows = 2 core matrices along K
+          const uint64_t dah = umma_desc(a_hi + ko, 128, C::SBO), dal = umma_desc(a_lo + ko, 128, C::SBO);
+          const uint64_t dbh = umma_desc(b_hi + ko, 128, C::SBO), dbl = umma_desc(b_lo + ko, 128, C::SBO);
+          umma_bf16(tmem, dah, dbh, idesc, (ts > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16(tmem, dah, dbl, idesc, 1);
+          umma_bf16(tmem, dal, dbh, idesc, 1);
+        }
+        umma_commit(&mmad[o]);
+        if (ts == C::SPB - 1 || t == nst - 1) umma_commit(&accf[0]);
       }
     }
   } else if (warp > TCB_CONV / 32) {               // ---- drain: TMEM lanes 32 (warp % 4) ..
@@ -249,8 +277,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
         }
       }
     }
-  } else {                                          // ---- converters + MMA issue
-    const uint32_t idesc = umma_idesc_bf16(TCB_K, N);
+  } else {                                          // ---- converters
     // thread -> column col = 16 (w % CB) + (l & 15) and row quads q0, q0 + 2 QG, ... (q0 = (l >> 4) +
     // 2 (w / CB)): per warp instruction the FP64 reads are two 128 B row segments and the 8 B
     // operand stores two 128 B core-matrix rows (no bank conflicts)
@@ -297,26 +324,8 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);        // this warp is done reading F[s]
-      fence_async_smem();
-      tc_fence_before();
-      conv_sync();
-      if (tid == 0) {
-        const int j = t / C::SPB, ts = t % C::SPB;     // accumulator block j, stage ts within it
-        if (ts == 0 && j >= 1) mbar_wait(&acce[0], (j - 1) & 1);   // block j - 1 drained
-        tc_fence_after();
-        const uint32_t a_hi = smem_u32(Ahi), a_lo = smem_u32(Alo), b_hi = smem_u32(Bhi), b_lo = smem_u32(Blo);
-#pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk) {
-          const uint32_t ko = kk * 256;                // 16 rows = 2 core matrices along K
-          const uint64_t dah = umma_desc(a_hi + ko, 128, C::SBO), dal = umma_desc(a_lo + ko, 128, C::SBO);
-          const uint64_t dbh = umma_desc(b_hi + ko, 128, C::SBO), dbl = umma_desc(b_lo + ko, 128, C::SBO);
-          umma_bf16(tmem, dah, dbh, idesc, (ts > 0 || kk > 0) ? 1u : 0u);
-          umma_bf16(tmem, dah, dbl, idesc, 1);
-          umma_bf16(tmem, dal, dbh, idesc, 1);
-        }
-        umma_commit(&mmad[o]);
-        if (ts == C::SPB - 1 || t == nst - 1) umma_commit(&accf[0]);
-      }
+      fence_async_smem();                           // operand stores -> the tensor core's async proxy
+      mbar_arrive(&conv[o]);
     }
   }
   __syncthreads();
