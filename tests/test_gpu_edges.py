@@ -1,0 +1,72 @@
+"""Degenerate shapes and argument errors through the C ABI: the smallest problems the method
+admits (k = 1, n = 2), k = n - 1 (a single row below the top block) up to k = 128 = KMAX, the
+same for CSR, and the statuses of invalid or unsupported shapes."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2602_23778_b200 as p
+    from paper_2602_23778_b200 import build
+    build.build()
+    p.lib()
+    return p
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("n,k", [(2, 1), (5, 4), (33, 32), (64, 63), (129, 128)])
+def test_dense_k_is_n_minus_1(pkg, n, k):
+    p = synth.small_dense(n, k, m=4, seed=n, signs=True)
+    R = pkg.Refiner.dense(p.A.cuda(), k)
+    op = oracle.Operator(A=p.A.numpy())
+    X = p.X0.cuda().clone()
+    for t in range(3):
+        xin = X.cpu().numpy()
+        s, st = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK
+        assert rel(X.cpu().numpy(), ref.X) <= TOL, t
+        assert st.flipped == ref.stats.flipped
+
+
+def test_csr_k_is_n_minus_1(pkg):
+    p = synth.small_laplacian((5, 4), (1.0, 1.37), 19, noise=1e-5, seed=3)
+    R = pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k)
+    op = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy())
+    X = p.X0.cuda().clone()
+    for t in range(3):
+        xin = X.cpu().numpy()
+        s, _ = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK
+        assert rel(X.cpu().numpy(), ref.X) <= TOL, t
+
+
+@pytest.mark.parametrize("n,k,status", [(100, 0, "REFINE_E_INVALID"), (100, 100, "REFINE_E_INVALID"),
+                                        (100, 150, "REFINE_E_INVALID"), (300, 129, "REFINE_E_UNSUPPORTED")])
+def test_invalid_shapes(pkg, n, k, status):
+    A = torch.eye(n, dtype=torch.float64, device="cuda")
+    with pytest.raises(pkg.RefineError) as ei:
+        pkg.Refiner.dense(A, k)
+    assert ei.value.status == getattr(pkg, status)
+
+
+def test_wrong_tensor_kinds(pkg):
+    A = torch.eye(64, dtype=torch.float64, device="cuda")
+    with pytest.raises(TypeError):
+        pkg.Refiner.dense(A.float(), 4)                 # FP32 A
+    with pytest.raises(TypeError):
+        pkg.Refiner.dense(A.t()[:, :32], 4)             # non-contiguous
+    with pytest.raises(TypeError):
+        pkg.Refiner.dense(A.cpu(), 4)                   # host tensor on the device entry point
