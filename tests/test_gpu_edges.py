@@ -70,3 +70,54 @@ def test_wrong_tensor_kinds(pkg):
         pkg.Refiner.dense(A.t()[:, :32], 4)             # non-contiguous
     with pytest.raises(TypeError):
         pkg.Refiner.dense(A.cpu(), 4)                   # host tensor on the device entry point
+
+
+@pytest.mark.parametrize("n,k,opt", [(33, 32, {"mixed": 2}), (129, 128, {"mixed": 2}), (129, 128, {"emul": True}),
+                                     (17, 16, {"emul": True})])
+def test_tensor_core_paths_k_is_n_minus_1(pkg, n, k, opt):
+    """NEXT-2 (bf16x3) and INT8 passes with a single row below the top block."""
+    p = synth.small_dense(n, k, m=4, seed=n + 7, signs=True)
+    R = pkg.Refiner.dense(p.A.cuda(), k, **opt)
+    op = oracle.Operator(A=p.A.numpy())
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, _ = R.refine_sweep(X, stats=True)
+    ref = oracle.sweep(op, xin)
+    assert s == pkg.REFINE_OK and ref.status == oracle.OK
+    sig = np.where(np.sum(ref.X * xin, axis=0) < 0, -1.0, 1.0)
+    corr = np.linalg.norm(ref.X - xin * sig)
+    # mixed: 1e-2 of the correction (tests/test_gpu_mixed.py); emul: the FP64 bar
+    tol = 1e-2 * corr + 1e-10 * np.linalg.norm(ref.X) if "mixed" in opt else 1e-10 * np.linalg.norm(ref.X)
+    assert np.linalg.norm(X.cpu().numpy() - ref.X) <= tol
+
+
+def _csr_of(A):
+    rp, ci, v = [0], [], []
+    for i in range(A.shape[0]):
+        nz = np.nonzero(A[i])[0]
+        ci.extend(nz.tolist())
+        v.extend(A[i, nz].tolist())
+        rp.append(len(ci))
+    return (torch.tensor(rp, dtype=torch.int32), torch.tensor(ci, dtype=torch.int32),
+            torch.tensor(v, dtype=torch.float64))
+
+
+@pytest.mark.parametrize("k", [8, 32])
+def test_csr_empty_rows(pkg, k):
+    """CSR rows without any nonzero (row / column zeroed, first and last rows included): W's rows
+    are exactly zero there and the sweep matches the oracle."""
+    p = synth.small_dense(400, k, m=8, seed=k, signs=True)
+    A = p.A.numpy().copy()
+    A[np.abs(A) < 1e-3] = 0.0                           # sparse-ish, symmetric
+    for r in (0, 17, 250, 399):
+        A[r, :] = 0.0
+        A[:, r] = 0.0
+    rp, ci, v = _csr_of(A)
+    R = pkg.Refiner.csr(rp.cuda(), ci.cuda(), v.cuda(), 400, k)
+    op = oracle.Operator(row_ptr=rp.numpy(), col_idx=ci.numpy(), val=v.numpy())
+    X = p.X0.cuda().clone()
+    xin = X.cpu().numpy()
+    s, _ = R.refine_sweep(X, stats=True)
+    ref = oracle.sweep(op, xin)
+    assert s == pkg.REFINE_OK and ref.status == oracle.OK
+    assert rel(X.cpu().numpy(), ref.X) <= TOL
