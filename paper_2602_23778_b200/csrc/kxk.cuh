@@ -498,7 +498,7 @@ RF_DEV void cluster_sync() {
   }
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__host__ __device__ constexpr int kxk_cluster(int k) { return k >= 64 ? 8 : (k > 32 ? 2 : 1); }
+__host__ __device__ constexpr int kxk_cluster(int k) { return k >= 64 ? 8 : (k >= 32 ? 4 : 1); }
 constexpr int KXK_SCRATCH_EXTRA = 64;   // doubles after the 16 k x k scratch matrices (cluster partials)
 
 // Xtop/Wtop: the top k rows of X^ (in/out) and W (un-flipped), ld k.
