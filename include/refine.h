@@ -84,7 +84,8 @@ typedef struct {
   double delta_c;        /* delta = delta_c * ||A - shift I||_inf * 2^-53; default 10 */
   int32_t beta_zero;     /* 0: beta_ij = -x_i^T x_j / 2; 1: beta_ij = 0      */
   int32_t normalize;     /* 1: normalise columns after each update; default 1              */
-  int32_t guard_window;  /* refine_run divergence guard window; default 3                                 */
+  int32_t guard_window;  /* refine_run divergence guard window, 0..4 (0 = off; outside -> REFINE_E_INVALID
+                            at init); default 3                                                          */
   double guard_factor;   /* refine_run divergence guard growth factor; default 10                         */
   int32_t square;        /* 1: the operator is A^2 - shift I applied as A (A X) (Sec. 5.2, PAPER.md:1218-1243;
                             smallest-|lambda| targets); ||.|| in delta / rel_resid is ||A||_inf^2 + |shift|
@@ -188,13 +189,14 @@ refine_status refine_run(refine_ctx* c, double* X, int32_t iters, double tol,
  * and solved by parallel Jacobi rotations on one CTA; Ritz pairs are ordered by
  * descending Ritz value, each eigenvector column signed so its largest entry is
  * positive (readings RR1-RR3).  ritz (host, k doubles, nullable) receives
- * D~.  Synchronises.  REFINE_E_INVALID if X^T X is not positive definite (X rank
+ * D~ (on every rank of a row partition: the values are broadcast with the k x k state).
+ * Synchronises.  REFINE_E_INVALID if X^T X is not positive definite (X rank
  * deficient); X is then unchanged. */
 refine_status refine_rayleigh_ritz(refine_ctx* c, double* X, double* ritz);
 
 /* Reorthogonalisation ("optionally reorthogonalize"): Cholesky QR,
  * X <- X L^{-T} with X^T X = L L^T (columns orthonormal, span kept).  gram_dev (host,
- * nullable) receives max |X^T X - I| before.  Synchronises.  REFINE_E_INVALID if X is
+ * nullable) receives max |X^T X - I| before (every rank).  Synchronises.  REFINE_E_INVALID if X is
  * rank deficient (X unchanged). */
 refine_status refine_reorthogonalize(refine_ctx* c, double* X, double* gram_dev);
 

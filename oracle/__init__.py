@@ -66,8 +66,8 @@ def lib():
         L.oracle_rr_dense.argtypes = [i64, i32, P, i64, d, P, P]
         L.oracle_rr_csr.argtypes = [i64, i32, P, P, P, d, P, P]
         L.oracle_jacobi_eig.argtypes = [i32, P, P, P]
-        L.oracle_sweep_tz_dense.argtypes = [i64, i32, P, i64, d, P, d, C.POINTER(Stats)]
-        L.oracle_sweep_tz_csr.argtypes = [i64, i32, P, P, P, d, P, d, C.POINTER(Stats)]
+        L.oracle_sweep_tz_dense.argtypes = [i64, i32, P, i64, d, P, d, C.POINTER(Stats), P]
+        L.oracle_sweep_tz_csr.argtypes = [i64, i32, P, P, P, d, P, d, C.POINTER(Stats), P]
         L.oracle_sweep_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, d, i32, i32, i32, C.POINTER(Stats), P]
         L.oracle_run_ex.argtypes = [C.c_int, i64, i32, P, i64, P, P, P, d, i32, P, i32, d, d, i32, i32,
                                     C.POINTER(i32), P]
@@ -181,6 +181,18 @@ def apply_h(Y, T, B, transpose=False):
 DEBUG_KEYS = ("W", "Y", "T", "sigma", "dtilde", "alpha", "V", "E", "Xtilde", "U")
 
 
+def _debug_buffers(n, k, debug):
+    """Host arrays for the sweep's intermediate dumps (oracle.c DBG_*) and the pointer table."""
+    if not debug:
+        return {}, None
+    shapes = {"W": (n, k), "Y": (n, k), "T": (k, k), "sigma": (k,), "dtilde": (k,), "alpha": (k,),
+              "V": (n, k), "E": (n, k), "Xtilde": (n, k), "U": (k, k)}
+    dbg = {key: np.zeros(shapes[key]) for key in DEBUG_KEYS}
+    arr = (C.c_void_p * len(DEBUG_KEYS))(*[dbg[key].ctypes.data for key in DEBUG_KEYS])
+    dbg["_keep"] = arr
+    return dbg, C.cast(arr, C.c_void_p)
+
+
 @dataclass
 class SweepResult:
     X: np.ndarray
@@ -211,14 +223,7 @@ def sweep(op: Operator, X, delta_c=10.0, beta_zero=False, normalize=True, debug=
     X = _f64(X).copy()
     n, k = X.shape
     st = Stats()
-    dbg = {}
-    dptr = None
-    if debug:
-        shapes = {"W": (n, k), "Y": (n, k), "T": (k, k), "sigma": (k,), "dtilde": (k,), "alpha": (k,),
-                  "V": (n, k), "E": (n, k), "Xtilde": (n, k), "U": (k, k)}
-        dbg = {key: np.zeros(shapes[key]) for key in DEBUG_KEYS}
-        arr = (C.c_void_p * len(DEBUG_KEYS))(*[dbg[key].ctypes.data for key in DEBUG_KEYS])
-        dptr = C.cast(arr, C.c_void_p)
+    dbg, dptr = _debug_buffers(n, k, debug)
     L = lib()
     if op.is_csr:
         s = L.oracle_sweep_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(X), delta_c, int(beta_zero),
@@ -265,21 +270,25 @@ def rayleigh_ritz(op: Operator, X):
     return s, Z, ritz
 
 
-def sweep_rr(op: Operator, X, delta_c=10.0):
+def sweep_rr(op: Operator, X, delta_c=10.0, debug=False):
     """Rayleigh-Ritz (Sec. 3.4) followed by one sweep with the top block of E_L zero and beta = 0
     (PAPER.md:460, 921-926): one iteration of the preprocessed refinement.  Returns
-    (SweepResult, ritz); the result's status is the RR status if RR fails."""
+    (SweepResult, ritz); the result's status is the RR status if RR fails.  debug: the top-zero
+    sweep's intermediates (as in sweep(); its input is the RR output Z, kept in debug["Z"])."""
     s, Z, ritz = rayleigh_ritz(op, X)
     st = Stats()
     if s != OK:
         return SweepResult(Z, s, st, {}), ritz
     n, k = Z.shape
+    dbg, dptr = _debug_buffers(n, k, debug)
+    if debug:
+        dbg["Z"] = Z.copy()
     L = lib()
     if op.is_csr:
-        s = L.oracle_sweep_tz_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(Z), delta_c, C.byref(st))
+        s = L.oracle_sweep_tz_csr(n, k, _p(op.rp), _p(op.ci), _p(op.v), op.shift, _p(Z), delta_c, C.byref(st), dptr)
     else:
-        s = L.oracle_sweep_tz_dense(n, k, _p(op.A), n, op.shift, _p(Z), delta_c, C.byref(st))
-    return SweepResult(Z, s, st, {}), ritz
+        s = L.oracle_sweep_tz_dense(n, k, _p(op.A), n, op.shift, _p(Z), delta_c, C.byref(st), dptr)
+    return SweepResult(Z, s, st, dbg), ritz
 
 
 def reorthogonalize(X):

@@ -620,16 +620,16 @@ int oracle_sweep_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci,
 
 /* one sweep after Rayleigh-Ritz (top block of E_L zero, beta = 0) */
 int oracle_sweep_tz_dense(int64_t n, int32_t k, const double* A, int64_t lda, double shift, double* X,
-                          double delta_c, oracle_stats* st) {
+                          double delta_c, oracle_stats* st, double** dbg) {
   op_t op = {0, n, A, lda, NULL, NULL, NULL, shift};
   oracle_opts o; fill_opts(&o, delta_c, 1, 1); o.top_zero = 1;
-  return sweep(&op, k, X, op_norm_inf(&op), &o, st, NULL);
+  return sweep(&op, k, X, op_norm_inf(&op), &o, st, dbg);
 }
 int oracle_sweep_tz_csr(int64_t n, int32_t k, const int32_t* rp, const int32_t* ci, const double* v, double shift,
-                        double* X, double delta_c, oracle_stats* st) {
+                        double* X, double delta_c, oracle_stats* st, double** dbg) {
   op_t op = {1, n, NULL, 0, rp, ci, v, shift};
   oracle_opts o; fill_opts(&o, delta_c, 1, 1); o.top_zero = 1;
-  return sweep(&op, k, X, op_norm_inf(&op), &o, st, NULL);
+  return sweep(&op, k, X, op_norm_inf(&op), &o, st, dbg);
 }
 
 /* =========================================================================

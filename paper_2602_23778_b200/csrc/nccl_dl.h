@@ -1,10 +1,11 @@
 // nccl_dl.h -- NCCL entry points resolved at run time (dlopen), so librefine.so has no link-time
 // dependency on NCCL and world == 1 never touches it.  The process's already-loaded libnccl
-// (torch's bundled NCCL 2.28) is found first; the nvidia-nccl wheel path is the fallback.
+// (torch's bundled NCCL 2.28) is found by its soname; REFINE_NCCL_PATH overrides the lookup.
 #pragma once
 #include <dlfcn.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -36,8 +37,10 @@ inline Nccl& nccl() {
   static bool tried = false;
   if (tried) return n;
   tried = true;
-  const char* names[] = {"libnccl.so.2", "libnccl.so",
-                         "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+  // REFINE_NCCL_PATH (a full path to libnccl.so.2) is tried first; otherwise the soname, which
+  // finds the copy the process already loaded (torch's) or the loader's search path.
+  const char* env = getenv("REFINE_NCCL_PATH");
+  const char* names[] = {env && env[0] ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
   void* h = nullptr;
   for (const char* nm : names) {
     h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);

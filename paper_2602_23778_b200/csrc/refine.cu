@@ -69,34 +69,47 @@ __global__ void run_check_kernel(int* status, RunState* rs, const double* stats,
   if (gate && reorth_tol > 0.0 && stats[6] > reorth_tol) *gate = ST_OK;
 }
 
+// ||A - shift I||_inf row sums with Neumaier-compensated accumulation (the oracle's summation
+// class, reading R4): each lane carries (s, c) over its strided columns, the 32 lane pairs are
+// combined by compensated adds, so delta = c ||A|| u agrees with the oracle's to O(u) even at a tie.
+struct Nsum { double s, c; };
+RF_DEV void nsum_add(Nsum& a, double x) {
+  const double t = a.s + x;
+  a.c += (fabs(a.s) >= fabs(x)) ? (a.s - t) + x : (x - t) + a.s;
+  a.s = t;
+}
 __global__ void absrow_max_dense_kernel(const double* A, int64_t lda, int64_t n_loc, int64_t n, int64_t row0,
                                         double shift, double* out_rows) {
   const int lane = threadIdx.x & 31;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = w; i < n_loc; i += nw) {
-    double s = 0.0;
+    Nsum s = {0.0, 0.0};
     for (int64_t l = lane; l < n; l += 32) {
       double a = A[i * lda + l];
       if (l == row0 + i) a -= shift;
-      s += fabs(a);
+      nsum_add(s, fabs(a));
     }
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out_rows[i] = s;
+    for (int o = 16; o; o >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, s.s, o), oc = __shfl_xor_sync(0xffffffffu, s.c, o);
+      nsum_add(s, os);
+      s.c += oc;
+    }
+    if (lane == 0) out_rows[i] = s.s + s.c;
   }
 }
 __global__ void absrow_max_csr_kernel(const int32_t* rp, const int32_t* ci, const double* v, int64_t n_loc,
                                       int64_t row0, double shift, double* out_rows) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_loc; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
+    Nsum s = {0.0, 0.0};
     bool diag = false;
     for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
       double a = v[p];
       if (ci[p] == row0 + i) { a -= shift; diag = true; }
-      s += fabs(a);
+      nsum_add(s, fabs(a));
     }
-    if (!diag) s += fabs(shift);
-    out_rows[i] = s;
+    if (!diag) nsum_add(s, fabs(shift));
+    out_rows[i] = s.s + s.c;
   }
 }
 __global__ void max_kernel(const double* x, int64_t n, double* out) {
@@ -122,6 +135,14 @@ __global__ void col_range_kernel(const int32_t* rp, const int32_t* ci, int64_t n
   }
   atomicMin(out, lo);
   atomicMax(out + 1, hi);
+}
+
+// X <- X~ for Rayleigh-Ritz / QR steps with opts.normalize == 0, behind the status word (a failed
+// or gate-closed step leaves X untouched, like every other kernel of the step)
+__global__ void copy_gated_kernel(const int* status, double* __restrict__ X, const double* __restrict__ Xt, int64_t cnt) {
+  if (*status != ST_OK) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    X[i] = Xt[i];
 }
 
 int pad_kp(int k) {
@@ -272,10 +293,10 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
 }
 
 // kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs
-static void launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
+static cudaError_t launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
   if (kxk_cluster(ws.k) == 1) {   // (a plain launch is an implicit 1-CTA cluster)
     kxk_finish_kernel<<<1, KXK_THREADS, FK_SMEM * 8, s>>>(ws, X, ws.W);
-    return;
+    return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kxk_cluster(ws.k), 1, 1);
@@ -289,7 +310,7 @@ static void launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kxk_finish_kernel, ws, X, (const double*)ws.W);
+  return cudaLaunchKernelEx(&cfg, kxk_finish_kernel, ws, X, (const double*)ws.W);
 }
 
 template <int KP>
@@ -509,7 +530,11 @@ struct Kern {
         c->mark();
         if (c->rank == 0) {
           cudaStreamWaitEvent(s, c->ev_join, 0);
-          launch_kxk_finish(ws, X, s);
+          const cudaError_t e = launch_kxk_finish(ws, X, s);
+          if (e != cudaSuccess) {   // (sticky: enqueue_phases reports it through the context)
+            cuda_fail(c, e, "kxk_finish launch");
+            return n;
+          }
           n += 1;
         }
         break;
@@ -541,7 +566,8 @@ struct Kern {
           normalize_kernel<<<c->sms * 8, 256, 0, s>>>(ws, X);
           ++n;
         } else {
-          cudaMemcpyAsync(X, ws.Xt, (size_t)c->n_loc * c->k * sizeof(double), cudaMemcpyDeviceToDevice, s);
+          copy_gated_kernel<<<c->sms * 4, 256, 0, s>>>(ws.status, X, ws.Xt, c->n_loc * c->k);
+          ++n;
         }
         c->mark();
         break;
@@ -595,7 +621,7 @@ static cudaError_t gather_geometry_un(refine_ctx* c, const std::vector<int32_t>&
   return cudaSuccess;
 }
 
-static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, int RG);
+static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, int RG, int nzcap);
 
 // batch size UN: the smallest of {5, 7, 8} covering 95% of the rows (the stencils' 5 / 7)
 template <int K>
@@ -614,7 +640,7 @@ static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp
   else if (p95 <= 7) e = gather_geometry_un<K, 7>(c, rp);
   else e = gather_geometry_un<K, 8>(c, rp);
   if (e != cudaSuccess) return e;
-  return gather_order(c, rp, GatherCfg<K>::RG);
+  return gather_order(c, rp, GatherCfg<K>::RG, GatherCfg<K>::NZCAP);
 }
 
 // Stencil-aware chunk order for the gather kernel (spmm_csr.cuh chunk_of): the row offsets present
@@ -622,7 +648,7 @@ static cudaError_t gather_geometry(refine_ctx* c, const std::vector<int32_t>& rp
 // lexicographic order) and a +-d3 reuse window larger than about a fifth of L2 select the tiled
 // order; the chunk size becomes the largest divisor of d2 not above R and not below the row groups.
 // REFINE_SPMM_ORDER=1 forces it whenever the structure is found (tests), =0 disables it.
-static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, int RG) {
+static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, int RG, int nzcap) {
   c->spmm_ord = make_int4(0, 0, 0, 0);
   const char* env = getenv("REFINE_SPMM_ORDER");
   if ((env && env[0] == '0') || c->multi || c->gather_R <= 0) return cudaSuccess;
@@ -654,6 +680,10 @@ static cudaError_t gather_order(refine_ctx* c, const std::vector<int32_t>& rp, i
   for (int r = std::min<int>(c->gather_R, (int)d2); r >= RG; --r)
     if (d2 % r == 0) { R = r; break; }                  // (r >= RG: every row group busy)
   if (R == 0) return cudaSuccess;
+  // the new chunks [q R, (q + 1) R) must each fit the staged nonzero buffer over ALL rows (the
+  // stencil test above only sampled the first rows); otherwise keep the identity order and old R
+  for (int64_t i = 0; i < c->n_loc; i += R)
+    if ((int64_t)rp[std::min<int64_t>(i + R, c->n_loc)] - rp[i] > nzcap) return cudaSuccess;
   c->gather_R = R;
   c->spmm_ord = make_int4((int)(d2 / R), (int)(d3 / d2), 16, (int)((c->n_loc + d3 - 1) / d3));   // 16 lines per tile
   return cudaSuccess;
@@ -719,6 +749,8 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.shift = shift;
   ws.beta_zero = c->opts.beta_zero;
   ws.kjudge = c->opts.kjudge;
+  // the divergence guard compares with the corr norm guard_window sweeps back (a 4-entry ring)
+  if (c->opts.guard_window < 0 || c->opts.guard_window > 4) return REFINE_E_INVALID;
   if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
   if (c->opts.mixed && (k % 16 != 0 || k < 32)) return REFINE_E_UNSUPPORTED;    // tcgen05 passes: 16 | k >= 32
   // ozaki.cuh: dense S1 for 16 | k <= 64, pass C for k == 128 -- at least one must apply
@@ -762,7 +794,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k, P = (size_t)world;
   const int nsplit_max = std::max(c->nsplit, c->oz_ns);
   const size_t wpart = (!c->csr && nsplit_max > 1) ? (size_t)nsplit_max * nk : 0;
-  c->bc_cnt = kk + k + 8 + 1;
+  c->bc_cnt = kk + k + 8 + k + 1;   // [Csig | scal | stats(8) | ritz(k) | status]
   size_t off = 0;
   auto take = [&](size_t cnt) { size_t o = off; off += (cnt + 31) & ~size_t(31); return o; };
   const size_t oW = take(nk), oXt = take(nk), oWp = take(wpart), oAg = take((size_t)c->n_ag * k * 4), oBp = take(bpart),
@@ -771,7 +803,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
                oScr = take(16 * kk + KXK_SCRATCH_EXTRA), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
-               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oRitz = take(k), oZd = take(k), oGate = take(1),
+               oNrS = take(k), oNrA = take(P * k), oCol = take(2), oZd = take(k), oGate = take(1),
                oBd = take(c->opts.mixed ? (size_t)c->sms * 2 * c->kp : 0);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
@@ -784,13 +816,14 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.nslot = b + oNs; ws.n_nslot = c->passc_grid;
   ws.alpha = b + oAl; ws.d = b + oD; ws.rd = b + oRd; ws.sigma = b + oSg; ws.U = b + oU; ws.L = b + oL;
   ws.T = b + oT; ws.Uinv = b + oUi; ws.E11 = b + oE; ws.ntop = b + oNt; ws.invn = b + oIn;
-  c->bc = b + oBc;                                                   // [Csig | scal | stats(8) | status]
+  c->bc = b + oBc;                                   // [Csig | scal | stats(8) | ritz(k) | status]
   ws.Csig = c->bc; ws.scal = c->bc + kk; ws.stats = c->bc + kk + k;
-  ws.status = reinterpret_cast<int*>(c->bc + kk + k + 8);
+  ws.ritz = c->bc + kk + k + 8;                      // (broadcast too: every rank reports the Ritz values)
+  ws.status = reinterpret_cast<int*>(c->bc + kk + 2 * k + 8);
   ws.scratch = b + oScr;
   ws.ag_send = b + oAgS; ws.ag_all = b + oAgA; ws.mg_all = c->multi ? b + oMgA : nullptr;
   ws.nrm_send = b + oNrS; ws.nrm_all = b + oNrA;
-  ws.ritz = b + oRitz; ws.zerod = b + oZd; ws.top_zero = 0;   // (the pool is zeroed below)
+  ws.zerod = b + oZd; ws.top_zero = 0;   // (the pool is zeroed below)
   ws.gate = reinterpret_cast<int*>(b + oGate);
   ws.want_gram = c->opts.reorth_tol > 0.0 ? 1 : 0;
   ws.normalize = c->opts.normalize ? 1 : 0;
@@ -1117,6 +1150,8 @@ static refine_status enqueue_phases(refine_ctx* c, double* X) {
   }
   c->launches = launches;
   RF_CK(c, cudaGetLastError());
+  for (int i = 0; i < nr; ++i)
+    if (ranks[i]->sticky != REFINE_OK) return c->sticky = ranks[i]->sticky;
   return REFINE_OK;
 }
 

@@ -11,6 +11,7 @@ import torch
 
 import oracle
 import synth
+from parity_util import compare_sweep
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -22,10 +23,6 @@ def pkg():
     build.build()
     p.lib()
     return p
-
-
-def rel(a, b):
-    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
@@ -47,16 +44,13 @@ def test_fullsize_one_step(pkg, name):
         s, st = R.refine_sweep(X, stats=True)
         assert s == pkg.REFINE_OK
         t0 = time.perf_counter()
-        ref = oracle.sweep(op, xin, debug=(p.kind == "csr"))
+        ref = oracle.sweep(op, xin, debug=True)
         dt = time.perf_counter() - t0
         assert ref.status == oracle.OK
-        e = rel(X.cpu().numpy(), ref.X)
-        sig = ref.debug["sigma"] if ref.debug else None
+        sig = ref.debug["sigma"]
+        e = compare_sweep(X.cpu().numpy(), ref, st, k=p.k, where=f"{name} t={t}")
         print(f"{name} t={t} one-step rel {e:.3e} (oracle {dt:.1f}s, {oracle.num_threads()} threads) "
-              f"corr gpu {st.corr_norm:.6e} oracle {ref.stats.corr_norm:.6e}")
-        assert e <= 1e-10
-        assert st.flipped == ref.stats.flipped
-        assert abs(st.rel_resid - ref.stats.rel_resid) <= 1e-8 * ref.stats.rel_resid + 1e-18
+              f"corr gpu {st.corr_norm:.6e} oracle {ref.stats.corr_norm:.6e} min_gap {st.min_gap:.3e}")
         if p.kind == "csr":
             Wg = R.debug(pkg.DBG_W).cpu().numpy()
             assert np.array_equal(Wg * sig, ref.debug["W"])

@@ -102,3 +102,40 @@ def test_divergence_falls_back_to_rayleigh_ritz(pkg):
     Q, _ = np.linalg.qr(X.cpu().numpy())
     Xt = p.X.numpy()
     assert np.linalg.norm(Xt - Q @ (Q.T @ Xt)) <= 100 * n * U
+
+
+def test_normalize_false_with_closed_reorth_gate(pkg):
+    """refine_run with normalize=False and a reorthogonalisation threshold that never triggers:
+    the gated Cholesky-QR step (enqueued every sweep behind the device gate) must leave X alone,
+    so the run equals the same run without the policy, bit for bit."""
+    p = synth.small_dense(600, 8, m=8, noise=1e-4, seed=4)
+    Ra = pkg.Refiner.dense(p.A.cuda(), p.k, normalize=False)
+    Rb = pkg.Refiner.dense(p.A.cuda(), p.k, normalize=False, reorth_tol=10.0)
+    Xa, Xb = p.X0.cuda().clone(), p.X0.cuda().clone()
+    sa, ia, _ = Ra.refine_run(Xa, 6, 0.0)
+    sb, ib, _ = Rb.refine_run(Xb, 6, 0.0)
+    assert sa == sb == pkg.REFINE_MAXITER and ia == ib == 6
+    assert torch.equal(Xa, Xb)
+
+
+@pytest.mark.parametrize("normalize", [True, False])
+def test_rank_deficient_leaves_X_unchanged(pkg, normalize):
+    """Rayleigh-Ritz and Cholesky QR on a rank-deficient X return REFINE_E_INVALID and leave X
+    untouched (refine.h), whether or not the step normalises."""
+    p = synth.small_dense(500, 6, m=8, seed=12)
+    R = pkg.Refiner.dense(p.A.cuda(), p.k, normalize=normalize)
+    X0 = p.X0.cuda().clone()
+    X0[:, 3] = X0[:, 1]
+    X = X0.clone()
+    s, _ = R.refine_rayleigh_ritz(X)
+    assert s == pkg.REFINE_E_INVALID and torch.equal(X, X0)
+    s, _ = R.refine_reorthogonalize(X)
+    assert s == pkg.REFINE_E_INVALID and torch.equal(X, X0)
+
+
+def test_guard_window_out_of_range_rejected(pkg):
+    p = synth.small_dense(200, 4, m=4, seed=1)
+    for w in (5, -1):
+        with pytest.raises(pkg.RefineError) as ei:
+            pkg.Refiner.dense(p.A.cuda(), p.k, guard_window=w)
+        assert ei.value.status == pkg.REFINE_E_INVALID

@@ -97,8 +97,24 @@ def test_sweep_after_rr_has_zero_top_block():
     """After RR the sweep's top block is zero by construction; the remaining
     correction is the lower block v_ij / d_j (first-order power step)."""
     p = synth.small_dense(256, 4, m=8, noise=1e-5, seed=6)
-    res, ritz = oracle.sweep_rr(dense_op(p), p.X0.numpy())
+    res, ritz = oracle.sweep_rr(dense_op(p), p.X0.numpy(), debug=True)
     assert res.status == oracle.OK and res.stats.delta_hits == 0
+    D = res.debug
+    k, n = p.k, p.n
+    E, V, d = D["E"], D["V"], D["dtilde"]
+    assert np.all(E[:k] == 0.0)                                    # e_ij = 0, i, j <= k (PAPER.md:921-926)
+    assert np.array_equal(E[k:], V[k:] / d)                        # e_ij = v_ij / d_j, i > k (line 6)
+    # independent route: X~ = Z' + H^ E~_L with H^ = I - Y T Y^T built explicitly (n x n), Z' the
+    # RR output in the sweep's sign frame, E~_L = [0; V_2 D^{-1}] with V = H^T (A Z' - Z' D)
+    Y, T, sig = D["Y"], D["T"], D["sigma"]
+    H = np.eye(n) - Y @ T @ Y.T
+    Zf = D["Z"] * sig
+    A = p.A.numpy()
+    Vref = H.T @ (A @ Zf - Zf * d)
+    tolv = 64 * U * np.abs(A).sum(axis=1).max()                  # rounding of A Z' (no cancellation bound)
+    assert np.abs(Vref[k:] - V[k:]).max() <= tolv
+    El = np.vstack([np.zeros((k, k)), Vref[k:] / d])
+    assert np.abs(D["Xtilde"] - (Zf + H @ El)).max() <= tolv / np.abs(d).min() + 1e-14
 
 
 @pytest.mark.parametrize("gap", [1e-9, 1e-12])
