@@ -247,7 +247,10 @@ int32_t refine_halo_plan(int32_t world, int32_t rank, const int64_t* row_begin, 
  * un-flipped modified-LU factor), 3 Y_1 (k x k, unit lower), 4 T (k x k),
  * 5 dtilde (k), 6 alpha (k), 7 E_11 (k x k), 8 Y (n_loc x k, materialised by
  * the tall-skinny triangular apply Y_2 = X_2 U^{-1}; expects the sweep's input X
- * in dst on entry), 9 status-independent stats vector (8 doubles). */
+ * in dst on entry), 9 status-independent stats vector (8 doubles), 10 clock64 phase
+ * log of the k x k kernels (REFINE_KXK_TIMING=1; 64 raw int64), 11 the CSR S1 kernel's
+ * geometry (9 doubles: stencil SpMM on, tile R, L, column blocks, grid, grid nx, ny, nz,
+ * gather rows per chunk). */
 refine_status refine_debug_get(refine_ctx* c, int32_t what, double* dst);
 
 #ifdef __cplusplus

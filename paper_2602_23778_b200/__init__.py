@@ -25,6 +25,7 @@ REFINE_E_CUDA, REFINE_E_NCCL, REFINE_E_NOMEM, REFINE_E_UNSUPPORTED = -4, -5, -6,
 
 # refine_debug_get selectors
 DBG_W, DBG_SIGMA, DBG_U, DBG_L, DBG_T, DBG_D, DBG_ALPHA, DBG_E11, DBG_Y, DBG_STATS = range(10)
+DBG_SPMM = 11   # S1 kernel geometry: [stencil on, R, L, nq, grid, nx, ny, nz, gather R]
 
 
 class refine_comm(C.Structure):
@@ -279,7 +280,7 @@ class Refiner:
         import torch
         k, nl = self.k, self.n_loc
         shapes = {DBG_W: (nl, k), DBG_SIGMA: (k,), DBG_U: (k, k), DBG_L: (k, k), DBG_T: (k, k), DBG_D: (k,),
-                  DBG_ALPHA: (k,), DBG_E11: (k, k), DBG_Y: (nl, k), DBG_STATS: (8,)}
+                  DBG_ALPHA: (k,), DBG_E11: (k, k), DBG_Y: (nl, k), DBG_STATS: (8,), DBG_SPMM: (9,)}
         if what == DBG_Y:
             dst = X_in.clone()
         else:

@@ -17,6 +17,7 @@
 // tests on one device, device copies between emulated ranks ("loopback": world > 1 with
 // nccl_id == NULL).
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <vector>
@@ -32,6 +33,7 @@
 #include "kxk.cuh"
 #include "passes.cuh"
 #include "spmm_csr.cuh"
+#include "spmm_stencil.cuh"
 #include "tc_passes.cuh"
 #include "ozaki.cuh"
 #include "nccl_dl.h"
@@ -190,6 +192,14 @@ struct refine_ctx {
   int64_t kchunk = 0;
   int gemm_gx = 0;
   int n_ag = 0, w_fin_grid = 0, spmm_grid = 0;
+  int n_ag_cur = 0;             // alpha/g slots written by this sweep's S1 kernel (kxk_rq reduces them)
+  // stencil SpMM (spmm_stencil.cuh): geometry, packed row records (owned), X tensor map cache
+  bool st_on = false;
+  StencilGeo st_geo{};
+  double* st_meta = nullptr;
+  int st_grid = 0, st_smem = 0;
+  CUtensorMap st_tm{};
+  const double* st_tm_x = nullptr;
   int passb_grid_y = 0, passc_grid = 0;
   RunState* run = nullptr;
   refine_status sticky = REFINE_OK;
@@ -245,11 +255,182 @@ template <> struct Tiles<32>  { static constexpr int G[5] = {128, 32, 16, 32, 2}
 template <> struct Tiles<64>  { static constexpr int G[5] = {128, 64, 16, 32, 2}; static constexpr int B[5] = {64, 128, 2, 4, 16}; static constexpr int C[4] = {64, 64, 2, 4}; };
 template <> struct Tiles<128> { static constexpr int G[5] = {64, 32, 32, 32, 2};  static constexpr int B[5] = {64, 64, 2, 2, 16};  static constexpr int C[4] = {128, 32, 2, 8}; };
 
+// ---------------------------------------------------------------- stencil SpMM (spmm_stencil.cuh)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static void* fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+// 4-D view {k, nx, ny, nz} of the row-major n x k block X, box {KC, R + 2, L + 2 hy, 1}
+static bool stencil_tensor_map(refine_ctx* c, const double* X) {
+  if (c->st_tm_x == X) return true;
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const StencilGeo& g = c->st_geo;
+  const cuuint64_t K = (cuuint64_t)c->k;
+  cuuint64_t dims[4] = {K, (cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
+  cuuint64_t strides[3] = {K * 8, K * 8 * g.nx, K * 8 * g.nx * g.ny};
+  cuuint32_t box[4] = {(cuuint32_t)g.KC, (cuuint32_t)g.Rb, (cuuint32_t)g.Lb, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(&c->st_tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  c->st_tm_x = X;
+  return true;
+}
+
+template <int KC, int NZR>
+static void stencil_kernel_launch(refine_ctx* c, const Ws& ws) {
+  spmm_stencil_kernel<KC, NZR><<<c->st_grid, ST_BLOCK, c->st_smem, c->stream>>>(ws, c->st_tm, c->st_meta, c->st_geo);
+}
+static bool stencil_launch(refine_ctx* c, const double* X, const Ws& ws) {
+  if (!stencil_tensor_map(c, X)) return false;
+  const int kc = c->st_geo.KC, nzr = c->st_geo.nzr;
+  if (kc == 32) nzr == 5 ? stencil_kernel_launch<32, 5>(c, ws) : stencil_kernel_launch<32, 7>(c, ws);
+  else if (kc == 16) nzr == 5 ? stencil_kernel_launch<16, 5>(c, ws) : stencil_kernel_launch<16, 7>(c, ws);
+  else nzr == 5 ? stencil_kernel_launch<8, 5>(c, ws) : stencil_kernel_launch<8, 7>(c, ws);
+  return true;
+}
+
+// Detect a 2-D / 3-D grid stencil in the CSR (every nonzero offset in {0, +-1, +-d2, +-d3}, no
+// wrap across lines / planes, <= 7 nonzeros per row), pick the tile, pack the row records and size
+// the persistent grid.  Single rank, not the squared operator.  REFINE_SPMM=gather disables it.
+static cudaError_t stencil_setup(refine_ctx* c) {
+  c->st_on = false;
+  const char* env = getenv("REFINE_SPMM");
+  const bool force = env && strcmp(env, "stencil") == 0;
+  if ((env && strcmp(env, "gather") == 0) || !c->csr || c->multi || c->opts.square) return cudaSuccess;
+  const int k = c->k;
+  const int KC = (k % 32 == 0) ? 32 : (k % 16 == 0) ? 16 : (k % 8 == 0) ? 8 : 0;
+  if (KC == 0 || k > KMAX) return cudaSuccess;
+  const int64_t n = c->n_loc;
+  std::vector<int32_t> rp(n + 1);
+  cudaError_t e = cudaMemcpy(rp.data(), c->rp, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  const int64_t nnz = (int64_t)rp[n] - rp[0];
+  if (nnz <= 0 || rp[0] != 0) return cudaSuccess;
+  std::vector<int32_t> ci(nnz);
+  if ((e = cudaMemcpy(ci.data(), c->ci, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+  std::vector<int64_t> lv;   // distinct nonzero |offsets|
+  for (int64_t i = 0; i < n; ++i)
+    for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t o = std::llabs((int64_t)ci[p] - i);
+      if (o == 0 || std::find(lv.begin(), lv.end(), o) != lv.end()) continue;
+      if (lv.size() == 3) return cudaSuccess;   // not a 2-D / 3-D axis stencil
+      lv.push_back(o);
+    }
+  std::sort(lv.begin(), lv.end());
+  if (getenv("REFINE_VERBOSE")) {
+    fprintf(stderr, "[refine] stencil offsets:");
+    for (auto v : lv) fprintf(stderr, " %lld", (long long)v);
+    fprintf(stderr, "\n");
+  }
+  StencilGeo g{};
+  int64_t chk_d2, chk_d3;
+  if (lv.size() == 3 && lv[0] == 1 && lv[2] % lv[1] == 0 && n % lv[2] == 0) {          // 3-D
+    g.nx = (int)lv[1]; g.ny = (int)(lv[2] / lv[1]); g.nz = (int)(n / lv[2]);
+    g.d2 = lv[1]; g.d3 = lv[2]; g.hy = 1;
+    chk_d2 = lv[1]; chk_d3 = lv[2];
+  } else if (lv.size() == 2 && lv[0] == 1 && n % lv[1] == 0) {                            // 2-D: swept along y
+    g.nx = (int)lv[1]; g.ny = 1; g.nz = (int)(n / lv[1]);
+    g.d2 = 0; g.d3 = lv[1]; g.hy = 0;
+    chk_d2 = lv[1]; chk_d3 = lv[1];
+  } else {
+    return cudaSuccess;
+  }
+  if (g.nx < 2 || g.nz < 1) return cudaSuccess;
+  // default: 3-D grids with k >= 64, where it measured faster than the gather kernel (cfg5: 2.24 vs
+  // 2.31 ms); 2-D grids at k = 32 measured slower (cfg4: 0.159-0.169 vs 0.147 ms).  REFINE_SPMM=stencil
+  // forces it wherever the structure allows (tests).
+  if (!force && !(g.hy && k >= 64)) return cudaSuccess;
+  int* dflag = nullptr;
+  if ((e = cudaMalloc(&dflag, 2 * sizeof(int))) != cudaSuccess) return e;
+  cudaMemsetAsync(dflag, 0, 2 * sizeof(int), c->stream);
+  stencil_check_kernel<<<c->sms * 4, 256, 0, c->stream>>>(c->rp, c->ci, n, g.nx, chk_d2, chk_d3, dflag);
+  int hf[2] = {1, 0};
+  e = cudaMemcpyAsync(hf, dflag, sizeof(hf), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dflag);
+  if (e != cudaSuccess) return e;
+  if (getenv("REFINE_VERBOSE"))
+    fprintf(stderr, "[refine] stencil check: grid %d x %d x %d, violations %d, max row %d\n", g.nx, g.ny, g.nz, hf[0],
+            hf[1]);
+  if (hf[0] != 0 || hf[1] > 7) return cudaSuccess;
+  g.nzr = hf[1] <= 5 ? 5 : 7;
+  g.KC = KC;
+  g.nq = k / KC;
+  // tile: maximise the staged-row reuse L R / ((L + 2 hy)(R + 2)) times the tile utilisation,
+  // 4 slots within the shared-memory budget (3-D: one CTA per SM; 2-D: two)
+  const int occ = g.hy ? 1 : 2;
+  const int budget = (occ == 1 ? 220 : 110) * 1024 - 128;
+  const int Ls3[] = {1, 2, 4, 5, 8, 10, 16}, Rs[] = {8, 16, 20, 24, 32, 40, 48, 64, 96, 128, 192};
+  double best = -1.0;
+  for (int L : Ls3) {
+    if (!g.hy && L != 1) continue;
+    for (int R : Rs) {
+      const int Rb = R + 2, Lb = L + 2 * g.hy;
+      const int box = KC * Rb * Lb * 8, meta = L * R * (g.nzr + 1) * 8;
+      const int slot = (box + meta + 127) & ~127;
+      if (ST_SLOTS * slot + 128 > budget || R > 2 * g.nx) continue;
+      const int ntx = (g.nx + R - 1) / R, nty = (g.ny + L - 1) / L;
+      const double util = (double)g.nx / (ntx * R) * ((double)g.ny / (nty * L));
+      const double score = (double)(L * R) / (Lb * Rb) * util;
+      if (score > best + 1e-9) {
+        best = score;
+        g.R = R; g.L = L; g.Rb = Rb; g.Lb = Lb; g.ntx = ntx; g.nty = nty;
+        g.box_bytes = box; g.meta_bytes = meta; g.slot_bytes = slot;
+      }
+    }
+  }
+  if (best <= 0.0) return cudaSuccess;
+  const int sms = (c->rank == 0 && c->sms > 1) ? c->sms - 1 : c->sms;   // one SM left to kxk_lu
+  const int nb = std::max(1, sms * occ / g.nq);
+  const int64_t pencils = (int64_t)g.ntx * g.nty;
+  int nseg = (int)std::min<int64_t>(g.nz, std::max<int64_t>(1, (8 * (int64_t)nb + pencils - 1) / pencils));
+  g.zlen = (g.nz + nseg - 1) / nseg;
+  g.nseg = (g.nz + g.zlen - 1) / g.zlen;
+  g.blocks = (int64_t)g.ntx * g.nty * g.nz;
+  const size_t meta_bytes = (size_t)g.blocks * g.meta_bytes;
+  if ((e = cudaMalloc(&c->st_meta, meta_bytes)) != cudaSuccess) return e;
+  cudaMemsetAsync(c->st_meta, 0, meta_bytes, c->stream);
+  if (g.nzr == 5) stencil_pack_kernel<5><<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, g, c->st_meta);
+  else stencil_pack_kernel<7><<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, g, c->st_meta);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  c->st_geo = g;
+  c->st_grid = nb * g.nq;
+  c->st_smem = std::max(ST_SLOTS * g.slot_bytes + 128, 128 + 8 * ST_THREADS * 16);   // (+ the final dd reduction)
+  auto attr = [&](auto kern) { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c->st_smem); };
+  if (KC == 32) e = g.nzr == 5 ? attr(spmm_stencil_kernel<32, 5>) : attr(spmm_stencil_kernel<32, 7>);
+  else if (KC == 16) e = g.nzr == 5 ? attr(spmm_stencil_kernel<16, 5>) : attr(spmm_stencil_kernel<16, 7>);
+  else e = g.nzr == 5 ? attr(spmm_stencil_kernel<8, 5>) : attr(spmm_stencil_kernel<8, 7>);
+  if (e != cudaSuccess) return e;
+  c->st_on = tensor_map_encoder() != nullptr;
+  if (getenv("REFINE_VERBOSE"))
+    fprintf(stderr, "[refine] stencil SpMM %s: tile R %d L %d, KC %d x %d, grid %d, segments %d x %d, slot %d B x %d\n",
+            c->st_on ? "on" : "off (no tensor-map encoder)", g.R, g.L, g.KC, g.nq, c->st_grid, g.nseg, g.zlen,
+            g.slot_bytes, ST_SLOTS);
+  return cudaSuccess;
+}
+
 // Xg: the rows gathered (X, or A X for the second product of the squared operator), Xo: own rows
 template <bool HALO>
 static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double* Xo, const Ws& ws) {
   cudaStream_t s = c->stream;
   const int g = c->spmm_grid;
+  c->n_ag_cur = g;                // the gather / per-row kernels write one slot per CTA
+  if (!HALO && c->st_on && Xg == Xo && ((uintptr_t)Xg % 16) == 0 && stencil_launch(c, Xg, ws)) {
+    c->n_ag_cur = c->st_grid / c->st_geo.nq;
+    return;
+  }
   if (vec && c->gather_R > 0) {   // vec: 16-byte aligned X / halo rows
     const int R = c->gather_R;
     const int4 ord = HALO ? make_int4(0, 0, 0, 0) : c->spmm_ord;
@@ -479,6 +660,7 @@ struct Kern {
           }
         }
         if (ph == 0 && c->multi) {
+          ws.n_ag = c->n_ag_cur;
           ag_local_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
           ++n;
         }
@@ -503,6 +685,7 @@ struct Kern {
         break;
       case 1:  // S2: alpha, Rayleigh quotients
         c->mark();
+        ws.n_ag = c->n_ag_cur;   // slots of the S1 kernel that ran (gather or stencil SpMM)
         kxk_rq_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
         n += 1;
         break;
@@ -790,7 +973,9 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->w_fin_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * wf_per_sm, c->n_loc / 2));
   c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 8, (c->n_loc + 7) / 8));
   if (c->csr) RF_CK(c, gather_setup(c));
-  c->n_ag = c->csr ? c->spmm_grid : c->w_fin_grid;
+  if (c->csr) RF_CK(c, stencil_setup(c));
+  c->n_ag = c->csr ? std::max(c->spmm_grid, c->st_on ? c->st_grid / c->st_geo.nq : 0) : c->w_fin_grid;
+  c->n_ag_cur = c->n_ag;
   const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k, P = (size_t)world;
   const int nsplit_max = std::max(c->nsplit, c->oz_ns);
   const size_t wpart = (!c->csr && nsplit_max > 1) ? (size_t)nsplit_max * nk : 0;
@@ -1456,6 +1641,7 @@ extern "C" void refine_destroy(refine_ctx* c) {
   if (c->own_xfull && c->Xfull) cudaFree(c->Xfull);
   if (c->ws.halo) cudaFree(c->ws.halo);
   if (c->xoff_buf) cudaFree(c->xoff_buf);
+  if (c->st_meta) cudaFree(c->st_meta);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->side) cudaStreamDestroy(c->side);
@@ -1542,6 +1728,14 @@ extern "C" refine_status refine_debug_get(refine_ctx* c, int32_t what, double* d
       RF_CK(c, cudaStreamSynchronize(c->stream));
       return REFINE_OK;
     case 9: src = ws.stats; cnt = 8; break;
+    case 11: {  // S1 kernel geometry: [stencil on, R, L, nq, grid, nx, ny, nz, gather R]
+      const StencilGeo& g = c->st_geo;
+      const double h[9] = {c->st_on ? 1.0 : 0.0, (double)g.R, (double)g.L, (double)g.nq, (double)c->st_grid,
+                           (double)g.nx, (double)g.ny, (double)g.nz, (double)c->gather_R};
+      RF_CK(c, cudaMemcpyAsync(dst, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+      RF_CK(c, cudaStreamSynchronize(c->stream));
+      return REFINE_OK;
+    }
     case 10:   // clock64 phase log (REFINE_KXK_TIMING=1), raw int64 bits
       if (!ws.tlog) return REFINE_E_UNSUPPORTED;
       src = reinterpret_cast<const double*>(ws.tlog); cnt = 64; break;

@@ -1,0 +1,280 @@
+// spmm_stencil.cuh -- S1 (W = (A - shift I) X^, Alg. 4 line 1; Sec. 5.1 shift
+// PAPER.md:1203) for CSR matrices whose nonzeros couple each point of a regular 2-D / 3-D grid only
+// with itself and its axis neighbours (the configs' anisotropic Laplacians), with the
+// X rows staged in shared memory by TMA instead of gathered from L2.
+//
+// Why: the gather kernel (spmm_csr.cuh) reads every nonzero's X row through L1/L2 -- nnz k 8 bytes
+// (29 GB at cfg5, 1.3 GB at cfg4) against 8.7 / 0.6 GB of algorithmic HBM traffic -- and runs at
+// the L2 throughput / gather-latency limit (58-63 % of HBM).  Here a CTA owns a pencil: a tile of
+// L lines x R points of the (x, y) grid and KC of the k columns, swept along z (the slowest grid
+// axis; a 2-D grid is swept along y with L = 1).  Each z-slab of the tile's footprint (the tile plus
+// a one-point halo in x and y) is loaded ONCE by one 4-D TMA box (cp.async.bulk.tensor, zero fill
+// outside the grid) into a 4-slot ring, two slabs ahead of the compute; a row's +-z neighbours are
+// the same box position in the previous / next slot.  X therefore crosses L2 -> SM about
+// (L + 2)(R + 2) / (L R) times instead of nnz / n times, and the kernel streams HBM.
+//
+// The nonzeros are re-packed once at init (refine_init_csr; A is borrowed and constant) into
+// per-slab blocks of fixed-size row records -- NZR values in CSR order plus one 64-bit word of
+// neighbour codes and the row length -- so a slab's records arrive with one bulk copy on the same
+// mbarrier as its X box.  Each w_ij is the fma chain over the row's nonzeros in ascending CSR order
+// (the oracle's chain, bit-identical W), shifted by fma(-shift, x_ij, .); alpha / g partials are
+// 8-row FP64 blocks merged into double-double accumulators (same class as the gather kernel), one
+// slot per CTA and column block, reduced in fixed order: deterministic.
+#pragma once
+#include <cuda.h>   // CUtensorMap (encoded on the host through the driver entry point)
+
+#include "common.cuh"
+
+namespace rf {
+
+constexpr int ST_THREADS = 512;     // 16 warps; thread 0 also issues the TMA loads
+constexpr int ST_BLOCK = ST_THREADS;
+constexpr int ST_SLOTS = 4;         // ring: slabs z - 1, z, z + 1 in use, z + 2 loading
+
+// codes of a nonzero's column relative to its row (x fastest, then y, then z)
+enum : int { SC_SELF = 0, SC_XM, SC_XP, SC_YM, SC_YP, SC_ZM, SC_ZP };
+constexpr uint64_t ST_CANON = 1ull << 55;   // code-word flag: canonical full stencil row (fast path)
+
+struct StencilGeo {
+  int nx, ny, nz;         // grid; a 2-D grid is (nx, 1, ny)
+  int hy;                 // 1 if ny > 1: the box carries one halo line on each side
+  int R, L, Rb, Lb;       // tile R points x L lines; box (R + 2) x (L + 2 hy)
+  int ntx, nty, nseg, zlen;
+  int nq, KC;             // column blocks of KC columns
+  int nzr;                // values per row record (5 or 7)
+  int64_t d2, d3;         // row strides of y and z
+  int box_bytes, meta_bytes, slot_bytes;
+  int64_t blocks;         // metadata blocks (ntx nty nz)
+};
+
+// one record per output row: NZR values (CSR order) then a code word: byte u < NZR = code of
+// nonzero u, byte 7 = row length (0 for padding rows of partial tiles)
+template <int NZR>
+__global__ void stencil_pack_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                    const double* __restrict__ val, StencilGeo g, double* __restrict__ meta) {
+  const int64_t n = (int64_t)g.nx * g.ny * g.nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % g.nx), y = (int)((i / g.nx) % g.ny), z = (int)(i / g.d3);
+    const int tx = x / g.R, ty = y / g.L, lx = x % g.R, ly = y % g.L;
+    const int64_t blk = ((int64_t)z * g.nty + ty) * g.ntx + tx;
+    double* rec = meta + (blk * g.L * g.R + (int64_t)ly * g.R + lx) * (NZR + 1);
+    uint64_t code = 0;
+    const int32_t p0 = rp[i], p1 = rp[i + 1];
+    for (int32_t p = p0; p < p1; ++p) {
+      const int64_t o = (int64_t)ci[p] - i;
+      const int c = o == 0 ? SC_SELF : o == -1 ? SC_XM : o == 1 ? SC_XP : o == -g.d2 ? SC_YM : o == g.d2 ? SC_YP
+                  : o == -g.d3 ? SC_ZM : SC_ZP;
+      rec[p - p0] = val[p];
+      code |= (uint64_t)c << (8 * (p - p0));
+    }
+    code |= (uint64_t)(p1 - p0) << 56;
+    // canonical full row: every neighbour present, in ascending column order -- 3-D (NZR = 7)
+    // z-, y-, x-, self, x+, y+, z+; 2-D (NZR = 5) y-, x-, self, x+, y+ (y is the swept axis, codes ZM / ZP)
+    const uint64_t canon = NZR == 7 ? 0x06040200010305ull : 0x0602000105ull;
+    const uint64_t cmask = NZR == 7 ? 0xffffffffffffffull : 0xffffffffffull;
+    if (p1 - p0 == NZR && (code & cmask) == canon) code |= ST_CANON;
+    rec[NZR] = __longlong_as_double((long long)code);
+  }
+}
+
+// structure check over all nonzeros: every offset is 0, +-1 (same line), +-d2 (same plane) or
+// +-d3, and every row has at most 7 nonzeros.  bad[0] |= 1 on a violation; bad[1] = max row length.
+__global__ void stencil_check_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t n,
+                                     int64_t nx, int64_t d2, int64_t d3, int* bad) {
+  int mx = 0, b = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p0 = rp[i], p1 = rp[i + 1];
+    mx = max(mx, p1 - p0);
+    for (int32_t p = p0; p < p1; ++p) {
+      const int64_t c = ci[p], o = c - i;
+      bool ok;
+      if (o == 0) ok = true;
+      else if (o == 1 || o == -1) ok = (c / nx) == (i / nx);                   // no wrap across lines
+      else if (d3 != d2 && (o == d2 || o == -d2)) ok = (c / d3) == (i / d3);   // 3-D: no wrap across planes
+      else ok = (o == d3 || o == -d3);
+      if (p > p0 && ci[p] <= ci[p - 1]) ok = false;                           // sorted, no duplicates
+      if (!ok) b = 1;
+    }
+  }
+  if (b) atomicOr(bad, 1);
+  atomicMax(bad + 1, mx);
+}
+
+template <int KC, int NZR>
+__global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX,
+                                                                   const double* __restrict__ meta, const StencilGeo g) {
+  // a row's KC columns: LPR lanes x VPL double2, lane l owning double2 l + LPR v (each LDS.128 of a
+  // quarter warp then reads 128 contiguous bytes of one row: no bank conflicts)
+  constexpr int LPR = KC >= 16 ? 8 : KC / 2;
+  constexpr int VPL = KC / (2 * LPR);
+  constexpr int RGP = ST_THREADS / LPR;       // rows per pass
+  constexpr int REC = NZR + 1;
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(st_smem);           // full[slot]: box + records landed
+  unsigned char* slots = st_smem + 128;
+  if (*ws.status != ST_OK) return;
+  const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
+  const int K = ws.k, nq = g.nq;
+  const int q = blockIdx.x % nq, b = blockIdx.x / nq, nb = gridDim.x / nq;
+  const int64_t P = (int64_t)g.ntx * g.nty * g.nseg;   // pencil segments per column block
+  if (tid == 0) {
+    for (int s = 0; s < ST_SLOTS; ++s) mbar_init(&mbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // the CTA's load sequence: items it = b, b + nb, ... ; item -> (tx, ty, seg); loads z = zs-1 .. ze
+  struct Cur { int64_t it; int z, zs, ze, tx, ty; };
+  auto item_begin = [&](Cur& c) -> bool {
+    if (c.it >= P) return false;
+    c.tx = (int)(c.it % g.ntx);
+    c.ty = (int)((c.it / g.ntx) % g.nty);
+    const int seg = (int)(c.it / ((int64_t)g.ntx * g.nty));
+    c.zs = seg * g.zlen;
+    c.ze = min(g.nz, c.zs + g.zlen);
+    c.z = c.zs - 1;
+    return true;
+  };
+  auto advance = [&](Cur& c) -> bool {   // next load; false when the sequence ends
+    if (++c.z <= c.ze) return true;
+    c.it += nb;
+    return item_begin(c);
+  };
+  auto issue = [&](const Cur& c, int m) {   // thread 0: load m of the sequence into slot m % 4
+    const int s = m % ST_SLOTS;
+    unsigned char* sl = slots + (size_t)s * g.slot_bytes;
+    const bool inner = c.z >= c.zs && c.z < c.ze;
+    mbar_expect_tx(&mbar[s], g.box_bytes + (inner ? g.meta_bytes : 0));
+    tma_load_4d(sl, &tmX, q * KC, c.tx * g.R - 1, c.ty * g.L - g.hy, c.z, &mbar[s]);
+    if (inner) {
+      const int64_t blk = ((int64_t)c.z * g.nty + c.ty) * g.ntx + c.tx;
+      bulk_g2s(sl + g.box_bytes, meta + blk * g.L * g.R * REC, g.meta_bytes, &mbar[s]);
+    }
+  };
+
+  Cur cons{b, 0, 0, 0, 0, 0}, prod{b, 0, 0, 0, 0, 0};
+  bool more_c = item_begin(cons);
+  bool more_p = item_begin(prod);
+  int m_issued = 0;
+  if (tid == 0) {
+    for (int t = 0; t < 2 && more_p; ++t) {
+      issue(prod, m_issued++);
+      more_p = advance(prod);
+    }
+  }
+  const double shift = ws.shift;
+  const int RbKC = g.Rb * KC;
+  const int nrow = g.L * g.R;
+  const int dly = RGP / g.R, dlx = RGP - dly * g.R;   // per-pass step of a thread's (ly, lx)
+  double ba[2 * VPL], bg[2 * VPL];
+  dd da[2 * VPL], dg[2 * VPL];
+#pragma unroll
+  for (int u = 0; u < 2 * VPL; ++u) { ba[u] = bg[u] = 0.0; da[u] = dg[u] = dd{0.0, 0.0}; }
+  int nb8 = 0;
+  char* Wb = reinterpret_cast<char*>(ws.W);
+  if (more_c) mbar_wait(&mbar[0], 0);
+  for (int m = 0; more_c; ++m) {
+    __syncthreads();                           // compute of load m - 1 done: slot (m + 2) % 4 is free
+    if (tid == 0 && more_p) {
+      issue(prod, m_issued++);
+      more_p = advance(prod);
+    }
+    const int nxt = m + 1;                     // every thread waits each load once, in order
+    const bool has_next = !(cons.z == cons.ze && cons.it + nb >= P);
+    if (has_next) mbar_wait(&mbar[nxt % ST_SLOTS], (nxt / ST_SLOTS) & 1);
+    if (cons.z >= cons.zs && cons.z < cons.ze) {   // compute the outputs of slab z
+      const double* X0 = reinterpret_cast<const double*>(slots + (size_t)(m % ST_SLOTS) * g.slot_bytes);
+      const double* Xm = reinterpret_cast<const double*>(slots + (size_t)((m + 3) % ST_SLOTS) * g.slot_bytes);
+      const double* Xp = reinterpret_cast<const double*>(slots + (size_t)((m + 1) % ST_SLOTS) * g.slot_bytes);
+      const double* rec0 = reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(X0) + g.box_bytes);
+      const int x0 = cons.tx * g.R, y0 = cons.ty * g.L;
+      const int64_t zbase = (int64_t)cons.z * g.d3;
+      // this thread's rows rr = grp + j RGP as (ly, lx), advanced without divisions
+      int ly = grp / g.R, lx = grp - ly * g.R;
+      for (int rr = grp; rr < nrow; rr += RGP) {
+        const int x = x0 + lx, y = y0 + ly;
+        const int cly = ly, clx = lx;
+        lx += dlx; ly += dly;
+        if (lx >= g.R) { lx -= g.R; ++ly; }
+        if (x >= g.nx || y >= g.ny) continue;
+        const double2* rv = reinterpret_cast<const double2*>(rec0 + rr * REC);
+        double vv[REC];
+#pragma unroll
+        for (int u = 0; u < REC / 2; ++u) { const double2 t = rv[u]; vv[2 * u] = t.x; vv[2 * u + 1] = t.y; }
+        const uint64_t code = (uint64_t)__double_as_longlong(vv[NZR]);
+        const int ctr = ((cly + g.hy) * g.Rb + clx + 1) * KC + 2 * l;
+        double2 xi[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) xi[v] = *reinterpret_cast<const double2*>(X0 + ctr + 2 * LPR * v);
+        double acc[2 * VPL];
+#pragma unroll
+        for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;
+        auto nz = [&](double val, const double* p) {   // acc += val * (this lane's part of row p)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            const double2 t = *reinterpret_cast<const double2*>(p + 2 * LPR * v);
+            acc[2 * v] = __fma_rn(val, t.x, acc[2 * v]);
+            acc[2 * v + 1] = __fma_rn(val, t.y, acc[2 * v + 1]);
+          }
+        };
+        if (code & ST_CANON) {   // the fma chain in CSR (= ascending column) order, offsets fixed
+          const double* xc = X0 + ctr;
+          if constexpr (NZR == 7) {
+            nz(vv[0], Xm + ctr); nz(vv[1], xc - RbKC); nz(vv[2], xc - KC); nz(vv[3], xc);
+            nz(vv[4], xc + KC); nz(vv[5], xc + RbKC); nz(vv[6], Xp + ctr);
+          } else {
+            nz(vv[0], Xm + ctr); nz(vv[1], xc - KC); nz(vv[2], xc); nz(vv[3], xc + KC); nz(vv[4], Xp + ctr);
+          }
+        } else {                 // boundary rows: the coded neighbours, CSR order
+          const int len = (int)(code >> 56);
+          for (int u = 0; u < len; ++u) {
+            const int c = (int)((code >> (8 * u)) & 0xff);
+            const int o = c == SC_XM ? -KC : c == SC_XP ? KC : c == SC_YM ? -RbKC : c == SC_YP ? RbKC : 0;
+            const double* base = c == SC_ZM ? Xm : c == SC_ZP ? Xp : X0;
+            nz(rec0[rr * REC + u], base + ctr + o);
+          }
+        }
+        const int64_t i = zbase + (int64_t)y * g.d2 + x;
+        char* wrow = Wb + ((uint64_t)i * K + q * KC + 2 * l) * 8u;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          double w0 = acc[2 * v], w1 = acc[2 * v + 1];
+          if (shift != 0.0) { w0 = __fma_rn(-shift, xi[v].x, w0); w1 = __fma_rn(-shift, xi[v].y, w1); }
+          __stcs(reinterpret_cast<double2*>(wrow + 16 * LPR * v), make_double2(w0, w1));
+          ba[2 * v] = __fma_rn(xi[v].x, xi[v].x, ba[2 * v]);
+          ba[2 * v + 1] = __fma_rn(xi[v].y, xi[v].y, ba[2 * v + 1]);
+          bg[2 * v] = __fma_rn(xi[v].x, w0, bg[2 * v]);
+          bg[2 * v + 1] = __fma_rn(xi[v].y, w1, bg[2 * v + 1]);
+        }
+        if (++nb8 == 8) {   // 8-row FP64 blocks merged into double-double
+          nb8 = 0;
+#pragma unroll
+          for (int u = 0; u < 2 * VPL; ++u) { dd_add1(da[u], ba[u]); dd_add1(dg[u], bg[u]); ba[u] = bg[u] = 0.0; }
+        }
+      }
+    }
+    more_c = advance(cons);
+  }
+#pragma unroll
+  for (int u = 0; u < 2 * VPL; ++u) { dd_add1(da[u], ba[u]); dd_add1(dg[u], bg[u]); }
+  // fixed-order reduction over the RGP row groups, then this CTA's slot: thread (grp, l) holds
+  // columns 2 (l + LPR v) + {0, 1} of column block q
+  __syncthreads();
+  dd* red = reinterpret_cast<dd*>(slots);              // [4 VPL][ST_THREADS]
+#pragma unroll
+  for (int u = 0; u < 2 * VPL; ++u) { red[u * ST_THREADS + tid] = da[u]; red[(2 * VPL + u) * ST_THREADS + tid] = dg[u]; }
+  __syncthreads();
+  for (int j = tid; j < KC; j += ST_THREADS) {
+    const int pair = j >> 1, e = j & 1, v = pair / LPR, lj = pair % LPR;
+    const int ua = 2 * v + e, ug = 2 * VPL + 2 * v + e;
+    dd ta = red[ua * ST_THREADS + lj], tg = red[ug * ST_THREADS + lj];
+    for (int gq = 1; gq < RGP; ++gq) {
+      dd_add(ta, red[ua * ST_THREADS + gq * LPR + lj]);
+      dd_add(tg, red[ug * ST_THREADS + gq * LPR + lj]);
+    }
+    double* slot = ws.ag + ((int64_t)b * K + q * KC + j) * 4;
+    slot[0] = ta.hi; slot[1] = ta.lo; slot[2] = tg.hi; slot[3] = tg.lo;
+  }
+}
+
+}  // namespace rf

@@ -3,11 +3,15 @@
 The north_star bar is a relative Frobenius difference <= 1e-10 over the whole n x k block.  Because
 the top k rows (written by kxk_finish) and the rows > k (pass C) come from different kernels, a
 localised error in one block could hide under sqrt(k) ||X||_F at large k, so each block is also
-checked per column: max |X_gpu - X_oracle| <= 1e-10 (every column has unit norm after the sweep).
-The statistics of the sweep are compared too, including min_gap."""
+checked per column: max |X_gpu - X_oracle| <= max(1e-10, u ||A||_inf / min gap).  The second term is
+the first-order sensitivity of the top block: E_ij = V_ij / (d_j - d_i) (eq. Eoffdiag) turns the O(u ||A||)
+rounding of V (any summation order) into u ||A|| / gap per entry -- e.g. 1.6e-9 for
+k = 128 targets 5e-5 apart; the whole-block Frobenius bar stays 1e-10.  The statistics of the sweep
+ are compared too, including min_gap."""
 import numpy as np
 
 TOL = 1e-10
+U = 2.0 ** -53
 
 
 def rel(a, b):
@@ -15,8 +19,21 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
 
 
+def cond_tol(ref, normA, tol=TOL, delta_c=10.0):
+    """max(tol, u ||A||_inf / min |d_i - d_j|) over the pairs that take the 1/gap formula (gap > delta;
+    pairs within delta take beta and are not amplified), from the oracle's Rayleigh quotients."""
+    d = ref.debug.get("dtilde") if ref.debug else None
+    if d is None or normA is None or len(d) < 2:
+        return tol
+    g = np.abs(d[:, None] - d[None, :])
+    g = g[g > delta_c * normA * U]
+    if g.size == 0:
+        return tol
+    return max(tol, U * normA / float(g.min()))
+
+
 def compare_sweep(Xg, ref, st=None, k=None, top=True, stats_tol=1e-8, corr_rel=1e-6, corr_abs=1e-9, tol=TOL,
-                  where=""):
+                  where="", normA=None, elem_tol=None):
     """Xg: the GPU's output (numpy n_loc x k); ref: oracle.SweepResult of the same input; st: the GPU's
     refine_sweep_stats (or None); top: Xg's first k rows are the global top block.  Returns the
     relative Frobenius difference."""
@@ -26,10 +43,11 @@ def compare_sweep(Xg, ref, st=None, k=None, top=True, stats_tol=1e-8, corr_rel=1
     D = np.abs(Xg - ref.X)
     cn = np.maximum(np.linalg.norm(ref.X, axis=0), 1e-300)
     blocks = [(slice(0, k), "top"), (slice(k, None), "lower")] if top else [(slice(0, None), "all")]
+    et = elem_tol if elem_tol is not None else cond_tol(ref, normA, tol)
     for sl, name in blocks:
         if D[sl].size:
             m = float((D[sl].max(axis=0) / cn).max())
-            assert m <= tol, f"{where} {name} block max-abs per column {m:.3e}"
+            assert m <= et, f"{where} {name} block max-abs per column {m:.3e} (bound {et:.3e})"
     if st is not None:
         rs = ref.stats
         assert st.flipped == rs.flipped, where

@@ -8,8 +8,10 @@ Rayleigh-quotient gaps sit far from the threshold delta = c ||A - shift I||_inf 
 
 * an exact tie: A diagonal with lambda_1 = lambda_2 and identical perturbations of the two tied
   columns -> d_1 == d_2 bit for bit on both sides;
-* near ties on a dense Q diag(lambda) Q^T: target gaps 2^-50 lambda (hit) and 2^-40 lambda (no hit),
-  start noise 1e-10 so the Rayleigh quotients stay within O(eps^2 ||A||) of lambda;
+* near ties on a dense Q diag(lambda) Q^T: target gaps 2^-50 lambda (hit), 2^-40 lambda (no hit, just
+  above delta: ill-conditioned, so X is compared within u ||A||_inf / gap) and 2^-16 lambda (no hit,
+  well separated: the 1e-10 bar), start noise 1e-10 so the Rayleigh quotients stay within
+  O(eps^2 ||A||) of lambda;
 * the degenerate sine modes (p, q) / (q, p) of an isotropic Dirichlet Laplacian (CSR): the two
   modes of a pair have the same eigenvalue, their computed Rayleigh quotients differ by rounding.
 
@@ -22,7 +24,7 @@ import torch
 
 import oracle
 import synth
-from parity_util import compare_sweep
+from parity_util import compare_sweep, cond_tol
 
 pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
@@ -85,10 +87,16 @@ def _check(pkg, R, op, X0, k, beta_zero, expect_hits):
         assert ref.stats.delta_hits > 0
     else:
         assert ref.stats.delta_hits == 0
-    compare_sweep(X.cpu().numpy(), ref, st, k=k, where=f"beta_zero={beta_zero}")
+    # Without a hit, E_ij = V_ij / gap amplifies the O(u ||A||) rounding of V by 1 / gap: a gap just
+    # above delta (2^-40 lambda here) makes one-step agreement to 1e-10 impossible for ANY two
+    # summation orders, so the bar is max(1e-10, u ||A||_inf / gap) there; the branch
+    # decision itself (delta_hits, which formula each entry used) must still agree exactly.
+    ctol = cond_tol(ref, op.norm_inf())
+    compare_sweep(X.cpu().numpy(), ref, st, k=k, where=f"beta_zero={beta_zero}", tol=ctol, elem_tol=ctol,
+                  corr_rel=max(1e-6, ctol))
     E11 = R.debug(pkg.DBG_E11).cpu().numpy()
     Eo = ref.debug["E"][:k]
-    assert np.abs(E11 - Eo).max() <= 1e-12, np.abs(E11 - Eo).max()
+    assert np.abs(E11 - Eo).max() <= max(1e-12, ctol * max(1.0, np.abs(Eo).max())), np.abs(E11 - Eo).max()
     if expect_hits:
         hit = np.abs(d[:, None] - d[None, :]) <= delta
         np.fill_diagonal(hit, False)
@@ -113,7 +121,7 @@ def test_delta_exact_tie_dense(pkg, world, beta_zero):
     assert st.delta_hits == 2 and st.min_gap == 0.0
 
 
-@pytest.mark.parametrize("g,hit", [(2.0 ** -50, True), (2.0 ** -40, False)])
+@pytest.mark.parametrize("g,hit", [(2.0 ** -50, True), (2.0 ** -40, False), (2.0 ** -16, False)])
 @pytest.mark.parametrize("beta_zero", [False, True])
 @pytest.mark.parametrize("world", [1, 2])
 def test_delta_near_tie_dense_both_sides(pkg, g, hit, beta_zero, world):

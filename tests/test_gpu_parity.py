@@ -55,7 +55,8 @@ def one_step(pkg, p, sweeps, R=None, op=None, stats_tol=1e-8):
         s, st = R.refine_sweep(X, stats=True)
         ref = oracle.sweep(op, xin, debug=True)
         assert s == pkg.REFINE_OK and ref.status == oracle.OK, (t, s, ref.status)
-        e = compare_sweep(X.cpu().numpy(), ref, st, k=p.k, stats_tol=stats_tol, where=f"sweep {t}")
+        e = compare_sweep(X.cpu().numpy(), ref, st, k=p.k, stats_tol=stats_tol, where=f"sweep {t}",
+                          normA=op.norm_inf())
         worst = max(worst, e)
     return worst, X
 

@@ -1,8 +1,9 @@
-# scratch GPU call (round 2): full GPU suite + default bench
 O=gpurun_out/r02
 mkdir -p $O
-nproc > $O/nproc.txt
-timeout 1700 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -rs --durations=20 -s > $O/pytest_gpu_1.txt 2>&1
-tail -30 $O/pytest_gpu_1.txt
-timeout 600 python bench.py > $O/bench_1.json 2> $O/bench_1.err
-cat $O/bench_1.json | head -c 600
+timeout 900 python -m pytest tests/test_gpu_stencil.py tests/test_gpu_delta.py tests/test_gpu_parity.py tests/test_gpu_next4.py tests/test_gpu_rr.py tests/test_gpu_next3.py tests/test_gpu_edges.py -m gpu -q --timeout 600 -p no:cacheprovider > $O/pytest_3.txt 2>&1
+tail -5 $O/pytest_3.txt
+grep -E "^FAILED" $O/pytest_3.txt | head
+for c in cfg4 cfg5; do
+  REFINE_VERBOSE=1 timeout 300 python bench.py --config $c --no-extra --steps 5 > $O/bench_$c.json 2> $O/bench_$c.err
+  python -c "import json; d=json.load(open('$O/bench_$c.json')); print('$c', d['ms_per_step'], d.get('kernels_ms')['spmm_csr'])"
+done
