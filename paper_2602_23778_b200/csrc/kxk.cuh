@@ -501,7 +501,34 @@ RF_DEV void cluster_sync() {
 __host__ __device__ constexpr int kxk_cluster(int k) { return k >= 64 ? 8 : (k >= 32 ? 4 : 1); }
 constexpr int KXK_SCRATCH_EXTRA = 64;   // doubles after the 16 k x k scratch matrices (cluster partials)
 
+// Small k (k <= KXK_SMALL): the whole k x k chain in ONE CTA with every k x k operand resident in
+// shared memory and each product one output element per thread (a plain fma chain over ascending p):
+// no cluster barriers, no global scratch round trips and no per-product panel staging -- the chain is
+// latency bound at these sizes (measured 29 us at k = 4, 39 us at k = 16 with the DMMA / L2-scratch form).
+constexpr int KXK_SMALL = 32;
+constexpr int KXK_SMALL_MATS = 20;   // k x k matrices resident in shared memory (see kxk_finish_kernel<true>)
+// layout: 20 k x k matrices | column-sum partials (8 x 7 x k) | d copy (k) | sigma, d, alpha, rr2 (4 k) | 64 spare
+__host__ __device__ constexpr int kxk_small_smem_doubles(int k) { return KXK_SMALL_MATS * k * k + 8 * 7 * k + k + 4 * k + 64; }
+RF_DEV void smem_mm(int k, double alpha, const double* A, bool ta, const double* B, double beta, const double* C0,
+                    double* C) {
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < k * k) {
+    const int i = t / k, j = t - i * k;
+    const double* a = ta ? A + i : A + i * k;
+    const int as = ta ? k : 1;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int p = 0; p < k; ++p) acc = fma(a[p * as], B[p * k + j], acc);
+    const double v = alpha * acc;
+    C[i * k + j] = (beta != 0.0) ? fma(beta, C0[i * k + j], v) : v;
+  }
+  __syncthreads();
+}
+
 // Xtop/Wtop: the top k rows of X^ (in/out) and W (un-flipped), ld k.
+// SMALL (k <= KXK_SMALL, one CTA): scratch, L, T, E_11 and X~_1 live in shared memory, products by smem_mm.
+template <bool SMALL>
 __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* __restrict__ Xtop,
                                                                  const double* __restrict__ Wtop) {
   extern __shared__ __align__(16) double sm[];
@@ -509,18 +536,31 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   __shared__ double s_red[4][KMAX];
   if (*ws.status != ST_OK) return;
   const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
-  const int crank = (int)cluster_ctarank(), ncl = (int)cluster_nctarank();
+  const int crank = SMALL ? 0 : (int)cluster_ctarank(), ncl = SMALL ? 1 : (int)cluster_nctarank();
   const int per = (((k + ncl - 1) / ncl) + 7) & ~7;
   const int r0 = min(k, crank * per), r1 = min(k, r0 + per), nr = r1 - r0;
-  double* S = ws.scratch;
+  double* S = SMALL ? sm : ws.scratch;
   double *Xp = S, *R1 = S + kk, *Mp = S + 2 * kk, *Gp = S + 3 * kk, *Ui = S + 4 * kk, *Z = S + 5 * kk,
          *P = S + 6 * kk, *V1 = S + 7 * kk, *Pt = S + 8 * kk, *GPt = S + 9 * kk, *S2 = S + 10 * kk,
          *Qm = S + 11 * kk, *B = S + 12 * kk, *LB = S + 13 * kk, *UB = S + 14 * kk;
-  double* part = S + 16 * kk;                          // [0, 8): delta hits, [8, 16): gram max per CTA
-  const double* sig = ws.sigma;
-  const double* d = ws.d;
+  // SMALL: copies of L, T and the CTA's E_11 / X~_1 in shared memory (matrices 15..17)
+  const double* Lm = SMALL ? S + 16 * kk : ws.L;
+  const double* Tm = SMALL ? S + 17 * kk : ws.T;
+  double* E11 = SMALL ? S + 18 * kk : ws.E11;
+  double* Xt1 = SMALL ? S + 19 * kk : ws.Xt;
+  double* part = SMALL ? sm + kxk_small_smem_doubles(k) - 64 : S + 16 * kk;   // [0, 8): delta hits, [8, 16): gram max per CTA
+  double* cs_base = SMALL ? S + KXK_SMALL_MATS * kk : sm;   // column-sum partials (after the matrices when SMALL)
+  double* vec = cs_base + 8 * 7 * k + k;               // SMALL: sigma, d, alpha, rr2 copies
+  const double* sig = SMALL ? vec : ws.sigma;
+  const double* d = SMALL ? vec + k : ws.d;
+  const double* alp = SMALL ? vec + 2 * k : ws.alpha;
+  const double* rr2p = SMALL ? vec + 3 * k : ws.rr2;
   // this CTA's rows of C = alpha op(A) B + beta C0 (k x k operands, B not transposed)
   auto rgemm = [&](double alpha, const double* A, bool ta, const double* Bm, double beta, const double* C0, double* C) {
+    if (SMALL) {
+      smem_mm(k, alpha, A, ta, Bm, beta, C0, C);
+      return;
+    }
     if (nr > 0)
       cta_gemm_fullk(nr, k, k, alpha, ta ? A + r0 : A + r0 * k, k, ta, Bm, k, beta, C0 ? C0 + r0 * k : nullptr, k,
                      C + r0 * k, k, sm);
@@ -538,26 +578,53 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 21);
   }
+  if (SMALL) {   // every global input of the chain into shared memory in one round trip
+    for (int e = tid; e < kk; e += nt) {
+      cp_async8(S + 16 * kk + e, ws.L + e, true);
+      cp_async8(S + 17 * kk + e, ws.T + e, true);
+      cp_async8(Xp + e, Xtop + e, true);
+      cp_async8(R1 + e, Wtop + e, true);
+      cp_async8(Mp + e, ws.M2 + e, true);
+      cp_async8(Gp + e, ws.G2 + e, true);
+      cp_async8(Ui + e, ws.Uinv + e, true);
+    }
+    for (int j = tid; j < k; j += nt) {
+      cp_async8(vec + j, ws.sigma + j, true);
+      cp_async8(vec + k + j, ws.d + j, true);
+      cp_async8(vec + 2 * k + j, ws.alpha + j, true);
+      cp_async8(vec + 3 * k + j, ws.rr2 + j, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  // (SMALL: in place on the shared copies; each element is read and written by one thread)
+  const double* srcX = SMALL ? Xp : Xtop;
+  const double* srcW = SMALL ? R1 : Wtop;
+  const double* srcM = SMALL ? Mp : ws.M2;
+  const double* srcG = SMALL ? Gp : ws.G2;
+  const double* srcU = SMALL ? Ui : ws.Uinv;
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
-    const double xp = Xtop[e] * sig[j];
+    const double xp = srcX[e] * sig[j];
+    const double w = srcW[e];
     Xp[e] = xp;
-    R1[e] = fma(-xp, d[j], Wtop[e] * sig[j]);
-    Mp[e] = sig[i] * ws.M2[e] * sig[j];
-    Gp[e] = sig[i] * ws.G2[e] * sig[j];
-    Ui[e] = sig[i] * ws.Uinv[e];                      // U'^{-1} = Sigma U^{-1}
+    R1[e] = fma(-xp, d[j], w * sig[j]);
+    Mp[e] = sig[i] * srcM[e] * sig[j];
+    Gp[e] = sig[i] * srcG[e] * sig[j];
+    Ui[e] = sig[i] * srcU[e];                         // U'^{-1} = Sigma U^{-1}
   }
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 22);
-  rgemm(1.0, ws.L, true, R1, 0.0, nullptr, Z);        // Z = L^T R_1
+  rgemm(1.0, Lm, true, R1, 0.0, nullptr, Z);        // Z = L^T R_1
   rgemm(1.0, Ui, true, Mp, 1.0, Z, Z);                //   + U'^{-T} M'
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 23);
-  rgemm(1.0, ws.T, true, Z, 0.0, nullptr, P);         // P = T^T Z
+  rgemm(1.0, Tm, true, Z, 0.0, nullptr, P);         // P = T^T Z
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 24);
-  rgemm(-1.0, ws.L, false, P, 1.0, R1, V1);           // V_1 = R_1 - L P
+  rgemm(-1.0, Lm, false, P, 1.0, R1, V1);           // V_1 = R_1 - L P
   rgemm(1.0, Ui, false, P, 0.0, nullptr, Pt);         // P~ = U'^{-1} P
   // E_11 (line 6): beta needs the Gram G = X'^T X' = X'_1^T X'_1 + G'
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
@@ -567,7 +634,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     if (ws.top_zero) {                                 // after Rayleigh-Ritz
       v = 0.0;
     } else if (i == j) {
-      v = (1.0 - ws.alpha[i]) / 2.0;
+      v = (1.0 - alp[i]) / 2.0;
     } else {
       const double gap = d[j] - d[i];
       if (fabs(gap) <= ws.delta) {
@@ -579,7 +646,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
         v = V1[e] / gap;
       }
     }
-    ws.E11[e] = v;
+    E11[e] = v;
   }
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 25);
@@ -588,14 +655,14 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     for (int j = tid & 31; j < k; j += 32) S2[i * k + j] = (Mp[i * k + j] - GPt[i * k + j]) / d[j];
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 26);
-  rgemm(1.0, ws.L, true, ws.E11, 0.0, nullptr, Qm);   // Qm = L^T E_11
+  rgemm(1.0, Lm, true, E11, 0.0, nullptr, Qm);   // Qm = L^T E_11
   rgemm(1.0, Ui, true, S2, 1.0, Qm, Qm);              //   + U'^{-T} S2
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 27);
-  rgemm(1.0, ws.T, false, Qm, 0.0, nullptr, B);       // B = T Qm
+  rgemm(1.0, Tm, false, Qm, 0.0, nullptr, B);       // B = T Qm
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 28);
-  rgemm(1.0, ws.L, false, B, 0.0, nullptr, LB);       // L B
+  rgemm(1.0, Lm, false, B, 0.0, nullptr, LB);       // L B
   rgemm(1.0, Ui, false, B, 0.0, nullptr, UB);         // U'^{-1} B
   // S7 folded into this kernel: the column norms of X~ over the
   // rows >= top follow from the pass-B sums, with x~_i = w'_i D^-1 - x'_i C' and w' = r' + x' D:
@@ -608,7 +675,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   for (int l = r0 + (tid >> 5); l < r1; l += 32)
     for (int j = tid & 31; j < k; j += 32) {
     const int e = l * k + j;
-    ws.Xt[e] = Xp[e] + (ws.E11[e] - LB[e]);            // X~_1 = X'_1 + (E_11 - L B)  (top rows of X~)
+    Xt1[e] = Xp[e] + (E11[e] - LB[e]);                 // X~_1 = X'_1 + (E_11 - L B)  (top rows of X~)
     Cp[e] = Pt[e] / d[j] + UB[e];
     ws.Csig[e] = sig[l] * Cp[e];                       // Csig = Sigma (P~ D^{-1} + U'^{-1} B)
   }
@@ -636,8 +703,8 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     // (fixed partition, groups combined in order -- deterministic)
     constexpr int NQ = 7;
     const int NG = min(8, k);                          // row groups (a short combine chain)
-    double* cs = sm;                                   // [NG][NQ][k] partials (cta_gemm's panel space)
-    double* sd = sm + (size_t)NG * NQ * k;             // d
+    double* cs = cs_base;                              // [NG][NQ][k] partials (cta_gemm's panel space)
+    double* sd = cs_base + (size_t)NG * NQ * k;        // d
     for (int j = tid; j < k; j += nt) sd[j] = d[j];
     if (tid < NG * k) {
       const int g = tid / k, j = tid % k;
@@ -645,7 +712,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
       double q[NQ] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       for (int l = g; l < k; l += NG) {
         const int e = l * k + j;
-        const double x = ws.Xt[e], r = R1[e], ee = ws.E11[e], pt = Pt[e], c = Cp[e];
+        const double x = Xt1[e], r = R1[e], ee = E11[e], pt = Pt[e], c = Cp[e];
         q[0] = fma(x, x, q[0]);                        // ||x~_1j||^2 (top rows)
         q[1] = fma(r, r, q[1]);                        // ||R_1j||^2
         q[2] = fma(ee, ee, q[2]);                      // ||E_11 j||^2
@@ -658,6 +725,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
       for (int u = 0; u < NQ; ++u) cs[((size_t)g * NQ + u) * k + j] = q[u];
     }
     __syncthreads();
+    RF_TSTAMP(ws, 33);
     if (tid < k) {
       const int j = tid;
       double q[NQ];
@@ -668,8 +736,8 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
       }
       const double nt2 = q[0];
       ws.ntop[j] = nt2;
-      const double e2 = (ws.rr2[j] - 2.0 * q[3] + q[4]) / (d[j] * d[j]);
-      s_red[0][j] = q[1] + ws.rr2[j];
+      const double e2 = (rr2p[j] - 2.0 * q[3] + q[4]) / (d[j] * d[j]);
+      s_red[0][j] = q[1] + rr2p[j];
       s_red[1][j] = (ws.kjudge > 0 && j >= ws.kjudge) ? 0.0 : q[2] + e2;   // K > k: judge the leading kjudge
       double mg = INFINITY;
       for (int i = 0; i < k; ++i)
@@ -678,7 +746,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
       s_red[3][j] = (sig[j] < 0.0) ? 1.0 : 0.0;
       // column norm of X~: top rows + the identity above -> 1 / ||x~_j||
       const double dj = sd[j];
-      const double t1 = fma(dj, fma(dj, Gp[j * k + j], 2.0 * Mp[j * k + j]), ws.rr2[j]) / (dj * dj);
+      const double t1 = fma(dj, fma(dj, Gp[j * k + j], 2.0 * Mp[j * k + j]), rr2p[j]) / (dj * dj);
       const double tail = t1 - 2.0 * q[5] / dj + q[6];
       const double nrm = sqrt(nt2 + tail);
       const double inv = ws.normalize ? 1.0 / nrm : 1.0;
@@ -687,6 +755,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
       ws.scal[j] = sig[j] / d[j] * inv;
     }
     __syncthreads();
+    RF_TSTAMP(ws, 34);
     if (tid == 0) {
       double rr = 0.0, en = 0.0, mg = INFINITY, fl = 0.0, hits = 0.0, gmax = -1.0;
       for (int j = 0; j < k; ++j) { rr += s_red[0][j]; en += s_red[1][j]; mg = fmin(mg, s_red[2][j]); fl += s_red[3][j]; }
@@ -709,8 +778,9 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     const double inv = ws.invn[j];
-    Xtop[e] = ws.Xt[e] * inv;                          // final top rows of X
+    Xtop[e] = Xt1[e] * inv;                            // final top rows of X
     ws.Csig[e] *= inv;
+    if (SMALL) { ws.E11[e] = E11[e]; ws.Xt[e] = Xt1[e]; }   // (the global copies: debug / Rayleigh-Ritz readers)
   }
   if (crank == 0) RF_TSTAMP(ws, 32);
 }

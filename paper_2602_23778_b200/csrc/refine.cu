@@ -475,8 +475,12 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
 
 // kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs
 static cudaError_t launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
+  if (ws.k <= KXK_SMALL) {   // one CTA, everything in shared memory
+    kxk_finish_kernel<true><<<1, KXK_THREADS, kxk_small_smem_doubles(ws.k) * 8, s>>>(ws, X, ws.W);
+    return cudaGetLastError();
+  }
   if (kxk_cluster(ws.k) == 1) {   // (a plain launch is an implicit 1-CTA cluster)
-    kxk_finish_kernel<<<1, KXK_THREADS, FK_SMEM * 8, s>>>(ws, X, ws.W);
+    kxk_finish_kernel<false><<<1, KXK_THREADS, FK_SMEM * 8, s>>>(ws, X, ws.W);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -491,7 +495,7 @@ static cudaError_t launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kxk_finish_kernel, ws, X, (const double*)ws.W);
+  return cudaLaunchKernelEx(&cfg, kxk_finish_kernel<false>, ws, X, (const double*)ws.W);
 }
 
 template <int KP>
@@ -962,7 +966,9 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   RF_CK(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   RF_CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RF_CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-  RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_SMEM * 8));
+  RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FK_SMEM * 8));
+  RF_CK(c, cudaFuncSetAttribute(kxk_finish_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kxk_small_smem_doubles(KXK_SMALL) * 8));
   RF_CK(c, cudaFuncSetAttribute(rr_kxk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM * 8));
   // workspace sizes (doubles)
   size_t bpart = 0, brr = 0, nslot = 0;

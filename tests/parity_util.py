@@ -54,7 +54,8 @@ def compare_sweep(Xg, ref, st=None, k=None, top=True, stats_tol=1e-8, corr_rel=1
         assert st.delta_hits == rs.delta_hits, (where, st.delta_hits, rs.delta_hits)
         assert abs(st.rel_resid - rs.rel_resid) <= stats_tol * max(rs.rel_resid, 1e-300) + 1e-18, where
         # ||E_L||_F carries the same 1/gap-amplified rounding as X~ (absolute floor 1e-9 ~ 1e-10 ||X||_F)
-        assert abs(st.corr_norm - rs.corr_norm) <= corr_rel * rs.corr_norm + corr_abs, where
+        assert abs(st.corr_norm - rs.corr_norm) <= corr_rel * rs.corr_norm + corr_abs, \
+            (where, st.corr_norm, rs.corr_norm, corr_rel)
         if "dtilde" in ref.debug:
             dmax = float(np.abs(ref.debug["dtilde"]).max())
         else:

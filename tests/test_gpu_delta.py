@@ -93,7 +93,7 @@ def _check(pkg, R, op, X0, k, beta_zero, expect_hits):
     # decision itself (delta_hits, which formula each entry used) must still agree exactly.
     ctol = cond_tol(ref, op.norm_inf())
     compare_sweep(X.cpu().numpy(), ref, st, k=k, where=f"beta_zero={beta_zero}", tol=ctol, elem_tol=ctol,
-                  corr_rel=max(1e-6, ctol))
+                  corr_rel=max(1e-6, ctol), corr_abs=max(1e-9, k * ctol))
     E11 = R.debug(pkg.DBG_E11).cpu().numpy()
     Eo = ref.debug["E"][:k]
     assert np.abs(E11 - Eo).max() <= max(1e-12, ctol * max(1.0, np.abs(Eo).max())), np.abs(E11 - Eo).max()

@@ -4,6 +4,7 @@ os.environ["REFINE_KXK_TIMING"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth, paper_2602_23778_b200 as pkg
 for (n, k) in [(256, 4), (4096, 16), (8192, 32), (8192, 64), (8192, 128)]:
+    torch.cuda.synchronize()
     p = synth.small_dense(n, k, m=8, seed=3, signs=True, device="cuda")
     R = pkg.Refiner.dense(p.A, k)
     X = p.X0.clone()
@@ -11,6 +12,10 @@ for (n, k) in [(256, 4), (4096, 16), (8192, 32), (8192, 64), (8192, 128)]:
         R.refine_sweep(X, stats=True)
     t = torch.zeros(64, dtype=torch.float64, device="cuda")
     R.refine_debug_get(10, t)
-    v = t.cpu().numpy().view(np.int64)[20:36]
+    a = t.cpu().numpy().view(np.int64)
+    v = a[20:33]
     v = v[v != 0]
     print(f"k={k}: total {(v[-1] - v[0]) / 1.965e3:.1f} us  phases " + " ".join(f"{x / 1.965e3:.1f}" for x in np.diff(v)))
+    if a[33] and a[34]:
+        print(f"   stats phase: column sums {(a[33] - a[30]) / 1.965e3:.1f} us, per-column {(a[34] - a[33]) / 1.965e3:.1f} us, "
+              f"tail {(a[31] - a[34]) / 1.965e3:.1f} us")
