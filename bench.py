@@ -322,30 +322,22 @@ def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak, n_loc=None):
             "traffic": traffic, "share_of_step": kern[top] / ms_step}
 
 
-def cpu_baseline(name, budget_s=25.0):
-    """The oracle as it stands, on the host cores, on a bounded sample of the workload.
-    Sample: the same config family at reduced n (dense: n scaled so one oracle sweep is
-    ~seconds; CSR: the full config if it fits the budget), converted to full-size sweeps/s
-    by the ratio of algorithmic flops (SURVEY.md 8(d) F_alg)."""
-    import numpy as np
+def cpu_baseline(name, budget_s=25.0, one_core=True):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload: the config
+    itself at FULL size (A built on the GPU by synth, copied to the host), timed per oracle sweep with
+    a wall clock, median over as many sweeps as fit the budget (at least one; cfg3 ~3.4 s per sweep
+    on 16 cores, cfg5 ~34 s).  one_core: also cfg1 / cfg2 with a single OpenMP thread."""
     import oracle
     import synth
-    full = {"cfg1": (256, 4), "cfg2": (4096, 16), "cfg2b": (4096, 16), "cfg3": (32768, 64)}
-    if name in full:
-        n_full, k = full[name]
-        n_s = min(n_full, 8192)
-        p = synth.make_config(name, device="cuda" if n_s > 4096 else "cpu", n=n_s)
+    import torch
+    p = synth.make_config(name, device="cuda" if name == "cfg3" and torch.cuda.is_available() else "cpu")
+    if p.kind == "dense":
         op = oracle.Operator(A=p.A.cpu().numpy())
-        X = p.X0.cpu().numpy()
-        f_full = 2.0 * n_full * n_full * k + 8.0 * n_full * k * k
-        f_s = 2.0 * n_s * n_s * k + 8.0 * n_s * k * k
-        sample = f"{name} family at n={n_s} (k={k}), oracle sweeps until {budget_s:.0f}s budget; scaled by F_alg ratio"
     else:
-        p = synth.make_config(name, device="cpu")
-        op = oracle.Operator(row_ptr=p.row_ptr.numpy(), col_idx=p.col_idx.numpy(), val=p.val.numpy())
-        X = p.X0.numpy()
-        f_full = f_s = 1.0
-        sample = f"{name} at full size, oracle sweeps until {budget_s:.0f}s budget"
+        op = oracle.Operator(row_ptr=p.row_ptr.cpu().numpy(), col_idx=p.col_idx.cpu().numpy(),
+                             val=p.val.cpu().numpy())
+    X = p.X0.cpu().numpy()
+    del p
     times = []
     t_start = time.perf_counter()
     while True:
@@ -356,15 +348,35 @@ def cpu_baseline(name, budget_s=25.0):
         if time.perf_counter() - t_start > budget_s or len(times) >= 20:
             break
     sec = statistics.median(times)
-    return {"value": (1.0 / sec) * (f_s / f_full), "unit": "sweeps/s", "cores": oracle.num_threads(),
-            "kind": "oracle", "sample": sample, "oracle_s_per_sample_sweep": sec, "sample_sweeps": len(times)}
+    out = {"value": 1.0 / sec, "unit": "sweeps/s", "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"{name} at full size from X0, {len(times)} consecutive oracle sweeps (median), "
+                     f"{budget_s:.0f}s budget", "oracle_s_per_sweep": sec, "sample_sweeps": len(times),
+           "affinity_cores": len(os.sched_getaffinity(0)), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+    if one_core:
+        code = ("import time,statistics,sys,oracle,synth;r={}\n"
+                "for c in ('cfg1','cfg2'):\n"
+                " p=synth.make_config(c);op=oracle.Operator(A=p.A.numpy());X=p.X0.numpy();ts=[]\n"
+                " for _ in range(5 if c=='cfg2' else 50):\n"
+                "  t=time.perf_counter();X=oracle.sweep(op,X).X;ts.append(time.perf_counter()-t)\n"
+                " r[c]=1.0/statistics.median(ts)\n"
+                "print(r, oracle.num_threads())")
+        try:
+            env = dict(os.environ, OMP_NUM_THREADS="1", PYTHONPATH=ROOT)
+            o = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True,
+                               timeout=120).stdout.strip().rsplit(" ", 1)
+            import ast
+            out["one_core_sweeps_s"] = ast.literal_eval(o[0])
+            out["one_core_threads"] = int(o[1])
+        except Exception as e:
+            out["one_core_sweeps_s"] = {"error": repr(e)}
+    return out
 
 
 def run_reference(args, world, rank):
     """--impl reference: the oracle (plain CPU FP64 program) timed as it stands."""
     if rank != 0:
         return
-    cb = cpu_baseline(args.config, budget_s=max(5.0, 150.0 / max(args.steps + args.warmup, 1)))
+    cb = cpu_baseline(args.config, budget_s=max(5.0, 150.0 / max(args.steps + args.warmup, 1)), one_core=False)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "sweeps/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -53,8 +53,9 @@ struct RunState {   // device-resident refine_run bookkeeping
 // After each sweep of refine_run: convergence (||E_L||_F <= tol; or rel_resid <=
 // resid_tol), divergence (non-finite; the growth guard), and the
 // reorthogonalisation gate (gram_dev of the sweep's input > reorth_tol).
-__global__ void run_check_kernel(int* status, RunState* rs, const double* stats, double tol, int window,
-                                 double factor, double resid_tol, double reorth_tol, int* gate) {
+__device__ __forceinline__ void run_check_kernel_body(int* status, RunState* rs, const double* stats, double tol,
+                                                      int window, double factor, double resid_tol, double reorth_tol,
+                                                      int* gate) {
   if (gate) *gate = 1;
   if (*status != ST_OK) return;
   const double c = stats[1];
@@ -70,6 +71,10 @@ __global__ void run_check_kernel(int* status, RunState* rs, const double* stats,
   rs->hist[t & 3] = c;
   if (gate && reorth_tol > 0.0 && stats[6] > reorth_tol) *gate = ST_OK;
 }
+__global__ void run_check_kernel(int* status, RunState* rs, const double* stats, double tol, int window,
+                                 double factor, double resid_tol, double reorth_tol, int* gate) {
+  run_check_kernel_body(status, rs, stats, tol, window, factor, resid_tol, reorth_tol, gate);
+}
 
 // ||A - shift I||_inf row sums with Neumaier-compensated accumulation (the oracle's summation
 // class, reading R4): each lane carries (s, c) over its strided columns, the 32 lane pairs are
@@ -80,6 +85,16 @@ RF_DEV void nsum_add(Nsum& a, double x) {
   a.c += (fabs(a.s) >= fabs(x)) ? (a.s - t) + x : (x - t) + a.s;
   a.s = t;
 }
+// refine_run as ONE graph launch (single rank): a conditional WHILE node whose body is one sweep
+// (+ the gated reorthogonalisation) followed by this check; the loop continues while the status is
+// OK and fewer than iters sweeps ran, so nothing is launched after convergence or divergence.
+__global__ void run_cond_kernel(int* status, RunState* rs, const double* stats, double tol, int window,
+                                double factor, double resid_tol, double reorth_tol, int* gate, int iters,
+                                cudaGraphConditionalHandle h) {
+  run_check_kernel_body(status, rs, stats, tol, window, factor, resid_tol, reorth_tol, gate);
+  cudaGraphSetConditional(h, (*status == ST_OK && rs->done < iters) ? 1u : 0u);
+}
+
 __global__ void absrow_max_dense_kernel(const double* A, int64_t lda, int64_t n_loc, int64_t n, int64_t row0,
                                         double shift, double* out_rows) {
   const int lane = threadIdx.x & 31;
@@ -1509,6 +1524,53 @@ extern "C" refine_status refine_sweep_host(refine_ctx* c, const double* X_host_i
   return map_status(ds);
 }
 
+// The sweep loop of refine_run as one CUDA graph with a conditional WHILE node (single rank).  Returns
+// false (nothing enqueued, error state cleared) if the graph cannot be built, so the caller falls
+// back to enqueuing iters sweeps.
+static bool run_as_graph(refine_ctx* c, double* X, int32_t iters, double tol, bool reorth) {
+  if (c->multi || c->loopback || getenv("REFINE_RUN_NO_GRAPH")) return false;
+  if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) return false;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  bool ok = false;
+  do {
+    if (cudaGraphCreate(&g, 0) != cudaSuccess) break;
+    cudaGraphConditionalHandle h;
+    if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) break;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (cudaGraphAddNode(&node, g, nullptr, 0, &np) != cudaSuccess) break;
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    if (cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+        cudaSuccess)
+      break;
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    refine_status st = enqueue_phases(c, X);
+    run_cond_kernel<<<1, 1, 0, c->stream>>>(c->ws.status, c->run, c->ws.stats, tol, c->opts.guard_window,
+                                            c->opts.guard_factor, c->opts.resid_tol, c->opts.reorth_tol,
+                                            reorth ? c->ws.gate : nullptr, iters, h);
+    if (st == REFINE_OK && reorth) st = enqueue_rr(c, X, 1, true);
+    c->stream = user;
+    cudaGraph_t cap = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &cap);
+    if (st != REFINE_OK || e != cudaSuccess) break;
+    if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) break;
+    ok = cudaGraphLaunch(ge, c->stream) == cudaSuccess;
+  } while (0);
+  if (ge) cudaGraphExecDestroy(ge);     // (destruction is deferred until the launch completes)
+  if (g) cudaGraphDestroy(g);
+  if (!ok) {
+    cudaGetLastError();                 // clear a non-sticky error from the attempt
+    c->sticky = REFINE_OK;
+  }
+  return ok;
+}
+
 extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, double tol, int32_t* iters_done,
                                     refine_sweep_stats* last) {
   if (!c || !X || iters < 0) return REFINE_E_INVALID;
@@ -1521,7 +1583,8 @@ extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, dou
   // reorthogonalisation policy: single rank (the gated pipeline's collectives would
   // run unconditionally at world > 1)
   const bool reorth = c->opts.reorth_tol > 0.0 && !c->multi;
-  for (int t = 0; t < iters; ++t) {
+  const bool graphed = iters > 0 && run_as_graph(c, X, iters, tol, reorth);
+  for (int t = 0; t < iters && !graphed; ++t) {
     refine_status st = enqueue_phases(c, X);
     if (st != REFINE_OK) return st;
     for (auto* r : ranks)      // every rank holds the same stats after the broadcast: same decision

@@ -379,3 +379,31 @@ def test_csr_stencil_chunk_order(pkg, dims, k, monkeypatch):
     ref = oracle.sweep(op, xin, debug=True)
     assert rel(X.cpu().numpy(), ref.X) <= TOL
     assert np.array_equal(R.debug(pkg.DBG_W).cpu().numpy() * ref.debug["sigma"], ref.debug["W"])
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_run_conditional_graph_equals_enqueued_loop(pkg, kind, monkeypatch):
+    """refine_run as one CUDA graph with a conditional WHILE node (single rank) gives bit for bit the
+    result, status and sweep count of the enqueue-every-sweep loop (REFINE_RUN_NO_GRAPH=1), both when
+    it converges early and when it exhausts the budget; with the reorthogonalisation policy too."""
+    if kind == "dense":
+        p = synth.make_config("cfg1")
+    else:
+        p = synth.small_laplacian((40, 37), (1.0, 1.37), 8, noise=1e-5)
+    res = {}
+    for mode in ("graph", "loop"):
+        if mode == "loop":
+            monkeypatch.setenv("REFINE_RUN_NO_GRAPH", "1")
+        for iters, tol, kw in ((60, 1e-12, {}), (3, 1e-30, {}), (8, 1e-30, {"reorth_tol": 1e-30})):
+            R = refiner(pkg, p, **kw)
+            X = p.X0.cuda().clone()
+            s, it, st = R.refine_run(X, iters, tol)
+            res[(mode, iters, tol, tuple(kw))] = (s, it, st.corr_norm, X.cpu().numpy())
+    for key, (s, it, c, X) in res.items():
+        if key[0] != "graph":
+            continue
+        s2, it2, c2, X2 = res[("loop",) + key[1:]]
+        assert (s, it) == (s2, it2), (key, s, it, s2, it2)
+        assert c == c2 and np.array_equal(X, X2), key
+    if kind == "dense":      # cfg1 converges in ~8 sweeps: the while loop stopped there
+        assert res[("graph", 60, 1e-12, ())][0] == pkg.REFINE_OK and res[("graph", 60, 1e-12, ())][1] < 60

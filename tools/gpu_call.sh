@@ -1,8 +1,4 @@
 O=gpurun_out/r02
 mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_delta.py tests/test_gpu_parity.py tests/test_gpu_next4.py tests/test_gpu_rr.py tests/test_gpu_next3.py tests/test_gpu_edges.py tests/test_gpu_mixed.py tests/test_gpu_stencil.py -m gpu -q --timeout 600 -p no:cacheprovider > $O/pytest_5.txt 2>&1
-tail -2 $O/pytest_5.txt; grep -E "^FAILED" $O/pytest_5.txt | head
-for c in cfg1 cfg2; do
-  timeout 300 python bench.py --config $c --no-extra --steps 20 > $O/bench_$c.json 2> $O/bench_$c.err
-  python -c "import json; d=json.load(open('$O/bench_$c.json')); print('$c', d['ms_per_step'], d.get('kernels_ms'))"
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_next4.py tests/test_gpu_emul.py tests/test_gpu_accuracy.py -m gpu -q --timeout 600 -p no:cacheprovider -x > $O/pytest_6.txt 2>&1
+tail -3 $O/pytest_6.txt; grep -E "^FAILED|Error" $O/pytest_6.txt | head
