@@ -67,6 +67,14 @@ RF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar)
                "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
+// 2-D TMA tile load (box at signed coordinates (c0 = inner, c1)), as tma_load_4d
+RF_DEV void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(mbar))
+      : "memory");
+}
 // 4-D TMA tile load (cp.async.bulk.tensor; SASS UTMALDG) of the box at signed coordinates
 // (c0..c3) of the tensor map (a __grid_constant__ kernel parameter); elements outside the tensor
 // are zero-filled and still counted in the transaction bytes.

@@ -9,6 +9,8 @@
 // 148 SMs busy at cfg3 (256 row tiles x 4 splits = 1024 CTAs, 2 resident per SM); the
 // split partials are summed in fixed order by w_finish (deterministic).
 #pragma once
+#include <cuda.h>   // CUtensorMap
+
 #include "common.cuh"
 
 namespace rf {
@@ -146,6 +148,118 @@ gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
     }
   }
 }
+
+// ---------------------------------------------------------------- TMA-fed variant (north_star "DMMA
+// tiled kernel fed by TMA"): the same tiles, DMMA fragments and epilogue, but every stage of A and X^
+// arrives by cp.async.bulk.tensor (SASS UTMALDG) issued by ONE producer warp into an STAGES-deep ring of
+// 128-byte-swizzled boxes (16 doubles wide, so the 8-row x 4-column A fragment reads and 4-row x 8-column
+// B fragment reads are bank-conflict free without padding), with full / empty mbarriers between the
+// producer and the consumer warps -- no per-thread copy instructions or address arithmetic in the
+// main loop.  Out-of-range rows / columns (ragged n_loc, K tail, k < NT) are zero-filled by the TMA
+// unit.  Requires lda and k even (16-byte row strides) and 16-byte aligned A and X.
+template <int NT, int BM, int BK>
+struct GemmTmaCfg {
+  static constexpr int A_BOXES = BK / 16, B_BOXES = NT / 16;
+  static constexpr int A_BOX_BYTES = BM * 128, B_BOX_BYTES = BK * 128;
+  static constexpr int STAGE_BYTES = A_BOXES * A_BOX_BYTES + B_BOXES * B_BOX_BYTES;
+};
+template <int NT, int BM, int WM, int WN, int BK, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<NT, BM, WM, WN, BK, STAGES>::THREADS + 32)
+gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int32_t k,
+                   int64_t M, int64_t K, int64_t kchunk, double* __restrict__ out, int64_t out_split_stride,
+                   const int* __restrict__ status) {
+  using C = GemmCfg<NT, BM, WM, WN, BK, STAGES>;
+  using T = GemmTmaCfg<NT, BM, BK>;
+  static_assert(BK % 16 == 0 && NT % 16 == 0, "16-double TMA boxes");
+  if (*status != ST_OK) return;
+  extern __shared__ __align__(1024) unsigned char gsm[];
+  // [STAGES x stage] ring (1024-byte aligned for the 128-byte swizzle), then the mbarriers
+  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * T::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t ke = (kb + kchunk < K) ? kb + kchunk : K;
+  const int nk = (int)((ke - kb + BK - 1) / BK);
+  out += (int64_t)blockIdx.y * out_split_stride;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == C::WARPS) {   // producer warp
+    if (lane == 0) {
+      for (int it = 0; it < nk; ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        unsigned char* st = ring + s * T::STAGE_BYTES;
+        const int k0 = (int)(kb + (int64_t)it * BK);
+        mbar_expect_tx(&full[s], T::STAGE_BYTES);
+#pragma unroll
+        for (int b = 0; b < T::A_BOXES; ++b) tma_load_2d(st + b * T::A_BOX_BYTES, &tmA, k0 + 16 * b, (int)m0, &full[s]);
+#pragma unroll
+        for (int b = 0; b < T::B_BOXES; ++b)
+          tma_load_2d(st + T::A_BOXES * T::A_BOX_BYTES + b * T::B_BOX_BYTES, &tmX, 16 * b, k0, &full[s]);
+      }
+    }
+    return;
+  }
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int ar = wm * WM + (lane >> 2), ac = lane & 3;   // A frag: rows ar + 8 i, column kk + ac
+  const int br = lane & 3, bc = wn * WN + (lane >> 2);   // B frag: row kk + br, columns bc + 8 j
+  const int sw = lane >> 2;                              // = (A frag row) & 7
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const unsigned char* st = ring + s * T::STAGE_BYTES;
+    const unsigned char* bs = st + T::A_BOXES * T::A_BOX_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[C::MI], b[C::NI];
+      const int ca = (kk & 15) + ac;                                   // column within the A box
+      const unsigned char* abox = st + (kk >> 4) * T::A_BOX_BYTES;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+        a[i] = *reinterpret_cast<const double*>(abox + (ar + 8 * i) * 128 + ((((ca >> 1) ^ sw)) << 4) + (ca & 1) * 8);
+      const int rb = kk + br, rsw = rb & 7;
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int cb = bc + 8 * j, cc = cb & 15;
+        b[j] = *reinterpret_cast<const double*>(bs + (cb >> 4) * T::B_BOX_BYTES + rb * 128 + (((cc >> 1) ^ rsw) << 4) +
+                                                (cc & 1) * 8);
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+  }
+  // epilogue (as gemm_ax_kernel): fragment (i, j) -> rows m0 + wm WM + 8 i + lane / 4,
+  // cols wn WN + 8 j + 2 (lane % 4) + {0, 1}; k is even on this path
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int64_t r = m0 + wm * WM + i * 8 + (lane >> 2);
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) {
+      const int c = wn * WN + j * 8 + 2 * (lane & 3);
+      if (c < k) *reinterpret_cast<double2*>(out + r * k + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+  }
+}
+template <int NT, int BM, int BK, int STAGES>
+constexpr int gemm_tma_smem() { return STAGES * GemmTmaCfg<NT, BM, BK>::STAGE_BYTES + 1024 + 2 * STAGES * 8; }
 
 // Sum the S split partials in fixed order s = 0..S-1, apply the shift
 // (w = fma(-shift, x, w)), write W, and emit per-block double-double partials of

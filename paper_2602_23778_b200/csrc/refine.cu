@@ -204,6 +204,10 @@ struct refine_ctx {
   size_t pool_bytes = 0;
   // dense GEMM launch
   int gemm_bm = 0, nsplit = 1;
+  // TMA-fed dense S1 (gemm_ax_tma_kernel): A's tensor map (fixed at init), X's (cached per pointer)
+  bool gemm_tma = false;
+  CUtensorMap tm_A{}, tm_X{};
+  const double* tm_X_ptr = nullptr;
   int64_t kchunk = 0;
   int gemm_gx = 0;
   int n_ag = 0, w_fin_grid = 0, spmm_grid = 0;
@@ -300,6 +304,25 @@ static bool stencil_tensor_map(refine_ctx* c, const double* X) {
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   c->st_tm_x = X;
+  return true;
+}
+
+// dense S1 tensor maps: 2-D {cols, rows} views, 16-double boxes with the 128-byte swizzle
+static bool encode_2d(CUtensorMap* m, const double* base, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc || ((uintptr_t)base % 16) != 0 || (ld * 8) % 16 != 0) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 8};
+  cuuint32_t box[2] = {16, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool gemm_x_map(refine_ctx* c, const double* X) {   // X (n x k) -> boxes of 16 (K rows) x 16 columns
+  if (c->tm_X_ptr == X) return true;
+  if (!encode_2d(&c->tm_X, X, (uint64_t)c->k, (uint64_t)c->n, (uint64_t)c->k, 16)) return false;
+  c->tm_X_ptr = X;
   return true;
 }
 
@@ -523,6 +546,12 @@ struct Kern {
   using BC = PassBCfg<KP, BTA, BTB, BWA, BWB, BBR>;
   using CC = PassCCfg<KP, CNC, CBM, CWM, CWN>;
   static constexpr auto gemm = gemm_ax_kernel<KP, GBM, GWM, GWN, GBK, GST>;
+  // TMA-fed S1 (KP >= 16): BK = 16 K-steps in a TST-deep ring, the cp.async kernel's warp tiles
+  static constexpr bool TMA_OK = KP >= 16;
+  static constexpr int TBK = 16, TST = 4;
+  using TGC = GemmCfg<KP, GBM, GWM, GWN, TBK, TST>;
+  static constexpr int T_SMEM = gemm_tma_smem<(KP >= 16 ? KP : 16), GBM, TBK, TST>();
+  static constexpr auto gemm_tma = gemm_ax_tma_kernel<(KP >= 16 ? KP : 16), GBM, GWM, (KP >= 16 ? GWN : 16), TBK, TST>;
   // k = 128: pass B2 (all-a CTA tiles, balanced 7-unit grid); smaller k: the 2-D tiled pass B
   // (measured faster there: cfg4 0.19 vs 0.22 ms, cfg3 0.034 vs 0.039 ms)
   static constexpr bool B2 = KP >= 128;
@@ -555,7 +584,13 @@ struct Kern {
     int occ = 1;
     // dense GEMM: split-K so the grid fills whole waves of resident CTAs
     if (!c->csr) {
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm, GC::THREADS, GC::SMEM))) return e;
+      if (c->gemm_tma && TMA_OK) {
+        if ((e = cudaFuncSetAttribute(gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM))) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_tma, TGC::THREADS + 32, T_SMEM))) return e;
+      } else {
+        c->gemm_tma = false;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm, GC::THREADS, GC::SMEM))) return e;
+      }
       occ = std::max(occ, 1);
       const int slots = c->sms * occ;
       c->gemm_bm = GBM;
@@ -664,8 +699,12 @@ struct Kern {
             const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
             double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
             if (pass == 0) c->mark();
-            gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
-                c->A, c->lda, Xb, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
+            if (TMA_OK && c->gemm_tma && bv16 && gemm_x_map(c, Xb))
+              gemm_tma<<<dim3(c->gemm_gx, c->nsplit), TGC::THREADS + 32, T_SMEM, s>>>(
+                  c->tm_A, c->tm_X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, ws.status);
+            else
+              gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
+                  c->A, c->lda, Xb, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
             if (last) c->mark();
             w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(wp, X, c->nsplit, c->n_loc * c->k);
             n += 2;
@@ -976,6 +1015,12 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.multi = c->multi ? 1 : 0;
   ws.row0 = row_begin; ws.row1 = row_end;
   ws.halo = nullptr; ws.halo_lo = row_begin;
+  if (!c->csr) {   // TMA-fed S1: A row stride and base 16-byte aligned, k even; REFINE_GEMM_TMA=0 disables
+    const char* ge = getenv("REFINE_GEMM_TMA");
+    c->gemm_tma = !(ge && ge[0] == '0') && k % 2 == 0 && c->kp >= 16 &&
+                  encode_2d(&c->tm_A, c->A, (uint64_t)n, (uint64_t)c->n_loc, (uint64_t)c->lda,
+                            (uint32_t)dispatch(c->kp, [&](auto K) { return decltype(K)::GBM; }));
+  }
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
   RF_CK(c, cudaFuncSetAttribute(kxk_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
   RF_CK(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
