@@ -490,7 +490,10 @@ struct PassCCfg {
   static constexpr int MI = WM / 8, NI = WN / 8;
 };
 
-template <int KP, int NC, int BM, int WARPS_M, int WARPS_N>
+// NORM: also the column sums of x~^2 into ws.nslot (Rayleigh-Ritz / QR steps, which normalise afterwards).
+// A sweep's Csig and scal already carry 1 / ||x~_j|| (kxk_finish), so its pass C skips them: the two
+// DFMA per element cost far more than their pipe share next to the DMMAs.
+template <int KP, int NC, int BM, int WARPS_M, int WARPS_N, bool NORM = true>
 __global__ void __launch_bounds__(PassCCfg<KP, NC, BM, WARPS_M, WARPS_N>::THREADS)
 passC_kernel(Ws ws, const double* X, double* out, int vec16) {
   using C = PassCCfg<KP, NC, BM, WARPS_M, WARPS_N>;
@@ -590,15 +593,18 @@ passC_kernel(Ws ws, const double* X, double* out, int vec16) {
         const double x1 = __fma_rn(w[i][j][1], ssc[cl + 1], -acc[i][j][1]);
         if (vec16 && c < k) {
           *reinterpret_cast<double2*>(out + g * k + c) = make_double2(x0, x1);
-          nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]);
-          nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]);
+          if (NORM) {
+            nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]);
+            nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]);
+          }
         } else {
-          if (c < k) { out[g * k + c] = x0; nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
-          if (c + 1 < k) { out[g * k + c + 1] = x1; nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
+          if (c < k) { out[g * k + c] = x0; if (NORM) nacc[j][0] = __fma_rn(x0, x0, nacc[j][0]); }
+          if (c + 1 < k) { out[g * k + c + 1] = x1; if (NORM) nacc[j][1] = __fma_rn(x1, x1, nacc[j][1]); }
         }
       }
     }
   }
+  if (!NORM) return;
   // column norm partials: slot rows (wm, lane/4) reduced in fixed order
 #pragma unroll
   for (int j = 0; j < C::NI; ++j) {

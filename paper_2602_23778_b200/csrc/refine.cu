@@ -564,7 +564,8 @@ struct Kern {
   static constexpr int B_SMEM = B2 ? B2C::SMEM : BC::SMEM;
   static constexpr int B_NT = B2 ? B2C::NT : BC::NTILES;
   static constexpr size_t B_TILE = B2 ? (size_t)B2C::TA * B2C::TB : (size_t)BTA * BTB;
-  static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN>;
+  static constexpr auto passC = passC_kernel<KP, CNC, CBM, CWM, CWN, true>;       // RR / QR steps (norm sums)
+  static constexpr auto passC_sweep = passC_kernel<KP, CNC, CBM, CWM, CWN, false>; // a sweep (norms folded earlier)
   static constexpr int TKP = KP >= 32 ? KP : 32;   // tcgen05 passes (NEXT-2) exist for KP >= 32
   static_assert(CNC == KP, "pass C writes X in place: one CTA must own whole rows (all k columns)");
 
@@ -573,6 +574,7 @@ struct Kern {
     if ((e = cudaFuncSetAttribute(gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passB, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(passC, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(passC_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM))) return e;
     if (KP == 128 && c->opts.emul)   // pass C on the INT8 tensor cores (ozaki.cuh)
       if ((e = cudaFuncSetAttribute(passC_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZC_SMEM))) return e;
     if (KP >= 32 && c->opts.mixed) {   // NEXT-2 tcgen05 passes (tc_passes.cuh)
@@ -788,7 +790,7 @@ struct Kern {
           else if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
             passC_tc_kernel<TKP><<<c->sms, TCC_THREADS, TccCfg<TKP>::SMEM, s>>>(ws, X, X);
           else
-            passC<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, X, xv16);
+            passC_sweep<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, X, xv16);
           n += 1;
           break;
         }
