@@ -89,14 +89,16 @@ typedef struct {
   double guard_factor;   /* refine_run divergence guard growth factor; default 10                         */
   int32_t square;        /* 1: the operator is A^2 - shift I applied as A (A X) (Sec. 5.2, PAPER.md:1218-1243;
                             smallest-|lambda| targets); ||.|| in delta / rel_resid is ||A||_inf^2 + |shift|
-                            (reading SQ1).  world == 1 only (REFINE_E_UNSUPPORTED otherwise).  Default 0  */
+                            (reading SQ1).  At world > 1 the rows of T = A X are exchanged between the two
+                            products (halo / all-gather, as for X).  Default 0                            */
   int32_t kjudge;        /* > 0: refine all k columns but judge ||E_L||_F (stats, refine_run's stopping
                             test) on the leading kjudge columns (K > k).  Default 0 = all */
   double resid_tol;      /* > 0: refine_run also stops (REFINE_OK) when rel_resid <= resid_tol
                             (PAPER.md:495-499).  Default 0 = off                                            */
   double reorth_tol;     /* > 0: sweeps report gram_dev, and refine_run reorthogonalises (Cholesky QR,
                             refine_reorthogonalize) the output of every sweep whose input had
-                            gram_dev > reorth_tol.  world == 1.  Default 0 = off            */
+                            gram_dev > reorth_tol.  world == 1: behind a device gate (no host
+                            sync); world > 1: the host reads the gate after each sweep.  Default 0 = off */
   int32_t rr_fallback;   /* 1: when refine_run's divergence guard trips, continue with refine_sweep_rr
                             iterations instead of returning REFINE_DIVERGED        */
   int32_t mixed;         /* NEXT-2 ("matrix-matrix multiplications in the applications

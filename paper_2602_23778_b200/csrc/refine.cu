@@ -212,6 +212,8 @@ struct refine_ctx {
   int gemm_gx = 0;
   int n_ag = 0, w_fin_grid = 0, spmm_grid = 0;
   int n_ag_cur = 0;             // alpha/g slots written by this sweep's S1 kernel (kxk_rq reduces them)
+  int s1_only = -1;             // opts.square at world > 1: phase 0 runs only product 0 / 1 (an exchange between)
+  double* Tfull = nullptr;      // loopback, dense, opts.square: the gathered T = A X of all emulated ranks
   // stencil SpMM (spmm_stencil.cuh): geometry, packed row records (owned), X tensor map cache
   bool st_on = false;
   StencilGeo st_geo{};
@@ -661,8 +663,8 @@ struct Kern {
     const bool xv16 = (c->k % 2 == 0) && ((uintptr_t)X % 16 == 0);
     switch (ph) {
       case 0:    // S1 (+ S2 partials); S3 (kxk_lu, X^_1 only) forked onto the side stream
-      case 10:   // Rayleigh-Ritz: S1 only (W = (A - shift I) X)
-        if (ph == 0 && ws.top > 0) {
+      case 10: {  // Rayleigh-Ritz: S1 only (W = (A - shift I) X)
+        if (ph == 0 && ws.top > 0 && c->s1_only != 1) {
           cudaEventRecord(c->ev_fork, s);
           cudaStreamWaitEvent(c->side, c->ev_fork, 0);
           kxk_lu_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8,
@@ -672,12 +674,14 @@ struct Kern {
         }
         // S1: W = A X - shift X, or (opts.square, Sec. 5.2) T = A X into X~'s buffer, then
         // W = A T - shift X; the alpha / g partials are those of the last product.
-        for (int pass = 0; pass < (c->opts.square ? 2 : 1); ++pass) {
-          const bool last = pass + 1 == (c->opts.square ? 2 : 1);
+        // (world > 1: T's rows from the other ranks are exchanged between the products, s1_only)
+        const int npass = c->opts.square ? 2 : 1;
+        const int pass0 = c->s1_only == 1 ? 1 : 0, pass1 = c->s1_only == 0 ? 1 : npass;
+        for (int pass = pass0; pass < pass1; ++pass) {
+          const bool last = pass + 1 == npass;
           Ws wp = ws;
           if (!last) wp.shift = 0.0;
           const double* Xg = pass ? ws.Xt : X;                   // operand of this product
-          if (pass) cudaMemcpyAsync(ws.Xt, ws.W, (size_t)c->n_loc * c->k * 8, cudaMemcpyDeviceToDevice, s);
           if (!c->csr && c->oz_ns > 0) {   // A X on the INT8 tensor cores (ozaki.cuh)
             const double* Xb = c->multi ? c->Xfull : Xg;           // B operand: all n rows
             double* out = (c->oz_ns == 1) ? ws.W : ws.Wpart;
@@ -718,13 +722,15 @@ struct Kern {
             else launch_spmm<false>(c, vec, Xg, X, wp);
             n += 1;
           }
+          if (!last) cudaMemcpyAsync(ws.Xt, ws.W, (size_t)c->n_loc * c->k * 8, cudaMemcpyDeviceToDevice, s);   // T = A X
         }
-        if (ph == 0 && c->multi) {
+        if (ph == 0 && c->multi && pass1 == npass) {
           ws.n_ag = c->n_ag_cur;
           ag_local_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
           ++n;
         }
         break;
+      }
       case 11: {  // Rayleigh-Ritz: pass B with D = 0 -> M2 = X_2^T W_2, G2 = X_2^T X_2
         Ws wz = ws;
         wz.d = ws.zerod;
@@ -994,7 +1000,6 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.kjudge = c->opts.kjudge;
   // the divergence guard compares with the corr norm guard_window sweeps back (a 4-entry ring)
   if (c->opts.guard_window < 0 || c->opts.guard_window > 4) return REFINE_E_INVALID;
-  if (c->opts.square && (world > 1 || c->multi)) return REFINE_E_UNSUPPORTED;   // (single-rank only)
   if (c->opts.mixed && (k % 16 != 0 || k < 32)) return REFINE_E_UNSUPPORTED;    // tcgen05 passes: 16 | k >= 32
   // ozaki.cuh: dense S1 for 16 | k <= 64, pass C for k == 128 -- at least one must apply
   const bool emul_s1 = c->opts.emul && !c->csr && k % 16 == 0 && k <= 64;
@@ -1221,6 +1226,7 @@ static refine_status init_any(refine_ctx* c, int64_t n, int32_t k, int64_t row_b
     }
     c->csr = c->kids[0]->csr;
     c->kp = c->kids[0]->kp;
+    if (!c->csr && c->opts.square) RF_CK(c, cudaMalloc(&c->Tfull, (size_t)n * k * sizeof(double)));
     return REFINE_OK;
   }
   make_rank(c, row_begin);
@@ -1298,7 +1304,7 @@ extern "C" refine_status refine_init_csr(refine_ctx** out, int64_t n, int32_t k,
 }
 
 // ---------------------------------------------------------------- sweeps
-enum { C_X = 0, C_AG, C_MG, C_BC, C_NRM };
+enum { C_X = 0, C_AG, C_MG, C_BC, C_NRM, C_T };   // C_T: T = A X rows (opts.square)
 
 static refine_status nccl_fail(refine_ctx* c, int r, const char* what) {
   Nccl& N = nccl();
@@ -1347,6 +1353,18 @@ static refine_status collective(refine_ctx* c, int which, double* X) {
           for (int r = 0; r < P; ++r)
             RF_CK(c, cudaMemcpyAsync(kid->ws.nrm_all + r * k, K[r]->ws.nrm_send, k * 8, D2D, s));
         break;
+      case C_T:   // every rank's T (its ws.Xt block): dense -> one full copy, CSR -> each rank's halo rows
+        if (!c->csr) {
+          for (auto* kid : K) RF_CK(c, cudaMemcpyAsync(c->Tfull + kid->row_begin * k, kid->ws.Xt, kid->n_loc * k * 8, D2D, s));
+          for (auto* kid : K) kid->Xfull = c->Tfull;
+        } else {
+          for (auto* kid : K)
+            for (auto& g : kid->hrecv) {
+              const refine_ctx* o = K[g.peer];
+              RF_CK(c, cudaMemcpyAsync(kid->ws.halo + g.off * k, o->ws.Xt + (g.row - o->row_begin) * k, g.cnt * k * 8, D2D, s));
+            }
+        }
+        break;
     }
     return REFINE_OK;
   }
@@ -1379,6 +1397,20 @@ static refine_status collective(refine_ctx* c, int which, double* X) {
     case C_NRM:
       RF_NC(c, N.AllGather(c->ws.nrm_send, c->ws.nrm_all, k, ncclDouble, c->comm, s));
       break;
+    case C_T:   // as C_X, for T = A X (ws.Xt)
+      RF_NC(c, N.GroupStart());
+      if (!c->csr) {
+        for (int r = 0; r < c->world; ++r) {
+          double* dst = c->Xfull + c->rb_all[r] * k;
+          RF_NC(c, N.Broadcast(r == c->rank ? c->ws.Xt : dst, dst, (c->re_all[r] - c->rb_all[r]) * k, ncclDouble, r,
+                               c->comm, s));
+        }
+      } else {
+        for (auto& g : c->hsend) RF_NC(c, N.Send(c->ws.Xt + g.off * k, g.cnt * k, ncclDouble, g.peer, c->comm, s));
+        for (auto& g : c->hrecv) RF_NC(c, N.Recv(c->ws.halo + g.off * k, g.cnt * k, ncclDouble, g.peer, c->comm, s));
+      }
+      RF_NC(c, N.GroupEnd());
+      break;
   }
   return REFINE_OK;
 }
@@ -1393,11 +1425,17 @@ static refine_status enqueue_phases(refine_ctx* c, double* X) {
   refine_status st;
   if (multi && (st = collective(c, C_X, X)) != REFINE_OK) return st;
   int launches = 0;
+  const bool split_s1 = multi && c->opts.square;   // T = A X, exchange T's rows, then W = A T - shift X
   for (int ph = 0; ph < 6; ++ph) {
-    for (int i = 0; i < nr; ++i) {
-      refine_ctx* r = ranks[i];
-      double* Xr = c->loopback ? X + r->row_begin * c->k : X;
-      launches += dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, ph, Xr); });
+    for (int part = 0; part < ((ph == 0 && split_s1) ? 2 : 1); ++part) {
+      if (part == 1 && (st = collective(c, C_T, X)) != REFINE_OK) return st;
+      for (int i = 0; i < nr; ++i) {
+        refine_ctx* r = ranks[i];
+        double* Xr = c->loopback ? X + r->row_begin * c->k : X;
+        r->s1_only = (ph == 0 && split_s1) ? part : -1;
+        launches += dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, ph, Xr); });
+        r->s1_only = -1;
+      }
     }
     if (multi && after[ph] >= 0 && (st = collective(c, after[ph], X)) != REFINE_OK) return st;
   }
@@ -1425,8 +1463,10 @@ static refine_status launch_sweep(refine_ctx* c, double* X) {
     cudaStream_t user = c->stream;
     RF_CK(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
     c->stream = c->cap_stream;
+    for (auto* kid : c->kids) kid->stream = c->cap_stream;   // loopback: every emulated rank's launches
     refine_status st = enqueue_sweep(c, X);
     c->stream = user;
+    for (auto* kid : c->kids) kid->stream = user;
     cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
     if (st != REFINE_OK) return st;
     RF_CK(c, e);
@@ -1455,15 +1495,21 @@ static refine_status enqueue_rr(refine_ctx* c, double* X, int mode = 0, bool gat
   static const int after[5] = {-1, C_MG, C_BC, C_NRM, -1}, after_ro[5] = {C_MG, C_BC, C_NRM, -1, -1};
   const int* phases = mode == 0 ? ph_rr : ph_ro;
   const int* aft = mode == 0 ? after : after_ro;
+  const bool split_s1 = c->multi && c->opts.square;   // (as in enqueue_phases)
   for (int q = 0; q < 5 && phases[q] >= 0; ++q) {
-    for (int i = 0; i < nr; ++i) {
-      refine_ctx* r = ranks[i];
-      double* Xr = c->loopback ? X + r->row_begin * c->k : X;
-      r->gated = gated;
-      r->in_rr = true;
-      dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, phases[q], Xr); });
-      r->gated = false;
-      r->in_rr = false;
+    for (int part = 0; part < ((phases[q] == 10 && split_s1) ? 2 : 1); ++part) {
+      if (part == 1 && (st = collective(c, C_T, X)) != REFINE_OK) return st;
+      for (int i = 0; i < nr; ++i) {
+        refine_ctx* r = ranks[i];
+        double* Xr = c->loopback ? X + r->row_begin * c->k : X;
+        r->gated = gated;
+        r->in_rr = true;
+        r->s1_only = (phases[q] == 10 && split_s1) ? part : -1;
+        dispatch(r->kp, [&](auto K) { return decltype(K)::phase(r, phases[q], Xr); });
+        r->gated = false;
+        r->in_rr = false;
+        r->s1_only = -1;
+      }
     }
     if (c->multi && aft[q] >= 0 && (st = collective(c, aft[q], X)) != REFINE_OK) return st;
   }
@@ -1627,9 +1673,12 @@ extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, dou
     RF_CK(c, cudaMemsetAsync(r->run, 0, sizeof(RunState), c->stream));
     RF_CK(c, cudaMemsetAsync(r->ws.status, 0, sizeof(int), c->stream));
   }
-  // reorthogonalisation policy: single rank (the gated pipeline's collectives would
-  // run unconditionally at world > 1)
+  // reorthogonalisation policy: single rank -- behind a device gate, no host sync;
   const bool reorth = c->opts.reorth_tol > 0.0 && !c->multi;
+  // world > 1: the gated pipeline's collectives cannot be skipped on the device, so the host reads the
+  // gate after each sweep (one synchronisation per sweep, only with the policy on) and enqueues the
+  // Cholesky-QR step when it is open -- every rank reads the same broadcast statistics: same decision
+  const bool reorth_host = c->opts.reorth_tol > 0.0 && c->multi;
   const bool graphed = iters > 0 && run_as_graph(c, X, iters, tol, reorth);
   for (int t = 0; t < iters && !graphed; ++t) {
     refine_status st = enqueue_phases(c, X);
@@ -1637,8 +1686,16 @@ extern "C" refine_status refine_run(refine_ctx* c, double* X, int32_t iters, dou
     for (auto* r : ranks)      // every rank holds the same stats after the broadcast: same decision
       run_check_kernel<<<1, 1, 0, c->stream>>>(r->ws.status, r->run, r->ws.stats, tol, c->opts.guard_window,
                                                c->opts.guard_factor, c->opts.resid_tol, c->opts.reorth_tol,
-                                               reorth ? r->ws.gate : nullptr);
+                                               (reorth || reorth_host) ? r->ws.gate : nullptr);
     if (reorth && (st = enqueue_rr(c, X, 1, true)) != REFINE_OK) return st;
+    if (reorth_host) {
+      int h[2] = {0, 0};
+      RF_CK(c, cudaMemcpyAsync(&h[0], ctx0(c)->ws.status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      RF_CK(c, cudaMemcpyAsync(&h[1], ctx0(c)->ws.gate, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      RF_CK(c, cudaStreamSynchronize(c->stream));
+      if (h[0] != ST_OK) break;
+      if (h[1] == ST_OK && (st = enqueue_rr(c, X, 1, false)) != REFINE_OK) return st;
+    }
     RF_CK(c, cudaGetLastError());
   }
   RunState rs;
@@ -1685,8 +1742,7 @@ extern "C" refine_status refine_get_status(refine_ctx* c) {
 
 extern "C" refine_status refine_set_graph(refine_ctx* c, int32_t enable) {
   if (!c) return REFINE_E_INVALID;
-  if (c->loopback && enable) return REFINE_E_UNSUPPORTED;
-  c->use_graph = enable != 0;
+  c->use_graph = enable != 0;   // (loopback and NCCL ranks too: the collectives are captured with the kernels)
   if (!c->use_graph && c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; c->gX = nullptr; }
   return REFINE_OK;
 }
@@ -1755,6 +1811,7 @@ extern "C" void refine_destroy(refine_ctx* c) {
   c->kids.clear();
   if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
   if (c->own_xfull && c->Xfull) cudaFree(c->Xfull);
+  if (c->Tfull) cudaFree(c->Tfull);
   if (c->ws.halo) cudaFree(c->ws.halo);
   if (c->xoff_buf) cudaFree(c->xoff_buf);
   if (c->st_meta) cudaFree(c->st_meta);

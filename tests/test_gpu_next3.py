@@ -105,8 +105,34 @@ def test_kjudge_stats_and_run(pkg):
     assert s == pkg.REFINE_OK and so == oracle.OK and abs(it - ito) <= 1
 
 
-def test_square_multirank_unsupported(pkg):
-    q, Lv, L, alpha = laplacian_square_problem((9, 7), (1.0, 1.37), 3)
-    with pytest.raises(pkg.RefineError):
-        pkg.Refiner.csr(q.row_ptr.cuda(), q.col_idx.cuda(), torch.from_numpy(Lv).cuda(), q.n, q.k, shift=alpha,
-                        square=True, world=2)
+@pytest.mark.parametrize("kind,world", [("csr", 2), ("csr", 3), ("dense", 2), ("dense", 3)])
+def test_square_row_partition(pkg, kind, world):
+    """opts.square at world > 1 (loopback ranks): the rows of T = A X are exchanged between the two
+    products (CSR halo of T, dense all-gather of T); one-step parity with the oracle, agreement with the
+    single-rank run, and CUDA-graph replay equal to direct launches."""
+    q, Lv, L, alpha = laplacian_square_problem((17, 13), (1.0, 1.37), 4)
+
+    def make(w):
+        if kind == "csr":
+            return pkg.Refiner.csr(q.row_ptr.cuda(), q.col_idx.cuda(), torch.from_numpy(Lv).cuda(), q.n, q.k,
+                                   shift=alpha, square=True, world=w)
+        return pkg.Refiner.dense(torch.from_numpy(L).cuda(), q.k, shift=alpha, square=True, world=w)
+    op = (oracle.Operator(row_ptr=q.row_ptr.numpy(), col_idx=q.col_idx.numpy(), val=Lv, shift=alpha, square=True)
+          if kind == "csr" else oracle.Operator(A=L, shift=alpha, square=True))
+    R = make(world)
+    X = q.X0.cuda().clone()
+    for t in range(3):
+        xin = X.cpu().numpy()
+        s, st = R.refine_sweep(X, stats=True)
+        ref = oracle.sweep(op, xin)
+        assert s == pkg.REFINE_OK and ref.status == oracle.OK
+        assert rel(X.cpu().numpy(), ref.X) <= 1e-10, t
+    X1, Xp, Xg = (q.X0.cuda().clone() for _ in range(3))
+    make(1).refine_sweep(X1)
+    R2 = make(world)
+    R2.refine_sweep(Xp)
+    assert rel(Xp.cpu().numpy(), X1.cpu().numpy()) <= 1e-13
+    R2.refine_set_graph(True)
+    R2.refine_sweep(Xg)
+    R2.refine_set_graph(False)
+    assert torch.equal(Xg, Xp)

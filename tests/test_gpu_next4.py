@@ -87,6 +87,25 @@ def test_reorth_policy(pkg):
     assert np.abs(Xg.T @ Xg - np.eye(k)).max() <= 1e-12
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_reorth_policy_row_partition(pkg, world):
+    """The reorthogonalisation policy at world > 1 (loopback ranks; the host reads the device gate
+    after each sweep): the same iteration count as the oracle's policy loop and the 100 n u accuracy."""
+    n, k = 300, 5
+    p = synth.small_dense(n, k, m=8, noise=1e-7, seed=7, fp32=False)
+    X0 = p.X0.numpy() @ (np.eye(k) + 3e-3 * np.random.default_rng(2).standard_normal((k, k)))
+    op = oracle.Operator(A=p.A.numpy())
+    R = pkg.Refiner.dense(p.A.cuda(), k, reorth_tol=1e-6, world=world)
+    X = torch.from_numpy(X0).cuda()
+    s, it, st = R.refine_run(X, 200, 1e-13)
+    Xo, so, ito, ho = oracle.run_policy(op, X0, 200, 1e-13, reorth_tol=1e-6)
+    assert s == pkg.REFINE_OK and so == oracle.OK and abs(it - ito) <= 1
+    Xg, Xt = X.cpu().numpy(), p.X.numpy()
+    sg = np.sign(np.sum(Xg * Xt, 0))
+    assert np.abs(Xg * sg - Xt).max() <= 100 * n * U
+    assert np.abs(Xg.T @ Xg - np.eye(k)).max() <= 1e-12
+
+
 def test_divergence_falls_back_to_rayleigh_ritz(pkg):
     n, k = 256, 4
     p = synth.small_dense(n, k, m=8, lam_target=np.array([10.0, 9.0, 9.0 + 9e-12, 8.0]), rest=1.0,

@@ -407,3 +407,48 @@ def test_run_conditional_graph_equals_enqueued_loop(pkg, kind, monkeypatch):
         assert c == c2 and np.array_equal(X, X2), key
     if kind == "dense":      # cfg1 converges in ~8 sweeps: the while loop stopped there
         assert res[("graph", 60, 1e-12, ())][0] == pkg.REFINE_OK and res[("graph", 60, 1e-12, ())][1] < 60
+
+
+@pytest.mark.parametrize("kind,world", [("dense", 2), ("dense", 3), ("csr", 2), ("csr", 4)])
+def test_graph_replay_row_partition(pkg, kind, world):
+    """refine_set_graph at world > 1: the loopback ranks' kernels and collective copies are captured into
+    one graph; replay equals direct launches bit for bit."""
+    if kind == "dense":
+        p = synth.small_dense(1003, 16, m=8, seed=17, signs=True)
+        mk = lambda: pkg.Refiner.dense(p.A.cuda(), p.k, world=world)
+    else:
+        p = synth.small_laplacian((24, 22, 21), (1.0, 1.13, 1.29), 32)
+        mk = lambda: pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k, world=world)
+    Ra, Rb = mk(), mk()
+    Xa, Xb = p.X0.cuda().clone(), p.X0.cuda().clone()
+    Rb.refine_set_graph(True)
+    for _ in range(3):
+        Ra.refine_sweep(Xa)
+        Rb.refine_sweep(Xb)
+    assert torch.equal(Xa, Xb)
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_nccl_path_single_rank_graph(pkg, kind, monkeypatch):
+    """The NCCL calls (group broadcast / send-recv, all-gathers, broadcast) captured in the sweep's CUDA
+    graph on a 1-rank communicator (REFINE_FORCE_NCCL=1): replay equals direct launches."""
+    monkeypatch.setenv("REFINE_FORCE_NCCL", "1")
+    try:
+        nid = pkg.refine_nccl_id()
+    except pkg.RefineError:
+        pytest.skip("NCCL not loadable")
+    if kind == "dense":
+        p = synth.small_dense(777, 12, m=8, seed=23, signs=True)
+        mk = lambda i: pkg.Refiner.dense(p.A.cuda(), p.k, world=1, rank=0, nccl_id=i)
+    else:
+        p = synth.small_laplacian((30, 21), (1.0, 1.37), 8)
+        mk = lambda i: pkg.Refiner.csr(p.row_ptr.cuda(), p.col_idx.cuda(), p.val.cuda(), p.n, p.k, world=1, rank=0,
+                                       nccl_id=i)
+    Ra = mk(nid)
+    Rb = mk(pkg.refine_nccl_id())
+    Xa, Xb = p.X0.cuda().clone(), p.X0.cuda().clone()
+    Rb.refine_set_graph(True)
+    for _ in range(3):
+        Ra.refine_sweep(Xa)
+        Rb.refine_sweep(Xb)
+    assert torch.equal(Xa, Xb)
