@@ -41,6 +41,12 @@ RF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 RF_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The sweep's kernels are launched with cudaLaunchAttributeProgrammaticStreamSerialization (refine.cu
+// launch_k), so a kernel's CTAs may be scheduled while its predecessor drains; every such kernel
+// waits here before touching memory the predecessor writes (a no-op for an ordinary launch).
+RF_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier + bulk / tensor copies
 RF_DEV void mbar_init(uint64_t* mbar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count));
@@ -60,6 +66,10 @@ RF_DEV void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
 RF_DEV void mbar_arrive(uint64_t* mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
 }
+// Order this thread's view of prior generic-proxy shared-memory accesses (other threads' reads,
+// acquired through an mbarrier wait) before its subsequent async-proxy operations on them (TMA /
+// bulk-copy refills of a ring slot, tcgen05 reads of operands stored with st.shared).
+RF_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 // 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16), completing on mbar
 RF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(

@@ -33,6 +33,7 @@ gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
                int64_t M, int64_t K, int64_t kchunk, double* __restrict__ out, int64_t out_split_stride,
                int a_vec16, int b_vec16, const int* __restrict__ status) {
   using C = GemmCfg<NT, BM, WM, WN, BK, STAGES>;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*status != ST_OK) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -171,6 +172,7 @@ gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   using C = GemmCfg<NT, BM, WM, WN, BK, STAGES>;
   using T = GemmTmaCfg<NT, BM, BK>;
   static_assert(BK % 16 == 0 && NT % 16 == 0, "16-double TMA boxes");
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*status != ST_OK) return;
   extern __shared__ __align__(1024) unsigned char gsm[];
   // [STAGES x stage] ring (1024-byte aligned for the 128-byte swizzle), then the mbarriers
@@ -195,7 +197,12 @@ gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
         const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        if (it >= STAGES) {
+          mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          // the consumers read stage s with generic-proxy loads; order them before the async-proxy
+          // (TMA) writes that refill it
+          fence_async_smem();
+        }
         unsigned char* st = ring + s * T::STAGE_BYTES;
         const int k0 = (int)(kb + (int64_t)it * BK);
         mbar_expect_tx(&full[s], T::STAGE_BYTES);
@@ -268,6 +275,7 @@ constexpr int gemm_tma_smem() { return STAGES * GemmTmaCfg<NT, BM, BK>::STAGE_BY
 __global__ void __launch_bounds__(256) w_finish_kernel(Ws ws, const double* __restrict__ X, int nsplit,
                                                       int64_t split_stride) {
   __shared__ dd sa[256], sg[256];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int R = 256 / k;                     // rows processed in parallel (k <= 128)

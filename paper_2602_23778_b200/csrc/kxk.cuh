@@ -323,6 +323,7 @@ __device__ void reduce_ag_slots(const Ws& ws, dd* pa, dd* pg) {
 // world > 1: this rank's alpha/g double-double vector (4 doubles per column) for the all-gather
 __global__ void __launch_bounds__(KXK_THREADS) ag_local_kernel(Ws ws) {
   __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   reduce_ag_slots(ws, pa, pg);
   if (threadIdx.x < ws.k) {
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(KXK_THREADS) ag_local_kernel(Ws ws) {
 __global__ void __launch_bounds__(KXK_THREADS) kxk_rq_kernel(Ws ws) {
   __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
   __shared__ int s_bad;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   RF_TSTAMP(ws, 0);
   const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_rq_kernel(Ws ws) {
 __global__ void __launch_bounds__(KXK_THREADS) kxk_lu_kernel(Ws ws, const double* __restrict__ Xtop) {
   extern __shared__ __align__(16) double Q[];
   __shared__ int s_bad;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
   for (int e = tid; e < k * k; e += nt) Q[e] = Xtop[e];
@@ -534,6 +537,7 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_hits;
   __shared__ double s_red[4][KMAX];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
   const int crank = SMALL ? 0 : (int)cluster_ctarank(), ncl = SMALL ? 1 : (int)cluster_nctarank();
@@ -844,6 +848,7 @@ __global__ void __launch_bounds__(KXK_THREADS) rr_kxk_kernel(Ws ws, const double
   __shared__ double s_cs[KMAX / 2 + 1], s_sn[KMAX / 2 + 1], s_red[KXK_THREADS / 32];
   __shared__ int s_p[KMAX / 2 + 1], s_q[KMAX / 2 + 1], s_ord[KMAX], s_bad;
   __shared__ double s_d[KMAX];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
   double* S = ws.scratch;
@@ -994,6 +999,7 @@ __global__ void __launch_bounds__(KXK_THREADS) rr_kxk_kernel(Ws ws, const double
 // top block (deterministic; was one thread per column, latency bound at ~40 us for 444 slots).
 __global__ void __launch_bounds__(KXK_THREADS) norm_reduce_kernel(Ws ws) {
   __shared__ double part[KXK_THREADS];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x;
   const int P = KXK_THREADS / k, j = tid % k, p = tid / k;

@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(const int8_t* __
   extern __shared__ __align__(16) unsigned char oz_raw[];
   __shared__ __align__(8) uint64_t full[OZ_STAGES], empty[OZ_STAGES], accb;
   __shared__ uint32_t tmem_base;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*status != ST_OK) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t rt = blockIdx.x;
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const d
   __shared__ int32_t sh[4][OZC_TN];             // row exponents of slab t in sh[t % 4] (read by its
                                                 // epilogue before it releases TMEM; slab t + 4's
                                                 // converter runs only after that, via opfree / acce)
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = ws.k;                           // == 128
@@ -385,7 +387,10 @@ __global__ void __launch_bounds__(OZC_THREADS, 1) passC_oz_kernel(Ws ws, const d
     if (lane == 0) {
       for (int t = 0; t < nst; ++t) {
         const int s = t % OZC_NS;
-        if (t >= OZC_NS) mbar_wait(&empty[s], ((t / OZC_NS) - 1) & 1);
+        if (t >= OZC_NS) {
+          mbar_wait(&empty[s], ((t / OZC_NS) - 1) & 1);
+          fence_async_smem();                       // converters' generic reads of slot s -> the refill
+        }
         const int64_t r0 = rb + (int64_t)t * OZC_TN;
         const uint32_t bytes = (uint32_t)min((int64_t)OZC_TN, re - r0) * OZC_K * 8;
         mbar_expect_tx(&full[s], bytes);

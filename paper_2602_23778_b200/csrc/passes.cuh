@@ -62,6 +62,7 @@ passB_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double sd[KP];
   __shared__ double srr[THREADS];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wa = warp / WARPS_B, wb = warp % WARPS_B;
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(PB_RED_THREADS) passB_reduce_kernel(Ws ws, int
   using C = PassBCfg<KP, TA, TB, WARPS_A, WARPS_B, BR>;
   constexpr int NR = PB_RED_THREADS / 32;              // contiguous chunk ranges per element
   __shared__ double part[NR][33];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int total = k * 2 * k + k;
@@ -270,6 +272,7 @@ passB2_kernel(Ws ws, const double* __restrict__ X, int vec16) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double sd[KP];
   __shared__ double srr[2][THREADS];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wa = warp / C::WB, wb = warp % C::WB;
@@ -433,6 +436,7 @@ __global__ void __launch_bounds__(PB_RED_THREADS) passB2_reduce_kernel(Ws ws, in
   using C = PassB2Cfg<KP>;
   constexpr int NR = PB_RED_THREADS / 32;              // contiguous chunk ranges per element
   __shared__ double part[NR][33];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int total = k * 2 * k + k;
@@ -500,6 +504,7 @@ passC_kernel(Ws ws, const double* X, double* out, int vec16) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double ssc[NC];
   __shared__ double sred[WARPS_M * 8][NC];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
@@ -625,6 +630,7 @@ passC_kernel(Ws ws, const double* X, double* out, int vec16) {
 __global__ void __launch_bounds__(256) normalize_kernel(Ws ws, double* __restrict__ X) {
   __shared__ double sinv[KMAX];
   __shared__ int sbad;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   if (ws.multi) {         // combine the gathered per-rank column sums in rank order

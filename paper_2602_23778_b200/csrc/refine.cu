@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <utility>
 #include <vector>
 #include <cmath>
 #include <cstdio>
@@ -57,6 +58,7 @@ __device__ __forceinline__ void run_check_kernel_body(int* status, RunState* rs,
                                                       int window, double factor, double resid_tol, double reorth_tol,
                                                       int* gate) {
   if (gate) *gate = 1;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*status != ST_OK) return;
   const double c = stats[1];
   const int t = rs->done;
@@ -157,6 +159,7 @@ __global__ void col_range_kernel(const int32_t* rp, const int32_t* ci, int64_t n
 // X <- X~ for Rayleigh-Ritz / QR steps with opts.normalize == 0, behind the status word (a failed
 // or gate-closed step leaves X untouched, like every other kernel of the step)
 __global__ void copy_gated_kernel(const int* status, double* __restrict__ X, const double* __restrict__ Xt, int64_t cnt) {
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*status != ST_OK) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
     X[i] = Xt[i];
@@ -206,6 +209,7 @@ struct refine_ctx {
   int gemm_bm = 0, nsplit = 1;
   // TMA-fed dense S1 (gemm_ax_tma_kernel): A's tensor map (fixed at init), X's (cached per pointer)
   bool gemm_tma = false;
+  bool pdl = true;              // programmatic dependent launch of the sweep's kernels (launch_k)
   CUtensorMap tm_A{}, tm_X{};
   const double* tm_X_ptr = nullptr;
   int64_t kchunk = 0;
@@ -266,6 +270,25 @@ static refine_status cuda_fail(refine_ctx* c, cudaError_t e, const char* what) {
     cudaError_t e_ = (expr);                                    \
     if (e_ != cudaSuccess) return cuda_fail((c), e_, #expr);    \
   } while (0)
+
+// Launch with programmatic dependent launch (PDL) when pdl: the kernel may be scheduled while its
+// stream predecessor drains and waits in griddep_wait() -- the sweep is a chain of short kernels whose
+// launch latency otherwise sits between every pair (REFINE_PDL=0 disables it).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- per-KP kernel tables
 template <int KP> struct Tiles;
@@ -330,7 +353,8 @@ static bool gemm_x_map(refine_ctx* c, const double* X) {   // X (n x k) -> boxes
 
 template <int KC, int NZR>
 static void stencil_kernel_launch(refine_ctx* c, const Ws& ws) {
-  spmm_stencil_kernel<KC, NZR><<<c->st_grid, ST_BLOCK, c->st_smem, c->stream>>>(ws, c->st_tm, c->st_meta, c->st_geo);
+  launch_k(c->pdl, spmm_stencil_kernel<KC, NZR>, dim3(c->st_grid), dim3(ST_BLOCK), c->st_smem, c->stream, ws, c->st_tm,
+           (const double*)c->st_meta, c->st_geo);
 }
 static bool stencil_launch(refine_ctx* c, const double* X, const Ws& ws) {
   if (!stencil_tensor_map(c, X)) return false;
@@ -474,7 +498,7 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
   if (vec && c->gather_R > 0) {   // vec: 16-byte aligned X / halo rows
     const int R = c->gather_R;
     const int4 ord = HALO ? make_int4(0, 0, 0, 0) : c->spmm_ord;
-    auto go = [&](auto kern) { kern<<<g, 256, 0, s>>>(ws, c->rp, c->xoff, c->val, Xg, R, Xo, ord); };
+    auto go = [&](auto kern) { launch_k(c->pdl, kern, dim3(g), dim3(256), 0, s, ws, c->rp, c->xoff, c->val, Xg, R, Xo, ord); };
 #define RF_GATHER_K(KK)                                                          \
   case KK:                                                                       \
     if (c->gather_un == 5) go(spmm_gather_kernel<KK, HALO, 5>);                  \
@@ -514,27 +538,28 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
 }
 
 // kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs
-static cudaError_t launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s) {
-  if (ws.k <= KXK_SMALL) {   // one CTA, everything in shared memory
-    kxk_finish_kernel<true><<<1, KXK_THREADS, kxk_small_smem_doubles(ws.k) * 8, s>>>(ws, X, ws.W);
-    return cudaGetLastError();
-  }
-  if (kxk_cluster(ws.k) == 1) {   // (a plain launch is an implicit 1-CTA cluster)
-    kxk_finish_kernel<false><<<1, KXK_THREADS, FK_SMEM * 8, s>>>(ws, X, ws.W);
-    return cudaGetLastError();
-  }
+static cudaError_t launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s, bool pdl) {
+  static const bool no_small = getenv("REFINE_KXK_SMALL") && getenv("REFINE_KXK_SMALL")[0] == '0';
+  if (ws.k <= KXK_SMALL && !no_small)   // one CTA, everything in shared memory
+    return launch_k(pdl, kxk_finish_kernel<true>, dim3(1), dim3(KXK_THREADS), kxk_small_smem_doubles(ws.k) * 8, s, ws,
+                    X, (const double*)ws.W);
+  if (kxk_cluster(ws.k) == 1)   // (a plain launch is an implicit 1-CTA cluster)
+    return launch_k(pdl, kxk_finish_kernel<false>, dim3(1), dim3(KXK_THREADS), FK_SMEM * 8, s, ws, X,
+                    (const double*)ws.W);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kxk_cluster(ws.k), 1, 1);
   cfg.blockDim = dim3(KXK_THREADS, 1, 1);
   cfg.dynamicSmemBytes = FK_SMEM * 8;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kxk_cluster(ws.k);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kxk_finish_kernel<false>, ws, X, (const double*)ws.W);
 }
 
@@ -706,13 +731,14 @@ struct Kern {
             double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
             if (pass == 0) c->mark();
             if (TMA_OK && c->gemm_tma && bv16 && gemm_x_map(c, Xb))
-              gemm_tma<<<dim3(c->gemm_gx, c->nsplit), TGC::THREADS + 32, T_SMEM, s>>>(
-                  c->tm_A, c->tm_X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, ws.status);
+              launch_k(c->pdl, gemm_tma, dim3(c->gemm_gx, c->nsplit), dim3(TGC::THREADS + 32), T_SMEM, s,
+                       c->tm_A, c->tm_X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, ws.status);
             else
-              gemm<<<dim3(c->gemm_gx, c->nsplit), GC::THREADS, GC::SMEM, s>>>(
-                  c->A, c->lda, Xb, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
+              launch_k(c->pdl, gemm, dim3(c->gemm_gx, c->nsplit), dim3(GC::THREADS), GC::SMEM, s, c->A, c->lda, Xb,
+                       c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
             if (last) c->mark();
-            w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(wp, X, c->nsplit, c->n_loc * c->k);
+            launch_k(c->pdl, w_finish_kernel, dim3(c->w_fin_grid), dim3(256), 0, s, wp, (const double*)X, c->nsplit,
+                     c->n_loc * c->k);
             n += 2;
           } else {
             if (pass == 0) c->mark();
@@ -752,7 +778,7 @@ struct Kern {
       case 1:  // S2: alpha, Rayleigh quotients
         c->mark();
         ws.n_ag = c->n_ag_cur;   // slots of the S1 kernel that ran (gather or stencil SpMM)
-        kxk_rq_kernel<<<1, KXK_THREADS, 0, s>>>(ws);
+        launch_k(c->pdl, kxk_rq_kernel, dim3(1), dim3(KXK_THREADS), 0, s, ws);
         n += 1;
         break;
       case 2:  // S4 reductions
@@ -768,18 +794,21 @@ struct Kern {
           break;
         }
         if (B2 && B2C::PAIRED)
-          passB<<<dim3(7 * (c->passb_grid_y / 2)), B_THREADS, B_SMEM, s>>>(ws, X, xv16);
+          launch_k(c->pdl, passB, dim3(7 * (c->passb_grid_y / 2)), dim3(B_THREADS), B_SMEM, s, ws, (const double*)X,
+                   (int)xv16);
         else
-          passB<<<dim3(B_NT, c->passb_grid_y), B_THREADS, B_SMEM, s>>>(ws, X, xv16);
+          launch_k(c->pdl, passB, dim3(B_NT, c->passb_grid_y), dim3(B_THREADS), B_SMEM, s, ws, (const double*)X,
+                   (int)xv16);
         c->mark();
-        passBred<<<(2 * c->k * c->k + c->k + 31) / 32, PB_RED_THREADS, 0, s>>>(ws, c->passb_grid_y);
+        launch_k(c->pdl, passBred, dim3((2 * c->k * c->k + c->k + 31) / 32), dim3(PB_RED_THREADS), 0, s, ws,
+                 c->passb_grid_y);
         n += 2;
         break;
       case 3:  // k x k algebra (rank 0), after the side-stream S3 joins
         c->mark();
         if (c->rank == 0) {
           cudaStreamWaitEvent(s, c->ev_join, 0);
-          const cudaError_t e = launch_kxk_finish(ws, X, s);
+          const cudaError_t e = launch_kxk_finish(ws, X, s, c->pdl);
           if (e != cudaSuccess) {   // (sticky: enqueue_phases reports it through the context)
             cuda_fail(c, e, "kxk_finish launch");
             return n;
@@ -796,7 +825,8 @@ struct Kern {
           else if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
             passC_tc_kernel<TKP><<<c->sms, TCC_THREADS, TccCfg<TKP>::SMEM, s>>>(ws, X, X);
           else
-            passC_sweep<<<dim3(c->passc_grid, 1), CC::THREADS, CC::SMEM, s>>>(ws, X, X, xv16);
+            launch_k(c->pdl, passC_sweep, dim3(c->passc_grid, 1), dim3(CC::THREADS), CC::SMEM, s, ws,
+                     (const double*)X, X, (int)xv16);
           n += 1;
           break;
         }
@@ -1022,6 +1052,10 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.multi = c->multi ? 1 : 0;
   ws.row0 = row_begin; ws.row1 = row_end;
   ws.halo = nullptr; ws.halo_lo = row_begin;
+  {
+    const char* pe = getenv("REFINE_PDL");
+    c->pdl = !(pe && pe[0] == '0');
+  }
   if (!c->csr) {   // TMA-fed S1: A row stride and base 16-byte aligned, k even; REFINE_GEMM_TMA=0 disables
     const char* ge = getenv("REFINE_GEMM_TMA");
     c->gemm_tma = !(ge && ge[0] == '0') && k % 2 == 0 && c->kp >= 16 &&

@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(Ws ws, const int32_t* __r
                                                        const double* __restrict__ X,      // own rows (x_i)
                                                        const double* __restrict__ Xloc) {  // gathered rows
   __shared__ dd sa[8][KMAX], sg[8][KMAX];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int k = ws.k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(256, 2) spmm_csr_vec_kernel(Ws ws, const int32
                                                            const double* __restrict__ Xloc) {
   constexpr int RPW = 32 / LPR, K = 2 * VPL * LPR, MAXNZ = (VPL > 1) ? 4 : 8, SLOTS = 8 * RPW;
   __shared__ dd sa[SLOTS][K], sg[SLOTS][K];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, l = lane % LPR, slot = warp * RPW + sub;
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(256, GatherCfg<K, UN_, LPR_, MINB_>::MINB) spm
   __shared__ int32_t s_off[2][NZCAP];
   __shared__ double s_v[2][NZCAP];
   __shared__ dd s_acc[4 * VPL][256];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
   const int64_t n = ws.n_loc, G = gridDim.x;

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   extern __shared__ __align__(128) unsigned char st_smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(st_smem);           // full[slot]: box + records landed
   unsigned char* slots = st_smem + 128;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
   const int K = ws.k, nq = g.nq;
@@ -142,6 +143,9 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   };
   auto issue = [&](const Cur& c, int m) {   // thread 0: load m of the sequence into slot m % 4
     const int s = m % ST_SLOTS;
+    // (the slot was last read by generic-proxy loads before the CTA barrier: order them before the
+    //  async-proxy TMA / bulk writes that refill it)
+    fence_async_smem();
     unsigned char* sl = slots + (size_t)s * g.slot_bytes;
     const bool inner = c.z >= c.zs && c.z < c.ze;
     mbar_expect_tx(&mbar[s], g.box_bytes + (inner ? g.meta_bytes : 0));

@@ -47,7 +47,6 @@ RF_DEV void umma_commit(uint64_t* mbar) {
 }
 RF_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 RF_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-RF_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 // 16 consecutive FP32 accumulator columns of this warp's 32 TMEM lanes
 RF_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -137,6 +136,7 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
   __shared__ __align__(8) uint64_t full[NS], empty[NS], mmad[TCB_NO], conv[TCB_NO], accf[2], acce[2];
   __shared__ uint32_t tmem_base;
   __shared__ double sd[KP];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t rows = ws.n_loc - ws.top;
@@ -182,7 +182,10 @@ __global__ void __launch_bounds__(TCB_THREADS, 1) passB_tc_kernel(Ws ws, const d
     if (lane == 0) {
       for (int t = 0; t < nst; ++t) {
         const int s = t % NS;
-        if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+        if (t >= NS) {
+          mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+          fence_async_smem();                       // converters' generic reads of slot s -> the refill
+        }
         const int64_t r0 = rb + (int64_t)t * TK;
         const uint32_t bytes = (uint32_t)min((int64_t)TK, re - r0) * k * 8;
         unsigned char* f = F + s * 2 * C::ROWB;
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
   __shared__ __align__(8) uint64_t full[TCC_NS], empty[TCC_NS], opfree, accf[TCC_NT], acce[TCC_NT];
   __shared__ uint32_t tmem_base;
   __shared__ double ssc[KP];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = ws.k;                                // k % 16 == 0, KP / 2 < k <= KP
@@ -442,7 +446,10 @@ __global__ void __launch_bounds__(TCC_THREADS, 1) passC_tc_kernel(Ws ws, const d
     if (lane == 0) {
       for (int t = 0; t < nst; ++t) {
         const int s = t % TCC_NS;
-        if (t >= TCC_NS) mbar_wait(&empty[s], ((t / TCC_NS) - 1) & 1);
+        if (t >= TCC_NS) {
+          mbar_wait(&empty[s], ((t / TCC_NS) - 1) & 1);
+          fence_async_smem();                       // converters' generic reads of slot s -> the refill
+        }
         const int64_t r0 = rb + (int64_t)t * SROWS;
         const uint32_t bytes = (uint32_t)min((int64_t)SROWS, re - r0) * k * 8;
         mbar_expect_tx(&full[s], bytes);

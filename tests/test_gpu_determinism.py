@@ -1,0 +1,63 @@
+"""Run-to-run determinism: every kernel of the sweep sums in a fixed order, so repeating a sweep from
+the same input must give bit-identical outputs.  Many repeats per kernel family catch rare races
+(e.g. a TMA ring slot refilled before the consumers' generic-proxy reads were ordered: ~1-2 % of
+sweeps at cfg2 before the fence.proxy.async fix) -- tools/race_hunt.py localises a failure."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2602_23778_b200 as p
+    from paper_2602_23778_b200 import build
+    build.build()
+    p.lib()
+    assert torch.cuda.is_available()
+    return p
+
+
+def repeat_bitwise(pkg, R, X0, reps):
+    X = X0.clone()
+    for _ in range(2):
+        R.refine_sweep(X)
+    xin = X.clone()
+    first = None
+    for _ in range(reps):
+        Y = xin.clone()
+        R.refine_sweep(Y)
+        y = Y.cpu().numpy()
+        if first is None:
+            first = y
+        else:
+            assert np.array_equal(first, y)
+
+
+CASES = [("cfg2 (TMA GEMM k=16, one-CTA k x k)", "cfg2", {}, 150),
+         ("cfg1", "cfg1", {}, 100),
+         ("dense 2000x64 (TMA GEMM, clustered k x k)", ("dense", 2000, 64), {}, 60),
+         ("dense 1500x128", ("dense", 1500, 128), {}, 40),
+         ("mixed 2000x64 (tcgen05 passes)", ("dense", 2000, 64), {"mixed": 2}, 40),
+         ("emul 2000x64 (INT8 S1)", ("dense", 2000, 64), {"emul": True}, 40),
+         ("csr 3-D k=128 (TMA stencil SpMM)", ("lap", (40, 33, 17), 128), {}, 40),
+         ("csr 2-D k=32 (gather SpMM)", ("lap", (100, 91), 32), {}, 60)]
+
+
+@pytest.mark.parametrize("what,spec,opts,reps", CASES, ids=[c[0] for c in CASES])
+def test_repeat_bitwise(pkg, what, spec, opts, reps):
+    if isinstance(spec, str):
+        p = synth.make_config(spec, device="cuda")
+    elif spec[0] == "dense":
+        p = synth.small_dense(spec[1], spec[2], m=8, seed=spec[1] + spec[2], signs=True, device="cuda")
+    else:
+        co = (1.0, 1.37) if len(spec[1]) == 2 else (1.0, 1.13, 1.29)
+        p = synth.small_laplacian(spec[1], co, spec[2], device="cuda")
+    if p.kind == "dense":
+        R = pkg.Refiner.dense(p.A, p.k, **opts)
+    else:
+        R = pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k, **opts)
+    repeat_bitwise(pkg, R, p.X0, reps)
