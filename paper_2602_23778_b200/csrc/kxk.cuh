@@ -333,11 +333,8 @@ __global__ void __launch_bounds__(KXK_THREADS) ag_local_kernel(Ws ws) {
 }
 
 // ---------------------------------------------------------------- kxk_rq (S2: alpha, Rayleigh quotients)
-__global__ void __launch_bounds__(KXK_THREADS) kxk_rq_kernel(Ws ws) {
-  __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
-  __shared__ int s_bad;
-  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
-  if (*ws.status != ST_OK) return;
+// body shared by kxk_rq_kernel and sweep_tail_kernel (tail_small.cuh): pa, pg: KXK_THREADS dd each
+__device__ void kxk_rq_body(const Ws& ws, dd* pa, dd* pg, int& s_bad) {
   RF_TSTAMP(ws, 0);
   const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
 
@@ -375,16 +372,20 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_rq_kernel(Ws ws) {
   __syncthreads();
   if (tid == 0 && s_bad != ST_OK) atomicCAS(ws.status, ST_OK, s_bad);
 }
+__global__ void __launch_bounds__(KXK_THREADS) kxk_rq_kernel(Ws ws) {
+  __shared__ dd pa[KXK_THREADS], pg[KXK_THREADS];
+  __shared__ int s_bad;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
+  if (*ws.status != ST_OK) return;
+  kxk_rq_body(ws, pa, pg, s_bad);
+}
 
 // ---------------------------------------------------------------- kxk_lu
 // S3 on the top k x k block: needs only X^_1, so it runs on a side stream concurrently with
 // S1 / S2 / passB (joined before kxk_finish).  Rank 0 only.
 // Shared memory: Q (k x k, the in-place modified LU); for k <= 64 also Ls, Ts, Us (L, T, U^{-1}).
-__global__ void __launch_bounds__(KXK_THREADS) kxk_lu_kernel(Ws ws, const double* __restrict__ Xtop) {
-  extern __shared__ __align__(16) double Q[];
-  __shared__ int s_bad;
-  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
-  if (*ws.status != ST_OK) return;
+// body shared by kxk_lu_kernel and sweep_tail_kernel; Q: max(4 k^2 (k <= 64) or k^2, PANEL_SMEM) doubles
+__device__ void kxk_lu_body(const Ws& ws, const double* __restrict__ Xtop, double* Q, int& s_bad) {
   const int k = ws.k, tid = threadIdx.x, nt = KXK_THREADS;
   for (int e = tid; e < k * k; e += nt) Q[e] = Xtop[e];
   if (tid == 0) s_bad = ST_OK;
@@ -477,6 +478,13 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_lu_kernel(Ws ws, const double
   RF_TSTAMP(ws, 5);
   if (tid == 0 && s_bad != ST_OK) atomicCAS(ws.status, ST_OK, s_bad);
 }
+__global__ void __launch_bounds__(KXK_THREADS) kxk_lu_kernel(Ws ws, const double* __restrict__ Xtop) {
+  extern __shared__ __align__(16) double Q[];
+  __shared__ int s_bad;
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
+  if (*ws.status != ST_OK) return;
+  kxk_lu_body(ws, Xtop, Q, s_bad);
+}
 
 // ---------------------------------------------------------------- kxk_finish
 // One thread-block cluster of kxk_cluster(k) CTAs (1024 threads each): CTA r owns rows
@@ -532,13 +540,8 @@ RF_DEV void smem_mm(int k, double alpha, const double* A, bool ta, const double*
 // Xtop/Wtop: the top k rows of X^ (in/out) and W (un-flipped), ld k.
 // SMALL (k <= KXK_SMALL, one CTA): scratch, L, T, E_11 and X~_1 live in shared memory, products by smem_mm.
 template <bool SMALL>
-__global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* __restrict__ Xtop,
-                                                                 const double* __restrict__ Wtop) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_hits;
-  __shared__ double s_red[4][KMAX];
-  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
-  if (*ws.status != ST_OK) return;
+__device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const double* __restrict__ Wtop, double* sm,
+                                int& s_hits, double (*s_red)[KMAX]) {
   const int k = ws.k, kk = k * k, tid = threadIdx.x, nt = KXK_THREADS;
   const int crank = SMALL ? 0 : (int)cluster_ctarank(), ncl = SMALL ? 1 : (int)cluster_nctarank();
   const int per = (((k + ncl - 1) / ncl) + 7) & ~7;
@@ -787,6 +790,16 @@ __global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* 
     if (SMALL) { ws.E11[e] = E11[e]; ws.Xt[e] = Xt1[e]; }   // (the global copies: debug / Rayleigh-Ritz readers)
   }
   if (crank == 0) RF_TSTAMP(ws, 32);
+}
+template <bool SMALL>
+__global__ void __launch_bounds__(KXK_THREADS) kxk_finish_kernel(Ws ws, double* __restrict__ Xtop,
+                                                                 const double* __restrict__ Wtop) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_hits;
+  __shared__ double s_red[4][KMAX];
+  griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
+  if (*ws.status != ST_OK) return;
+  kxk_finish_body<SMALL>(ws, Xtop, Wtop, sm, s_hits, s_red);
 }
 
 // ---------------------------------------------------------------- rr_kxk (Rayleigh-Ritz, Sec. 3.4)
