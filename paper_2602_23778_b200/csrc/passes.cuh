@@ -12,6 +12,8 @@
 //   the normalisation.  Persistent CTAs keep a column block of Csig in shared memory.
 // normalize (S7): x_ij = x~_ij / ||x~_j||, X~ buffer -> X.
 #pragma once
+#include <cuda.h>   // CUtensorMap
+
 #include "common.cuh"
 
 namespace rf {
@@ -426,6 +428,164 @@ passB2_kernel(Ws ws, const double* __restrict__ X, int vec16) {
       for (int q = 1; q < THREADS / rcpr; ++q) { s0 += srr[0][q * rcpr + tid]; s1 += srr[1][q * rcpr + tid]; }
       ws.brr[cidx * KP + b0 + rcol] = s0;
       if (rpair == 2) ws.brr[cidx * KP + b0 + rcol + 1] = s1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- pass B at k = 128, fed by TMA
+// Same units (7 per pair of row chunks), warp tiles, skipped G warp tiles and partial-slot layout as
+// passB2_kernel, but the X^ and W slabs of each 16-row stage arrive as 128-byte-swizzled 2-D TMA boxes
+// (16 doubles wide) issued by one producer warp into a 4-stage full / empty mbarrier ring (the dense
+// GEMM's scheme, gemm_dense.cuh): no per-thread copies in the main loop.  R = W - X D is formed in
+// place in the W boxes by the consumer threads (thread t always owns column t % 64 -> its share of
+// rr_j), then a named barrier among the consumers, then the DMMAs.
+template <int KP>
+struct PassB2TmaCfg {
+  static constexpr int TA = KP, TB = 64, NT = 2 * KP / TB;
+  static constexpr int WA = 2, WB = 4, WARPS = WA * WB, THREADS = WARPS * 32;
+  static constexpr int WTA = TA / WA, WTB = TB / WB, MI = WTA / 8, NI = WTB / 8;
+  static constexpr int BR = 32, ST = 4;
+  static constexpr int XBOXES = KP / 16, WBOXES = TB / 16, BOX = BR * 128;
+  static constexpr int STAGE = (XBOXES + WBOXES) * BOX;
+  static constexpr int SMEM = ST * STAGE + 1024 + 2 * ST * 8;
+};
+// byte offset of element (r, c) in an array of 16-column swizzled boxes of BR rows
+template <int BR>
+RF_DEV int swz_off(int r, int c) {
+  return (c >> 4) * (BR * 128) + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) + (c & 1) * 8;
+}
+template <int KP>
+__global__ void __launch_bounds__(PassB2TmaCfg<KP>::THREADS + 32, 1)
+passB2_tma_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW) {
+  using C = PassB2TmaCfg<KP>;
+  constexpr int BR = C::BR, TB = C::TB, ST = C::ST;
+  extern __shared__ __align__(1024) unsigned char pbsm[];
+  __shared__ double sd[KP];
+  __shared__ double srr[C::THREADS];
+  griddep_wait();
+  if (*ws.status != ST_OK) return;
+  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pbsm) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + ST * C::STAGE);
+  uint64_t* empty = full + ST;
+  const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // units: per pair of row chunks R0, R1, X1 for each chunk plus one X0 unit spanning both
+  const int u = blockIdx.x, pair = u / 7, w7 = u % 7;
+  const int64_t nchunk = 2 * (int64_t)(gridDim.x / 7);
+  int tb, span = 1;
+  int64_t cidx;
+  if (w7 < 6) { tb = (w7 % 3 == 2) ? 3 : (w7 % 3); cidx = 2 * pair + w7 / 3; }
+  else { tb = 2; cidx = 2 * pair; span = 2; }
+  const int b0 = tb * TB;
+  const int rw = (b0 < KP) ? min(TB, KP - b0) : 0;           // R columns of this tile
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + nchunk - 1) / nchunk + 31) / 32 * 32;   // (passB2's chunking; a multiple of BR)
+  const int64_t rb = ws.top + cidx * per;
+  const int64_t re = (rb + span * per < ws.n_loc) ? rb + span * per : ws.n_loc;
+  const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
+  for (int j = tid; j < KP; j += blockDim.x) sd[j] = (j < k) ? ws.d[j] : 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == C::WARPS) {   // producer warp
+    if (lane == 0) {
+      const uint32_t bytes = (C::XBOXES + (rw > 0 ? C::WBOXES : 0)) * C::BOX;
+      for (int it = 0; it < nit; ++it) {
+        const int s = it % ST;
+        if (it >= ST) {
+          mbar_wait(&empty[s], ((it / ST) - 1) & 1);
+          fence_async_smem();                     // consumers' generic reads / R writes of stage s -> refill
+        }
+        unsigned char* st = ring + s * C::STAGE;
+        const int r0 = (int)(rb + (int64_t)it * BR);
+        mbar_expect_tx(&full[s], bytes);
+#pragma unroll
+        for (int b = 0; b < C::XBOXES; ++b) tma_load_2d(st + b * C::BOX, &tmX, 16 * b, r0, &full[s]);
+        if (rw > 0) {
+#pragma unroll
+          for (int b = 0; b < C::WBOXES; ++b)
+            tma_load_2d(st + (C::XBOXES + b) * C::BOX, &tmW, b0 + 16 * b, r0, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int wa = warp / C::WB, wb = warp % C::WB;
+  const int a_lo = wa * C::WTA, bw = b0 + wb * C::WTB;
+  const bool active = !(bw >= KP && a_lo >= (bw - KP) + C::WTB);   // below G's diagonal: no MMAs
+  const int rcol = tid % TB;                                        // this thread's R column b0 + rcol
+  const double drc = sd[b0 + rcol < KP ? b0 + rcol : 0];
+  double rr = 0.0;
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int it = 0; it < nit; ++it) {
+    const int s = it % ST;
+    mbar_wait(&full[s], (it / ST) & 1);
+    const unsigned char* xs = ring + s * C::STAGE;
+    unsigned char* wsb = ring + s * C::STAGE + C::XBOXES * C::BOX;
+    if (rw > 0) {   // R = W - X D in place (rows beyond the matrix are zero-filled: R = 0)
+#pragma unroll
+      for (int q = 0; q < BR * TB / C::THREADS; ++q) {
+        const int r = tid / TB + q * (C::THREADS / TB);
+        double* wp = reinterpret_cast<double*>(wsb + swz_off<BR>(r, rcol));
+        const double x = *reinterpret_cast<const double*>(xs + swz_off<BR>(r, b0 + rcol));
+        const double v = __fma_rn(-x, drc, *wp);
+        *wp = v;
+        rr = __fma_rn(v, v, rr);
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(C::THREADS) : "memory");   // consumers only
+    }
+    if (active) {
+#pragma unroll
+      for (int kk = 0; kk < BR; kk += 4) {
+        const int row = kk + (lane & 3);
+        double a[C::MI], bv[C::NI];
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+          a[i] = *reinterpret_cast<const double*>(xs + swz_off<BR>(row, a_lo + i * 8 + (lane >> 2)));
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int cb8 = bw + j * 8;                                 // all R or all X (warp-uniform)
+          bv[j] = (cb8 < KP) ? *reinterpret_cast<const double*>(wsb + swz_off<BR>(row, cb8 - b0 + (lane >> 2)))
+                             : *reinterpret_cast<const double*>(xs + swz_off<BR>(row, cb8 - KP + (lane >> 2)));
+        }
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bv[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (active) {
+    for (int q = 0; q < span; ++q) {          // a two-chunk unit stores its sum in the first slot, 0 in the second
+      double* out = ws.bpart + ((cidx + q) * C::NT + tb) * (C::TA * TB);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int ra = a_lo + i * 8 + (lane >> 2);
+          const int cb = wb * C::WTB + j * 8 + 2 * (lane & 3);
+          out[ra * TB + cb] = q ? 0.0 : acc[i][j][0];
+          out[ra * TB + cb + 1] = q ? 0.0 : acc[i][j][1];
+        }
+    }
+  }
+  if (rw > 0) {   // threads rcol, rcol + 64, ... share R column b0 + rcol: fixed-order sum
+    srr[tid] = rr;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(C::THREADS) : "memory");
+    if (tid < TB && b0 + tid < KP) {
+      double sacc = srr[tid];
+      for (int q = 1; q < C::THREADS / TB; ++q) sacc += srr[q * TB + tid];
+      ws.brr[cidx * KP + b0 + tid] = sacc;
     }
   }
 }

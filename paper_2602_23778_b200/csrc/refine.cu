@@ -212,6 +212,10 @@ struct refine_ctx {
   bool pdl = true;              // programmatic dependent launch of the sweep's kernels (launch_k)
   CUtensorMap tm_A{}, tm_X{};
   const double* tm_X_ptr = nullptr;
+  // TMA-fed pass B at k = 128 (passB2_tma_kernel): X's map (cached per pointer) and W's (fixed)
+  bool pb_tma = false;
+  CUtensorMap tm_Xb{}, tm_Wb{};
+  const double* tm_Xb_ptr = nullptr;
   int64_t kchunk = 0;
   int gemm_gx = 0;
   int n_ag = 0, w_fin_grid = 0, spmm_grid = 0;
@@ -343,6 +347,13 @@ static bool encode_2d(CUtensorMap* m, const double* base, uint64_t cols, uint64_
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static int PB2_TMA_WAVES = getenv("REFINE_PB2_WAVES") ? atoi(getenv("REFINE_PB2_WAVES")) : 2;   // (1 / 2 / 3 measured within 0.5 %)
+static bool passb_x_map(refine_ctx* c, const double* X) {   // local X rows -> boxes of 16 rows x 16 columns
+  if (c->tm_Xb_ptr == X) return true;
+  if (!encode_2d(&c->tm_Xb, X, (uint64_t)c->k, (uint64_t)c->n_loc, (uint64_t)c->k, PassB2TmaCfg<128>::BR)) return false;
+  c->tm_Xb_ptr = X;
+  return true;
 }
 static bool gemm_x_map(refine_ctx* c, const double* X) {   // X (n x k) -> boxes of 16 (K rows) x 16 columns
   if (c->tm_X_ptr == X) return true;
@@ -647,7 +658,12 @@ struct Kern {
     const int64_t rows = std::max<int64_t>(c->n_loc - c->ws.top, 1);
     const int64_t max_chunks = std::max<int64_t>((rows + 255) / 256, 1);   // >= 256 rows per chunk
     c->passb_grid_y = (int)std::min<int64_t>(std::max(c->sms * occ / B_NT, 1), max_chunks);
-    if (B2 && B2C::PAIRED) {   // 7 balanced units per pair of chunks (passB2_kernel)
+    if (B2 && B2C::PAIRED) {   // 7 balanced units per pair of chunks (passB2_kernel / passB2_tma_kernel)
+      if (c->pb_tma) {   // one CTA per SM: one wave of units
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passB2_tma_kernel<128>, PassB2TmaCfg<128>::THREADS + 32,
+                                                               PassB2TmaCfg<128>::SMEM))) return e;
+        occ = std::max(occ, 1) * PB2_TMA_WAVES;
+      }
       const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * occ / 7, std::max<int64_t>(max_chunks / 2, 1)));
       c->passb_grid_y = 2 * pairs;
     }
@@ -793,7 +809,10 @@ struct Kern {
           n += 2;
           break;
         }
-        if (B2 && B2C::PAIRED)
+        if (B2 && B2C::PAIRED && c->pb_tma && xv16 && passb_x_map(c, X))
+          launch_k(c->pdl, passB2_tma_kernel<128>, dim3(7 * (c->passb_grid_y / 2)), dim3(PassB2TmaCfg<128>::THREADS + 32),
+                   PassB2TmaCfg<128>::SMEM, s, ws, c->tm_Xb, c->tm_Wb);
+        else if (B2 && B2C::PAIRED)
           launch_k(c->pdl, passB, dim3(7 * (c->passb_grid_y / 2)), dim3(B_THREADS), B_SMEM, s, ws, (const double*)X,
                    (int)xv16);
         else
@@ -1062,6 +1081,13 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                   encode_2d(&c->tm_A, c->A, (uint64_t)n, (uint64_t)c->n_loc, (uint64_t)c->lda,
                             (uint32_t)dispatch(c->kp, [&](auto K) { return decltype(K)::GBM; }));
   }
+  if (c->kp == 128) {   // TMA-fed pass B at k = 128 (REFINE_PASSB_TMA=0 disables)
+    const char* pe = getenv("REFINE_PASSB_TMA");
+    c->pb_tma = !(pe && pe[0] == '0') && k % 2 == 0 && tensor_map_encoder() != nullptr;
+    if (c->pb_tma)
+      RF_CK(c, cudaFuncSetAttribute(passB2_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    PassB2TmaCfg<128>::SMEM));
+  }
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
   RF_CK(c, cudaFuncSetAttribute(kxk_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
   RF_CK(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -1102,7 +1128,9 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->pool_bytes = bytes;
   RF_CK(c, cudaMemsetAsync(c->pool, 0, bytes, c->stream));
   double* b = (double*)c->pool;
-  ws.W = b + oW; ws.Xt = b + oXt; ws.Wpart = wpart ? b + oWp : nullptr; ws.ag = b + oAg; ws.n_ag = c->n_ag;
+  ws.W = b + oW; ws.Xt = b + oXt;
+  if (c->pb_tma)   // W's tensor map for the TMA-fed pass B (W lives in the pool)
+    c->pb_tma = encode_2d(&c->tm_Wb, ws.W, (uint64_t)k, (uint64_t)c->n_loc, (uint64_t)k, PassB2TmaCfg<128>::BR); ws.Wpart = wpart ? b + oWp : nullptr; ws.ag = b + oAg; ws.n_ag = c->n_ag;
   ws.bpart = b + oBp; ws.brr = b + oBrr; ws.n_chunk = c->passb_grid_y;
   ws.M2 = b + oMg; ws.G2 = ws.M2 + kk; ws.rr2 = ws.M2 + 2 * kk;        // contiguous [M2 | G2 | rr2]
   ws.nslot = b + oNs; ws.n_nslot = c->passc_grid;
