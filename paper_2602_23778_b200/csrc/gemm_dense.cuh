@@ -286,20 +286,39 @@ __global__ void __launch_bounds__(256) w_finish_kernel(Ws ws, const double* __re
   const int64_t re = (rb + rows_per < ws.n_loc) ? rb + rows_per : ws.n_loc;
   dd a = {0.0, 0.0}, g = {0.0, 0.0};
   if (r < R) {
-    for (int64_t i = rb + r; i < re; i += R) {
-      const int64_t e = i * k + j;
-      double w;
-      if (nsplit == 1) {
-        w = ws.W[e];
-      } else {
-        w = ws.Wpart[e];
-        for (int s = 1; s < nsplit; ++s) w = __dadd_rn(w, ws.Wpart[s * split_stride + e]);
+    // 4 rows per step with every load issued before the sums (the row order of the dd accumulation
+    // and the split order of each sum are unchanged: bit-identical to one row at a time)
+    for (int64_t i0 = rb + r; i0 < re; i0 += 4 * R) {
+      double w[4], x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * R;
+        const int64_t e = i * k + j;
+        const bool ok = i < re;
+        w[u] = ok ? (nsplit == 1 ? ws.W[e] : ws.Wpart[e]) : 0.0;
+        x[u] = ok ? X[e] : 0.0;
       }
-      const double x = X[e];
-      if (ws.shift != 0.0) w = __fma_rn(-ws.shift, x, w);
-      ws.W[e] = w;
-      dd_add_prod(a, x, x);
-      dd_add_prod(g, x, w);
+      for (int s = 1; s < nsplit; ++s) {
+        double p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = i0 + u * R;
+          p[u] = (i < re) ? ws.Wpart[s * split_stride + i * k + j] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = __dadd_rn(w[u], p[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * R;
+        if (i < re) {
+          double wv = w[u];
+          if (ws.shift != 0.0) wv = __fma_rn(-ws.shift, x[u], wv);
+          ws.W[i * k + j] = wv;
+          dd_add_prod(a, x[u], x[u]);
+          dd_add_prod(g, x[u], wv);
+        }
+      }
     }
   }
   sa[tid] = a;

@@ -1102,7 +1102,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   dispatch(c->kp, [&](auto K) { decltype(K)::sizes(c, bpart, brr, nslot); return 0; });
   // w_finish blocks = alpha/g slots that kxk_rq reduces on one SM: 4 per SM where w_finish streams
   // a large W (cfg3: 2 per SM doubles its time), 2 per SM below (cfg2: kxk_rq 15.8 -> 12.2 us)
-  const int wf_per_sm = (c->n_loc * (int64_t)k >= (int64_t)1 << 20) ? 4 : 2;
+  const int wf_per_sm = getenv("REFINE_WF_PER_SM") ? atoi(getenv("REFINE_WF_PER_SM")) : ((c->n_loc * (int64_t)k >= (int64_t)1 << 20) ? 4 : 2);
   c->w_fin_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * wf_per_sm, c->n_loc / 2));
   c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 8, (c->n_loc + 7) / 8));
   if (c->csr) RF_CK(c, gather_setup(c));

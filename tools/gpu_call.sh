@@ -1,5 +1,6 @@
 O=gpurun_out/r02
 mkdir -p $O
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"passB2_tma|passC_kernel" -c 2 -f -o $O/pb_cfg5 python bench.py --config cfg5 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
-python tools/ncu_summary.py report $O/pb_cfg5.ncu-rep $O/ncu_pb_cfg5.json > /dev/null
-ls -la $O/pb_cfg5.ncu-rep
+for w in 1 2 4; do
+  REFINE_WF_PER_SM=$w timeout 300 python bench.py --config cfg3 --no-extra --steps 10 > $O/bench_cfg3.json 2> $O/bench_cfg3.err
+  python -c "import json; d=json.load(open('$O/bench_cfg3.json')); print('wf=$w cfg3', d['ms_per_step'], d['kernels_ms']['w_finish'], d['kernels_ms']['kxk_rq'])"
+done
