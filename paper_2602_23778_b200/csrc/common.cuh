@@ -175,6 +175,7 @@ struct Ws {
   int32_t want_gram; // 1: kxk_finish reports max |X^T X - I| of the sweep's input in stats[6] (else -1)
   int* gate;         // refine_run reorthogonalisation gate: ST_OK when the gated pipeline must run
   int32_t normalize; // opts.normalize: kxk_finish folds 1/||x~_j|| into the top rows, Csig and scal
+  int32_t kxk_h;     // 1: kxk_lu precomputes H1..H4 (scratch + 16 k^2 ..) for the clustered kxk_finish
   double* bdiag;     // tcgen05 pass B: FP64 partials of diag(X_2^T R_2), diag(X_2^T X_2) (n_chunk x 2 kp)
 };
 

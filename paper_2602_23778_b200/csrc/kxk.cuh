@@ -475,6 +475,25 @@ __device__ void kxk_lu_body(const Ws& ws, const double* __restrict__ Xtop, doubl
     cta_trinv(k, ws.L, false, Linv, tmp, Q);
     cta_gemm(k, k, k, -1.0, Up, k, false, Linv, k, true, 0.0, nullptr, 0, ws.T, k, Q);
   }
+  if (ws.kxk_h) {
+    // the T products of kxk_finish's chain, moved off its critical path (this kernel overlaps S1 /
+    // S2 / pass B on the side stream).  With U'^{-1} = Sigma U^{-1}:
+    //   P = T^T (L^T R_1 + U'^{-T} M')  =>  V_1 = R_1 - H1^T R_1 - H3^T M',  P~ = H2^T R_1 + H4^T M'
+    //   B = T (L^T E_11 + U'^{-T} S2)   =>  L B = H1 E_11 + H2 S2,          U'^{-1} B = H3 E_11 + H4 S2
+    // with H1 = L T L^T, H2 = L T U'^{-T}, H3 = U'^{-1} T L^T, H4 = U'^{-1} T U'^{-T} (identities exact in
+    // real arithmetic; every factor O(1) for near-orthonormal X^, so no cancellation is introduced).
+    const int kk = k * k;
+    double* H = ws.scratch + 16 * kk;
+    double *LT = ws.scratch + 20 * kk, *UT = ws.scratch + 21 * kk, *UiS = ws.scratch + 22 * kk;
+    __syncthreads();
+    for (int e = tid; e < kk; e += nt) UiS[e] = ws.sigma[e / k] * ws.Uinv[e];
+    cta_gemm(k, k, k, 1.0, ws.L, k, false, ws.T, k, false, 0.0, nullptr, 0, LT, k, Q);       // L T
+    cta_gemm(k, k, k, 1.0, UiS, k, false, ws.T, k, false, 0.0, nullptr, 0, UT, k, Q);        // U'^{-1} T
+    cta_gemm(k, k, k, 1.0, LT, k, false, ws.L, k, true, 0.0, nullptr, 0, H, k, Q);           // H1
+    cta_gemm(k, k, k, 1.0, LT, k, false, UiS, k, true, 0.0, nullptr, 0, H + kk, k, Q);       // H2
+    cta_gemm(k, k, k, 1.0, UT, k, false, ws.L, k, true, 0.0, nullptr, 0, H + 2 * kk, k, Q);  // H3
+    cta_gemm(k, k, k, 1.0, UT, k, false, UiS, k, true, 0.0, nullptr, 0, H + 3 * kk, k, Q);   // H4
+  }
   RF_TSTAMP(ws, 5);
   if (tid == 0 && s_bad != ST_OK) atomicCAS(ws.status, ST_OK, s_bad);
 }
@@ -510,7 +529,8 @@ RF_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 __host__ __device__ constexpr int kxk_cluster(int k) { return k >= 64 ? 8 : (k >= 32 ? 4 : 1); }
-constexpr int KXK_SCRATCH_EXTRA = 64;   // doubles after the 16 k x k scratch matrices (cluster partials)
+constexpr int KXK_SCRATCH_MATS = 24;    // k x k scratch matrices: kxk_finish 0..15, H1..H4 16..19, kxk_lu temps 20..22
+constexpr int KXK_SCRATCH_EXTRA = 64;   // doubles after them (cluster partials)
 
 // Small k (k <= KXK_SMALL): the whole k x k chain in ONE CTA with every k x k operand resident in
 // shared memory and each product one output element per thread (a plain fma chain over ascending p):
@@ -555,7 +575,9 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   const double* Tm = SMALL ? S + 17 * kk : ws.T;
   double* E11 = SMALL ? S + 18 * kk : ws.E11;
   double* Xt1 = SMALL ? S + 19 * kk : ws.Xt;
-  double* part = SMALL ? sm + kxk_small_smem_doubles(k) - 64 : S + 16 * kk;   // [0, 8): delta hits, [8, 16): gram max per CTA
+  double* part = SMALL ? sm + kxk_small_smem_doubles(k) - 64 : S + KXK_SCRATCH_MATS * kk;   // [0, 8): delta hits, [8, 16): gram max
+  const bool useH = !SMALL && ws.kxk_h;                // the precomputed H1..H4 of kxk_lu (scratch + 16 k^2)
+  const double* H = S + 16 * kk;
   double* cs_base = SMALL ? S + KXK_SMALL_MATS * kk : sm;   // column-sum partials (after the matrices when SMALL)
   double* vec = cs_base + 8 * 7 * k + k;               // SMALL: sigma, d, alpha, rr2 copies
   const double* sig = SMALL ? vec : ws.sigma;
@@ -624,6 +646,14 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   }
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 22);
+  if (useH) {   // one stage instead of three (the T products were done by kxk_lu)
+    rgemm(-1.0, H, true, R1, 1.0, R1, V1);            // V_1 = R_1 - H1^T R_1
+    rgemm(-1.0, H + 2 * kk, true, Mp, 1.0, V1, V1);   //       - H3^T M'
+    rgemm(1.0, H + kk, true, R1, 0.0, nullptr, Pt);   // P~ = H2^T R_1
+    rgemm(1.0, H + 3 * kk, true, Mp, 1.0, Pt, Pt);    //    + H4^T M'
+    if (crank == 0) RF_TSTAMP(ws, 23);
+    if (crank == 0) RF_TSTAMP(ws, 24);
+  } else {
   rgemm(1.0, Lm, true, R1, 0.0, nullptr, Z);        // Z = L^T R_1
   rgemm(1.0, Ui, true, Mp, 1.0, Z, Z);                //   + U'^{-T} M'
   cluster_sync();
@@ -633,6 +663,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   if (crank == 0) RF_TSTAMP(ws, 24);
   rgemm(-1.0, Lm, false, P, 1.0, R1, V1);           // V_1 = R_1 - L P
   rgemm(1.0, Ui, false, P, 0.0, nullptr, Pt);         // P~ = U'^{-1} P
+  }
   // E_11 (line 6): beta needs the Gram G = X'^T X' = X'_1^T X'_1 + G'
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
     for (int j = tid & 31; j < k; j += 32) {
@@ -662,6 +693,14 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
     for (int j = tid & 31; j < k; j += 32) S2[i * k + j] = (Mp[i * k + j] - GPt[i * k + j]) / d[j];
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 26);
+  if (useH) {   // L B and U'^{-1} B directly (one stage instead of three)
+    rgemm(1.0, H, false, E11, 0.0, nullptr, LB);          // L B = H1 E_11
+    rgemm(1.0, H + kk, false, S2, 1.0, LB, LB);           //     + H2 S2
+    rgemm(1.0, H + 2 * kk, false, E11, 0.0, nullptr, UB); // U'^{-1} B = H3 E_11
+    rgemm(1.0, H + 3 * kk, false, S2, 1.0, UB, UB);       //           + H4 S2
+    if (crank == 0) RF_TSTAMP(ws, 27);
+    if (crank == 0) RF_TSTAMP(ws, 28);
+  } else {
   rgemm(1.0, Lm, true, E11, 0.0, nullptr, Qm);   // Qm = L^T E_11
   rgemm(1.0, Ui, true, S2, 1.0, Qm, Qm);              //   + U'^{-T} S2
   cluster_sync();
@@ -671,6 +710,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   if (crank == 0) RF_TSTAMP(ws, 28);
   rgemm(1.0, Lm, false, B, 0.0, nullptr, LB);       // L B
   rgemm(1.0, Ui, false, B, 0.0, nullptr, UB);         // U'^{-1} B
+  }
   // S7 folded into this kernel: the column norms of X~ over the
   // rows >= top follow from the pass-B sums, with x~_i = w'_i D^-1 - x'_i C' and w' = r' + x' D:
   //   ||x~_2j||^2 = (rr_j + 2 d_j M'_jj + d_j^2 G'_jj) / d_j^2 - (2 / d_j) sum_l C'_lj (M'_lj + d_j G'_lj)

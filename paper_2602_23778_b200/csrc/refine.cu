@@ -1119,7 +1119,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oBrr = take(brr), oMg = take(2 * kk + k), oNs = take(nslot),
                oAl = take(k), oD = take(k), oRd = take(k), oSg = take(k), oU = take(kk), oL = take(kk),
                oT = take(kk), oUi = take(kk), oE = take(kk), oBc = take(c->bc_cnt), oNt = take(k), oIn = take(k),
-               oScr = take(16 * kk + KXK_SCRATCH_EXTRA), oRows = take((size_t)c->n_loc), oRun = take(8),
+               oScr = take(KXK_SCRATCH_MATS * kk + KXK_SCRATCH_EXTRA), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
                oNrS = take(k), oNrA = take(P * k), oCol = take(2), oZd = take(k), oGate = take(1),
                oBd = take(c->opts.mixed ? (size_t)c->sms * 2 * c->kp : 0);
@@ -1147,6 +1147,11 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.gate = reinterpret_cast<int*>(b + oGate);
   ws.want_gram = c->opts.reorth_tol > 0.0 ? 1 : 0;
   ws.normalize = c->opts.normalize ? 1 : 0;
+  {   // the clustered kxk_finish (k > KXK_SMALL, or REFINE_KXK_SMALL=0) takes kxk_lu's H1..H4 (REFINE_KXK_H=0: off)
+    const char* sm_ = getenv("REFINE_KXK_SMALL");
+    const char* he = getenv("REFINE_KXK_H");
+    ws.kxk_h = (!(he && he[0] == '0') && (k > KXK_SMALL || (sm_ && sm_[0] == '0'))) ? 1 : 0;
+  }
   ws.bdiag = nullptr;
   c->bdiag = c->opts.mixed ? b + oBd : nullptr;
   c->run = reinterpret_cast<RunState*>(b + oRun);
