@@ -32,6 +32,7 @@ namespace rf {
 
 constexpr int KXK_THREADS = 1024;
 __device__ long long* g_gemm_tlog = nullptr;   // optional phase log of one cta_gemm call (timing builds)
+__device__ long long* g_fullk_tlog = nullptr;  // ... and of one cta_gemm_fullk call
 constexpr int PANEL = 32;
 constexpr int LDA_P = PANEL + 4;                  // As[i][p]: A-fragment reads (8 rows x 4) conflict-free
 constexpr int LDB_P = KMAX + 8;                   // Bs[p][j]: B-fragment reads (4 rows x 8) conflict-free
@@ -171,8 +172,50 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
   const int lda_s = Kp + 4, ldb_s = Np + 8;
   double* As = sm;                      // [Mp][lda_s]  As[i][p] = op(A)(i, p)
   double* Bs = sm + Mp * lda_s;         // [Kp][ldb_s]  Bs[p][j] = B(p, j)
+  long long* fl = g_fullk_tlog;
+  if (fl && tid == 0) fl[0] = clock64();
   __syncthreads();
-  if (__isGlobal(A) && __isGlobal(B)) {
+  const bool v16 = ((K | N | M | lda | ldb) & 1) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
+  if (__isGlobal(A) && __isGlobal(B) && v16) {
+    // 16-byte copies, (row, column-pair) walked without divisions (one per thread up front): the
+    // 8-byte / division form cost ~10 us per k = 128 product, mostly issue
+    {   // B: K rows x N / 2 pairs
+      const int n2 = N / 2, step = KXK_THREADS;
+      int p = tid / n2, j = tid - p * n2;
+      const int dp = step / n2, dj = step - dp * n2;
+      for (int e = tid; e < K * n2; e += step) {
+        cp_async16(Bs + p * ldb_s + 2 * j, B + (size_t)p * ldb + 2 * j, true);
+        p += dp; j += dj;
+        if (j >= n2) { j -= n2; ++p; }
+      }
+    }
+    if (!ta) {   // op(A) = A: M rows x K / 2 pairs
+      const int k2 = K / 2;
+      int i = tid / k2, q = tid - i * k2;
+      const int di = KXK_THREADS / k2, dq = KXK_THREADS - di * k2;
+      for (int e = tid; e < M * k2; e += KXK_THREADS) {
+        cp_async16(As + i * lda_s + 2 * q, A + (size_t)i * lda + 2 * q, true);
+        i += di; q += dq;
+        if (q >= k2) { q -= k2; ++i; }
+      }
+    } else {     // op(A)(i, p) = A[p][i]: K rows of M contiguous entries, transposed element-wise
+      for (int e = tid; e < M * K; e += KXK_THREADS) {
+        const int p = e / M, i = e - p * M;
+        cp_async8(As + i * lda_s + p, A + (size_t)p * lda + i, true);
+      }
+    }
+    // zero padding (K, M, N are multiples of 8 on the clustered path except a ragged k: pad explicitly)
+    for (int e = tid; e < Mp * (Kp - K) + (Mp - M) * Kp; e += KXK_THREADS) {
+      if (e < Mp * (Kp - K)) As[(e / (Kp - K)) * lda_s + K + e % (Kp - K)] = 0.0;
+      else { const int f = e - Mp * (Kp - K); As[(M + f / Kp) * lda_s + f % Kp] = 0.0; }
+    }
+    for (int e = tid; e < (Kp - K) * Np + K * (Np - N); e += KXK_THREADS) {
+      if (e < (Kp - K) * Np) Bs[(K + e / Np) * ldb_s + e % Np] = 0.0;
+      else { const int f = e - (Kp - K) * Np; Bs[(f / (Np - N)) * ldb_s + N + f % (Np - N)] = 0.0; }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else if (__isGlobal(A) && __isGlobal(B)) {
     for (int e = tid; e < Mp * Kp; e += KXK_THREADS) {
       int i, p;
       if (ta) { i = e % Mp; p = e / Mp; } else { p = e % Kp; i = e / Kp; }
@@ -198,6 +241,7 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
     }
   }
   __syncthreads();
+  if (fl && tid == 0) fl[1] = clock64();
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     const int tile = warp + 32 * t;
@@ -215,7 +259,9 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
       }
     }
   }
+  if (fl && tid == 0) fl[2] = clock64();
   __syncthreads();
+  if (fl && tid == 0) { fl[3] = clock64(); g_fullk_tlog = nullptr; }
 }
 
 // Inverse of a k x k triangular matrix S (ld k) into R (ld k).  upper: S upper triangular;
@@ -597,6 +643,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   if (tid == 0) s_hits = 0;
   if (crank == 0) RF_TSTAMP(ws, 20);
   if (ws.tlog && tid == 0 && crank == 0) g_gemm_tlog = ws.tlog + 40;
+  if (ws.tlog && tid == 0 && crank == 0) g_fullk_tlog = ws.tlog + 56;
   if (ws.multi) {   // [M2 | G2 | rr2] of every rank, summed in rank order (M2, G2, rr2 are contiguous)
     const int64_t cnt = 2 * kk + k;
     for (int64_t e = crank * nt + tid; e < cnt; e += (int64_t)ncl * nt) {

@@ -16,6 +16,9 @@ for (n, k) in [(256, 4), (4096, 16), (8192, 32), (8192, 64), (8192, 128)]:
     v = a[20:33]
     v = v[v != 0]
     print(f"k={k}: total {(v[-1] - v[0]) / 1.965e3:.1f} us  phases " + " ".join(f"{x / 1.965e3:.1f}" for x in np.diff(v)))
+    if a[56] and a[59]:
+        print(f"   first cta_gemm_fullk: staging {(a[57] - a[56]) / 1.965e3:.2f} us, DMMA+stores {(a[58] - a[57]) / 1.965e3:.2f} us, "
+              f"final barrier {(a[59] - a[58]) / 1.965e3:.2f} us")
     if a[33] and a[34]:
         print(f"   stats phase: column sums {(a[33] - a[30]) / 1.965e3:.1f} us, per-column {(a[34] - a[33]) / 1.965e3:.1f} us, "
               f"tail {(a[31] - a[34]) / 1.965e3:.1f} us")
