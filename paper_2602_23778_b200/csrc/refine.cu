@@ -209,6 +209,7 @@ struct refine_ctx {
   int gemm_bm = 0, nsplit = 1;
   // TMA-fed dense S1 (gemm_ax_tma_kernel): A's tensor map (fixed at init), X's (cached per pointer)
   bool gemm_tma = false;
+  int gemm_tbk = 16;            // K rows per TMA stage of the dense S1 (X^ box height)
   bool pdl = true;              // programmatic dependent launch of the sweep's kernels (launch_k)
   CUtensorMap tm_A{}, tm_X{};
   const double* tm_X_ptr = nullptr;
@@ -357,7 +358,7 @@ static bool passb_x_map(refine_ctx* c, const double* X) {   // local X rows -> b
 }
 static bool gemm_x_map(refine_ctx* c, const double* X) {   // X (n x k) -> boxes of 16 (K rows) x 16 columns
   if (c->tm_X_ptr == X) return true;
-  if (!encode_2d(&c->tm_X, X, (uint64_t)c->k, (uint64_t)c->n, (uint64_t)c->k, 16)) return false;
+  if (!encode_2d(&c->tm_X, X, (uint64_t)c->k, (uint64_t)c->n, (uint64_t)c->k, (uint32_t)c->gemm_tbk)) return false;
   c->tm_X_ptr = X;
   return true;
 }
@@ -586,7 +587,7 @@ struct Kern {
   static constexpr auto gemm = gemm_ax_kernel<KP, GBM, GWM, GWN, GBK, GST>;
   // TMA-fed S1 (KP >= 16): BK = 16 K-steps in a TST-deep ring, the cp.async kernel's warp tiles
   static constexpr bool TMA_OK = KP >= 16;
-  static constexpr int TBK = 16, TST = 4;
+  static constexpr int TBK = 16, TST = 4;   // (k = 16 measured: 32-row stages 35.0 us, 8 stages 35.5 us, this 31 us)
   using TGC = GemmCfg<KP, GBM, GWM, GWN, TBK, TST>;
   static constexpr int T_SMEM = gemm_tma_smem<(KP >= 16 ? KP : 16), GBM, TBK, TST>();
   static constexpr auto gemm_tma = gemm_ax_tma_kernel<(KP >= 16 ? KP : 16), GBM, GWM, (KP >= 16 ? GWN : 16), TBK, TST>;
@@ -625,6 +626,7 @@ struct Kern {
     // dense GEMM: split-K so the grid fills whole waves of resident CTAs
     if (!c->csr) {
       if (c->gemm_tma && TMA_OK) {
+        c->gemm_tbk = TBK;
         if ((e = cudaFuncSetAttribute(gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM))) return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_tma, TGC::THREADS + 32, T_SMEM))) return e;
       } else {
