@@ -30,6 +30,7 @@ namespace rf {
 constexpr int ST_THREADS = 512;     // 16 warps; thread 0 also issues the TMA loads
 constexpr int ST_BLOCK = ST_THREADS;
 constexpr int ST_SLOTS = 4;         // ring: slabs z - 1, z, z + 1 in use, z + 2 loading
+constexpr int ST_WARPS = ST_THREADS / 32;
 
 // codes of a nonzero's column relative to its row (x fastest, then y, then z)
 enum : int { SC_SELF = 0, SC_XM, SC_XP, SC_YM, SC_YP, SC_ZM, SC_ZP };
@@ -111,15 +112,17 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   constexpr int REC = NZR + 1;
   extern __shared__ __align__(128) unsigned char st_smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(st_smem);           // full[slot]: box + records landed
+  int* done = reinterpret_cast<int*>(st_smem + 64);                 // warps through iteration m (slot m % 4)
   unsigned char* slots = st_smem + 128;
   griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
   const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
+  auto lane0 = [&]() { return (tid & 31) == 0; };
   const int K = ws.k, nq = g.nq;
   const int q = blockIdx.x % nq, b = blockIdx.x / nq, nb = gridDim.x / nq;
   const int64_t P = (int64_t)g.ntx * g.nty * g.nseg;   // pencil segments per column block
   if (tid == 0) {
-    for (int s = 0; s < ST_SLOTS; ++s) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < ST_SLOTS; ++s) { mbar_init(&mbar[s], 1); done[s] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -141,10 +144,10 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
     c.it += nb;
     return item_begin(c);
   };
-  auto issue = [&](const Cur& c, int m) {   // thread 0: load m of the sequence into slot m % 4
+  auto issue = [&](const Cur& c, int m) {   // one lane 0: load m of the sequence into slot m % 4
     const int s = m % ST_SLOTS;
-    // (the slot was last read by generic-proxy loads before the CTA barrier: order them before the
-    //  async-proxy TMA / bulk writes that refill it)
+    // (the slot was last read by generic-proxy loads, ordered before this thread by the counter:
+    //  order them before the async-proxy TMA / bulk writes that refill it)
     fence_async_smem();
     unsigned char* sl = slots + (size_t)s * g.slot_bytes;
     const bool inner = c.z >= c.zs && c.z < c.ze;
@@ -156,13 +159,17 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
     }
   };
 
+  // No CTA-wide barrier per slab: the slot of load m - 1 (read as X+ / X0 / X- by iterations m - 2 .. m)
+  // is refilled with load m + 3 by the LAST warp to finish iteration m (a shared counter per slot);
+  // every lane 0 tracks the load sequence so whichever warp is last can issue.
   Cur cons{b, 0, 0, 0, 0, 0}, prod{b, 0, 0, 0, 0, 0};
   bool more_c = item_begin(cons);
   bool more_p = item_begin(prod);
   int m_issued = 0;
-  if (tid == 0) {
-    for (int t = 0; t < 2 && more_p; ++t) {
-      issue(prod, m_issued++);
+  if (lane0()) {
+    for (int t = 0; t < 3 && more_p; ++t) {
+      if (tid == 0) issue(prod, m_issued);
+      ++m_issued;
       more_p = advance(prod);
     }
   }
@@ -178,11 +185,6 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   char* Wb = reinterpret_cast<char*>(ws.W);
   if (more_c) mbar_wait(&mbar[0], 0);
   for (int m = 0; more_c; ++m) {
-    __syncthreads();                           // compute of load m - 1 done: slot (m + 2) % 4 is free
-    if (tid == 0 && more_p) {
-      issue(prod, m_issued++);
-      more_p = advance(prod);
-    }
     const int nxt = m + 1;                     // every thread waits each load once, in order
     const bool has_next = !(cons.z == cons.ze && cons.it + nb >= P);
     if (has_next) mbar_wait(&mbar[nxt % ST_SLOTS], (nxt / ST_SLOTS) & 1);
@@ -256,6 +258,16 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
           for (int u = 0; u < 2 * VPL; ++u) { dd_add1(da[u], ba[u]); dd_add1(dg[u], bg[u]); ba[u] = bg[u] = 0.0; }
         }
       }
+    }
+    __syncwarp();                              // this warp's reads of iteration m are done
+    if (lane0()) {
+      __threadfence_block();
+      const int old = atomicAdd(&done[m % ST_SLOTS], 1);   // (monotonic: ST_WARPS arrivals per use)
+      if (old % ST_WARPS == ST_WARPS - 1) {    // last warp through iteration m: slot of load m - 1 is free
+        __threadfence_block();
+        if (more_p) issue(prod, m_issued);
+      }
+      if (more_p) { ++m_issued; more_p = advance(prod); }
     }
     more_c = advance(cons);
   }
