@@ -785,6 +785,123 @@ passC_kernel(Ws ws, const double* X, double* out, int vec16) {
   }
 }
 
+// ---------------------------------------------------------------- pass C at k = 128, ping-pong
+// A sweep's pass C (NORM = false) with two consumer groups of 8 warps that take alternate 32-row
+// tiles: one group's epilogue (w s - acc, stores) overlaps the other group's DMMAs, instead of all
+// 16 warps leaving the DMMA pipe idle together at every tile boundary.  The X tiles arrive as eight
+// 128-byte-swizzled 16-column TMA boxes (the pass-B tensor map) in a 2-stage ring (stage = group);
+// the last warp of a group through its tile's DMMAs refills the stage with the group's next tile (no
+// producer warp: 16 warps keep 128 registers).  All of Csig stays resident (padded rows,
+// conflict-free B fragments).  Same DMMA k-order and epilogue fma as passC_kernel (identical
+// results); in place, rows >= top only.
+struct PassCPPCfg {
+  static constexpr int KP = 128, BR = 32, GROUPS = 2, GWARPS = 8;
+  static constexpr int WARPS = GROUPS * GWARPS, THREADS = WARPS * 32, BLOCK = THREADS;
+  static constexpr int WM_ = 2, WN_ = 4, WTM = BR / WM_, WTN = KP / WN_, MI = WTM / 8, NI = WTN / 8;
+  static constexpr int LDC = KP + 8;
+  static constexpr int BOX = BR * 128, STAGE = (KP / 16) * BOX;
+  static constexpr int SMEM = GROUPS * STAGE + KP * LDC * 8 + 1024 + 2 * GROUPS * 8;
+};
+__global__ void __launch_bounds__(PassCPPCfg::BLOCK, 1)
+passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restrict__ out) {
+  using C = PassCPPCfg;
+  constexpr int BR = C::BR, KP = C::KP;
+  extern __shared__ __align__(1024) unsigned char pcsm[];
+  __shared__ double ssc[KP];
+  griddep_wait();
+  if (*ws.status != ST_OK) return;
+  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pcsm) + 1023) & ~uintptr_t(1023));
+  double* Cs = reinterpret_cast<double*>(ring + C::GROUPS * C::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(Cs + KP * C::LDC);
+  int* done = reinterpret_cast<int*>(full + C::GROUPS);             // warps through a tile's DMMAs (monotonic)
+  const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t ntile = (rows + BR - 1) / BR;
+  const int njt = (int)((ntile > blockIdx.x) ? (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);   // this CTA's tiles
+  auto issue = [&](int j) {   // tile j of this CTA -> stage j % 2
+    const int s = j % C::GROUPS;
+    const int r0 = (int)(ws.top + (blockIdx.x + (int64_t)j * gridDim.x) * BR);
+    mbar_expect_tx(&full[s], C::STAGE);
+#pragma unroll
+    for (int b = 0; b < KP / 16; ++b) tma_load_2d(ring + s * C::STAGE + b * C::BOX, &tmX, 16 * b, r0, &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < C::GROUPS; ++s) { mbar_init(&full[s], 1); done[s] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int j = 0; j < C::GROUPS && j < njt; ++j) issue(j);
+  }
+  for (int e = tid; e < KP * KP; e += blockDim.x) {
+    const int l = e / KP, j = e % KP;
+    Cs[l * C::LDC + j] = (l < k && j < k) ? ws.Csig[l * k + j] : 0.0;
+  }
+  for (int j = tid; j < KP; j += blockDim.x) ssc[j] = (j < k) ? ws.scal[j] : 0.0;
+  __syncthreads();
+  const int grp = warp / C::GWARPS, gw = warp % C::GWARPS;
+  const int wm = gw / C::WN_, wn = gw % C::WN_;
+  for (int j = grp; j < njt; j += C::GROUPS) {
+    const int s = j % C::GROUPS;
+    const int64_t r0 = ws.top + (blockIdx.x + (int64_t)j * gridDim.x) * BR;
+    double w[C::MI][C::NI][2];   // this thread's W entries, loaded ahead of the MMAs
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int64_t g = r0 + wm * C::WTM + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int jn = 0; jn < C::NI; ++jn) {
+        const int c = wn * C::WTN + jn * 8 + 2 * (lane & 3);
+        if (g < ws.n_loc && c < k) {
+          const double2 v = *reinterpret_cast<const double2*>(ws.W + g * k + c);
+          w[i][jn][0] = v.x; w[i][jn][1] = v.y;
+        } else {
+          w[i][jn][0] = w[i][jn][1] = 0.0;
+        }
+      }
+    }
+    double acc[C::MI][C::NI][2];
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int jn = 0; jn < C::NI; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+    mbar_wait(&full[s], (j / C::GROUPS) & 1);
+    const unsigned char* xs = ring + s * C::STAGE;
+#pragma unroll 4
+    for (int kk = 0; kk < KP; kk += 4) {
+      double a[C::MI], b[C::NI];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+        a[i] = *reinterpret_cast<const double*>(xs + swz_off<BR>(wm * C::WTM + i * 8 + (lane >> 2), kk + (lane & 3)));
+#pragma unroll
+      for (int jn = 0; jn < C::NI; ++jn) b[jn] = Cs[(kk + (lane & 3)) * C::LDC + wn * C::WTN + jn * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int jn = 0; jn < C::NI; ++jn) dmma(acc[i][jn][0], acc[i][jn][1], a[i], b[jn]);
+    }
+    __syncwarp();                                // this warp's reads of the stage are done
+    if (lane == 0) {
+      __threadfence_block();
+      const int old = atomicAdd(&done[s], 1);
+      if (old % C::GWARPS == C::GWARPS - 1 && j + C::GROUPS < njt) {   // last of the group: refill the stage
+        __threadfence_block();
+        fence_async_smem();
+        issue(j + C::GROUPS);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int64_t g = r0 + wm * C::WTM + i * 8 + (lane >> 2);
+      if (g >= ws.n_loc) continue;
+#pragma unroll
+      for (int jn = 0; jn < C::NI; ++jn) {
+        const int cl = wn * C::WTN + jn * 8 + 2 * (lane & 3);
+        if (cl >= k) continue;
+        const double x0 = __fma_rn(w[i][jn][0], ssc[cl], -acc[i][jn][0]);
+        const double x1 = __fma_rn(w[i][jn][1], ssc[cl + 1], -acc[i][jn][1]);
+        *reinterpret_cast<double2*>(out + g * k + cl) = make_double2(x0, x1);
+      }
+    }
+  }
+}
+
 // x_ij *= 1/||x~_j||.  The thread count is a multiple of k/2 on the vector path, so every
 // thread always scales the same column pair (no per-element index arithmetic).
 __global__ void __launch_bounds__(256) normalize_kernel(Ws ws, double* __restrict__ X) {

@@ -215,6 +215,7 @@ struct refine_ctx {
   const double* tm_X_ptr = nullptr;
   // TMA-fed pass B at k = 128 (passB2_tma_kernel): X's map (cached per pointer) and W's (fixed)
   bool pb_tma = false;
+  bool pc_pp = false;            // k = 128: ping-pong pass C (passC_pp_kernel)
   CUtensorMap tm_Xb{}, tm_Wb{};
   const double* tm_Xb_ptr = nullptr;
   int64_t kchunk = 0;
@@ -845,6 +846,8 @@ struct Kern {
             passC_oz_kernel<<<c->sms, OZC_THREADS, OZC_SMEM, s>>>(ws, X, X);
           else if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
             passC_tc_kernel<TKP><<<c->sms, TCC_THREADS, TccCfg<TKP>::SMEM, s>>>(ws, X, X);
+          else if (KP == 128 && c->pc_pp && xv16 && passb_x_map(c, X))   // ping-pong pass C (X's pass-B map)
+            launch_k(c->pdl, passC_pp_kernel, dim3(c->sms), dim3(PassCPPCfg::BLOCK), PassCPPCfg::SMEM, s, ws, c->tm_Xb, X);
           else
             launch_k(c->pdl, passC_sweep, dim3(c->passc_grid, 1), dim3(CC::THREADS), CC::SMEM, s, ws,
                      (const double*)X, X, (int)xv16);
@@ -1089,6 +1092,11 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
     if (c->pb_tma)
       RF_CK(c, cudaFuncSetAttribute(passB2_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     PassB2TmaCfg<128>::SMEM));
+    // k = 128 (even): the ping-pong pass C (passC_pp_kernel; REFINE_PASSC_PP=0 disables)
+    const char* ce = getenv("REFINE_PASSC_PP");
+    c->pc_pp = !(ce && ce[0] == '0') && c->k == 128 && tensor_map_encoder() != nullptr;
+    if (c->pc_pp)
+      RF_CK(c, cudaFuncSetAttribute(passC_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PassCPPCfg::SMEM));
   }
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
   RF_CK(c, cudaFuncSetAttribute(kxk_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
