@@ -590,6 +590,156 @@ passB2_tma_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_c
   }
 }
 
+// ---------------------------------------------------------------- pass B at k = 128, ping-pong
+// passB2_tma_kernel's units, ring and slot layout, but the CTA's 64 tile columns are split between
+// two consumer groups of 8 warps (32 columns each, 4 x 2 warp tiles of 32 x 16).  Each group forms
+// R for its own columns and meets at its own named barrier, so while one group forms R the other
+// can issue DMMAs, and the groups drift apart instead of idling the DMMA pipe together at every
+// stage.  No producer warp (16 warps keep 128 registers): the last of the 16 warps through a stage
+// refills it.  Same per-element DMMA k-order as passB2_tma_kernel (identical partials); rr_j is
+// summed over the 8 threads of a column in a fixed order.
+struct PassB2PPCfg {
+  static constexpr int KP = 128, TA = KP, TB = 64, NT = 2 * KP / TB;
+  static constexpr int GROUPS = 2, GWARPS = 8, WARPS = GROUPS * GWARPS, THREADS = WARPS * 32, GTHREADS = GWARPS * 32;
+  static constexpr int GCOLS = TB / GROUPS, WA = 4, WB = 2;
+  static constexpr int WTA = TA / WA, WTB = GCOLS / WB, MI = WTA / 8, NI = WTB / 8;
+  static constexpr int BR = 32, ST = 4;
+  static constexpr int XBOXES = KP / 16, WBOXES = TB / 16, BOX = BR * 128;
+  static constexpr int STAGE = (XBOXES + WBOXES) * BOX;
+  static constexpr int SMEM = ST * STAGE + 1024 + ST * 8 + ST * 4;
+};
+__global__ void __launch_bounds__(PassB2PPCfg::THREADS, 1)
+passB2_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW) {
+  using C = PassB2PPCfg;
+  constexpr int BR = C::BR, TB = C::TB, ST = C::ST, KP = C::KP;
+  extern __shared__ __align__(1024) unsigned char pbsm[];
+  __shared__ double sd[KP];
+  __shared__ double srr[C::THREADS];
+  griddep_wait();
+  if (*ws.status != ST_OK) return;
+  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pbsm) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + ST * C::STAGE);
+  int* done = reinterpret_cast<int*>(full + ST);                    // warps through a stage (monotonic)
+  const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // units: per pair of row chunks R0, R1, X1 for each chunk plus one X0 unit spanning both
+  const int u = blockIdx.x, pair = u / 7, w7 = u % 7;
+  const int64_t nchunk = 2 * (int64_t)(gridDim.x / 7);
+  int tb, span = 1;
+  int64_t cidx;
+  if (w7 < 6) { tb = (w7 % 3 == 2) ? 3 : (w7 % 3); cidx = 2 * pair + w7 / 3; }
+  else { tb = 2; cidx = 2 * pair; span = 2; }
+  const int b0 = tb * TB;
+  const bool rtile = b0 < KP;                                 // all 64 columns are R columns (else X)
+  const int64_t rows = ws.n_loc - ws.top;
+  const int64_t per = ((rows + nchunk - 1) / nchunk + 31) / 32 * 32;   // (passB2's chunking; a multiple of BR)
+  const int64_t rb = ws.top + cidx * per;
+  const int64_t re = (rb + span * per < ws.n_loc) ? rb + span * per : ws.n_loc;
+  const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
+  auto issue = [&](int it) {
+    const int s = it % ST;
+    unsigned char* st = ring + s * C::STAGE;
+    const int r0 = (int)(rb + (int64_t)it * BR);
+    mbar_expect_tx(&full[s], (C::XBOXES + (rtile ? C::WBOXES : 0)) * C::BOX);
+#pragma unroll
+    for (int b = 0; b < C::XBOXES; ++b) tma_load_2d(st + b * C::BOX, &tmX, 16 * b, r0, &full[s]);
+    if (rtile) {
+#pragma unroll
+      for (int b = 0; b < C::WBOXES; ++b) tma_load_2d(st + (C::XBOXES + b) * C::BOX, &tmW, b0 + 16 * b, r0, &full[s]);
+    }
+  };
+  for (int j = tid; j < KP; j += blockDim.x) sd[j] = (j < k) ? ws.d[j] : 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); done[s] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int it = 0; it < ST && it < nit; ++it) issue(it);
+  }
+  __syncthreads();
+  const int grp = warp / C::GWARPS, gw = warp % C::GWARPS, gtid = tid - grp * C::GTHREADS;
+  const int wa = gw / C::WB, wb = gw % C::WB;
+  const int a_lo = wa * C::WTA, bw = b0 + grp * C::GCOLS + wb * C::WTB;   // warp tile column (padded [R | X])
+  const bool active = !(bw >= KP && a_lo >= (bw - KP) + C::WTB);          // below G's diagonal: no MMAs
+  const int rcol = grp * C::GCOLS + gtid % C::GCOLS;                       // this thread's R column (in the tile)
+  const double drc = rtile ? sd[b0 + rcol] : 0.0;
+  double rr = 0.0;
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int it = 0; it < nit; ++it) {
+    const int s = it % ST;
+    mbar_wait(&full[s], (it / ST) & 1);
+    const unsigned char* xs = ring + s * C::STAGE;
+    unsigned char* wsb = ring + s * C::STAGE + C::XBOXES * C::BOX;
+    if (rtile) {   // R = W - X D in place for this group's columns (zero-filled rows: R = 0)
+#pragma unroll
+      for (int q = 0; q < BR * C::GCOLS / C::GTHREADS; ++q) {
+        const int r = gtid / C::GCOLS + q * (C::GTHREADS / C::GCOLS);
+        double* wp = reinterpret_cast<double*>(wsb + swz_off<BR>(r, rcol));
+        const double x = *reinterpret_cast<const double*>(xs + swz_off<BR>(r, b0 + rcol));
+        const double v = __fma_rn(-x, drc, *wp);
+        *wp = v;
+        rr = __fma_rn(v, v, rr);
+      }
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(C::GTHREADS) : "memory");   // this group only
+    }
+    if (active) {
+#pragma unroll
+      for (int kk = 0; kk < BR; kk += 4) {
+        const int row = kk + (lane & 3);
+        double a[C::MI], bv[C::NI];
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+          a[i] = *reinterpret_cast<const double*>(xs + swz_off<BR>(row, a_lo + i * 8 + (lane >> 2)));
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int cb8 = bw + j * 8;                                 // all R or all X (warp-uniform)
+          bv[j] = (cb8 < KP) ? *reinterpret_cast<const double*>(wsb + swz_off<BR>(row, cb8 - b0 + (lane >> 2)))
+                             : *reinterpret_cast<const double*>(xs + swz_off<BR>(row, cb8 - KP + (lane >> 2)));
+        }
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], bv[j]);
+      }
+    }
+    __syncwarp();                                // this warp's reads / R writes of the stage are done
+    if (lane == 0) {
+      __threadfence_block();
+      const int old = atomicAdd(&done[s], 1);
+      if (old % C::WARPS == C::WARPS - 1 && it + ST < nit) {   // last of the 16 warps: refill the stage
+        __threadfence_block();
+        fence_async_smem();
+        issue(it + ST);
+      }
+    }
+  }
+  if (active) {
+    for (int q = 0; q < span; ++q) {          // a two-chunk unit stores its sum in the first slot, 0 in the second
+      double* out = ws.bpart + ((cidx + q) * C::NT + tb) * (C::TA * TB);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int ra = a_lo + i * 8 + (lane >> 2);
+          const int cb = (bw - b0) + j * 8 + 2 * (lane & 3);
+          out[ra * TB + cb] = q ? 0.0 : acc[i][j][0];
+          out[ra * TB + cb + 1] = q ? 0.0 : acc[i][j][1];
+        }
+    }
+  }
+  if (rtile) {   // the 8 threads of a column (gtid = c % 32 + 32 q within its group): fixed-order sum
+    srr[tid] = rr;
+    __syncthreads();
+    if (tid < TB && b0 + tid < KP) {
+      const int g = tid / C::GCOLS, cc = tid % C::GCOLS;
+      double sacc = srr[g * C::GTHREADS + cc];
+      for (int q = 1; q < C::GTHREADS / C::GCOLS; ++q) sacc += srr[g * C::GTHREADS + cc + q * C::GCOLS];
+      ws.brr[cidx * KP + b0 + tid] = sacc;
+    }
+  }
+}
+
 // Sum pass-B2 partials over chunks in fixed order -> M2, G2 (mirrored from its upper triangle), rr2.
 template <int KP>
 __global__ void __launch_bounds__(PB_RED_THREADS) passB2_reduce_kernel(Ws ws, int nchunk) {

@@ -215,7 +215,8 @@ struct refine_ctx {
   const double* tm_X_ptr = nullptr;
   // TMA-fed pass B at k = 128 (passB2_tma_kernel): X's map (cached per pointer) and W's (fixed)
   bool pb_tma = false;
-  bool pc_pp = false;            // k = 128: ping-pong pass C (passC_pp_kernel)
+  bool pc_pp = false;
+  bool pb_pp = false;            // k = 128: ping-pong pass B (passB2_pp_kernel)            // k = 128: ping-pong pass C (passC_pp_kernel)
   CUtensorMap tm_Xb{}, tm_Wb{};
   const double* tm_Xb_ptr = nullptr;
   int64_t kchunk = 0;
@@ -812,7 +813,10 @@ struct Kern {
           n += 2;
           break;
         }
-        if (B2 && B2C::PAIRED && c->pb_tma && xv16 && passb_x_map(c, X))
+        if (B2 && B2C::PAIRED && c->pb_tma && c->pb_pp && xv16 && passb_x_map(c, X))
+          launch_k(c->pdl, passB2_pp_kernel, dim3(7 * (c->passb_grid_y / 2)), dim3(PassB2PPCfg::THREADS),
+                   PassB2PPCfg::SMEM, s, ws, c->tm_Xb, c->tm_Wb);
+        else if (B2 && B2C::PAIRED && c->pb_tma && xv16 && passb_x_map(c, X))
           launch_k(c->pdl, passB2_tma_kernel<128>, dim3(7 * (c->passb_grid_y / 2)), dim3(PassB2TmaCfg<128>::THREADS + 32),
                    PassB2TmaCfg<128>::SMEM, s, ws, c->tm_Xb, c->tm_Wb);
         else if (B2 && B2C::PAIRED)
@@ -1092,6 +1096,11 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
     if (c->pb_tma)
       RF_CK(c, cudaFuncSetAttribute(passB2_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     PassB2TmaCfg<128>::SMEM));
+    // the ping-pong pass B (passB2_pp_kernel; REFINE_PASSB_PP=0 keeps passB2_tma_kernel)
+    const char* bpe = getenv("REFINE_PASSB_PP");
+    c->pb_pp = c->pb_tma && !(bpe && bpe[0] == '0');
+    if (c->pb_pp)
+      RF_CK(c, cudaFuncSetAttribute(passB2_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PassB2PPCfg::SMEM));
     // k = 128 (even): the ping-pong pass C (passC_pp_kernel; REFINE_PASSC_PP=0 disables)
     const char* ce = getenv("REFINE_PASSC_PP");
     c->pc_pp = !(ce && ce[0] == '0') && c->k == 128 && tensor_map_encoder() != nullptr;
