@@ -28,6 +28,10 @@ RF_DEV void dmma(double& c0, double& c1, double a, double b) {
 
 // ---------------------------------------------------------------- cp.async
 RF_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// 1024-byte-aligned start inside a dynamic shared-memory array, derived by integer offset from the
+// __shared__ array itself: the compiler then keeps the shared window (LDS / STS) for everything
+// addressed through it -- a round trip through uintptr_t makes every access a generic LD / ST
+RF_DEV unsigned char* smem_align1024(unsigned char* p) { return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u); }
 RF_DEV void cp_async16(void* smem, const void* gmem, bool pred) {
   // src-size 0 zero-fills the 16 bytes
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),

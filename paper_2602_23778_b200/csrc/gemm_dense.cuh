@@ -176,7 +176,7 @@ gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   if (*status != ST_OK) return;
   extern __shared__ __align__(1024) unsigned char gsm[];
   // [STAGES x stage] ring (1024-byte aligned for the 128-byte swizzle), then the mbarriers
-  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~uintptr_t(1023));
+  unsigned char* ring = smem_align1024(gsm);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * T::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -464,7 +464,7 @@ passB2_tma_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_c
   __shared__ double srr[C::THREADS];
   griddep_wait();
   if (*ws.status != ST_OK) return;
-  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pbsm) + 1023) & ~uintptr_t(1023));
+  unsigned char* ring = smem_align1024(pbsm);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + ST * C::STAGE);
   uint64_t* empty = full + ST;
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -617,7 +617,7 @@ passB2_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_co
   __shared__ double srr[C::THREADS];
   griddep_wait();
   if (*ws.status != ST_OK) return;
-  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pbsm) + 1023) & ~uintptr_t(1023));
+  unsigned char* ring = smem_align1024(pbsm);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + ST * C::STAGE);
   int* done = reinterpret_cast<int*>(full + ST);                    // warps through a stage (monotonic)
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -960,7 +960,7 @@ passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restri
   __shared__ double ssc[KP];
   griddep_wait();
   if (*ws.status != ST_OK) return;
-  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pcsm) + 1023) & ~uintptr_t(1023));
+  unsigned char* ring = smem_align1024(pcsm);
   double* Cs = reinterpret_cast<double*>(ring + C::GROUPS * C::STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(Cs + KP * C::LDC);
   int* done = reinterpret_cast<int*>(full + C::GROUPS);             // warps through a tile's DMMAs (monotonic)
