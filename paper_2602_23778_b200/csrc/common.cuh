@@ -74,6 +74,19 @@ RF_DEV void mbar_arrive(uint64_t* mbar) {
 // acquired through an mbarrier wait) before its subsequent async-proxy operations on them (TMA /
 // bulk-copy refills of a ring slot, tcgen05 reads of operands stored with st.shared).
 RF_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// Stage-release counter of the barrier-free rings (stencil SpMM, ping-pong passes B / C): lane 0 of
+// a warp whose reads of a stage are done (after __syncwarp) counts itself in with a release atomic;
+// returns true for the last of `nw` warps of this use of the stage, which then acquires (so every
+// warp's generic reads happen before) and proxy-fences before refilling the stage by TMA.  The
+// release / acquire pair compiles to MEMBAR.ALL.CTA (a __threadfence_block is fence.sc, MEMBAR.SC).
+RF_DEV bool stage_release_last(int* ctr, int nw) {
+  int old;
+  asm volatile("atom.release.cta.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_u32(ctr)) : "memory");
+  if (old % nw != nw - 1) return false;
+  asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+  fence_async_smem();
+  return true;
+}
 // 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16), completing on mbar
 RF_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -98,6 +111,20 @@ RF_DEV void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int
       "[%6];\n" ::"r"(smem_u32(dst)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(mbar))
       : "memory");
+}
+// L2 prefetches (no shared memory, no completion): the box tma_load_4d / tma_load_2d would load, and
+// a 1-D range (16-byte aligned, size a multiple of 16).  They put DRAM requests in flight ahead of
+// the shared-memory ring, whose depth alone (one or two loads per SM) is too small for HBM latency.
+RF_DEV void tma_prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(tmap), "r"(c0), "r"(c1),
+               "r"(c2), "r"(c3)
+               : "memory");
+}
+RF_DEV void tma_prefetch_2d(const void* tmap, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(tmap), "r"(c0), "r"(c1) : "memory");
+}
+RF_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // ---------------------------------------------------------------- double-double

@@ -704,15 +704,7 @@ passB2_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_co
       }
     }
     __syncwarp();                                // this warp's reads / R writes of the stage are done
-    if (lane == 0) {
-      __threadfence_block();
-      const int old = atomicAdd(&done[s], 1);
-      if (old % C::WARPS == C::WARPS - 1 && it + ST < nit) {   // last of the 16 warps: refill the stage
-        __threadfence_block();
-        fence_async_smem();
-        issue(it + ST);
-      }
-    }
+    if (lane == 0 && stage_release_last(&done[s], C::WARPS) && it + ST < nit) issue(it + ST);   // last of the 16 warps: refill
   }
   if (active) {
     for (int q = 0; q < span; ++q) {          // a two-chunk unit stores its sum in the first slot, 0 in the second
@@ -1027,15 +1019,7 @@ passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restri
         for (int jn = 0; jn < C::NI; ++jn) dmma(acc[i][jn][0], acc[i][jn][1], a[i], b[jn]);
     }
     __syncwarp();                                // this warp's reads of the stage are done
-    if (lane == 0) {
-      __threadfence_block();
-      const int old = atomicAdd(&done[s], 1);
-      if (old % C::GWARPS == C::GWARPS - 1 && j + C::GROUPS < njt) {   // last of the group: refill the stage
-        __threadfence_block();
-        fence_async_smem();
-        issue(j + C::GROUPS);
-      }
-    }
+    if (lane == 0 && stage_release_last(&done[s], C::GWARPS) && j + C::GROUPS < njt) issue(j + C::GROUPS);   // last of the group
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
       const int64_t g = r0 + wm * C::WTM + i * 8 + (lane >> 2);

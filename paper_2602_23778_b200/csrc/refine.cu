@@ -367,8 +367,12 @@ static bool gemm_x_map(refine_ctx* c, const double* X) {   // X (n x k) -> boxes
 
 template <int KC, int NZR>
 static void stencil_kernel_launch(refine_ctx* c, const Ws& ws) {
-  launch_k(c->pdl, spmm_stencil_kernel<KC, NZR>, dim3(c->st_grid), dim3(ST_BLOCK), c->st_smem, c->stream, ws, c->st_tm,
-           (const double*)c->st_meta, c->st_geo);
+  if (ws.shift != 0.0)
+    launch_k(c->pdl, spmm_stencil_kernel<KC, NZR, true>, dim3(c->st_grid), dim3(ST_BLOCK), c->st_smem, c->stream, ws,
+             c->st_tm, (const double*)c->st_meta, c->st_geo);
+  else
+    launch_k(c->pdl, spmm_stencil_kernel<KC, NZR, false>, dim3(c->st_grid), dim3(ST_BLOCK), c->st_smem, c->stream, ws,
+             c->st_tm, (const double*)c->st_meta, c->st_geo);
 }
 static bool stencil_launch(refine_ctx* c, const double* X, const Ws& ws) {
   if (!stencil_tensor_map(c, X)) return false;
@@ -425,7 +429,7 @@ static cudaError_t stencil_setup(refine_ctx* c) {
   } else {
     return cudaSuccess;
   }
-  if (g.nx < 2 || g.nz < 1) return cudaSuccess;
+  if (g.nx < 2 || g.nz < 1 || g.d3 * (int64_t)k >= INT32_MAX) return cudaSuccess;   // (32-bit in-plane W offsets)
   // default: 3-D grids with k >= 64, where it measured faster than the gather kernel (cfg5: 2.24 vs
   // 2.31 ms); 2-D grids at k = 32 measured slower (cfg4: 0.159-0.169 vs 0.147 ms).  REFINE_SPMM=stencil
   // forces it wherever the structure allows (tests).
@@ -477,6 +481,11 @@ static cudaError_t stencil_setup(refine_ctx* c) {
   g.zlen = (g.nz + nseg - 1) / nseg;
   g.nseg = (g.nz + g.zlen - 1) / g.zlen;
   g.blocks = (int64_t)g.ntx * g.nty * g.nz;
+  {  // alpha / g FP64 blocks of at most 8 rows per thread (rows per thread per slab: L R / rows per pass)
+    const int rgp = ST_THREADS / (KC >= 16 ? 8 : KC / 2);
+    const int rpt = (g.L * g.R + rgp - 1) / rgp;
+    g.mrg = std::max(1, 8 / rpt);
+  }
   const size_t meta_bytes = (size_t)g.blocks * g.meta_bytes;
   if ((e = cudaMalloc(&c->st_meta, meta_bytes)) != cudaSuccess) return e;
   cudaMemsetAsync(c->st_meta, 0, meta_bytes, c->stream);
@@ -487,9 +496,14 @@ static cudaError_t stencil_setup(refine_ctx* c) {
   c->st_grid = nb * g.nq;
   c->st_smem = std::max(ST_SLOTS * g.slot_bytes + 128, 128 + 8 * ST_THREADS * 16);   // (+ the final dd reduction)
   auto attr = [&](auto kern) { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c->st_smem); };
-  if (KC == 32) e = g.nzr == 5 ? attr(spmm_stencil_kernel<32, 5>) : attr(spmm_stencil_kernel<32, 7>);
-  else if (KC == 16) e = g.nzr == 5 ? attr(spmm_stencil_kernel<16, 5>) : attr(spmm_stencil_kernel<16, 7>);
-  else e = g.nzr == 5 ? attr(spmm_stencil_kernel<8, 5>) : attr(spmm_stencil_kernel<8, 7>);
+  for (int sh = 0; sh < 2 && e == cudaSuccess; ++sh) {
+    if (KC == 32) e = g.nzr == 5 ? (sh ? attr(spmm_stencil_kernel<32, 5, true>) : attr(spmm_stencil_kernel<32, 5, false>))
+                                 : (sh ? attr(spmm_stencil_kernel<32, 7, true>) : attr(spmm_stencil_kernel<32, 7, false>));
+    else if (KC == 16) e = g.nzr == 5 ? (sh ? attr(spmm_stencil_kernel<16, 5, true>) : attr(spmm_stencil_kernel<16, 5, false>))
+                                      : (sh ? attr(spmm_stencil_kernel<16, 7, true>) : attr(spmm_stencil_kernel<16, 7, false>));
+    else e = g.nzr == 5 ? (sh ? attr(spmm_stencil_kernel<8, 5, true>) : attr(spmm_stencil_kernel<8, 5, false>))
+                        : (sh ? attr(spmm_stencil_kernel<8, 7, true>) : attr(spmm_stencil_kernel<8, 7, false>));
+  }
   if (e != cudaSuccess) return e;
   c->st_on = tensor_map_encoder() != nullptr;
   if (getenv("REFINE_VERBOSE"))

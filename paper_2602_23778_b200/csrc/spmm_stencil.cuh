@@ -43,6 +43,7 @@ struct StencilGeo {
   int ntx, nty, nseg, zlen;
   int nq, KC;             // column blocks of KC columns
   int nzr;                // values per row record (5 or 7)
+  int mrg;                // slabs per FP64 alpha / g block (block = mrg x rows per thread per slab <= 8)
   int64_t d2, d3;         // row strides of y and z
   int box_bytes, meta_bytes, slot_bytes;
   int64_t blocks;         // metadata blocks (ntx nty nz)
@@ -101,23 +102,33 @@ __global__ void stencil_check_kernel(const int32_t* __restrict__ rp, const int32
   atomicMax(bad + 1, mx);
 }
 
-template <int KC, int NZR>
+template <int KC, int NZR, bool SHIFT>
 __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX,
                                                                    const double* __restrict__ meta, const StencilGeo g) {
   // a row's KC columns: LPR lanes x VPL double2, lane l owning double2 l + LPR v (each LDS.128 of a
   // quarter warp then reads 128 contiguous bytes of one row: no bank conflicts)
   constexpr int LPR = KC >= 16 ? 8 : KC / 2;
   constexpr int VPL = KC / (2 * LPR);
+  constexpr int NV = 2 * VPL;                 // columns per thread
   constexpr int RGP = ST_THREADS / LPR;       // rows per pass
+  constexpr int GPW = 32 / LPR;               // row groups per warp (lanes with equal l share columns)
   constexpr int REC = NZR + 1;
+  // alpha / g: every g.mrg slabs the 2 NV per-thread FP64 block sums [ba | bg] are combined over the
+  // warp's GPW row groups by a fixed xor butterfly on the lane bits 16, 8, .., LPR: the first SS stages
+  // reduce-scatter (each keeps half), the remaining RB stages reduce into the lower group; each thread
+  // then adds its NKEEP values into double-double accumulators (values NKEEP (gi >> RB) + j).
+  constexpr int LOG_GPW = GPW == 1 ? 0 : GPW == 2 ? 1 : GPW == 4 ? 2 : GPW == 8 ? 3 : 4;
+  constexpr int LOG_2NV = NV == 1 ? 1 : NV == 2 ? 2 : NV == 4 ? 3 : 4;
+  constexpr int SS = LOG_GPW < LOG_2NV ? LOG_GPW : LOG_2NV;
+  constexpr int RB = LOG_GPW - SS;
+  constexpr int NKEEP = (2 * NV) >> SS;
   extern __shared__ __align__(128) unsigned char st_smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(st_smem);           // full[slot]: box + records landed
   int* done = reinterpret_cast<int*>(st_smem + 64);                 // warps through iteration m (slot m % 4)
   unsigned char* slots = st_smem + 128;
   griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
-  const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR;
-  auto lane0 = [&]() { return (tid & 31) == 0; };
+  const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR, lane = tid & 31;
   const int K = ws.k, nq = g.nq;
   const int q = blockIdx.x % nq, b = blockIdx.x / nq, nb = gridDim.x / nq;
   const int64_t P = (int64_t)g.ntx * g.nty * g.nseg;   // pencil segments per column block
@@ -166,7 +177,7 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   bool more_c = item_begin(cons);
   bool more_p = item_begin(prod);
   int m_issued = 0;
-  if (lane0()) {
+  if (lane == 0) {
     for (int t = 0; t < 3 && more_p; ++t) {
       if (tid == 0) issue(prod, m_issued);
       ++m_issued;
@@ -176,13 +187,48 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   const double shift = ws.shift;
   const int RbKC = g.Rb * KC;
   const int nrow = g.L * g.R;
-  const int dly = RGP / g.R, dlx = RGP - dly * g.R;   // per-pass step of a thread's (ly, lx)
-  double ba[2 * VPL], bg[2 * VPL];
-  dd da[2 * VPL], dg[2 * VPL];
+  // per-thread constants of the tile walk: the first row (ly0, lx0) and the per-pass step (dly, dlx)
+  const int ly0 = grp / g.R, lx0 = grp - ly0 * g.R;
+  const int dly = RGP / g.R, dlx = RGP - dly * g.R;
+  const int64_t d2K = g.d2 * K, d3K = g.d3 * K;
+  const int d2i = (int)g.d2;
+  double ba[NV], bg[NV];
+  dd acc_dd[NKEEP];
 #pragma unroll
-  for (int u = 0; u < 2 * VPL; ++u) { ba[u] = bg[u] = 0.0; da[u] = dg[u] = dd{0.0, 0.0}; }
-  int nb8 = 0;
-  char* Wb = reinterpret_cast<char*>(ws.W);
+  for (int u = 0; u < NV; ++u) ba[u] = bg[u] = 0.0;
+#pragma unroll
+  for (int u = 0; u < NKEEP; ++u) acc_dd[u] = dd{0.0, 0.0};
+  auto merge = [&]() {
+    double v[2 * NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) { v[u] = ba[u]; v[NV + u] = bg[u]; ba[u] = bg[u] = 0.0; }
+#pragma unroll
+    for (int st = 0; st < LOG_GPW; ++st) {
+      const int m = 16 >> st;
+      const bool hi = (lane & m) != 0;
+      if (st < SS) {                       // reduce-scatter: keep half n of the values
+        const int n = (2 * NV) >> (st + 1);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (j < n) {
+            const double keep = hi ? v[n + j] : v[j], send = hi ? v[j] : v[n + j];
+            const double other = __shfl_xor_sync(0xffffffffu, send, m);
+            v[j] = hi ? __dadd_rn(other, keep) : __dadd_rn(keep, other);   // the lower group's value first
+          }
+        }
+      } else {                             // reduce into the lower group
+#pragma unroll
+        for (int j = 0; j < NKEEP; ++j) {
+          const double other = __shfl_xor_sync(0xffffffffu, v[j], m);
+          v[j] = hi ? 0.0 : __dadd_rn(v[j], other);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NKEEP; ++j) dd_add1(acc_dd[j], v[j]);
+  };
+  int mrg = 0;
+  double* const W = ws.W;
   if (more_c) mbar_wait(&mbar[0], 0);
   for (int m = 0; more_c; ++m) {
     const int nxt = m + 1;                     // every thread waits each load once, in order
@@ -194,27 +240,24 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
       const double* Xp = reinterpret_cast<const double*>(slots + (size_t)((m + 1) % ST_SLOTS) * g.slot_bytes);
       const double* rec0 = reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(X0) + g.box_bytes);
       const int x0 = cons.tx * g.R, y0 = cons.ty * g.L;
-      const int64_t zbase = (int64_t)cons.z * g.d3;
-      // this thread's rows rr = grp + j RGP as (ly, lx), advanced without divisions
-      int ly = grp / g.R, lx = grp - ly * g.R;
+      const int xlim = g.nx - x0, ylim = g.ny - y0;   // rows of the tile inside the grid: lx < xlim, ly < ylim
+      // W at (x0, y0, z), this thread's columns
+      double* const wz = W + ((int64_t)cons.z * d3K + (int64_t)y0 * d2K + (int64_t)x0 * K + q * KC + 2 * l);
+      int ly = ly0, lx = lx0;
       for (int rr = grp; rr < nrow; rr += RGP) {
-        const int x = x0 + lx, y = y0 + ly;
         const int cly = ly, clx = lx;
         lx += dlx; ly += dly;
         if (lx >= g.R) { lx -= g.R; ++ly; }
-        if (x >= g.nx || y >= g.ny) continue;
+        if (clx >= xlim || cly >= ylim) continue;
         const double2* rv = reinterpret_cast<const double2*>(rec0 + rr * REC);
         double vv[REC];
 #pragma unroll
         for (int u = 0; u < REC / 2; ++u) { const double2 t = rv[u]; vv[2 * u] = t.x; vv[2 * u + 1] = t.y; }
         const uint64_t code = (uint64_t)__double_as_longlong(vv[NZR]);
         const int ctr = ((cly + g.hy) * g.Rb + clx + 1) * KC + 2 * l;
-        double2 xi[VPL];
+        double acc[NV];
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) xi[v] = *reinterpret_cast<const double2*>(X0 + ctr + 2 * LPR * v);
-        double acc[2 * VPL];
-#pragma unroll
-        for (int u = 0; u < 2 * VPL; ++u) acc[u] = 0.0;
+        for (int u = 0; u < NV; ++u) acc[u] = 0.0;
         auto nz = [&](double val, const double* p) {   // acc += val * (this lane's part of row p)
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
@@ -223,13 +266,23 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
             acc[2 * v + 1] = __fma_rn(val, t.y, acc[2 * v + 1]);
           }
         };
+        const double* xc = X0 + ctr;
+        double2 xi[VPL];         // this row's own x (the diagonal nonzero's operand, and alpha / g)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) xi[v] = *reinterpret_cast<const double2*>(xc + 2 * LPR * v);
+        auto nzc = [&](double val) {   // acc += val * x_i (registers)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            acc[2 * v] = __fma_rn(val, xi[v].x, acc[2 * v]);
+            acc[2 * v + 1] = __fma_rn(val, xi[v].y, acc[2 * v + 1]);
+          }
+        };
         if (code & ST_CANON) {   // the fma chain in CSR (= ascending column) order, offsets fixed
-          const double* xc = X0 + ctr;
           if constexpr (NZR == 7) {
-            nz(vv[0], Xm + ctr); nz(vv[1], xc - RbKC); nz(vv[2], xc - KC); nz(vv[3], xc);
+            nz(vv[0], Xm + ctr); nz(vv[1], xc - RbKC); nz(vv[2], xc - KC); nzc(vv[3]);
             nz(vv[4], xc + KC); nz(vv[5], xc + RbKC); nz(vv[6], Xp + ctr);
           } else {
-            nz(vv[0], Xm + ctr); nz(vv[1], xc - KC); nz(vv[2], xc); nz(vv[3], xc + KC); nz(vv[4], Xp + ctr);
+            nz(vv[0], Xm + ctr); nz(vv[1], xc - KC); nzc(vv[2]); nz(vv[3], xc + KC); nz(vv[4], Xp + ctr);
           }
         } else {                 // boundary rows: the coded neighbours, CSR order
           const int len = (int)(code >> 56);
@@ -240,56 +293,50 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
             nz(rec0[rr * REC + u], base + ctr + o);
           }
         }
-        const int64_t i = zbase + (int64_t)y * g.d2 + x;
-        char* wrow = Wb + ((uint64_t)i * K + q * KC + 2 * l) * 8u;
+        double* wrow = wz + (cly * d2i + clx) * K;   // (d3 K < 2^31: checked at setup)
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
           double w0 = acc[2 * v], w1 = acc[2 * v + 1];
-          if (shift != 0.0) { w0 = __fma_rn(-shift, xi[v].x, w0); w1 = __fma_rn(-shift, xi[v].y, w1); }
-          __stcs(reinterpret_cast<double2*>(wrow + 16 * LPR * v), make_double2(w0, w1));
+          if constexpr (SHIFT) { w0 = __fma_rn(-shift, xi[v].x, w0); w1 = __fma_rn(-shift, xi[v].y, w1); }
+          __stcs(reinterpret_cast<double2*>(wrow + 2 * LPR * v), make_double2(w0, w1));
           ba[2 * v] = __fma_rn(xi[v].x, xi[v].x, ba[2 * v]);
           ba[2 * v + 1] = __fma_rn(xi[v].y, xi[v].y, ba[2 * v + 1]);
           bg[2 * v] = __fma_rn(xi[v].x, w0, bg[2 * v]);
           bg[2 * v + 1] = __fma_rn(xi[v].y, w1, bg[2 * v + 1]);
         }
-        if (++nb8 == 8) {   // 8-row FP64 blocks merged into double-double
-          nb8 = 0;
-#pragma unroll
-          for (int u = 0; u < 2 * VPL; ++u) { dd_add1(da[u], ba[u]); dd_add1(dg[u], bg[u]); ba[u] = bg[u] = 0.0; }
-        }
       }
+      if (++mrg == g.mrg) { mrg = 0; merge(); }   // (warp-uniform: every thread walks the same slabs)
     }
     __syncwarp();                              // this warp's reads of iteration m are done
-    if (lane0()) {
-      __threadfence_block();
-      const int old = atomicAdd(&done[m % ST_SLOTS], 1);   // (monotonic: ST_WARPS arrivals per use)
-      if (old % ST_WARPS == ST_WARPS - 1) {    // last warp through iteration m: slot of load m - 1 is free
-        __threadfence_block();
-        if (more_p) issue(prod, m_issued);
-      }
+    if (lane == 0) {
+      // (monotonic: ST_WARPS arrivals per use) last warp through iteration m: slot of load m - 1 is free
+      if (stage_release_last(&done[m % ST_SLOTS], ST_WARPS) && more_p) issue(prod, m_issued);
       if (more_p) { ++m_issued; more_p = advance(prod); }
     }
     more_c = advance(cons);
   }
-#pragma unroll
-  for (int u = 0; u < 2 * VPL; ++u) { dd_add1(da[u], ba[u]); dd_add1(dg[u], bg[u]); }
-  // fixed-order reduction over the RGP row groups, then this CTA's slot: thread (grp, l) holds
-  // columns 2 (l + LPR v) + {0, 1} of column block q
+  merge();
+  // fixed-order reduction over the warps, then this CTA's slot.  Thread (warp w, group gi, l) holds
+  // values NKEEP (gi >> RB) + j (j < NKEEP) of [ba | bg] for its columns: value t < NV is alpha of column
+  // u = t, else g of column u = t - NV; column u of lane l is 2 (l + LPR (u / 2)) + (u & 1).
   __syncthreads();
-  dd* red = reinterpret_cast<dd*>(slots);              // [4 VPL][ST_THREADS]
+  dd* red = reinterpret_cast<dd*>(slots);              // [ST_WARPS][2 NV][LPR]
+  {
+    const int gi = lane / LPR;
+    if ((gi & ((1 << RB) - 1)) == 0) {
 #pragma unroll
-  for (int u = 0; u < 2 * VPL; ++u) { red[u * ST_THREADS + tid] = da[u]; red[(2 * VPL + u) * ST_THREADS + tid] = dg[u]; }
-  __syncthreads();
-  for (int j = tid; j < KC; j += ST_THREADS) {
-    const int pair = j >> 1, e = j & 1, v = pair / LPR, lj = pair % LPR;
-    const int ua = 2 * v + e, ug = 2 * VPL + 2 * v + e;
-    dd ta = red[ua * ST_THREADS + lj], tg = red[ug * ST_THREADS + lj];
-    for (int gq = 1; gq < RGP; ++gq) {
-      dd_add(ta, red[ua * ST_THREADS + gq * LPR + lj]);
-      dd_add(tg, red[ug * ST_THREADS + gq * LPR + lj]);
+      for (int j = 0; j < NKEEP; ++j) red[((tid >> 5) * 2 * NV + NKEEP * (gi >> RB) + j) * LPR + l] = acc_dd[j];
     }
-    double* slot = ws.ag + ((int64_t)b * K + q * KC + j) * 4;
-    slot[0] = ta.hi; slot[1] = ta.lo; slot[2] = tg.hi; slot[3] = tg.lo;
+  }
+  __syncthreads();
+  for (int t = tid; t < 2 * NV * LPR; t += ST_THREADS) {
+    const int val = t / LPR, lj = t % LPR;
+    dd tot = red[val * LPR + lj];
+    for (int w = 1; w < ST_WARPS; ++w) dd_add(tot, red[(w * 2 * NV + val) * LPR + lj]);
+    const int u = val < NV ? val : val - NV;
+    const int j = 2 * (lj + LPR * (u / 2)) + (u & 1);   // column within the block
+    double* slot = ws.ag + ((int64_t)b * K + q * KC + j) * 4 + (val < NV ? 0 : 2);
+    slot[0] = tot.hi; slot[1] = tot.lo;
   }
 }
 
