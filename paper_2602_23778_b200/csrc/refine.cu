@@ -491,6 +491,8 @@ static cudaError_t stencil_setup(refine_ctx* c) {
   cudaMemsetAsync(c->st_meta, 0, meta_bytes, c->stream);
   if (g.nzr == 5) stencil_pack_kernel<5><<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, g, c->st_meta);
   else stencil_pack_kernel<7><<<c->sms * 8, 256, 0, c->stream>>>(c->rp, c->ci, c->val, g, c->st_meta);
+  if (g.nzr == 5) stencil_flag_kernel<5><<<c->sms * 4, 128, 0, c->stream>>>(g, c->st_meta);
+  else stencil_flag_kernel<7><<<c->sms * 4, 128, 0, c->stream>>>(g, c->st_meta);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   c->st_geo = g;
   c->st_grid = nb * g.nq;

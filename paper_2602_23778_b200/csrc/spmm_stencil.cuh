@@ -21,7 +21,8 @@
 // 8-row FP64 blocks merged into double-double accumulators (same class as the gather kernel), one
 // slot per CTA and column block, reduced in fixed order: deterministic.
 #pragma once
-#include <cuda.h>   // CUtensorMap (encoded on the host through the driver entry point)
+#include <cuda.h>
+#include <type_traits>   // CUtensorMap (encoded on the host through the driver entry point)
 
 #include "common.cuh"
 
@@ -35,6 +36,7 @@ constexpr int ST_WARPS = ST_THREADS / 32;
 // codes of a nonzero's column relative to its row (x fastest, then y, then z)
 enum : int { SC_SELF = 0, SC_XM, SC_XP, SC_YM, SC_YP, SC_ZM, SC_ZP };
 constexpr uint64_t ST_CANON = 1ull << 55;   // code-word flag: canonical full stencil row (fast path)
+constexpr uint64_t ST_SLAB_CANON = 1ull << 54;   // on record 0 of a slab block: every in-grid row canonical
 
 struct StencilGeo {
   int nx, ny, nz;         // grid; a 2-D grid is (nx, 1, ny)
@@ -76,6 +78,21 @@ __global__ void stencil_pack_kernel(const int32_t* __restrict__ rp, const int32_
     const uint64_t cmask = NZR == 7 ? 0xffffffffffffffull : 0xffffffffffull;
     if (p1 - p0 == NZR && (code & cmask) == canon) code |= ST_CANON;
     rec[NZR] = __longlong_as_double((long long)code);
+  }
+}
+
+// per slab block: ST_SLAB_CANON on record 0 if every in-grid row of the block is canonical (padding
+// rows of partial tiles have length 0 and are skipped by the kernel's bounds test)
+template <int NZR>
+__global__ void stencil_flag_kernel(StencilGeo g, double* __restrict__ meta) {
+  for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; blk < g.blocks; blk += (int64_t)gridDim.x * blockDim.x) {
+    double* rec = meta + blk * g.L * g.R * (NZR + 1);
+    bool all = true;
+    for (int r = 0; r < g.L * g.R; ++r) {
+      const uint64_t code = (uint64_t)__double_as_longlong(rec[r * (NZR + 1) + NZR]);
+      if ((code >> 56) != 0 && !(code & ST_CANON)) all = false;
+    }
+    if (all) rec[NZR] = __longlong_as_double((long long)((uint64_t)__double_as_longlong(rec[NZR]) | ST_SLAB_CANON));
   }
 }
 
@@ -243,6 +260,9 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
       const int xlim = g.nx - x0, ylim = g.ny - y0;   // rows of the tile inside the grid: lx < xlim, ly < ylim
       // W at (x0, y0, z), this thread's columns
       double* const wz = W + ((int64_t)cons.z * d3K + (int64_t)y0 * d2K + (int64_t)x0 * K + q * KC + 2 * l);
+      // rows of the slab; ALL: every in-grid row of this slab block is a canonical full stencil row
+      // (flag on record 0, set at init), so no row waits on its code word before its neighbour loads
+      auto rows = [&](auto all_canon) {
       int ly = ly0, lx = lx0;
       for (int rr = grp; rr < nrow; rr += RGP) {
         const int cly = ly, clx = lx;
@@ -253,7 +273,6 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
         double vv[REC];
 #pragma unroll
         for (int u = 0; u < REC / 2; ++u) { const double2 t = rv[u]; vv[2 * u] = t.x; vv[2 * u + 1] = t.y; }
-        const uint64_t code = (uint64_t)__double_as_longlong(vv[NZR]);
         const int ctr = ((cly + g.hy) * g.Rb + clx + 1) * KC + 2 * l;
         double acc[NV];
 #pragma unroll
@@ -277,6 +296,7 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
             acc[2 * v + 1] = __fma_rn(val, xi[v].y, acc[2 * v + 1]);
           }
         };
+        const uint64_t code = decltype(all_canon)::value ? ST_CANON : (uint64_t)__double_as_longlong(vv[NZR]);
         if (code & ST_CANON) {   // the fma chain in CSR (= ascending column) order, offsets fixed
           if constexpr (NZR == 7) {
             nz(vv[0], Xm + ctr); nz(vv[1], xc - RbKC); nz(vv[2], xc - KC); nzc(vv[3]);
@@ -305,6 +325,9 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
           bg[2 * v + 1] = __fma_rn(xi[v].y, w1, bg[2 * v + 1]);
         }
       }
+      };
+      if ((uint64_t)__double_as_longlong(rec0[NZR]) & ST_SLAB_CANON) rows(std::true_type{});
+      else rows(std::false_type{});
       if (++mrg == g.mrg) { mrg = 0; merge(); }   // (warp-uniform: every thread walks the same slabs)
     }
     __syncwarp();                              // this warp's reads of iteration m are done

@@ -47,7 +47,9 @@ def geometry(pkg, R):
 CASES = [((64, 61), (1.0, 1.37), 8), ((64, 61), (1.0, 1.37), 32), ((64, 61), (1.0, 1.37), 128),
          ((200, 7), (1.0, 1.37), 16), ((24, 22, 21), (1.0, 1.13, 1.29), 8), ((24, 22, 21), (1.0, 1.13, 1.29), 32),
          ((24, 22, 21), (1.0, 1.13, 1.29), 64), ((24, 22, 21), (1.0, 1.13, 1.29), 128),
-         ((37, 29, 11), (1.0, 1.13, 1.29), 48), ((17, 15, 13), (1.0, 1.13, 1.29), 16)]
+         ((37, 29, 11), (1.0, 1.13, 1.29), 48), ((17, 15, 13), (1.0, 1.13, 1.29), 16),
+         # tiles away from every x / y face: slab blocks whose rows are all canonical (the no-code-word path)
+         ((72, 40, 10), (1.0, 1.13, 1.29), 32), ((72, 40, 10), (1.0, 1.13, 1.29), 128), ((600, 9), (1.0, 1.37), 32)]
 
 
 @pytest.mark.parametrize("dims,coeffs,k", CASES)
