@@ -545,7 +545,11 @@ passB2_tma_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_c
     if (active) {
 #pragma unroll
       for (int kk = 0; kk < BR; kk += 4) {
-        const int row = kk + (lane & 3);
+        // the 4 k rows of this DMMA step: {8 (kk / 8) + (kk / 4) % 2 + 2 t}, t = lane & 3 -- rows whose
+        // r % 8 differ by 2, so with the 128-byte swizzle the 4 rows x 4 columns of a half-warp hit 8
+        // distinct 16-byte chunks (adjacent rows kk + t mapped 2 rows onto the same chunks: 2-way
+        // bank conflicts on every fragment load)
+        const int row = (kk & ~7) + ((kk >> 2) & 1) + 2 * (lane & 3);
         double a[C::MI], bv[C::NI];
 #pragma unroll
         for (int i = 0; i < C::MI; ++i)
@@ -686,7 +690,11 @@ passB2_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_co
     if (active) {
 #pragma unroll
       for (int kk = 0; kk < BR; kk += 4) {
-        const int row = kk + (lane & 3);
+        // the 4 k rows of this DMMA step: {8 (kk / 8) + (kk / 4) % 2 + 2 t}, t = lane & 3 -- rows whose
+        // r % 8 differ by 2, so with the 128-byte swizzle the 4 rows x 4 columns of a half-warp hit 8
+        // distinct 16-byte chunks (adjacent rows kk + t mapped 2 rows onto the same chunks: 2-way
+        // bank conflicts on every fragment load)
+        const int row = (kk & ~7) + ((kk >> 2) & 1) + 2 * (lane & 3);
         double a[C::MI], bv[C::NI];
 #pragma unroll
         for (int i = 0; i < C::MI; ++i)
@@ -1007,12 +1015,17 @@ passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restri
     const unsigned char* xs = ring + s * C::STAGE;
 #pragma unroll 4
     for (int kk = 0; kk < KP; kk += 4) {
+      // the 4 k columns of this DMMA step: {2s, 2s + 1, 2s + 8, 2s + 9} of its 16-column box (s = (kk / 4) % 4),
+      // two 16-byte chunks 4 apart, so the 8 rows x 4 columns of a fragment load hit distinct chunks under
+      // the 128-byte swizzle (columns kk .. kk + 3 put rows r and r ^ 1 on the same chunks)
+      const int t = lane & 3;
+      const int kc = (kk & ~15) + 2 * ((kk >> 2) & 3) + (t & 1) + 8 * (t >> 1);
       double a[C::MI], b[C::NI];
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
-        a[i] = *reinterpret_cast<const double*>(xs + swz_off<BR>(wm * C::WTM + i * 8 + (lane >> 2), kk + (lane & 3)));
+        a[i] = *reinterpret_cast<const double*>(xs + swz_off<BR>(wm * C::WTM + i * 8 + (lane >> 2), kc));
 #pragma unroll
-      for (int jn = 0; jn < C::NI; ++jn) b[jn] = Cs[(kk + (lane & 3)) * C::LDC + wn * C::WTN + jn * 8 + (lane >> 2)];
+      for (int jn = 0; jn < C::NI; ++jn) b[jn] = Cs[kc * C::LDC + wn * C::WTN + jn * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
 #pragma unroll
