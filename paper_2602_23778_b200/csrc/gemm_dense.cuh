@@ -5,9 +5,11 @@
 // Shape: M = n_loc rows of A (row-major, lda), N = k (padded to NT), K = n.
 // A is streamed from HBM exactly once; X^ (n x k, 16 MiB at cfg3) stays L2-resident.
 // CTA tile BM x NT, K step BK, STAGES-deep cp.async pipeline; warps tile the CTA
-// output in WM x WN blocks of m8n8 DMMA fragments.  Split-K over gridDim.y makes
+// output in WM x WN blocks of m8n8 DMMA fragments.  Split-K over gridDim.x (row tiles over
+// gridDim.y, so a tile's splits are launched side by side and its fix-up overlaps later tiles) makes
 // 148 SMs busy at cfg3 (256 row tiles x 4 splits = 1024 CTAs, 2 resident per SM); the
-// split partials are summed in fixed order by w_finish (deterministic).
+// split partials are summed in fixed order by the last CTA of each row tile (fused_finish), or by
+// w_finish (deterministic either way).
 #pragma once
 #include <cuda.h>   // CUtensorMap
 
@@ -26,12 +28,114 @@ struct GemmCfg {
   static constexpr int MI = WM / 8, NI = WN / 8;
 };
 
+// Sum the S split partials of rows [rb, re) in fixed order s = 0..S-1, apply the shift
+// (w = fma(-shift, x, w)), write W, and write the double-double partials of
+// alpha_j = sum x_ij^2 and g_j = sum x_ij w_ij into alpha/g slot `slot` of Ws::ag.
+// NTH threads (tid < NTH) take NTH / k rows side by side; sa, sg: NTH doubles-doubles of scratch.
+// A fixed row range per slot and fixed orders everywhere: deterministic.
+template <int NTH>
+RF_DEV void tile_finish(const Ws& ws, const double* __restrict__ X, int nsplit, int64_t split_stride, int64_t rb,
+                        int64_t re, int slot, int tid, dd* sa, dd* sg) {
+  const int k = ws.k;
+  const int R = NTH / k;                     // rows processed in parallel (k <= NTH)
+  const int r = tid / k, j = tid % k;
+  dd a = {0.0, 0.0}, g = {0.0, 0.0};
+  if (r < R) {
+    // 4 rows per step with every load issued before the sums (the row order of the dd accumulation
+    // and the split order of each sum are unchanged: bit-identical to one row at a time)
+    for (int64_t i0 = rb + r; i0 < re; i0 += 4 * R) {
+      double w[4], x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * R;
+        const int64_t e = i * k + j;
+        const bool ok = i < re;
+        w[u] = ok ? (nsplit == 1 ? ws.W[e] : ws.Wpart[e]) : 0.0;
+        x[u] = ok ? X[e] : 0.0;
+      }
+      // splits 1.. in batches of 4: every load of a batch in flight before its (split-ordered) sums
+      // (4 x 4 values: the fused fix-up must stay within the GEMM main loop's register budget)
+      for (int s0 = 1; s0 < nsplit; s0 += 4) {
+        double p[4][4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * R;
+            p[b][u] = (s0 + b < nsplit && i < re) ? ws.Wpart[(s0 + b) * split_stride + i * k + j] : 0.0;
+          }
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (s0 + b < nsplit) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] = __dadd_rn(w[u], p[b][u]);
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * R;
+        if (i < re) {
+          double wv = w[u];
+          if (ws.shift != 0.0) wv = __fma_rn(-ws.shift, x[u], wv);
+          ws.W[i * k + j] = wv;
+          dd_add_prod(a, x[u], x[u]);
+          dd_add_prod(g, x[u], wv);
+        }
+      }
+    }
+  }
+  sa[tid] = a;
+  sg[tid] = g;
+}
+// second half of tile_finish, after a barrier over the NTH threads: the fixed-order sum over the R row groups
+template <int NTH>
+RF_DEV void tile_finish_slot(const Ws& ws, int slot, int tid, const dd* sa, const dd* sg) {
+  const int k = ws.k, R = NTH / k;
+  if (tid < k) {
+    dd ta = sa[tid], tg = sg[tid];
+    for (int q = 1; q < R; ++q) { dd_add(ta, sa[q * k + tid]); dd_add(tg, sg[q * k + tid]); }
+    double* sl = ws.ag + ((int64_t)slot * k + tid) * 4;
+    sl[0] = ta.hi; sl[1] = ta.lo; sl[2] = tg.hi; sl[3] = tg.lo;
+  }
+}
+// Split-K fix-up fused into the GEMM (FusedFinish::on): every CTA stores its partial tile, the LAST of
+// the nsplit CTAs of a row tile (a per-tile arrival counter; threadfence reduction) sums the partials
+// in split order and does w_finish's work for the tile's rows into alpha/g slot = the row tile, then
+// re-arms the counter.  Saves the w_finish launch and its second pass over the partials.
+struct FusedFinish {
+  Ws ws;                    // W, Wpart, shift, ag, k, n_loc
+  const double* X;          // the shift operand (the sweep's X^)
+  int* cnt;                 // per row-tile arrival counters (zero between launches)
+  int on;
+};
+// called by the NTH consumer threads after their partial-tile stores; bar(): a barrier over them
+template <int NTH, int BM, typename Bar>
+RF_DEV void fused_finish(const FusedFinish& f, int nsplit, int64_t split_stride, int64_t m0, int tid, void* scratch,
+                         int* s_flag, Bar bar) {
+  __threadfence();                                  // this CTA's partial stores -> visible device-wide
+  bar();
+  if (tid == 0) {
+    const int old = atomicAdd(&f.cnt[blockIdx.y], 1);
+    *s_flag = (old == nsplit - 1);
+    if (old == nsplit - 1) f.cnt[blockIdx.y] = 0;   // re-arm (every other split has arrived)
+  }
+  bar();
+  if (!*s_flag) return;
+  __threadfence();                                  // (acquire side of the counter)
+  dd* sa = reinterpret_cast<dd*>(scratch);
+  dd* sg = sa + NTH;
+  const int64_t re = (m0 + BM < f.ws.n_loc) ? m0 + BM : f.ws.n_loc;
+  tile_finish<NTH>(f.ws, f.X, nsplit, split_stride, m0, re, blockIdx.y, tid, sa, sg);
+  bar();
+  tile_finish_slot<NTH>(f.ws, blockIdx.y, tid, sa, sg);
+}
+
 // out[m][j] = sum_{l in [kb, ke)} A[m][l] X[l][j], m in [0, M), j in [0, k)
 template <int NT, int BM, int WM, int WN, int BK, int STAGES>
 __global__ void __launch_bounds__(GemmCfg<NT, BM, WM, WN, BK, STAGES>::THREADS)
 gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ X, int32_t k,
                int64_t M, int64_t K, int64_t kchunk, double* __restrict__ out, int64_t out_split_stride,
-               int a_vec16, int b_vec16, const int* __restrict__ status) {
+               int a_vec16, int b_vec16, const int* __restrict__ status, const FusedFinish fin) {
   using C = GemmCfg<NT, BM, WM, WN, BK, STAGES>;
   griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*status != ST_OK) return;
@@ -40,11 +144,11 @@ gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
   double* Bs = smem + STAGES * C::A_STAGE;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;   // row tile
+  const int64_t kb = (int64_t)blockIdx.x * kchunk;   // split
   const int64_t ke = (kb + kchunk < K) ? kb + kchunk : K;
   const int nk = (int)((ke - kb + BK - 1) / BK);
-  out += (int64_t)blockIdx.y * out_split_stride;
+  out += (int64_t)blockIdx.x * out_split_stride;
 
   // per-thread copy coordinates are the same for every stage: precompute them once
   constexpr int ACH16 = BM * BK / 2, BCH16 = BK * NT / 2;
@@ -148,6 +252,11 @@ gemm_ax_kernel(const double* __restrict__ A, int64_t lda, const double* __restri
       }
     }
   }
+  if (fin.on) {   // (the pipeline is drained: the stage buffers are free scratch)
+    __shared__ int s_last;
+    fused_finish<C::THREADS, BM>(fin, (int)gridDim.x, out_split_stride, m0, tid, smem, &s_last,
+                                 [] { __syncthreads(); });
+  }
 }
 
 // ---------------------------------------------------------------- TMA-fed variant (north_star "DMMA
@@ -168,7 +277,7 @@ template <int NT, int BM, int WM, int WN, int BK, int STAGES>
 __global__ void __launch_bounds__(GemmCfg<NT, BM, WM, WN, BK, STAGES>::THREADS + 32)
 gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int32_t k,
                    int64_t M, int64_t K, int64_t kchunk, double* __restrict__ out, int64_t out_split_stride,
-                   const int* __restrict__ status) {
+                   const int* __restrict__ status, const FusedFinish fin) {
   using C = GemmCfg<NT, BM, WM, WN, BK, STAGES>;
   using T = GemmTmaCfg<NT, BM, BK>;
   static_assert(BK % 16 == 0 && NT % 16 == 0, "16-double TMA boxes");
@@ -180,11 +289,11 @@ gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * T::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;   // row tile
+  const int64_t kb = (int64_t)blockIdx.x * kchunk;   // split
   const int64_t ke = (kb + kchunk < K) ? kb + kchunk : K;
   const int nk = (int)((ke - kb + BK - 1) / BK);
-  out += (int64_t)blockIdx.y * out_split_stride;
+  out += (int64_t)blockIdx.x * out_split_stride;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -264,72 +373,26 @@ gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       if (c < k) *reinterpret_cast<double2*>(out + r * k + c) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
   }
+  if (fin.on) {   // consumer warps only (the producer has returned); every stage has been consumed
+    __shared__ int s_last;
+    fused_finish<C::THREADS, BM>(fin, (int)gridDim.x, out_split_stride, m0, tid, ring, &s_last,
+                                 [] { asm volatile("bar.sync 1, %0;\n" ::"n"(C::THREADS) : "memory"); });
+  }
 }
 template <int NT, int BM, int BK, int STAGES>
 constexpr int gemm_tma_smem() { return STAGES * GemmTmaCfg<NT, BM, BK>::STAGE_BYTES + 1024 + 2 * STAGES * 8; }
 
-// Sum the S split partials in fixed order s = 0..S-1, apply the shift
-// (w = fma(-shift, x, w)), write W, and emit per-block double-double partials of
-// alpha_j = sum x_ij^2 and g_j = sum x_ij w_ij into Ws::ag.
-// Block b owns a fixed contiguous row range, so the result is deterministic.
 __global__ void __launch_bounds__(256) w_finish_kernel(Ws ws, const double* __restrict__ X, int nsplit,
                                                       int64_t split_stride) {
   __shared__ dd sa[256], sg[256];
   griddep_wait();   // (programmatic dependent launch: the predecessor's writes are visible after this)
   if (*ws.status != ST_OK) return;
-  const int k = ws.k;
-  const int R = 256 / k;                     // rows processed in parallel (k <= 128)
-  const int tid = threadIdx.x;
-  const int r = tid / k, j = tid % k;
   const int64_t rows_per = (ws.n_loc + gridDim.x - 1) / gridDim.x;
   const int64_t rb = (int64_t)blockIdx.x * rows_per;
   const int64_t re = (rb + rows_per < ws.n_loc) ? rb + rows_per : ws.n_loc;
-  dd a = {0.0, 0.0}, g = {0.0, 0.0};
-  if (r < R) {
-    // 4 rows per step with every load issued before the sums (the row order of the dd accumulation
-    // and the split order of each sum are unchanged: bit-identical to one row at a time)
-    for (int64_t i0 = rb + r; i0 < re; i0 += 4 * R) {
-      double w[4], x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + u * R;
-        const int64_t e = i * k + j;
-        const bool ok = i < re;
-        w[u] = ok ? (nsplit == 1 ? ws.W[e] : ws.Wpart[e]) : 0.0;
-        x[u] = ok ? X[e] : 0.0;
-      }
-      for (int s = 1; s < nsplit; ++s) {
-        double p[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t i = i0 + u * R;
-          p[u] = (i < re) ? ws.Wpart[s * split_stride + i * k + j] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = __dadd_rn(w[u], p[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t i = i0 + u * R;
-        if (i < re) {
-          double wv = w[u];
-          if (ws.shift != 0.0) wv = __fma_rn(-ws.shift, x[u], wv);
-          ws.W[i * k + j] = wv;
-          dd_add_prod(a, x[u], x[u]);
-          dd_add_prod(g, x[u], wv);
-        }
-      }
-    }
-  }
-  sa[tid] = a;
-  sg[tid] = g;
+  tile_finish<256>(ws, X, nsplit, split_stride, rb, re, blockIdx.x, threadIdx.x, sa, sg);
   __syncthreads();
-  if (tid < k) {
-    dd ta = sa[tid], tg = sg[tid];
-    for (int q = 1; q < R; ++q) { dd_add(ta, sa[q * k + tid]); dd_add(tg, sg[q * k + tid]); }
-    double* slot = ws.ag + ((int64_t)blockIdx.x * k + tid) * 4;
-    slot[0] = ta.hi; slot[1] = ta.lo; slot[2] = tg.hi; slot[3] = tg.lo;
-  }
+  tile_finish_slot<256>(ws, blockIdx.x, threadIdx.x, sa, sg);
 }
 
 }  // namespace rf

@@ -223,6 +223,8 @@ struct refine_ctx {
   int gemm_gx = 0;
   int n_ag = 0, w_fin_grid = 0, spmm_grid = 0;
   int n_ag_cur = 0;             // alpha/g slots written by this sweep's S1 kernel (kxk_rq reduces them)
+  bool wfuse = false;           // dense S1: split-K fix-up / shift / alpha-g in the GEMM (fused_finish), no w_finish
+  int* gemm_cnt = nullptr;      // its per-row-tile arrival counters (in the pool)
   int s1_only = -1;             // opts.square at world > 1: phase 0 runs only product 0 / 1 (an exchange between)
   double* Tfull = nullptr;      // loopback, dense, opts.square: the gathered T = A X of all emulated ranks
   // stencil SpMM (spmm_stencil.cuh): geometry, packed row records (owned), X tensor map cache
@@ -759,23 +761,33 @@ struct Kern {
             }
             if (last) c->mark();
             w_finish_kernel<<<c->w_fin_grid, 256, 0, s>>>(wp, X, c->oz_ns, c->n_loc * c->k);
+            c->n_ag_cur = c->w_fin_grid;
             n += 4;
           } else if (!c->csr) {
             const double* Xb = c->multi ? c->Xfull : Xg;           // B operand: all n rows
             const bool bv16 = xv16 && ((uintptr_t)Xb % 16 == 0);
             const bool av16 = (c->n % 2 == 0) && (c->lda % 2 == 0) && ((uintptr_t)c->A % 16 == 0) && (c->kchunk % 2 == 0);
             double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
+            // split-K fix-up + shift + alpha/g partials in the GEMM's last CTA per row tile (fused_finish),
+            // else by w_finish
+            const FusedFinish fin{wp, X, c->gemm_cnt, c->wfuse ? 1 : 0};
             if (pass == 0) c->mark();
             if (TMA_OK && c->gemm_tma && bv16 && gemm_x_map(c, Xb))
-              launch_k(c->pdl, gemm_tma, dim3(c->gemm_gx, c->nsplit), dim3(TGC::THREADS + 32), T_SMEM, s,
-                       c->tm_A, c->tm_X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, ws.status);
+              launch_k(c->pdl, gemm_tma, dim3(c->nsplit, c->gemm_gx), dim3(TGC::THREADS + 32), T_SMEM, s,
+                       c->tm_A, c->tm_X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, ws.status, fin);
             else
-              launch_k(c->pdl, gemm, dim3(c->gemm_gx, c->nsplit), dim3(GC::THREADS), GC::SMEM, s, c->A, c->lda, Xb,
-                       c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status);
+              launch_k(c->pdl, gemm, dim3(c->nsplit, c->gemm_gx), dim3(GC::THREADS), GC::SMEM, s, c->A, c->lda, Xb,
+                       c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status, fin);
             if (last) c->mark();
-            launch_k(c->pdl, w_finish_kernel, dim3(c->w_fin_grid), dim3(256), 0, s, wp, (const double*)X, c->nsplit,
-                     c->n_loc * c->k);
-            n += 2;
+            if (c->wfuse) {
+              c->n_ag_cur = c->gemm_gx;
+              n += 1;
+            } else {
+              c->n_ag_cur = c->w_fin_grid;
+              launch_k(c->pdl, w_finish_kernel, dim3(c->w_fin_grid), dim3(256), 0, s, wp, (const double*)X, c->nsplit,
+                       c->n_loc * c->k);
+              n += 2;
+            }
           } else {
             if (pass == 0) c->mark();
             const bool vec = xv16 && (c->k & (c->k - 1)) == 0 && c->k >= 2 &&
@@ -1142,7 +1154,12 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   c->spmm_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms * 8, (c->n_loc + 7) / 8));
   if (c->csr) RF_CK(c, gather_setup(c));
   if (c->csr) RF_CK(c, stencil_setup(c));
-  c->n_ag = c->csr ? std::max(c->spmm_grid, c->st_on ? c->st_grid / c->st_geo.nq : 0) : c->w_fin_grid;
+  // fused split-K fix-up: the last CTA of a row tile reads its nsplit partials, so only for a few splits
+  // (measured: cfg1 (4 splits) 43.9 -> 43.0 us, cfg3 (4) 4.28 -> 4.27 ms, cfg2 (28 splits) 78 -> 84 us)
+  const char* wf = getenv("REFINE_WFUSE");
+  c->wfuse = !c->csr && c->oz_ns == 0 && (wf ? wf[0] != '0' : c->nsplit <= 8);
+  c->n_ag = c->csr ? std::max(c->spmm_grid, c->st_on ? c->st_grid / c->st_geo.nq : 0)
+                   : std::max(c->w_fin_grid, c->wfuse ? c->gemm_gx : 0);
   c->n_ag_cur = c->n_ag;
   const size_t nk = (size_t)c->n_loc * k, kk = (size_t)k * k, P = (size_t)world;
   const int nsplit_max = std::max(c->nsplit, c->oz_ns);
@@ -1157,7 +1174,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
                oScr = take(KXK_SCRATCH_MATS * kk + KXK_SCRATCH_EXTRA), oRows = take((size_t)c->n_loc), oRun = take(8),
                oAgS = take(4 * k), oAgA = take(P * 4 * k), oMgA = take(c->multi ? P * (2 * kk + k) : 0),
                oNrS = take(k), oNrA = take(P * k), oCol = take(2), oZd = take(k), oGate = take(1),
-               oBd = take(c->opts.mixed ? (size_t)c->sms * 2 * c->kp : 0);
+               oBd = take(c->opts.mixed ? (size_t)c->sms * 2 * c->kp : 0), oCnt = take(c->wfuse ? (size_t)c->gemm_gx : 0);
   const size_t bytes = off * 8 + 64;
   RF_CK(c, cudaMalloc(&c->pool, bytes));
   c->pool_bytes = bytes;
@@ -1179,6 +1196,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
   ws.ag_send = b + oAgS; ws.ag_all = b + oAgA; ws.mg_all = c->multi ? b + oMgA : nullptr;
   ws.nrm_send = b + oNrS; ws.nrm_all = b + oNrA;
   ws.zerod = b + oZd; ws.top_zero = 0;   // (the pool is zeroed below)
+  c->gemm_cnt = c->wfuse ? reinterpret_cast<int*>(b + oCnt) : nullptr;   // (zeroed with the pool)
   ws.gate = reinterpret_cast<int*>(b + oGate);
   ws.want_gram = c->opts.reorth_tol > 0.0 ? 1 : 0;
   ws.normalize = c->opts.normalize ? 1 : 0;
@@ -1856,7 +1874,7 @@ extern "C" int32_t refine_kernels_per_sweep(const refine_ctx* c) {
     for (auto* kid : c->kids) n += refine_kernels_per_sweep(kid);
     return n;
   }
-  const int per = (c->csr ? 7 : 8) + (c->oz_ns > 0 ? 2 : 0);   // incl. kxk_lu (side stream); emul S1: X slicing
+  const int per = ((c->csr || c->wfuse) ? 7 : 8) + (c->oz_ns > 0 ? 2 : 0);   // incl. kxk_lu (side stream); emul S1: X slicing; w_finish unless fused
   if (!c->multi) return per;
   return per + 1 - (c->rank == 0 ? 0 : 2);   // + ag_local; kxk_lu / kxk_finish on rank 0 only
 }

@@ -121,3 +121,25 @@ def test_csr_empty_rows(pkg, k):
     ref = oracle.sweep(op, xin)
     assert s == pkg.REFINE_OK and ref.status == oracle.OK
     assert rel(X.cpu().numpy(), ref.X) <= TOL
+
+
+@pytest.mark.parametrize("n,k,shift", [(256, 4, 0.0), (1000, 16, 0.0), (3001, 64, 0.75), (777, 13, 0.0)])
+def test_fused_split_k_finish_matches_w_finish(pkg, n, k, shift, monkeypatch):
+    """Dense S1's split-K fix-up fused into the GEMM (the last CTA of a row tile sums the partials,
+    applies the shift and writes the alpha/g slot; REFINE_WFUSE=1) against the separate w_finish kernel
+    (REFINE_WFUSE=0): W bit-identical (same split order), X~ equal to rounding, both at oracle parity."""
+    p = synth.small_dense(n, k, m=8, seed=n, signs=True)
+    op = oracle.Operator(A=p.A.numpy(), shift=shift)
+    outs = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("REFINE_WFUSE", fuse)
+        R = pkg.Refiner.dense(p.A.cuda(), k, shift=shift)
+        X = p.X0.cuda().clone()
+        xin = X.cpu().numpy()
+        s, st = R.refine_sweep(X, stats=True)
+        assert s == pkg.REFINE_OK
+        outs[fuse] = (R.debug(pkg.DBG_W).cpu().numpy(), X.cpu().numpy())
+        ref = oracle.sweep(op, xin)
+        assert rel(X.cpu().numpy(), ref.X) <= TOL, fuse
+    assert np.array_equal(outs["1"][0], outs["0"][0])
+    assert rel(outs["1"][1], outs["0"][1]) <= 1e-13

@@ -30,12 +30,12 @@ void run(const char* name, const double* A, const double* X, double* out, int64_
     const int ns = (int)((n + kchunk - 1) / kchunk);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
-    kern<<<dim3(gx, ns), C::THREADS, C::SMEM>>>(A, n, X, k, n, n, kchunk, out, n * k, 1, 1, status);
+    kern<<<dim3(ns, gx), C::THREADS, C::SMEM>>>(A, n, X, k, n, n, kchunk, out, n * k, 1, 1, status, rf::FusedFinish{});
     CK(cudaDeviceSynchronize());
     cudaEventRecord(e0);
     const int reps = 5;
     for (int r = 0; r < reps; ++r)
-      kern<<<dim3(gx, ns), C::THREADS, C::SMEM>>>(A, n, X, k, n, n, kchunk, out, n * k, 1, 1, status);
+      kern<<<dim3(ns, gx), C::THREADS, C::SMEM>>>(A, n, X, k, n, n, kchunk, out, n * k, 1, 1, status, rf::FusedFinish{});
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);

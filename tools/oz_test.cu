@@ -43,9 +43,9 @@ int main(int argc, char** argv) {
   const int64_t kchunk = (n / ns + 31) / 32 * 32;
   cudaMalloc(&W1, ns * n * k * 8); cudaMalloc(&W2, ns * n * k * 8);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  g<<<dim3((n + 127) / 128, ns), GC::THREADS, GC::SMEM>>>(A, n, X, k, n, n, kchunk, W1, n * k, 1, 1, st);
+  g<<<dim3(ns, (n + 127) / 128), GC::THREADS, GC::SMEM>>>(A, n, X, k, n, n, kchunk, W1, n * k, 1, 1, st, rf::FusedFinish{});
   cudaEventRecord(a);
-  g<<<dim3((n + 127) / 128, ns), GC::THREADS, GC::SMEM>>>(A, n, X, k, n, n, kchunk, W1, n * k, 1, 1, st);
+  g<<<dim3(ns, (n + 127) / 128), GC::THREADS, GC::SMEM>>>(A, n, X, k, n, n, kchunk, W1, n * k, 1, 1, st, rf::FusedFinish{});
   cudaEventRecord(b); cudaEventSynchronize(b);
   float ms1; cudaEventElapsedTime(&ms1, a, b);
   // init slicing
