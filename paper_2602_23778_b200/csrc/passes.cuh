@@ -637,12 +637,25 @@ passB2_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, const __grid_co
   const int64_t rows = ws.n_loc - ws.top;
   const int64_t per = ((rows + nchunk - 1) / nchunk + 31) / 32 * 32;   // (passB2's chunking; a multiple of BR)
   const int64_t rb = ws.top + cidx * per;
-  const int64_t re = (rb + span * per < ws.n_loc) ? rb + span * per : ws.n_loc;
-  const int nit = (re > rb) ? (int)((re - rb + BR - 1) / BR) : 0;
+  // stages of each of the unit's chunks (a two-chunk X0 unit interleaves them: stage s of chunk a, then
+  // stage s of chunk b, so it reads the X^ rows its two chunks' other units read at the same time and
+  // they stay in L2 for them -- reading chunk a then chunk b ran it twice as fast through each chunk as
+  // its siblings, so its X^ rows came from DRAM twice)
+  auto chunk_stages = [&](int64_t c0) -> int {
+    const int64_t e = (c0 + per < ws.n_loc) ? c0 + per : ws.n_loc;
+    return (e > c0) ? (int)((e - c0 + BR - 1) / BR) : 0;
+  };
+  const int nit_a = chunk_stages(rb), nit_b = (span == 2) ? chunk_stages(rb + per) : 0;
+  const int nit = nit_a + nit_b, nmin = nit_a < nit_b ? nit_a : nit_b;
+  auto stage_row = [&](int it) -> int64_t {
+    if (span == 1) return rb + (int64_t)it * BR;
+    if (it < 2 * nmin) return rb + (it & 1) * per + (int64_t)(it >> 1) * BR;
+    return rb + (nit_a > nit_b ? 0 : per) + (int64_t)(nmin + it - 2 * nmin) * BR;
+  };
   auto issue = [&](int it) {
     const int s = it % ST;
     unsigned char* st = ring + s * C::STAGE;
-    const int r0 = (int)(rb + (int64_t)it * BR);
+    const int r0 = (int)stage_row(it);
     mbar_expect_tx(&full[s], (C::XBOXES + (rtile ? C::WBOXES : 0)) * C::BOX);
 #pragma unroll
     for (int b = 0; b < C::XBOXES; ++b) tma_load_2d(st + b * C::BOX, &tmX, 16 * b, r0, &full[s]);

@@ -432,10 +432,11 @@ static cudaError_t stencil_setup(refine_ctx* c) {
     return cudaSuccess;
   }
   if (g.nx < 2 || g.nz < 1 || g.d3 * (int64_t)k >= INT32_MAX) return cudaSuccess;   // (32-bit in-plane W offsets)
-  // default: 3-D grids with k >= 64, where it measured faster than the gather kernel (cfg5: 2.24 vs
-  // 2.31 ms); 2-D grids at k = 32 measured slower (cfg4: 0.159-0.169 vs 0.147 ms).  REFINE_SPMM=stencil
-  // forces it wherever the structure allows (tests).
-  if (!force && !(g.hy && k >= 64)) return cudaSuccess;
+  // default: 3-D grids with k >= 64 (cfg5: 1.91 vs 2.31 ms for the gather kernel) and 2-D grids with
+  // k a multiple of 32 (cfg4: 0.123 vs 0.148 ms, once a CTA owns whole 128-point line segments at one
+  // CTA per SM and the slabs are split evenly -- 64-point segments at two CTAs per SM measured 0.173 ms).
+  // REFINE_SPMM=stencil forces it wherever the structure allows (tests).
+  if (!force && !(g.hy ? k >= 64 : k % 32 == 0)) return cudaSuccess;
   int* dflag = nullptr;
   if ((e = cudaMalloc(&dflag, 2 * sizeof(int))) != cudaSuccess) return e;
   cudaMemsetAsync(dflag, 0, 2 * sizeof(int), c->stream);
@@ -453,8 +454,9 @@ static cudaError_t stencil_setup(refine_ctx* c) {
   g.KC = KC;
   g.nq = k / KC;
   // tile: maximise the staged-row reuse L R / ((L + 2 hy)(R + 2)) times the tile utilisation,
-  // 4 slots within the shared-memory budget (3-D: one CTA per SM; 2-D: two)
-  const int occ = g.hy ? 1 : 2;
+  // 4 slots within the shared-memory budget of one CTA per SM (two per SM, i.e. half-size tiles and one
+  // row per thread per slab, measured 40 % slower on the 2-D cfg4: the per-slab overhead dominates)
+  const int occ = getenv("REFINE_ST_OCC") ? atoi(getenv("REFINE_ST_OCC")) : 1;
   const int budget = (occ == 1 ? 220 : 110) * 1024 - 128;
   const int Ls3[] = {1, 2, 4, 5, 8, 10, 16}, Rs[] = {8, 16, 20, 24, 32, 40, 48, 64, 96, 128, 192};
   double best = -1.0;
@@ -483,10 +485,12 @@ static cudaError_t stencil_setup(refine_ctx* c) {
   g.zlen = (g.nz + nseg - 1) / nseg;
   g.nseg = (g.nz + g.zlen - 1) / g.zlen;
   g.blocks = (int64_t)g.ntx * g.nty * g.nz;
-  {  // alpha / g FP64 blocks of at most 8 rows per thread (rows per thread per slab: L R / rows per pass)
+  {  // alpha / g FP64 blocks of at most 32 rows per thread (rows per thread per slab: L R / rows per pass),
+     // then double-double: 8 / 16 / 32 rows measured 1.930 / 1.913 / 1.906 ms at cfg5 (the merge shuffles);
+     // a block's same-sign x_ij^2 (or x_ij w_ij ~ d_j x_ij^2) terms carry <= 31 u / 2 of its own sum
     const int rgp = ST_THREADS / (KC >= 16 ? 8 : KC / 2);
     const int rpt = (g.L * g.R + rgp - 1) / rgp;
-    g.mrg = std::max(1, 8 / rpt);
+    g.mrg = std::max(1, (getenv("REFINE_ST_ROWS") ? atoi(getenv("REFINE_ST_ROWS")) : 32) / rpt);
   }
   const size_t meta_bytes = (size_t)g.blocks * g.meta_bytes;
   if ((e = cudaMalloc(&c->st_meta, meta_bytes)) != cudaSuccess) return e;

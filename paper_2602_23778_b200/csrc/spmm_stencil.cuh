@@ -148,28 +148,46 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   const int tid = threadIdx.x, grp = tid / LPR, l = tid % LPR, lane = tid & 31;
   const int K = ws.k, nq = g.nq;
   const int q = blockIdx.x % nq, b = blockIdx.x / nq, nb = gridDim.x / nq;
-  const int64_t P = (int64_t)g.ntx * g.nty * g.nseg;   // pencil segments per column block
+  // Work split (per column block, nb CTAs): R = pencils / nb full rounds -- round j gives CTA b the whole
+  // z extent of pencil b + nb j, so neighbouring CTAs sweep neighbouring pencils in step and share their x /
+  // y halo boxes in L2 -- then the pencils mod nb remaining pencils as nb equal contiguous ranges of slabs
+  // (pencil-major), so every CTA computes the same number of slabs (+-1).  (Fixed z segments dealt
+  // round-robin left 4 CTAs with a 12th segment while 32 had 11 at cfg5: 7 % of the kernel idle.)
+  const int64_t PEN = (int64_t)g.ntx * g.nty;
+  const int64_t NR = PEN / nb;
+  const int64_t Sr = (PEN - NR * nb) * g.nz, rs0 = Sr * b / nb, rs1 = Sr * (b + 1) / nb;
   if (tid == 0) {
     for (int s = 0; s < ST_SLOTS; ++s) { mbar_init(&mbar[s], 1); done[s] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  // the CTA's load sequence: items it = b, b + nb, ... ; item -> (tx, ty, seg); loads z = zs-1 .. ze
+  // the CTA's load sequence: items it = 0, 1, .. -> (pencil, z range [zs, ze)); loads z = zs - 1 .. ze
   struct Cur { int64_t it; int z, zs, ze, tx, ty; };
+  auto item_exists = [&](int64_t it) -> bool {
+    return it < NR || (rs0 < rs1 && (rs0 / g.nz + (it - NR)) * g.nz < rs1);
+  };
   auto item_begin = [&](Cur& c) -> bool {
-    if (c.it >= P) return false;
-    c.tx = (int)(c.it % g.ntx);
-    c.ty = (int)((c.it / g.ntx) % g.nty);
-    const int seg = (int)(c.it / ((int64_t)g.ntx * g.nty));
-    c.zs = seg * g.zlen;
-    c.ze = min(g.nz, c.zs + g.zlen);
+    if (!item_exists(c.it)) return false;
+    int64_t p;
+    if (c.it < NR) {
+      p = b + nb * c.it;
+      c.zs = 0;
+      c.ze = g.nz;
+    } else {
+      const int64_t t = rs0 / g.nz + (c.it - NR), base = t * g.nz;
+      p = NR * nb + t;
+      c.zs = (int)(rs0 > base ? rs0 - base : 0);
+      c.ze = (int)(rs1 - base < g.nz ? rs1 - base : g.nz);
+    }
+    c.tx = (int)(p % g.ntx);
+    c.ty = (int)(p / g.ntx);
     c.z = c.zs - 1;
     return true;
   };
   auto advance = [&](Cur& c) -> bool {   // next load; false when the sequence ends
     if (++c.z <= c.ze) return true;
-    c.it += nb;
+    ++c.it;
     return item_begin(c);
   };
   auto issue = [&](const Cur& c, int m) {   // one lane 0: load m of the sequence into slot m % 4
@@ -190,7 +208,7 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   // No CTA-wide barrier per slab: the slot of load m - 1 (read as X+ / X0 / X- by iterations m - 2 .. m)
   // is refilled with load m + 3 by the LAST warp to finish iteration m (a shared counter per slot);
   // every lane 0 tracks the load sequence so whichever warp is last can issue.
-  Cur cons{b, 0, 0, 0, 0, 0}, prod{b, 0, 0, 0, 0, 0};
+  Cur cons{0, 0, 0, 0, 0, 0}, prod{0, 0, 0, 0, 0, 0};
   bool more_c = item_begin(cons);
   bool more_p = item_begin(prod);
   int m_issued = 0;
@@ -249,7 +267,7 @@ __global__ void __launch_bounds__(ST_BLOCK, 1) spmm_stencil_kernel(Ws ws, const 
   if (more_c) mbar_wait(&mbar[0], 0);
   for (int m = 0; more_c; ++m) {
     const int nxt = m + 1;                     // every thread waits each load once, in order
-    const bool has_next = !(cons.z == cons.ze && cons.it + nb >= P);
+    const bool has_next = !(cons.z == cons.ze && !item_exists(cons.it + 1));
     if (has_next) mbar_wait(&mbar[nxt % ST_SLOTS], (nxt / ST_SLOTS) & 1);
     if (cons.z >= cons.zs && cons.z < cons.ze) {   // compute the outputs of slab z
       const double* X0 = reinterpret_cast<const double*>(slots + (size_t)(m % ST_SLOTS) * g.slot_bytes);

@@ -44,7 +44,8 @@ CASES = [("cfg2 (TMA GEMM k=16, one-CTA k x k)", "cfg2", {}, 150),
          ("mixed 2000x64 (tcgen05 passes)", ("dense", 2000, 64), {"mixed": 2}, 40),
          ("emul 2000x64 (INT8 S1)", ("dense", 2000, 64), {"emul": True}, 40),
          ("csr 3-D k=128 (TMA stencil SpMM)", ("lap", (40, 33, 17), 128), {}, 40),
-         ("csr 2-D k=32 (gather SpMM)", ("lap", (100, 91), 32), {}, 60)]
+         ("csr 2-D k=32 (TMA stencil SpMM, line segments)", ("lap", (100, 91), 32), {}, 60),
+         ("csr 2-D k=16 (gather SpMM)", ("lap", (100, 91), 16), {}, 60)]
 
 
 @pytest.mark.parametrize("what,spec,opts,reps", CASES, ids=[c[0] for c in CASES])

@@ -307,8 +307,10 @@ def test_repeat_bitwise_k128(pkg):
 # ------------------------------------------------------------------------------ CSR gather kernel
 
 @pytest.mark.parametrize("k", [2, 4, 8, 16, 64])
-def test_csr_gather_every_k(pkg, k):
-    """spmm_gather_kernel instantiations (k a power of two): bit-identical W, one-step parity."""
+def test_csr_gather_every_k(pkg, k, monkeypatch):
+    """spmm_gather_kernel instantiations (k a power of two): bit-identical W, one-step parity.
+    (REFINE_SPMM=gather: 2-D grids with k a multiple of 32 take the stencil kernel by default.)"""
+    monkeypatch.setenv("REFINE_SPMM", "gather")
     p = synth.small_laplacian((41, 37), (1.0, 1.37), k)
     R = refiner(pkg, p)
     op = op_of(p)

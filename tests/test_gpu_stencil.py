@@ -139,14 +139,17 @@ def test_non_stencil_matrix_takes_gather_kernel(pkg):
 
 
 def test_stencil_default_policy_fullsize(pkg, monkeypatch):
-    """Default policy at full size: cfg5 (3-D, k = 128) takes the stencil SpMM, cfg4 (2-D, k = 32) the
-    gather kernel (their parity runs in test_gpu_fullsize)."""
+    """Default policy at full size: cfg5 (3-D, k = 128) and cfg4 (2-D, k = 32) take the stencil SpMM
+    (their parity runs in test_gpu_fullsize), with one CTA per SM and 128-point line segments on the
+    2-D grid."""
     monkeypatch.delenv("REFINE_SPMM")
-    for name, want in (("cfg4", 0.0), ("cfg5", 1.0)):
+    for name, want in (("cfg4", 1.0), ("cfg5", 1.0)):
         p = synth.make_config(name, device="cuda")
         R = pkg.Refiner.csr(p.row_ptr, p.col_idx, p.val, p.n, p.k)
         geo = geometry(pkg, R)
         print(name, "S1 geometry [stencil, R, L, nq, grid, nx, ny, nz, gatherR]", geo.tolist())
         assert geo[0] == want
+        if name == "cfg4":
+            assert geo[1] == 128 and geo[2] == 1
         del R, p
         torch.cuda.empty_cache()
