@@ -32,7 +32,8 @@ namespace rf {
 
 constexpr int KXK_THREADS = 1024;
 __device__ long long* g_gemm_tlog = nullptr;   // optional phase log of one cta_gemm call (timing builds)
-__device__ long long* g_fullk_tlog = nullptr;  // ... and of one cta_gemm_fullk call
+__device__ long long* g_fullk_tlog = nullptr;  // ... and of the first two cta_gemm_fullk calls
+__device__ long long* g_fullk_tlog_first = nullptr;
 constexpr int PANEL = 32;
 constexpr int LDA_P = PANEL + 4;                  // As[i][p]: A-fragment reads (8 rows x 4) conflict-free
 constexpr int LDB_P = KMAX + 8;                   // Bs[p][j]: B-fragment reads (4 rows x 8) conflict-free
@@ -261,7 +262,7 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
   }
   if (fl && tid == 0) fl[2] = clock64();
   __syncthreads();
-  if (fl && tid == 0) { fl[3] = clock64(); g_fullk_tlog = nullptr; }
+  if (fl && tid == 0) { fl[3] = clock64(); g_fullk_tlog = (fl == g_fullk_tlog_first) ? fl + 4 : nullptr; }   // log the first two calls
 }
 
 // Inverse of a k x k triangular matrix S (ld k) into R (ld k).  upper: S upper triangular;
@@ -643,7 +644,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   if (tid == 0) s_hits = 0;
   if (crank == 0) RF_TSTAMP(ws, 20);
   if (ws.tlog && tid == 0 && crank == 0) g_gemm_tlog = ws.tlog + 40;
-  if (ws.tlog && tid == 0 && crank == 0) g_fullk_tlog = ws.tlog + 56;
+  if (ws.tlog && tid == 0 && crank == 0) g_fullk_tlog = g_fullk_tlog_first = ws.tlog + 56;
   if (ws.multi) {   // [M2 | G2 | rr2] of every rank, summed in rank order (M2, G2, rr2 are contiguous)
     const int64_t cnt = 2 * kk + k;
     for (int64_t e = crank * nt + tid; e < cnt; e += (int64_t)ncl * nt) {
