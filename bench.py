@@ -304,9 +304,16 @@ def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak, n_loc=None):
         t_f, t_b = fl / (fp64_peak * 1e12), by / (hbm_peak * 1e9)
         if t_f >= t_b:
             ach = fl / t / 1e12
-            return {"kernel": top, "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "frac": ach / fp64_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
-                    "per_launch_alg": f"{fl:.4g} flop", "peak_source": "DMMA FP64 microbenchmark"}
+            r = {"kernel": top, "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                 "frac": ach / fp64_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
+                 "per_launch_alg": f"{fl:.4g} flop", "peak_source": "DMMA FP64 microbenchmark"}
+            if top == "passB" and k == 128:
+                # Table 1 credits 4 n k^2 (M and G in full); passB2_pp_kernel issues M (2 n k^2) plus 20 of
+                # G's 32 warp tiles of 32 x 16 (those on or above its diagonal): 3.25 n k^2 executed
+                ex = 3.25 * rows * k * k
+                r["frac_executed"] = ex / t / 1e12 / fp64_peak
+                r["executed_flop"] = f"{ex:.4g} flop (M + the G warp tiles on / above the diagonal)"
+            return r
         ach = by / t / 1e9
         return {"kernel": top, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "traffic": traffic, "share_of_step": kern[top] / ms_step,
@@ -319,6 +326,18 @@ def roofline_for(p, kern, ms_step, fp64_peak, hbm_peak, n_loc=None):
                 "per_launch_alg": f"A + X + W = {by:.4g} bytes", "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     return {"kernel": top, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
             "traffic": traffic, "share_of_step": kern[top] / ms_step}
+
+
+def s1_roofline(p, kern):
+    """S1 (W = A X^) of a CSR config against HBM: algorithmic bytes A (values + column indices + row
+    pointers) + X^ read + W written, over the kernel's CUDA-event time (north_star: >= 70 %)."""
+    if p.kind != "csr" or "spmm_csr" not in kern:
+        return None
+    hbm, src, _ = peaks()
+    by = 12.0 * p.nnz + 4.0 * (p.n + 1) + 16.0 * p.n * p.k
+    ach = by / (kern["spmm_csr"] * 1e-3) / 1e9
+    return {"kernel": "spmm_csr", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "per_launch_alg": f"A + X + W = {by:.4g} bytes", "peak_source": src}
 
 
 def cpu_baseline(name, budget_s=25.0, one_core=True):
@@ -428,6 +447,8 @@ def main():
             "kernels_ms": kern,
             "roofline": roofline_for(p, kern, ms_prof or ms_max, fp64, hbm, n_loc=partition(p.n, world, rank)[1] - partition(p.n, world, rank)[0]),
             "gpu_launches": R.kernels_per_sweep() * args.steps}
+    if p.kind == "csr" and world == 1:
+        line["s1_roofline"] = s1_roofline(p, kern)
     if world == 1:
         mx = time_mixed(p, local, max(3, args.steps // 2))
         if mx:
@@ -458,6 +479,7 @@ def main():
             per[name] = {"sweeps_s": 1000.0 / qms, "ms_per_sweep": qms, "ms_per_sweep_instrumented": qprof,
                          "rayleigh_ritz_ms": qrr,
                          "kernels_ms": qk, "roofline": roofline_for(q, qk, qprof or qms, fp64, hbm),
+                         "s1_roofline": s1_roofline(q, qk),
                          "frac_of_sweep_roofline": max(qf / (fp64 * 1e12), qb / (hbm * 1e9)) / (qms * 1e-3)}
             del QR, QX
             torch.cuda.empty_cache()
