@@ -208,6 +208,7 @@ struct Ws {
   int32_t normalize; // opts.normalize: kxk_finish folds 1/||x~_j|| into the top rows, Csig and scal
   int32_t kxk_h;     // 1: kxk_lu precomputes H1..H4 (scratch + 16 k^2 ..) for the clustered kxk_finish
   double* bdiag;     // tcgen05 pass B: FP64 partials of diag(X_2^T R_2), diag(X_2^T X_2) (n_chunk x 2 kp)
+  int32_t fk_nobulk; // 1: kxk_finish's products stage with cp.async instead of bulk copies (REFINE_FK_BULK=0)
 };
 
 // X row of global index col: local rows first, else the halo (CSR row partition)

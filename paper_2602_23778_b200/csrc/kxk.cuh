@@ -164,6 +164,10 @@ __device__ __forceinline__ void cta_gemm(int M, int N, int K, double alpha, cons
 // cp.async copies (one L2 round trip per product instead of one per 32-deep panel).  Warp w owns
 // output tiles w and w + 32.  Starts and ends with a barrier.
 constexpr int FK_SMEM = 32 * (KMAX + 4) + KMAX * (KMAX + 8);   // doubles
+// bulk-copy staging of cta_gemm_fullk: an mbarrier and its phase, set up by kxk_finish_body (g_fk_bulk)
+__shared__ uint64_t g_fk_mbar;
+__shared__ uint32_t g_fk_phase;
+__shared__ int g_fk_bulk;
 __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, const double* A, int lda, bool ta,
                                             const double* B, int ldb, double beta, const double* C0, int ldc0,
                                             double* C, int ldc, double* sm) {
@@ -175,9 +179,37 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
   double* Bs = sm + Mp * lda_s;         // [Kp][ldb_s]  Bs[p][j] = B(p, j)
   long long* fl = g_fullk_tlog;
   if (fl && tid == 0) fl[0] = clock64();
+  const uint32_t par = g_fk_phase & 1;   // (before the barrier: thread 0 advances the phase after it)
   __syncthreads();
   const bool v16 = ((K | N | M | lda | ldb) & 1) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
-  if (__isGlobal(A) && __isGlobal(B) && v16) {
+  if (g_fk_bulk && __isGlobal(A) && __isGlobal(B) && v16) {
+    // one 1-D bulk copy (cp.async.bulk, the TMA engine) per row of B and of A (A not transposed), all
+    // completing on one mbarrier: ~160 row copies instead of ~9,000 16-byte cp.async per product
+    // (measured 3.4 - 6 us of staging per k = 128 product with cp.async)
+    if (tid == 0) mbar_expect_tx(&g_fk_mbar, (uint32_t)(K * N * 8 + (ta ? 0 : M * K * 8)));
+    if (tid < K || (!ta && tid < K + M)) {
+      asm volatile("fence.proxy.async;\n" ::: "memory");   // generic writes (this cluster's, acquired) -> async reads
+      if (tid < K) bulk_g2s(Bs + tid * ldb_s, B + (size_t)tid * ldb, (uint32_t)(N * 8), &g_fk_mbar);
+      else bulk_g2s(As + (tid - K) * lda_s, A + (size_t)(tid - K) * lda, (uint32_t)(K * 8), &g_fk_mbar);
+    }
+    if (ta)
+      for (int e = tid; e < M * K; e += KXK_THREADS) {
+        const int p = e / M, i = e - p * M;
+        cp_async8(As + i * lda_s + p, A + (size_t)p * lda + i, true);
+      }
+    for (int e = tid; e < Mp * (Kp - K) + (Mp - M) * Kp; e += KXK_THREADS) {
+      if (e < Mp * (Kp - K)) As[(e / (Kp - K)) * lda_s + K + e % (Kp - K)] = 0.0;
+      else { const int f = e - Mp * (Kp - K); As[(M + f / Kp) * lda_s + f % Kp] = 0.0; }
+    }
+    for (int e = tid; e < (Kp - K) * Np + K * (Np - N); e += KXK_THREADS) {
+      if (e < (Kp - K) * Np) Bs[(K + e / Np) * ldb_s + e % Np] = 0.0;
+      else { const int f = e - (Kp - K) * Np; Bs[(f / (Np - N)) * ldb_s + N + f % (Np - N)] = 0.0; }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    mbar_wait(&g_fk_mbar, par);
+    if (tid == 0) ++g_fk_phase;   // (every thread read it before the entry barrier)
+  } else if (__isGlobal(A) && __isGlobal(B) && v16) {
     // 16-byte copies, (row, column-pair) walked without divisions (one per thread up front): the
     // 8-byte / division form cost ~10 us per k = 128 product, mostly issue
     {   // B: K rows x N / 2 pairs
@@ -575,8 +607,13 @@ RF_DEV void cluster_sync() {
   }
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__host__ __device__ constexpr int kxk_cluster(int k) { return k >= 64 ? 8 : (k >= 32 ? 4 : 1); }
-constexpr int KXK_SCRATCH_MATS = 24;    // k x k scratch matrices: kxk_finish 0..15, H1..H4 16..19, kxk_lu temps 20..22
+// CTAs of kxk_finish's cluster: 16 (a non-portable cluster size) for k > 64, where the products are DMMA-
+// throughput bound on 8 SMs (k = 128: 4.7 us per product of 16 x 128 x 128 per CTA); rows per CTA stay a
+// multiple of 8, so k <= 64 gains nothing from more than 8
+__host__ __device__ constexpr int kxk_cluster(int k, bool allow16 = true) {
+  return k > 64 ? (allow16 ? 16 : 8) : (k >= 64 ? 8 : (k >= 32 ? 4 : 1));
+}
+constexpr int KXK_SCRATCH_MATS = 26;    // k x k scratch matrices: kxk_finish 0..15, H1..H4 16..19, kxk_lu temps 20..22, column partials 24..25
 constexpr int KXK_SCRATCH_EXTRA = 64;   // doubles after them (cluster partials)
 
 // Small k (k <= KXK_SMALL): the whole k x k chain in ONE CTA with every k x k operand resident in
@@ -622,7 +659,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   const double* Tm = SMALL ? S + 17 * kk : ws.T;
   double* E11 = SMALL ? S + 18 * kk : ws.E11;
   double* Xt1 = SMALL ? S + 19 * kk : ws.Xt;
-  double* part = SMALL ? sm + kxk_small_smem_doubles(k) - 64 : S + KXK_SCRATCH_MATS * kk;   // [0, 8): delta hits, [8, 16): gram max
+  double* part = SMALL ? sm + kxk_small_smem_doubles(k) - 64 : S + KXK_SCRATCH_MATS * kk;   // [0, 16): delta hits, [16, 32): gram max
   const bool useH = !SMALL && ws.kxk_h;                // the precomputed H1..H4 of kxk_lu (scratch + 16 k^2)
   const double* H = S + 16 * kk;
   double* cs_base = SMALL ? S + KXK_SMALL_MATS * kk : sm;   // column-sum partials (after the matrices when SMALL)
@@ -641,7 +678,16 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       cta_gemm_fullk(nr, k, k, alpha, ta ? A + r0 : A + r0 * k, k, ta, Bm, k, beta, C0 ? C0 + r0 * k : nullptr, k,
                      C + r0 * k, k, sm);
   };
-  if (tid == 0) s_hits = 0;
+  if (tid == 0) {
+    s_hits = 0;
+    g_fk_bulk = !SMALL && !ws.fk_nobulk && k > 64;   // (k = 64: cp.async staging measured faster, 60.8 vs 65.4 us)
+    g_fk_phase = 0;
+    if (!SMALL) {
+      mbar_init(&g_fk_mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+  }
+  if (!SMALL) __syncthreads();
   if (crank == 0) RF_TSTAMP(ws, 20);
   if (ws.tlog && tid == 0 && crank == 0) g_gemm_tlog = ws.tlog + 40;
   if (ws.tlog && tid == 0 && crank == 0) g_fullk_tlog = g_fullk_tlog_first = ws.tlog + 56;
@@ -788,20 +834,50 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
     __syncthreads();
     if (tid == 0) {
       for (int w = 1; w < nt / 32; ++w) m = fmax(m, s_red[0][w]);
-      part[8 + crank] = m;
+      part[16 + crank] = m;
+    }
+  }
+  constexpr int NQ = 7;
+  // clustered: each CTA sums the NQ per-column quantities over its own rows (fixed row order) into its
+  // slot of csp [ncl][NQ][k]; CTA 0 combines the slots in CTA order below (was: CTA 0 alone over all k
+  // rows, 7.7 us at k = 128)
+  double* csp = S + (KXK_SCRATCH_MATS - 2) * kk;       // 2 k^2 >= NQ ncl k for the cluster sizes used
+  if (!SMALL) {
+    double* qs = sm;                                   // [NQ][nr][k] (the product staging space is free)
+    for (int e = tid; e < nr * k; e += nt) {
+      const int r = e / k, j = e - r * k, ee = (r0 + r) * k + j;
+      const double dj = d[j];
+      const double x = Xt1[ee], rv = R1[ee], ev = E11[ee], pt = Pt[ee], c = Cp[ee];
+      double* q = qs + (size_t)r * k + j;
+      const size_t st = (size_t)nr * k;
+      q[0] = x * x;                                    // ||x~_1j||^2 (top rows)
+      q[st] = rv * rv;                                 // ||R_1j||^2
+      q[2 * st] = ev * ev;                             // ||E_11 j||^2
+      q[3 * st] = pt * Mp[ee];                         // (P~^T M')_jj
+      q[4 * st] = pt * GPt[ee];                        // (P~^T G' P~)_jj
+      q[5 * st] = c * fma(dj, Gp[ee], Mp[ee]);         // sum_l C'_lj (M'_lj + d_j G'_lj)
+      q[6 * st] = c * GC[ee];                          // (C'^T G' C')_jj
+    }
+    __syncthreads();
+    for (int t = tid; t < NQ * k; t += nt) {
+      const int u = t / k, j = t - u * k;
+      double a = 0.0;
+      for (int r = 0; r < nr; ++r) a += qs[((size_t)u * nr + r) * k + j];
+      csp[((size_t)crank * NQ + u) * k + j] = a;
     }
   }
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 30);
   if (crank == 0) {
-    // per-column sums over the k rows, by all 1024 threads: thread (g, j) takes rows l = g, g + NG, ..
-    // (fixed partition, groups combined in order -- deterministic)
-    constexpr int NQ = 7;
-    const int NG = min(8, k);                          // row groups (a short combine chain)
-    double* cs = cs_base;                              // [NG][NQ][k] partials (cta_gemm's panel space)
-    double* sd = cs_base + (size_t)NG * NQ * k;        // d
+    // SMALL: per-column sums over the k rows, by all 1024 threads: thread (g, j) takes rows l = g, g + NG, ..
+    // (fixed partition, groups combined in order -- deterministic); clustered: the CTAs' slots
+    const int NG = SMALL ? min(8, k) : ncl;            // partial groups (SMALL: a short combine chain)
+    double* cs = cs_base;                              // [NG][NQ][k] partials (clustered: the slots, copied in)
+    double* sd = cs_base + (size_t)(SMALL ? 8 : ncl) * NQ * k;   // d
     for (int j = tid; j < k; j += nt) sd[j] = d[j];
-    if (tid < NG * k) {
+    if (!SMALL)   // one L2 round trip for all slots (combining straight from global cost ~7 us at k = 128)
+      for (int e = tid; e < ncl * NQ * k; e += nt) cs[e] = csp[e];
+    if (SMALL && tid < NG * k) {
       const int g = tid / k, j = tid % k;
       const double dj = d[j];
       double q[NQ] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -820,6 +896,15 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       for (int u = 0; u < NQ; ++u) cs[((size_t)g * NQ + u) * k + j] = q[u];
     }
     __syncthreads();
+    {   // min_j |d_j - d_i| over i != j: 8 lanes per column, each over every 8th i, then a min over the lanes
+      const int j = tid >> 3, sl = tid & 7;
+      double mg = INFINITY;
+      if (j < k)
+        for (int i = sl; i < k; i += 8)
+          if (i != j) mg = fmin(mg, fabs(sd[j] - sd[i]));
+      for (int o = 1; o < 8; o <<= 1) mg = fmin(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+      if (j < k && sl == 0) s_red[2][j] = mg;
+    }
     RF_TSTAMP(ws, 33);
     if (tid < k) {
       const int j = tid;
@@ -834,10 +919,6 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       const double e2 = (rr2p[j] - 2.0 * q[3] + q[4]) / (d[j] * d[j]);
       s_red[0][j] = q[1] + rr2p[j];
       s_red[1][j] = (ws.kjudge > 0 && j >= ws.kjudge) ? 0.0 : q[2] + e2;   // K > k: judge the leading kjudge
-      double mg = INFINITY;
-      for (int i = 0; i < k; ++i)
-        if (i != j) mg = fmin(mg, fabs(sd[j] - sd[i]));
-      s_red[2][j] = mg;
       s_red[3][j] = (sig[j] < 0.0) ? 1.0 : 0.0;
       // column norm of X~: top rows + the identity above -> 1 / ||x~_j||
       const double dj = sd[j];
@@ -851,13 +932,21 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
     }
     __syncthreads();
     RF_TSTAMP(ws, 34);
-    if (tid == 0) {
+    if (tid < 32) {   // warp 0: lane sums over j = lane, lane + 32, .., then a xor butterfly (every lane equal)
       double rr = 0.0, en = 0.0, mg = INFINITY, fl = 0.0, hits = 0.0, gmax = -1.0;
-      for (int j = 0; j < k; ++j) { rr += s_red[0][j]; en += s_red[1][j]; mg = fmin(mg, s_red[2][j]); fl += s_red[3][j]; }
+      for (int j = tid; j < k; j += 32) { rr += s_red[0][j]; en += s_red[1][j]; mg = fmin(mg, s_red[2][j]); fl += s_red[3][j]; }
+      for (int o = 16; o > 0; o >>= 1) {
+        rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        en += __shfl_xor_sync(0xffffffffu, en, o);
+        mg = fmin(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+        fl += __shfl_xor_sync(0xffffffffu, fl, o);
+      }
+      if (tid == 0)
       for (int c = 0; c < ncl; ++c) {
         hits += part[c];
-        if (ws.want_gram) gmax = fmax(gmax, part[8 + c]);
+        if (ws.want_gram) gmax = fmax(gmax, part[16 + c]);
       }
+      if (tid == 0) {
       ws.stats[0] = sqrt(rr) / ws.normA;
       ws.stats[1] = sqrt(fmax(en, 0.0));
       ws.stats[2] = (k > 1) ? mg : 0.0;
@@ -865,6 +954,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       ws.stats[4] = (fl > 0.0) ? 1.0 : 0.0;
       ws.stats[5] = rr;
       ws.stats[6] = ws.want_gram ? gmax : -1.0;
+      }
     }
   }
   cluster_sync();

@@ -573,23 +573,50 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
   }
 }
 
-// kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs
+// kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs (16 for k > 64 when the device can
+// schedule a non-portable 16-CTA cluster of this kernel: checked once; REFINE_KXK_CL16=0 keeps 8)
+static bool kxk_allow16() {
+  static int ok = -1;
+  if (ok < 0) {
+    ok = 0;
+    const char* e = getenv("REFINE_KXK_CL16");
+    if (!(e && e[0] == '0') &&
+        cudaFuncSetAttribute(kxk_finish_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16, 1, 1);
+      cfg.blockDim = dim3(KXK_THREADS, 1, 1);
+      cfg.dynamicSmemBytes = FK_SMEM * 8;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kxk_finish_kernel<false>, &cfg) == cudaSuccess && nc >= 1) ok = 1;
+    }
+    cudaGetLastError();
+  }
+  return ok == 1;
+}
 static cudaError_t launch_kxk_finish(const Ws& ws, double* X, cudaStream_t s, bool pdl) {
   static const bool no_small = getenv("REFINE_KXK_SMALL") && getenv("REFINE_KXK_SMALL")[0] == '0';
   if (ws.k <= KXK_SMALL && !no_small)   // one CTA, everything in shared memory
     return launch_k(pdl, kxk_finish_kernel<true>, dim3(1), dim3(KXK_THREADS), kxk_small_smem_doubles(ws.k) * 8, s, ws,
                     X, (const double*)ws.W);
-  if (kxk_cluster(ws.k) == 1)   // (a plain launch is an implicit 1-CTA cluster)
+  const int ncl = kxk_cluster(ws.k, kxk_allow16());
+  if (ncl == 1)   // (a plain launch is an implicit 1-CTA cluster)
     return launch_k(pdl, kxk_finish_kernel<false>, dim3(1), dim3(KXK_THREADS), FK_SMEM * 8, s, ws, X,
                     (const double*)ws.W);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kxk_cluster(ws.k), 1, 1);
+  cfg.gridDim = dim3(ncl, 1, 1);
   cfg.blockDim = dim3(KXK_THREADS, 1, 1);
   cfg.dynamicSmemBytes = FK_SMEM * 8;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kxk_cluster(ws.k);
+  at[0].val.clusterDim.x = ncl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1210,6 +1237,7 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
     ws.kxk_h = (!(he && he[0] == '0') && (k > KXK_SMALL || (sm_ && sm_[0] == '0'))) ? 1 : 0;
   }
   ws.bdiag = nullptr;
+  ws.fk_nobulk = (getenv("REFINE_FK_BULK") && getenv("REFINE_FK_BULK")[0] == '0') ? 1 : 0;
   c->bdiag = c->opts.mixed ? b + oBd : nullptr;
   c->run = reinterpret_cast<RunState*>(b + oRun);
   ws.tlog = nullptr;
