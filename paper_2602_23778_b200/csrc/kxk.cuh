@@ -168,48 +168,69 @@ constexpr int FK_SMEM = 32 * (KMAX + 4) + KMAX * (KMAX + 8);   // doubles
 __shared__ uint64_t g_fk_mbar;
 __shared__ uint32_t g_fk_phase;
 __shared__ int g_fk_bulk;
+// Dual form (A2 != nullptr): also C2 = alpha2 op(A2) B + beta2 C02 with the same B, staged once; the
+// 2 ntile output tiles are dealt over the warps (so a k = 128 row block of 8 rows keeps all 32 warps busy).
 __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, const double* A, int lda, bool ta,
                                             const double* B, int ldb, double beta, const double* C0, int ldc0,
-                                            double* C, int ldc, double* sm) {
+                                            double* C, int ldc, double* sm, const double* A2 = nullptr,
+                                            double alpha2 = 0.0, double beta2 = 0.0, const double* C02 = nullptr,
+                                            double* C2 = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, ntile = tm * tn;
+  const int nA = A2 ? 2 : 1;
   const int Mp = tm * 8, Np = tn * 8, Kp = (K + 3) & ~3;
   const int lda_s = Kp + 4, ldb_s = Np + 8;
-  double* As = sm;                      // [Mp][lda_s]  As[i][p] = op(A)(i, p)
-  double* Bs = sm + Mp * lda_s;         // [Kp][ldb_s]  Bs[p][j] = B(p, j)
+  double* As = sm;                      // [nA][Mp][lda_s]  As[a][i][p] = op(A_a)(i, p)
+  double* Bs = sm + nA * Mp * lda_s;    // [Kp][ldb_s]      Bs[p][j] = B(p, j)
   long long* fl = g_fullk_tlog;
   if (fl && tid == 0) fl[0] = clock64();
   const uint32_t par = g_fk_phase & 1;   // (before the barrier: thread 0 advances the phase after it)
   __syncthreads();
-  const bool v16 = ((K | N | M | lda | ldb) & 1) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
-  if (g_fk_bulk && __isGlobal(A) && __isGlobal(B) && v16) {
-    // one 1-D bulk copy (cp.async.bulk, the TMA engine) per row of B and of A (A not transposed), all
-    // completing on one mbarrier: ~160 row copies instead of ~9,000 16-byte cp.async per product
-    // (measured 3.4 - 6 us of staging per k = 128 product with cp.async)
-    if (tid == 0) mbar_expect_tx(&g_fk_mbar, (uint32_t)(K * N * 8 + (ta ? 0 : M * K * 8)));
-    if (tid < K || (!ta && tid < K + M)) {
-      asm volatile("fence.proxy.async;\n" ::: "memory");   // generic writes (this cluster's, acquired) -> async reads
-      if (tid < K) bulk_g2s(Bs + tid * ldb_s, B + (size_t)tid * ldb, (uint32_t)(N * 8), &g_fk_mbar);
-      else bulk_g2s(As + (tid - K) * lda_s, A + (size_t)(tid - K) * lda, (uint32_t)(K * 8), &g_fk_mbar);
-    }
-    if (ta)
-      for (int e = tid; e < M * K; e += KXK_THREADS) {
-        const int p = e / M, i = e - p * M;
-        cp_async8(As + i * lda_s + p, A + (size_t)p * lda + i, true);
+  const bool v16 = ((K | N | M | lda | ldb) & 1) == 0 && (((uintptr_t)A | (uintptr_t)B | (uintptr_t)(A2 ? A2 : A)) & 15) == 0;
+  const bool glob = __isGlobal(A) && __isGlobal(B) && (!A2 || __isGlobal(A2));
+  auto zero_pad = [&]() {   // K, M, N are multiples of 8 on the clustered path except a ragged k: pad explicitly
+    for (int a = 0; a < nA; ++a) {
+      double* Aa = As + a * Mp * lda_s;
+      for (int e = tid; e < Mp * (Kp - K) + (Mp - M) * Kp; e += KXK_THREADS) {
+        if (e < Mp * (Kp - K)) Aa[(e / (Kp - K)) * lda_s + K + e % (Kp - K)] = 0.0;
+        else { const int f = e - Mp * (Kp - K); Aa[(M + f / Kp) * lda_s + f % Kp] = 0.0; }
       }
-    for (int e = tid; e < Mp * (Kp - K) + (Mp - M) * Kp; e += KXK_THREADS) {
-      if (e < Mp * (Kp - K)) As[(e / (Kp - K)) * lda_s + K + e % (Kp - K)] = 0.0;
-      else { const int f = e - Mp * (Kp - K); As[(M + f / Kp) * lda_s + f % Kp] = 0.0; }
     }
     for (int e = tid; e < (Kp - K) * Np + K * (Np - N); e += KXK_THREADS) {
       if (e < (Kp - K) * Np) Bs[(K + e / Np) * ldb_s + e % Np] = 0.0;
       else { const int f = e - (Kp - K) * Np; Bs[(f / (Np - N)) * ldb_s + N + f % (Np - N)] = 0.0; }
     }
+  };
+  auto stage_At = [&](const double* Aa, double* dst) {   // op(A)(i, p) = A[p][i]: element-wise transpose
+    for (int e = tid; e < M * K; e += KXK_THREADS) {
+      const int p = e / M, i = e - p * M;
+      cp_async8(dst + i * lda_s + p, Aa + (size_t)p * lda + i, true);
+    }
+  };
+  if (g_fk_bulk && glob && v16) {
+    // one 1-D bulk copy (cp.async.bulk, the TMA engine) per row of B and of A (A not transposed), all
+    // completing on one mbarrier: ~160 row copies instead of ~9,000 16-byte cp.async per product
+    // (measured 3.4 - 6 us of staging per k = 128 product with cp.async)
+    if (tid == 0) mbar_expect_tx(&g_fk_mbar, (uint32_t)(K * N * 8 + (ta ? 0 : nA * M * K * 8)));
+    if (tid < K || (!ta && tid < K + nA * M)) {
+      asm volatile("fence.proxy.async;\n" ::: "memory");   // generic writes (this cluster's, acquired) -> async reads
+      if (tid < K) {
+        bulk_g2s(Bs + tid * ldb_s, B + (size_t)tid * ldb, (uint32_t)(N * 8), &g_fk_mbar);
+      } else {
+        const int a = (tid - K) / M, i = (tid - K) - a * M;
+        bulk_g2s(As + (a * Mp + i) * lda_s, (a ? A2 : A) + (size_t)i * lda, (uint32_t)(K * 8), &g_fk_mbar);
+      }
+    }
+    if (ta) {
+      stage_At(A, As);
+      if (A2) stage_At(A2, As + Mp * lda_s);
+    }
+    zero_pad();
     cp_async_commit();
     cp_async_wait<0>();
     mbar_wait(&g_fk_mbar, par);
     if (tid == 0) ++g_fk_phase;   // (every thread read it before the entry barrier)
-  } else if (__isGlobal(A) && __isGlobal(B) && v16) {
+  } else if (glob && v16) {
     // 16-byte copies, (row, column-pair) walked without divisions (one per thread up front): the
     // 8-byte / division form cost ~10 us per k = 128 product, mostly issue
     {   // B: K rows x N / 2 pairs
@@ -222,51 +243,34 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
         if (j >= n2) { j -= n2; ++p; }
       }
     }
-    if (!ta) {   // op(A) = A: M rows x K / 2 pairs
-      const int k2 = K / 2;
-      int i = tid / k2, q = tid - i * k2;
-      const int di = KXK_THREADS / k2, dq = KXK_THREADS - di * k2;
-      for (int e = tid; e < M * k2; e += KXK_THREADS) {
-        cp_async16(As + i * lda_s + 2 * q, A + (size_t)i * lda + 2 * q, true);
-        i += di; q += dq;
-        if (q >= k2) { q -= k2; ++i; }
+    for (int a = 0; a < nA; ++a) {
+      const double* Aa = a ? A2 : A;
+      double* dst = As + a * Mp * lda_s;
+      if (!ta) {   // op(A) = A: M rows x K / 2 pairs
+        const int k2 = K / 2;
+        int i = tid / k2, q = tid - i * k2;
+        const int di = KXK_THREADS / k2, dq = KXK_THREADS - di * k2;
+        for (int e = tid; e < M * k2; e += KXK_THREADS) {
+          cp_async16(dst + i * lda_s + 2 * q, Aa + (size_t)i * lda + 2 * q, true);
+          i += di; q += dq;
+          if (q >= k2) { q -= k2; ++i; }
+        }
+      } else {
+        stage_At(Aa, dst);
       }
-    } else {     // op(A)(i, p) = A[p][i]: K rows of M contiguous entries, transposed element-wise
-      for (int e = tid; e < M * K; e += KXK_THREADS) {
-        const int p = e / M, i = e - p * M;
-        cp_async8(As + i * lda_s + p, A + (size_t)p * lda + i, true);
-      }
     }
-    // zero padding (K, M, N are multiples of 8 on the clustered path except a ragged k: pad explicitly)
-    for (int e = tid; e < Mp * (Kp - K) + (Mp - M) * Kp; e += KXK_THREADS) {
-      if (e < Mp * (Kp - K)) As[(e / (Kp - K)) * lda_s + K + e % (Kp - K)] = 0.0;
-      else { const int f = e - Mp * (Kp - K); As[(M + f / Kp) * lda_s + f % Kp] = 0.0; }
-    }
-    for (int e = tid; e < (Kp - K) * Np + K * (Np - N); e += KXK_THREADS) {
-      if (e < (Kp - K) * Np) Bs[(K + e / Np) * ldb_s + e % Np] = 0.0;
-      else { const int f = e - (Kp - K) * Np; Bs[(f / (Np - N)) * ldb_s + N + f % (Np - N)] = 0.0; }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-  } else if (__isGlobal(A) && __isGlobal(B)) {
-    for (int e = tid; e < Mp * Kp; e += KXK_THREADS) {
-      int i, p;
-      if (ta) { i = e % Mp; p = e / Mp; } else { p = e % Kp; i = e / Kp; }
-      const bool ok = p < K && i < M;
-      cp_async8(As + i * lda_s + p, ok ? (ta ? A + p * lda + i : A + i * lda + p) : A, ok);
-    }
-    for (int e = tid; e < Kp * Np; e += KXK_THREADS) {
-      const int j = e % Np, p = e / Np;
-      const bool ok = p < K && j < N;
-      cp_async8(Bs + p * ldb_s + j, ok ? B + p * ldb + j : B, ok);
-    }
+    zero_pad();
     cp_async_commit();
     cp_async_wait<0>();
   } else {
-    for (int e = tid; e < Mp * Kp; e += KXK_THREADS) {
-      int i, p;
-      if (ta) { i = e % Mp; p = e / Mp; } else { p = e % Kp; i = e / Kp; }
-      As[i * lda_s + p] = (p < K && i < M) ? (ta ? A[p * lda + i] : A[i * lda + p]) : 0.0;
+    for (int a = 0; a < nA; ++a) {
+      const double* Aa = a ? A2 : A;
+      double* dst = As + a * Mp * lda_s;
+      for (int e = tid; e < Mp * Kp; e += KXK_THREADS) {
+        int i, p;
+        if (ta) { i = e % Mp; p = e / Mp; } else { p = e % Kp; i = e / Kp; }
+        dst[i * lda_s + p] = (p < K && i < M) ? (ta ? Aa[p * lda + i] : Aa[i * lda + p]) : 0.0;
+      }
     }
     for (int e = tid; e < Kp * Np; e += KXK_THREADS) {
       const int j = e % Np, p = e / Np;
@@ -277,18 +281,22 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
   if (fl && tid == 0) fl[1] = clock64();
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    const int tile = warp + 32 * t;
-    if (tile < ntile) {
+    const int tt = warp + 32 * t;
+    if (tt < nA * ntile) {
+      const int a = tt >= ntile ? 1 : 0, tile = tt - a * ntile;
       const int i0 = (tile / tn) * 8, j0 = (tile % tn) * 8;
       double c0 = 0.0, c1 = 0.0;
-      const double* ap = As + (i0 + (lane >> 2)) * lda_s + (lane & 3);
+      const double* ap = As + (a * Mp + i0 + (lane >> 2)) * lda_s + (lane & 3);
       const double* bp = Bs + (lane & 3) * ldb_s + j0 + (lane >> 2);
 #pragma unroll 8
       for (int p = 0; p < Kp; p += 4) dmma(c0, c1, ap[p], bp[p * ldb_s]);
       const int i = i0 + (lane >> 2), j = j0 + 2 * (lane & 3);
+      const double al = a ? alpha2 : alpha, be = a ? beta2 : beta;
+      const double* Ci = a ? C02 : C0;
+      double* Co = a ? C2 : C;
       if (i < M) {
-        if (j < N) C[i * ldc + j] = (beta != 0.0) ? fma(beta, C0[i * ldc0 + j], alpha * c0) : alpha * c0;
-        if (j + 1 < N) C[i * ldc + j + 1] = (beta != 0.0) ? fma(beta, C0[i * ldc0 + j + 1], alpha * c1) : alpha * c1;
+        if (j < N) Co[i * ldc + j] = (be != 0.0) ? fma(be, Ci[i * ldc0 + j], al * c0) : al * c0;
+        if (j + 1 < N) Co[i * ldc + j + 1] = (be != 0.0) ? fma(be, Ci[i * ldc0 + j + 1], al * c1) : al * c1;
       }
     }
   }
@@ -678,6 +686,20 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       cta_gemm_fullk(nr, k, k, alpha, ta ? A + r0 : A + r0 * k, k, ta, Bm, k, beta, C0 ? C0 + r0 * k : nullptr, k,
                      C + r0 * k, k, sm);
   };
+  // two products with the same B (row blocks of C = alpha op(A) B + beta C0 and C2 = alpha2 op(A2) B + beta2 C02):
+  // B staged once for both, and twice the output tiles to spread over the warps
+  auto rgemm2 = [&](const double* Bm, bool ta, double alpha, const double* A, double beta, const double* C0, double* C,
+                    double alpha2, const double* A2, double beta2, const double* C02, double* C2) {
+    if (SMALL || per > 16) {
+      rgemm(alpha, A, ta, Bm, beta, C0, C);
+      rgemm(alpha2, A2, ta, Bm, beta2, C02, C2);
+      return;
+    }
+    if (nr > 0)
+      cta_gemm_fullk(nr, k, k, alpha, ta ? A + r0 : A + r0 * k, k, ta, Bm, k, beta, C0 ? C0 + r0 * k : nullptr, k,
+                     C + r0 * k, k, sm, ta ? A2 + r0 : A2 + r0 * k, alpha2, beta2, C02 ? C02 + r0 * k : nullptr,
+                     C2 + r0 * k);
+  };
   if (tid == 0) {
     s_hits = 0;
     g_fk_bulk = !SMALL && !ws.fk_nobulk && k > 64;   // (k = 64: cp.async staging measured faster, 60.8 vs 65.4 us)
@@ -741,10 +763,9 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 22);
   if (useH) {   // one stage instead of three (the T products were done by kxk_lu)
-    rgemm(-1.0, H, true, R1, 1.0, R1, V1);            // V_1 = R_1 - H1^T R_1
-    rgemm(-1.0, H + 2 * kk, true, Mp, 1.0, V1, V1);   //       - H3^T M'
-    rgemm(1.0, H + kk, true, R1, 0.0, nullptr, Pt);   // P~ = H2^T R_1
-    rgemm(1.0, H + 3 * kk, true, Mp, 1.0, Pt, Pt);    //    + H4^T M'
+    // V_1 = R_1 - H1^T R_1 - H3^T M',  P~ = H2^T R_1 + H4^T M'  (each B staged once for two products)
+    rgemm2(R1, true, -1.0, H, 1.0, R1, V1, 1.0, H + kk, 0.0, nullptr, Pt);
+    rgemm2(Mp, true, -1.0, H + 2 * kk, 1.0, V1, V1, 1.0, H + 3 * kk, 1.0, Pt, Pt);
     if (crank == 0) RF_TSTAMP(ws, 23);
     if (crank == 0) RF_TSTAMP(ws, 24);
   } else {
@@ -788,10 +809,9 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 26);
   if (useH) {   // L B and U'^{-1} B directly (one stage instead of three)
-    rgemm(1.0, H, false, E11, 0.0, nullptr, LB);          // L B = H1 E_11
-    rgemm(1.0, H + kk, false, S2, 1.0, LB, LB);           //     + H2 S2
-    rgemm(1.0, H + 2 * kk, false, E11, 0.0, nullptr, UB); // U'^{-1} B = H3 E_11
-    rgemm(1.0, H + 3 * kk, false, S2, 1.0, UB, UB);       //           + H4 S2
+    // L B = H1 E_11 + H2 S2,  U'^{-1} B = H3 E_11 + H4 S2
+    rgemm2(E11, false, 1.0, H, 0.0, nullptr, LB, 1.0, H + 2 * kk, 0.0, nullptr, UB);
+    rgemm2(S2, false, 1.0, H + kk, 1.0, LB, LB, 1.0, H + 3 * kk, 1.0, UB, UB);
     if (crank == 0) RF_TSTAMP(ws, 27);
     if (crank == 0) RF_TSTAMP(ws, 28);
   } else {
