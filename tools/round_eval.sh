@@ -14,7 +14,7 @@ for c in cfg1 cfg3 cfg4 cfg5; do
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_ax -c 1 -o $O/full_cfg3_gemm \
   python bench.py --config cfg3 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"spmm_gather|passB_kernel|passC_kernel|kxk_finish" -c 4 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"spmm_stencil|spmm_gather|passB_kernel|passC_kernel|kxk_finish" -c 4 \
   -o $O/full_cfg4 python bench.py --config cfg4 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"passB2|spmm_stencil|passC|kxk_finish" -c 6 \
   -o $O/full_cfg5 python bench.py --config cfg5 --steps 1 --warmup 3 --no-extra > /dev/null 2>&1
