@@ -191,17 +191,20 @@ __device__ __noinline__ void cta_gemm_fullk(int M, int N, int K, double alpha, c
   auto zero_pad = [&]() {   // K, M, N are multiples of 8 on the clustered path except a ragged k: pad explicitly
     for (int a = 0; a < nA; ++a) {
       double* Aa = As + a * Mp * lda_s;
+      #pragma unroll 1
       for (int e = tid; e < Mp * (Kp - K) + (Mp - M) * Kp; e += KXK_THREADS) {
         if (e < Mp * (Kp - K)) Aa[(e / (Kp - K)) * lda_s + K + e % (Kp - K)] = 0.0;
         else { const int f = e - Mp * (Kp - K); Aa[(M + f / Kp) * lda_s + f % Kp] = 0.0; }
       }
     }
+    #pragma unroll 1
     for (int e = tid; e < (Kp - K) * Np + K * (Np - N); e += KXK_THREADS) {
       if (e < (Kp - K) * Np) Bs[(K + e / Np) * ldb_s + e % Np] = 0.0;
       else { const int f = e - (Kp - K) * Np; Bs[(f / (Np - N)) * ldb_s + N + f % (Np - N)] = 0.0; }
     }
   };
   auto stage_At = [&](const double* Aa, double* dst) {   // op(A)(i, p) = A[p][i]: element-wise transpose
+    #pragma unroll 1
     for (int e = tid; e < M * K; e += KXK_THREADS) {
       const int p = e / M, i = e - p * M;
       cp_async8(dst + i * lda_s + p, Aa + (size_t)p * lda + i, true);
@@ -608,7 +611,7 @@ RF_DEV unsigned cluster_nctarank() {
   asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
   return r;
 }
-RF_DEV void cluster_sync() {
+__device__ __noinline__ void cluster_sync() {   // (noinline: one copy in the instruction cache)
   if (cluster_nctarank() == 1) {   // single CTA: a block barrier orders its global accesses too
     __syncthreads();
     return;
@@ -632,7 +635,7 @@ constexpr int KXK_SMALL = 32;
 constexpr int KXK_SMALL_MATS = 20;   // k x k matrices resident in shared memory (see kxk_finish_kernel<true>)
 // layout: 20 k x k matrices | column-sum partials (8 x 7 x k) | d copy (k) | sigma, d, alpha, rr2 (4 k) | 64 spare
 __host__ __device__ constexpr int kxk_small_smem_doubles(int k) { return KXK_SMALL_MATS * k * k + 8 * 7 * k + k + 4 * k + 64; }
-RF_DEV void smem_mm(int k, double alpha, const double* A, bool ta, const double* B, double beta, const double* C0,
+__device__ __noinline__ void smem_mm(int k, double alpha, const double* A, bool ta, const double* B, double beta, const double* C0,
                     double* C) {
   __syncthreads();
   const int t = threadIdx.x;
@@ -750,6 +753,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   const double* srcG = SMALL ? Gp : ws.G2;
   const double* srcU = SMALL ? Ui : ws.Uinv;
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
+#pragma unroll 1
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     const double xp = srcX[e] * sig[j];
@@ -781,6 +785,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   }
   // E_11 (line 6): beta needs the Gram G = X'^T X' = X'_1^T X'_1 + G'
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
+#pragma unroll 1
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     double v;
@@ -805,6 +810,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   if (crank == 0) RF_TSTAMP(ws, 25);
   rgemm(1.0, Gp, false, Pt, 0.0, nullptr, GPt);       // G' P~
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
+#pragma unroll 1
     for (int j = tid & 31; j < k; j += 32) S2[i * k + j] = (Mp[i * k + j] - GPt[i * k + j]) / d[j];
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 26);
@@ -834,6 +840,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   double* Cp = S + 15 * kk;                            // C' = P~ D^-1 + U'^-1 B
   double* GC = Z;                                      // G' C' (Z is dead)
   for (int l = r0 + (tid >> 5); l < r1; l += 32)
+#pragma unroll 1
     for (int j = tid & 31; j < k; j += 32) {
     const int e = l * k + j;
     Xt1[e] = Xp[e] + (E11[e] - LB[e]);                 // X~_1 = X'_1 + (E_11 - L B)  (top rows of X~)
@@ -901,6 +908,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       const int g = tid / k, j = tid % k;
       const double dj = d[j];
       double q[NQ] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
       for (int l = g; l < k; l += NG) {
         const int e = l * k + j;
         const double x = Xt1[e], r = R1[e], ee = E11[e], pt = Pt[e], c = Cp[e];
@@ -920,6 +928,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
       const int j = tid >> 3, sl = tid & 7;
       double mg = INFINITY;
       if (j < k)
+#pragma unroll 1
         for (int i = sl; i < k; i += 8)
           if (i != j) mg = fmin(mg, fabs(sd[j] - sd[i]));
       for (int o = 1; o < 8; o <<= 1) mg = fmin(mg, __shfl_xor_sync(0xffffffffu, mg, o));
@@ -932,6 +941,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
 #pragma unroll
       for (int u = 0; u < NQ; ++u) {
         q[u] = cs[(size_t)u * k + j];
+#pragma unroll 1
         for (int g = 1; g < NG; ++g) q[u] += cs[((size_t)g * NQ + u) * k + j];
       }
       const double nt2 = q[0];
@@ -954,6 +964,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
     RF_TSTAMP(ws, 34);
     if (tid < 32) {   // warp 0: lane sums over j = lane, lane + 32, .., then a xor butterfly (every lane equal)
       double rr = 0.0, en = 0.0, mg = INFINITY, fl = 0.0, hits = 0.0, gmax = -1.0;
+#pragma unroll 1
       for (int j = tid; j < k; j += 32) { rr += s_red[0][j]; en += s_red[1][j]; mg = fmin(mg, s_red[2][j]); fl += s_red[3][j]; }
       for (int o = 16; o > 0; o >>= 1) {
         rr += __shfl_xor_sync(0xffffffffu, rr, o);
@@ -980,6 +991,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 31);
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
+#pragma unroll 1
     for (int j = tid & 31; j < k; j += 32) {
     const int e = i * k + j;
     const double inv = ws.invn[j];

@@ -576,12 +576,12 @@ static void launch_spmm(refine_ctx* c, bool vec, const double* Xg, const double*
 // kxk_finish as one thread-block cluster of kxk_cluster(k) CTAs (16 for k > 64 when the device can
 // schedule a non-portable 16-CTA cluster of this kernel: checked once; REFINE_KXK_CL16=0 keeps 8)
 static bool kxk_allow16() {
+  const char* e = getenv("REFINE_KXK_CL16");   // (read per launch: tests switch it within one process)
+  if (e && e[0] == '0') return false;
   static int ok = -1;
   if (ok < 0) {
     ok = 0;
-    const char* e = getenv("REFINE_KXK_CL16");
-    if (!(e && e[0] == '0') &&
-        cudaFuncSetAttribute(kxk_finish_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    if (cudaFuncSetAttribute(kxk_finish_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(16, 1, 1);
       cfg.blockDim = dim3(KXK_THREADS, 1, 1);

@@ -3,7 +3,7 @@ import os, sys
 os.environ["REFINE_KXK_TIMING"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth, paper_2602_23778_b200 as pkg
-for (n, k) in [(8192, 64), (8192, 128)]:
+for (n, k) in [(256, 4), (4096, 16), (8192, 32), (8192, 64), (8192, 128)]:
     torch.cuda.synchronize()
     p = synth.small_dense(n, k, m=8, seed=3, signs=True, device="cuda")
     R = pkg.Refiner.dense(p.A, k)
