@@ -701,6 +701,7 @@ struct Kern {
         if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
         if (eff >= 0.9 && ctas >= 3 * slots) break;
       }
+      if (getenv("REFINE_NSPLIT")) best = std::max(1, std::min<int>(atoi(getenv("REFINE_NSPLIT")), (int)kiters));   // (measurements)
       c->nsplit = best;
       const int64_t kit = (kiters + best - 1) / best;
       c->kchunk = kit * GBK;
