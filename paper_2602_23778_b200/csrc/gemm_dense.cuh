@@ -107,7 +107,27 @@ struct FusedFinish {
   const double* X;          // the shift operand (the sweep's X^)
   int* cnt;                 // per row-tile arrival counters (zero between launches)
   int on;
+  // refine_sweep_host's overlapped upload (TMA GEMM only): X^ arrives in chunks of ready_rows rows on a
+  // copy stream, each followed by a 4-byte copy of `epoch` into ready[chunk]; the producer waits for
+  // the chunk of each K step before loading its X^ box, the fix-up for its tile's rows.  null: X^ resident
+  const unsigned* ready;
+  unsigned epoch;
+  int ready_rows;
 };
+// wait until rows [r0, r1) of X^ have arrived (see FusedFinish::ready); then order the copy engine's
+// writes before this thread's async-proxy (TMA) and generic reads
+RF_DEV void wait_rows(const FusedFinish& f, int64_t r0, int64_t r1) {
+  if (f.ready == nullptr || r1 <= r0) return;
+  for (int64_t c = r0 / f.ready_rows; c <= (r1 - 1) / f.ready_rows; ++c) {
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f.ready + c) : "memory");
+      if (v == f.epoch) break;
+      __nanosleep(256);
+    }
+  }
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
 // called by the NTH consumer threads after their partial-tile stores; bar(): a barrier over them
 template <int NTH, int BM, typename Bar>
 RF_DEV void fused_finish(const FusedFinish& f, int nsplit, int64_t split_stride, int64_t m0, int tid, void* scratch,
@@ -122,6 +142,10 @@ RF_DEV void fused_finish(const FusedFinish& f, int nsplit, int64_t split_stride,
   bar();
   if (!*s_flag) return;
   __threadfence();                                  // (acquire side of the counter)
+  if (f.ready) {                                    // (overlapped upload: the tile's X^ rows)
+    if (tid == 0) wait_rows(f, m0, (m0 + BM < f.ws.n_loc) ? m0 + BM : f.ws.n_loc);
+    bar();
+  }
   dd* sa = reinterpret_cast<dd*>(scratch);
   dd* sg = sa + NTH;
   const int64_t re = (m0 + BM < f.ws.n_loc) ? m0 + BM : f.ws.n_loc;
@@ -317,6 +341,7 @@ gemm_ax_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         mbar_expect_tx(&full[s], T::STAGE_BYTES);
 #pragma unroll
         for (int b = 0; b < T::A_BOXES; ++b) tma_load_2d(st + b * T::A_BOX_BYTES, &tmA, k0 + 16 * b, (int)m0, &full[s]);
+        wait_rows(fin, k0, (k0 + BK < K) ? k0 + BK : K);   // (overlapped upload only)
 #pragma unroll
         for (int b = 0; b < T::B_BOXES; ++b)
           tma_load_2d(st + T::A_BOXES * T::A_BOX_BYTES + b * T::B_BOX_BYTES, &tmX, 16 * b, k0, &full[s]);

@@ -246,6 +246,15 @@ struct refine_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // host-buffer entry point
   double* dX = nullptr;
+  // refine_sweep_host's overlapped upload (dense, TMA GEMM): X^ in chunks on the h2d stream, each chunk
+  // flagged by a 4-byte copy of the call's epoch into h2d_ready[chunk]; S1 starts on the first chunk
+  cudaStream_t h2d = nullptr;
+  cudaEvent_t ev_h2d = nullptr, ev_pre = nullptr;
+  unsigned* h2d_ready = nullptr;       // device, H2D_MAX_CHUNKS flags
+  unsigned* h2d_epoch_host = nullptr;  // pinned: the value the flag copies carry
+  unsigned h2d_epoch = 0;
+  int h2d_rows = 0;
+  bool h2d_on = false;
   int launches = 0;
   // live per-kernel timing (refine_profile_begin/end): events at every kernel boundary
   cudaEvent_t* prof_ev = nullptr;
@@ -762,6 +771,7 @@ struct Kern {
         if (ph == 0 && ws.top > 0 && c->s1_only != 1) {
           cudaEventRecord(c->ev_fork, s);
           cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+          if (c->h2d_on) cudaStreamWaitEvent(c->side, c->ev_h2d, 0);   // (overlapped upload: X^_1 present)
           kxk_lu_kernel<<<1, KXK_THREADS, std::max(c->k <= 64 ? 4 * c->k * c->k : c->k * c->k, PANEL_SMEM) * 8,
                           c->side>>>(ws, X);
           cudaEventRecord(c->ev_join, c->side);
@@ -802,15 +812,24 @@ struct Kern {
             double* out = (c->nsplit == 1) ? ws.W : ws.Wpart;
             // split-K fix-up + shift + alpha/g partials in the GEMM's last CTA per row tile (fused_finish),
             // else by w_finish
-            const FusedFinish fin{wp, X, c->gemm_cnt, c->wfuse ? 1 : 0};
+            FusedFinish fin{wp, X, c->gemm_cnt, c->wfuse ? 1 : 0};
             if (pass == 0) c->mark();
-            if (TMA_OK && c->gemm_tma && bv16 && gemm_x_map(c, Xb))
+            const bool tma = TMA_OK && c->gemm_tma && bv16 && gemm_x_map(c, Xb);
+            const bool poll = c->h2d_on && tma && !c->multi && pass == 0;   // S1 consumes X^ as it arrives
+            if (c->h2d_on && !poll) cudaStreamWaitEvent(s, c->ev_h2d, 0);
+            if (poll) {
+              fin.ready = c->h2d_ready;
+              fin.epoch = c->h2d_epoch;
+              fin.ready_rows = c->h2d_rows;
+            }
+            if (tma)
               launch_k(c->pdl, gemm_tma, dim3(c->nsplit, c->gemm_gx), dim3(TGC::THREADS + 32), T_SMEM, s,
                        c->tm_A, c->tm_X, c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, ws.status, fin);
             else
               launch_k(c->pdl, gemm, dim3(c->nsplit, c->gemm_gx), dim3(GC::THREADS), GC::SMEM, s, c->A, c->lda, Xb,
                        c->k, c->n_loc, c->n, c->kchunk, out, c->n_loc * c->k, av16, bv16, ws.status, fin);
             if (last) c->mark();
+            if (poll) cudaStreamWaitEvent(s, c->ev_h2d, 0);   // everything after S1 sees all of X^
             if (c->wfuse) {
               c->n_ag_cur = c->gemm_gx;
               n += 1;
@@ -1761,8 +1780,66 @@ extern "C" refine_status refine_sweep_host(refine_ctx* c, const double* X_host_i
   if (c->sticky != REFINE_OK) return c->sticky;
   const size_t bytes = (size_t)c->n_loc * c->k * sizeof(double);
   if (!c->dX) RF_CK(c, cudaMalloc(&c->dX, bytes));
-  RF_CK(c, cudaMemcpyAsync(c->dX, X_host_in, bytes, cudaMemcpyHostToDevice, c->stream));
-  refine_status st = launch_sweep(c, c->dX);
+  // Dense single rank with the TMA GEMM and >= 1 MiB of X^: upload in chunks on a copy stream while S1
+  // runs (its producer warps wait per K step for their chunk; REFINE_H2D_OVERLAP=0 disables); chunks
+  // are issued split-interleaved so every split-K CTA's first rows arrive first.
+  const bool ov_env = !(getenv("REFINE_H2D_OVERLAP") && getenv("REFINE_H2D_OVERLAP")[0] == '0');
+  const bool ov = ov_env && !c->csr && !c->multi && !c->loopback && c->oz_ns == 0 && !c->opts.square &&
+                  c->gemm_tma && bytes >= ((size_t)1 << 20) && c->kchunk > 0;
+  refine_status st;
+  if (ov) {
+    constexpr int H2D_MAX_CHUNKS = 64;
+    if (!c->h2d) {
+      RF_CK(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+      RF_CK(c, cudaEventCreateWithFlags(&c->ev_h2d, cudaEventDisableTiming));
+      RF_CK(c, cudaEventCreateWithFlags(&c->ev_pre, cudaEventDisableTiming));
+      RF_CK(c, cudaMalloc(&c->h2d_ready, H2D_MAX_CHUNKS * sizeof(unsigned)));
+      RF_CK(c, cudaMemsetAsync(c->h2d_ready, 0, H2D_MAX_CHUNKS * sizeof(unsigned), c->stream));
+      RF_CK(c, cudaMallocHost(&c->h2d_epoch_host, sizeof(unsigned)));
+    }
+    // (the previous call ended with a host sync, so its flag copies have read h2d_epoch_host)
+    if (++c->h2d_epoch == 0) ++c->h2d_epoch;
+    *c->h2d_epoch_host = c->h2d_epoch;
+    const int64_t n = c->n_loc, k = c->k;
+    const int64_t per_split = std::max<int64_t>(c->kchunk, 16);
+    // chunks of `rows` rows aligned globally, `rows` a multiple of 16 (one TMA K step) dividing the split's
+    // rows so that no chunk straddles two splits: 4 per split where that divides, else fewer
+    int64_t rows = per_split;
+    for (int d : {4, 2})
+      if (per_split % (16 * d) == 0) { rows = per_split / d; break; }
+    if (rows % 16 != 0 || (n + rows - 1) / rows > H2D_MAX_CHUNKS) rows = 0;
+    if (rows == 0) {   // (no suitable chunking: plain upload)
+      RF_CK(c, cudaMemcpyAsync(c->dX, X_host_in, bytes, cudaMemcpyHostToDevice, c->stream));
+      st = launch_sweep(c, c->dX);
+      if (st != REFINE_OK) return st;
+      RF_CK(c, cudaMemcpyAsync(X_host_out, c->dX, bytes, cudaMemcpyDeviceToHost, c->stream));
+      int ds0 = 0;
+      if ((st = read_stats(c, stats, &ds0)) != REFINE_OK) return st;
+      return map_status(ds0);
+    }
+    c->h2d_rows = (int)rows;
+    RF_CK(c, cudaEventRecord(c->ev_pre, c->stream));   // after earlier work on dX
+    RF_CK(c, cudaStreamWaitEvent(c->h2d, c->ev_pre, 0));
+    const int64_t cps = (per_split + rows - 1) / rows;   // chunks per split (the last split may have fewer)
+    const int64_t nch = (n + rows - 1) / rows;
+    for (int64_t p = 0; p < cps; ++p)
+      for (int64_t sp = 0; sp * per_split < n; ++sp) {
+        const int64_t r0 = sp * per_split + p * rows;
+        const int64_t r1 = std::min(std::min(r0 + rows, (sp + 1) * per_split), n);
+        if (r0 >= r1) continue;
+        const int64_t ch = r0 / rows;   // (rows divides per_split: r0 is chunk-aligned)
+        if (ch >= nch) continue;
+        RF_CK(c, cudaMemcpyAsync(c->dX + r0 * k, X_host_in + r0 * k, (size_t)(r1 - r0) * k * 8, cudaMemcpyHostToDevice, c->h2d));
+        RF_CK(c, cudaMemcpyAsync(c->h2d_ready + ch, c->h2d_epoch_host, sizeof(unsigned), cudaMemcpyHostToDevice, c->h2d));
+      }
+    RF_CK(c, cudaEventRecord(c->ev_h2d, c->h2d));
+    c->h2d_on = true;
+    st = enqueue_sweep(c, c->dX);   // (direct launches: the flags' epoch changes per call)
+    c->h2d_on = false;
+  } else {
+    RF_CK(c, cudaMemcpyAsync(c->dX, X_host_in, bytes, cudaMemcpyHostToDevice, c->stream));
+    st = launch_sweep(c, c->dX);
+  }
   if (st != REFINE_OK) return st;
   RF_CK(c, cudaMemcpyAsync(X_host_out, c->dX, bytes, cudaMemcpyDeviceToHost, c->stream));
   int ds = 0;
@@ -1976,6 +2053,11 @@ extern "C" void refine_destroy(refine_ctx* c) {
   if (c->pool) cudaFree(c->pool);
   if (c->ws.tlog) cudaFree(c->ws.tlog);
   if (c->dX) cudaFree(c->dX);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->ev_h2d) cudaEventDestroy(c->ev_h2d);
+  if (c->ev_pre) cudaEventDestroy(c->ev_pre);
+  if (c->h2d_ready) cudaFree(c->h2d_ready);
+  if (c->h2d_epoch_host) cudaFreeHost(c->h2d_epoch_host);
   if (c->oz_e) cudaFree(c->oz_e);
   if (c->oz_diag) cudaFree(c->oz_diag);
   if (c->oz_f) cudaFree(c->oz_f);

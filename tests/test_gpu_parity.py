@@ -167,6 +167,28 @@ def test_host_entry_point_matches_device(pkg):
     assert np.array_equal(Xh, Xd.cpu().numpy())
 
 
+@pytest.mark.parametrize("n,k", [(4096, 64), (6000, 32), (8192, 64)])
+def test_host_entry_overlapped_upload(pkg, monkeypatch, n, k):
+    """refine_sweep_host with the chunked upload overlapped with S1 (dense, TMA GEMM, >= 1 MiB of X^:
+    the GEMM's producer waits per K step for its chunk's flag, the fix-up for its rows): bit-identical to
+    the device sweep and to the plain upload, over several calls (the flags' epoch advances per call)."""
+    p = synth.small_dense(n, k, m=8, seed=n + k, signs=True)
+    R = refiner(pkg, p)
+    Xd = p.X0.cuda().clone()
+    Xh = p.X0.numpy().copy()
+    for _ in range(3):
+        R.refine_sweep(Xd)
+        s, st = R.refine_sweep_host(Xh)
+        assert s == pkg.REFINE_OK
+        assert np.array_equal(Xh, Xd.cpu().numpy())
+    monkeypatch.setenv("REFINE_H2D_OVERLAP", "0")
+    R2 = refiner(pkg, p)
+    Xp = p.X0.numpy().copy()
+    for _ in range(3):
+        R2.refine_sweep_host(Xp)
+    assert np.array_equal(Xp, Xh)
+
+
 # ------------------------------------------------------------------------------ CSR
 
 @pytest.mark.parametrize("dims,coeffs,k", [((40, 37), (1.0, 1.37), 6), ((64, 61), (1.0, 1.37), 32),
