@@ -172,7 +172,12 @@ refine_status refine_sweep(refine_ctx* c, double* X, refine_sweep_stats* stats);
 
 /* Same sweep with HOST buffers (end-to-end entry point): copies X_host_in
  * (n_loc x k) to the device, runs one sweep, copies the result to X_host_out
- * (may equal X_host_in) and synchronises.  Pinned memory gives full PCIe rate. */
+ * (may equal X_host_in) and synchronises.  Pinned memory gives full PCIe rate.
+ * Dense A, one rank, >= 1 MiB of X: the upload goes in chunks on a copy stream
+ * and S1 (the TMA GEMM) consumes each chunk as it lands (per-chunk flags); the
+ * result is bit-identical to the device-buffer sweep.  An upload that never
+ * completes ends the sweep with REFINE_DIVERGED after 5 s instead of hanging.
+ * REFINE_H2D_OVERLAP=0 uploads everything before the sweep. */
 refine_status refine_sweep_host(refine_ctx* c, const double* X_host_in, double* X_host_out,
                                 refine_sweep_stats* stats);
 

@@ -116,13 +116,23 @@ struct FusedFinish {
 };
 // wait until rows [r0, r1) of X^ have arrived (see FusedFinish::ready); then order the copy engine's
 // writes before this thread's async-proxy (TMA) and generic reads
+// (a failed upload never sets its flags: after 5 s the wait gives up and marks the sweep failed, rather
+// than hanging the device)
 RF_DEV void wait_rows(const FusedFinish& f, int64_t r0, int64_t r1) {
   if (f.ready == nullptr || r1 <= r0) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
   for (int64_t c = r0 / f.ready_rows; c <= (r1 - 1) / f.ready_rows; ++c) {
     unsigned v;
     while (true) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f.ready + c) : "memory");
       if (v == f.epoch) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+      if (t - t0 > 5000000000ull) {
+        atomicCAS(f.ws.status, ST_OK, ST_DIVERGED);
+        return;
+      }
       __nanosleep(256);
     }
   }
