@@ -752,6 +752,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
   const double* srcM = SMALL ? Mp : ws.M2;
   const double* srcG = SMALL ? Gp : ws.G2;
   const double* srcU = SMALL ? Ui : ws.Uinv;
+  if (crank == 0) RF_TSTAMP(ws, 35);
   for (int i = r0 + (tid >> 5); i < r1; i += 32)
 #pragma unroll 1
     for (int j = tid & 31; j < k; j += 32) {
@@ -764,6 +765,7 @@ __device__ void kxk_finish_body(const Ws& ws, double* __restrict__ Xtop, const d
     Gp[e] = sig[i] * srcG[e] * sig[j];
     Ui[e] = sig[i] * srcU[e];                         // U'^{-1} = Sigma U^{-1}
   }
+  if (crank == 0) RF_TSTAMP(ws, 36);
   cluster_sync();
   if (crank == 0) RF_TSTAMP(ws, 22);
   if (useH) {   // one stage instead of three (the T products were done by kxk_lu)

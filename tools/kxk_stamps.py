@@ -22,6 +22,9 @@ for (n, k) in [(256, 4), (4096, 16), (8192, 32), (8192, 64), (8192, 128)]:
     if a[60] and a[63]:
         print(f"   second cta_gemm_fullk: staging {(a[61] - a[60]) / 1.965e3:.2f} us, DMMA+stores {(a[62] - a[61]) / 1.965e3:.2f} us, "
               f"final barrier {(a[63] - a[62]) / 1.965e3:.2f} us")
+    if a[35] and a[36]:
+        print(f"   first phase: start -> elementwise {(a[35] - a[20]) / 1.965e3:.1f} us, elementwise {(a[36] - a[35]) / 1.965e3:.1f} us, "
+              f"cluster barrier {(a[22] - a[36]) / 1.965e3:.1f} us")
     if a[33] and a[34]:
         print(f"   stats phase: column sums {(a[33] - a[30]) / 1.965e3:.1f} us, per-column {(a[34] - a[33]) / 1.965e3:.1f} us, "
               f"tail {(a[31] - a[34]) / 1.965e3:.1f} us")
