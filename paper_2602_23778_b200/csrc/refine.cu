@@ -719,7 +719,8 @@ struct Kern {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, passB, B_THREADS, B_SMEM))) return e;
     occ = std::max(occ, 1);
     const int64_t rows = std::max<int64_t>(c->n_loc - c->ws.top, 1);
-    const int64_t max_chunks = std::max<int64_t>((rows + 255) / 256, 1);   // >= 256 rows per chunk
+    static const int64_t pb_min_rows = getenv("REFINE_PB_MINROWS") ? std::max(32, atoi(getenv("REFINE_PB_MINROWS"))) : 64;
+    const int64_t max_chunks = std::max<int64_t>((rows + pb_min_rows - 1) / pb_min_rows, 1);   // >= pb_min_rows rows per chunk
     c->passb_grid_y = (int)std::min<int64_t>(std::max(c->sms * occ / B_NT, 1), max_chunks);
     if (B2 && B2C::PAIRED) {   // 7 balanced units per pair of chunks (passB2_kernel / passB2_tma_kernel)
       if (c->pb_tma) {   // one CTA per SM: one wave of units
