@@ -181,6 +181,12 @@ def test_host_entry_overlapped_upload(pkg, monkeypatch, n, k):
         s, st = R.refine_sweep_host(Xh)
         assert s == pkg.REFINE_OK
         assert np.array_equal(Xh, Xd.cpu().numpy())
+    Xpin = p.X0.clone().pin_memory()                 # pinned: the chunk copies are truly asynchronous
+    R3 = refiner(pkg, p)
+    for _ in range(3):
+        s, st = R3.refine_sweep_host(Xpin)
+        assert s == pkg.REFINE_OK
+    assert np.array_equal(Xpin.numpy(), Xh)
     monkeypatch.setenv("REFINE_H2D_OVERLAP", "0")
     R2 = refiner(pkg, p)
     Xp = p.X0.numpy().copy()
