@@ -27,8 +27,9 @@ def pkg():
 
 @pytest.fixture(autouse=True)
 def force_stencil(monkeypatch):
-    """By default the library takes the stencil SpMM only for 3-D grids with k >= 64 (where it measured
-    faster); REFINE_SPMM=stencil makes every eligible matrix take it, so each case below exercises it."""
+    """By default the library takes the stencil SpMM for 3-D grids with k >= 64 and 2-D grids with k a
+    multiple of 32 (where it measured faster); REFINE_SPMM=stencil makes every eligible matrix take it,
+    so each case below exercises it (small grids: most CTAs get an empty slab range)."""
     monkeypatch.setenv("REFINE_SPMM", "stencil")
 
 
