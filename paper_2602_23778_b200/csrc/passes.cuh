@@ -957,41 +957,47 @@ passC_kernel(Ws ws, const double* X, double* out, int vec16) {
 // producer warp: 16 warps keep 128 registers).  All of Csig stays resident (padded rows,
 // conflict-free B fragments).  Same DMMA k-order and epilogue fma as passC_kernel (identical
 // results); in place, rows >= top only.
-struct PassCPPCfg {
-  static constexpr int KP = 128, BR = 32, GROUPS = 2, GWARPS = 8;
+// Generalised (round 2, late): ST ring stages shared by the two groups (tile j -> stage j % ST); with
+// ST = 3 a group's next tile is issued by the OTHER group one tile earlier (PassCPP3: 24-row tiles).
+template <int BR_, int ST_, int WM__, int WN__>
+struct PassCPPCfgT {
+  static constexpr int KP = 128, BR = BR_, GROUPS = 2, GWARPS = 8, ST = ST_;
   static constexpr int WARPS = GROUPS * GWARPS, THREADS = WARPS * 32, BLOCK = THREADS;
-  static constexpr int WM_ = 2, WN_ = 4, WTM = BR / WM_, WTN = KP / WN_, MI = WTM / 8, NI = WTN / 8;
+  static constexpr int WM_ = WM__, WN_ = WN__, WTM = BR / WM_, WTN = KP / WN_, MI = WTM / 8, NI = WTN / 8;
   static constexpr int LDC = KP + 8;
   static constexpr int BOX = BR * 128, STAGE = (KP / 16) * BOX;
-  static constexpr int SMEM = GROUPS * STAGE + KP * LDC * 8 + 1024 + 2 * GROUPS * 8;
+  static constexpr int SMEM = ST * STAGE + KP * LDC * 8 + 1024 + 2 * ST * 8;
 };
-__global__ void __launch_bounds__(PassCPPCfg::BLOCK, 1)
+using PassCPPCfg = PassCPPCfgT<32, 2, 2, 4>;
+using PassCPP3Cfg = PassCPPCfgT<24, 3, 1, 8>;
+using PassCPP4Cfg = PassCPPCfgT<16, 4, 1, 8>;
+template <class C>
+__global__ void __launch_bounds__(C::BLOCK, 1)
 passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restrict__ out) {
-  using C = PassCPPCfg;
   constexpr int BR = C::BR, KP = C::KP;
   extern __shared__ __align__(1024) unsigned char pcsm[];
   __shared__ double ssc[KP];
   griddep_wait();
   if (*ws.status != ST_OK) return;
   unsigned char* ring = smem_align1024(pcsm);
-  double* Cs = reinterpret_cast<double*>(ring + C::GROUPS * C::STAGE);
+  double* Cs = reinterpret_cast<double*>(ring + C::ST * C::STAGE);
   uint64_t* full = reinterpret_cast<uint64_t*>(Cs + KP * C::LDC);
-  int* done = reinterpret_cast<int*>(full + C::GROUPS);             // warps through a tile's DMMAs (monotonic)
+  int* done = reinterpret_cast<int*>(full + C::ST);                 // warps through a tile's DMMAs (monotonic)
   const int k = ws.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t rows = ws.n_loc - ws.top;
   const int64_t ntile = (rows + BR - 1) / BR;
   const int njt = (int)((ntile > blockIdx.x) ? (ntile - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);   // this CTA's tiles
-  auto issue = [&](int j) {   // tile j of this CTA -> stage j % 2
-    const int s = j % C::GROUPS;
+  auto issue = [&](int j) {   // tile j of this CTA -> stage j % ST
+    const int s = j % C::ST;
     const int r0 = (int)(ws.top + (blockIdx.x + (int64_t)j * gridDim.x) * BR);
     mbar_expect_tx(&full[s], C::STAGE);
 #pragma unroll
     for (int b = 0; b < KP / 16; ++b) tma_load_2d(ring + s * C::STAGE + b * C::BOX, &tmX, 16 * b, r0, &full[s]);
   };
   if (tid == 0) {
-    for (int s = 0; s < C::GROUPS; ++s) { mbar_init(&full[s], 1); done[s] = 0; }
+    for (int s = 0; s < C::ST; ++s) { mbar_init(&full[s], 1); done[s] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int j = 0; j < C::GROUPS && j < njt; ++j) issue(j);
+    for (int j = 0; j < C::ST && j < njt; ++j) issue(j);
   }
   for (int e = tid; e < KP * KP; e += blockDim.x) {
     const int l = e / KP, j = e % KP;
@@ -1002,7 +1008,7 @@ passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restri
   const int grp = warp / C::GWARPS, gw = warp % C::GWARPS;
   const int wm = gw / C::WN_, wn = gw % C::WN_;
   for (int j = grp; j < njt; j += C::GROUPS) {
-    const int s = j % C::GROUPS;
+    const int s = j % C::ST;
     const int64_t r0 = ws.top + (blockIdx.x + (int64_t)j * gridDim.x) * BR;
     double w[C::MI][C::NI][2];   // this thread's W entries, loaded ahead of the MMAs
 #pragma unroll
@@ -1024,7 +1030,7 @@ passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restri
     for (int i = 0; i < C::MI; ++i)
 #pragma unroll
       for (int jn = 0; jn < C::NI; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
-    mbar_wait(&full[s], (j / C::GROUPS) & 1);
+    mbar_wait(&full[s], (j / C::ST) & 1);
     const unsigned char* xs = ring + s * C::STAGE;
 #pragma unroll 4
     for (int kk = 0; kk < KP; kk += 4) {
@@ -1045,7 +1051,7 @@ passC_pp_kernel(Ws ws, const __grid_constant__ CUtensorMap tmX, double* __restri
         for (int jn = 0; jn < C::NI; ++jn) dmma(acc[i][jn][0], acc[i][jn][1], a[i], b[jn]);
     }
     __syncwarp();                                // this warp's reads of the stage are done
-    if (lane == 0 && stage_release_last(&done[s], C::GWARPS) && j + C::GROUPS < njt) issue(j + C::GROUPS);   // last of the group
+    if (lane == 0 && stage_release_last(&done[s], C::GWARPS) && j + C::ST < njt) issue(j + C::ST);   // last of the group
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
       const int64_t g = r0 + wm * C::WTM + i * 8 + (lane >> 2);

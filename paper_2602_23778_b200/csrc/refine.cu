@@ -215,7 +215,9 @@ struct refine_ctx {
   const double* tm_X_ptr = nullptr;
   // TMA-fed pass B at k = 128 (passB2_tma_kernel): X's map (cached per pointer) and W's (fixed)
   bool pb_tma = false;
-  bool pc_pp = false;
+  int pc_pp = 0;                 // k = 128: ping-pong pass C (1: 2 stages of 32 rows, 3: 3 stages of 24 rows)
+  CUtensorMap tm_Xc{};
+  const double* tm_Xc_ptr = nullptr;
   bool pb_pp = false;            // k = 128: ping-pong pass B (passB2_pp_kernel)            // k = 128: ping-pong pass C (passC_pp_kernel)
   CUtensorMap tm_Xb{}, tm_Wb{};
   const double* tm_Xb_ptr = nullptr;
@@ -367,6 +369,12 @@ static bool passb_x_map(refine_ctx* c, const double* X) {   // local X rows -> b
   if (c->tm_Xb_ptr == X) return true;
   if (!encode_2d(&c->tm_Xb, X, (uint64_t)c->k, (uint64_t)c->n_loc, (uint64_t)c->k, PassB2TmaCfg<128>::BR)) return false;
   c->tm_Xb_ptr = X;
+  return true;
+}
+static bool passc3_x_map(refine_ctx* c, const double* X, int rows) {   // local X rows -> boxes of `rows` x 16 columns
+  if (c->tm_Xc_ptr == X) return true;
+  if (!encode_2d(&c->tm_Xc, X, (uint64_t)c->k, (uint64_t)c->n_loc, (uint64_t)c->k, rows)) return false;
+  c->tm_Xc_ptr = X;
   return true;
 }
 static bool gemm_x_map(refine_ctx* c, const double* X) {   // X (n x k) -> boxes of 16 (K rows) x 16 columns
@@ -930,8 +938,15 @@ struct Kern {
             passC_oz_kernel<<<c->sms, OZC_THREADS, OZC_SMEM, s>>>(ws, X, X);
           else if (use_tc_c(c, X))   // NEXT-2: X_2 Csig on tcgen05
             passC_tc_kernel<TKP><<<c->sms, TCC_THREADS, TccCfg<TKP>::SMEM, s>>>(ws, X, X);
+          else if (KP == 128 && c->pc_pp == 4 && xv16 && passc3_x_map(c, X, PassCPP4Cfg::BR))   // 4 stages of 16 rows
+            launch_k(c->pdl, passC_pp_kernel<PassCPP4Cfg>, dim3(c->sms), dim3(PassCPP4Cfg::BLOCK), PassCPP4Cfg::SMEM, s,
+                     ws, c->tm_Xc, X);
+          else if (KP == 128 && c->pc_pp == 3 && xv16 && passc3_x_map(c, X, PassCPP3Cfg::BR))   // 3 stages of 24 rows
+            launch_k(c->pdl, passC_pp_kernel<PassCPP3Cfg>, dim3(c->sms), dim3(PassCPP3Cfg::BLOCK), PassCPP3Cfg::SMEM, s,
+                     ws, c->tm_Xc, X);
           else if (KP == 128 && c->pc_pp && xv16 && passb_x_map(c, X))   // ping-pong pass C (X's pass-B map)
-            launch_k(c->pdl, passC_pp_kernel, dim3(c->sms), dim3(PassCPPCfg::BLOCK), PassCPPCfg::SMEM, s, ws, c->tm_Xb, X);
+            launch_k(c->pdl, passC_pp_kernel<PassCPPCfg>, dim3(c->sms), dim3(PassCPPCfg::BLOCK), PassCPPCfg::SMEM, s, ws,
+                     c->tm_Xb, X);
           else
             launch_k(c->pdl, passC_sweep, dim3(c->passc_grid, 1), dim3(CC::THREADS), CC::SMEM, s, ws,
                      (const double*)X, X, (int)xv16);
@@ -1181,11 +1196,17 @@ static refine_status init_rank(refine_ctx* c, int64_t n, int32_t k, int64_t row_
     c->pb_pp = c->pb_tma && !(bpe && bpe[0] == '0');
     if (c->pb_pp)
       RF_CK(c, cudaFuncSetAttribute(passB2_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PassB2PPCfg::SMEM));
-    // k = 128 (even): the ping-pong pass C (passC_pp_kernel; REFINE_PASSC_PP=0 disables)
+    // k = 128 (even): the ping-pong pass C (passC_pp_kernel; REFINE_PASSC_PP=0 disables): 3 stages of 24
+    // rows by default (cfg5 4.00 ms), 1: 2 stages of 32 rows (4.15 ms), 4: 4 stages of 16 rows (4.01 ms)
     const char* ce = getenv("REFINE_PASSC_PP");
-    c->pc_pp = !(ce && ce[0] == '0') && c->k == 128 && tensor_map_encoder() != nullptr;
-    if (c->pc_pp)
-      RF_CK(c, cudaFuncSetAttribute(passC_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PassCPPCfg::SMEM));
+    c->pc_pp = (!(ce && ce[0] == '0') && c->k == 128 && tensor_map_encoder() != nullptr) ? ((ce && (ce[0] == '1' || ce[0] == '4')) ? ce[0] - '0' : 3) : 0;
+    if (c->pc_pp) {
+      RF_CK(c, cudaFuncSetAttribute(passC_pp_kernel<PassCPPCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, PassCPPCfg::SMEM));
+      RF_CK(c, cudaFuncSetAttribute(passC_pp_kernel<PassCPP3Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    PassCPP3Cfg::SMEM));
+      RF_CK(c, cudaFuncSetAttribute(passC_pp_kernel<PassCPP4Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    PassCPP4Cfg::SMEM));
+    }
   }
   RF_CK(c, (cudaError_t)dispatch(c->kp, [&](auto K) { return decltype(K)::setup(c); }));
   RF_CK(c, cudaFuncSetAttribute(kxk_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(KMAX * KMAX, std::max(PANEL_SMEM, 4 * 64 * 64)) * 8));
