@@ -500,3 +500,23 @@ def test_kxk_finish_variants(pkg, monkeypatch, env, k):
     p = synth.small_dense(1200, k, m=8, seed=7 + k, signs=True)
     worst, _ = one_step(pkg, p, 2)
     print(f"k={k} {env}: worst one-step rel diff {worst:.3e}")
+
+
+def test_passC_pp_variants_bitwise(pkg, monkeypatch):
+    """The k = 128 ping-pong pass C in its three ring shapes (passes.cuh PassCPPCfgT: 2 stages of 32 rows,
+    3 of 24 (default), 4 of 16): every output element has the same DMMA k-order and epilogue fma, so the
+    sweeps agree bit for bit; one-step parity with the oracle on the default."""
+    p = synth.small_dense(1500, 128, m=8, seed=1628, signs=True)
+    outs = []
+    for v in ("1", "3", "4"):
+        monkeypatch.setenv("REFINE_PASSC_PP", v)
+        R = refiner(pkg, p)
+        X = p.X0.cuda().clone()
+        for _ in range(2):
+            assert R.refine_sweep(X) == pkg.REFINE_OK
+        outs.append(X.cpu().numpy())
+        del R
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+    monkeypatch.setenv("REFINE_PASSC_PP", "3")
+    worst, _ = one_step(pkg, p, 2)
+    print(f"pass C variants: worst one-step rel diff {worst:.3e}")
